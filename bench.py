@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark of the RelayGen hot path on B200 (BASELINE.json metric).
+
+One step = one pass of the whole offline hot path over a
+batch of synthetic input resident in HBM: stats init, K1 relay_margin_rows
+over every logit row, K2 relay_cue_scan, K3 relay_segment_reduce, (N>1) the
+NCCL sum all-reduce of the uint64 statistics table (H6), the 4 KB table read
+back and relay_stats_finalize on the host (H7).
+
+Workload per rank (weak scaling): one Qwen3-32B-shaped reasoning trajectory of
+32,768 tokens x 151,936-vocab bf16 logits with 8 switch cues (configs[1]);
+at N = 8 the job is configs[3] (8 x 32,768 rows sharded by trajectory).
+Inputs (9.96 GB of logits per rank) are far larger than the 126 MB L2, so no
+flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl relay|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "logit rows/sec and HBM GB/s (fraction of ~8 TB/s) for margin+segment pass, 1/2/4/8 GPU"
+UNIT = "rows/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="relay", choices=["relay", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no clocks/e2e/baseline)")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6 for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def workload(cfg: str):
+    import synth
+    c = synth.CONFIGS[cfg]
+    return c
+
+
+def oracle_pass(rows_host, dtype, vocab, tokens, offs, cs_h, threads):
+    """The whole hot path in the oracle: margins, scan, windows, stats."""
+    import oracle
+    ref = oracle.margin_rows(rows_host, dtype=dtype, vocab=vocab, threads=threads)
+    m32 = ref["margin"].astype(np.float32)
+    oracle.analyze(m32, tokens, offs, cs_h.pat_tokens, cs_h.pat_offsets, cs_h.pat_cue, cs_h.n_cues,
+                   cs_h.terminator)
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    """--impl reference: the oracle, as it stands, on this box's host cores,
+    each step a contiguous sub-trajectory sample of the same workload."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import synth
+    c = workload(args.config)
+    vocab, dtype = c["vocab"], c["dtype"]
+    cs_h = synth.make_cueset(vocab, c["n_cues"], c["n_pat"], max_len=c["max_len"])
+    ts = synth.make_tokens(1, c["traj_len"], cs_h)
+    threads = cpu_threads()
+    # size the sample so a step takes ~1 s on this host (whole run: a few minutes)
+    probe = synth.make_logits(8, vocab, dtype, tokens=ts.tokens[:8], device="cpu")
+    host = synth.host_rows(probe, dtype)
+    t0 = time.perf_counter()
+    oracle_pass(host, dtype, vocab, ts.tokens[:8], None, cs_h, 1)
+    per_row = (time.perf_counter() - t0) / 8
+    budget = min(1.5, 150.0 / max(1, args.steps + args.warmup))
+    S = int(max(threads, min(c["traj_len"], budget * threads / max(per_row, 1e-9))))
+    S = max(threads, S // threads * threads)
+    L = synth.make_logits(S, vocab, dtype, tokens=ts.tokens[:S], device="cpu")
+    host = synth.host_rows(L, dtype)
+    toks = np.ascontiguousarray(ts.tokens[:S])
+    for _ in range(args.warmup):
+        oracle_pass(host, dtype, vocab, toks, None, cs_h, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle_pass(host, dtype, vocab, toks, None, cs_h, threads)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = S * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: oracle on a {S}-row contiguous sample of the "
+                   f"{c['traj_len']}-token x {vocab}-vocab {dtype} trajectory per step",
+                   "rows_per_step": S},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"{S} rows per step (plain C fp64 oracle, {threads} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_06454_b200 as relay
+    import synth
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = workload(args.config)
+    vocab, dtype, T = c["vocab"], c["dtype"], c["traj_len"]
+    cs_h = synth.make_cueset(vocab, c["n_cues"], c["n_pat"], max_len=c["max_len"])
+    cs = relay.CueSet.from_synth(cs_h)
+    # this rank's trajectory (weak scaling: one trajectory per rank)
+    ts = synth.make_tokens(1, T, cs_h, seed=synth.BASE_SEED + rank)
+    logits = synth.make_logits(T, vocab, dtype, tokens=ts.tokens, seed=synth.BASE_SEED + 17 * rank,
+                               device=dev, chunk_rows=2048)
+    tok = torch.as_tensor(ts.tokens, device=dev)
+    offs = torch.as_tensor(ts.traj_offsets, device=dev)
+    tep = torch.as_tensor(ts.think_end_pos, device=dev)
+    an = relay.Analyzer(cs, T, vocab, dev, rank=rank, world_size=world)
+    stream = torch.cuda.current_stream()
+    host_stats = torch.empty(an.stats.shape, dtype=torch.int64, pin_memory=True)
+
+    k1_ev = []
+
+    def step(timed=False):
+        relay.stats_init(an.stats, cs.n_cues, rank, world)
+        if timed:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        relay.margin_rows(logits, vocab=vocab, out=an.rows)
+        if timed:
+            e1.record(stream)
+            k1_ev.append((e0, e1))
+        relay.cue_scan(cs, tok, offs, an.cap, an.ws, an.scan)
+        relay.segment_reduce(cs, an.rows["margin"], an.scan, offs, tep, an.tau, an.stats, rank, world,
+                             an.ws, an.seg)
+        if world > 1:
+            dist.all_reduce(an.stats, op=dist.ReduceOp.SUM)     # H6: one NCCL all-reduce
+        host_stats.copy_(an.stats, non_blocking=True)
+        stream.synchronize()
+        return relay.stats_finalize(host_stats.numpy(), cs.n_cues, world)   # H7
+
+    for _ in range(args.warmup):
+        step()
+    clocks = Clocks(local)
+    if not args.profile:
+        clocks.start()
+        time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(timed=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop() if not args.profile else None
+    ms = t0.elapsed_time(t1)
+    k1_ms = statistics.mean(a.elapsed_time(b) for a, b in k1_ev)
+    if world > 1:
+        t = torch.tensor([ms, k1_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, k1_ms = float(t[0]), float(t[1])
+    rows_total = T * world * args.steps
+    value = rows_total / (ms / 1e3)
+    esz = {"bf16": 2, "f16": 2, "f32": 4}[dtype]
+    k1_bytes = T * (vocab * esz + 17)      # logits read + margin/top1/top2/lse/status written
+    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
+    pk = peaks()
+    peak = pk.get("hbm_gbs") or 6650.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank)
+    cpu = None
+    if rank == 0 and not args.no_baseline and not args.profile:
+        cpu = cpu_baseline(logits, ts, cs_h, dtype, vocab)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": f"{args.config}: {world} x one {T}-token trajectory x {vocab}-vocab "
+                       f"{dtype} logits (Qwen3-32B shape), {c['n_cues']} cues / {c['n_pat']} patterns, "
+                       "margin+cue-scan+segment-reduce+stats (H1-H7), one trajectory per rank",
+                       "rows_per_rank": T, "vocab": vocab, "l2": "inputs 9.96 GB/rank >> 126 MB L2, no flush",
+                       "parallelism": f"dp{world} (trajectory-sharded)"},
+            "hbm_gbs_step": (T * world * (vocab * esz + 17)) / (ms / 1e3 / args.steps) / 1e9 / world,
+            "roofline": {"kernel": "relay_margin_rows (K1)", "bound": "hbm", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if pk.get("hbm_gbs") else "fallback",
+                         "frac_of_8TBs": achieved / 8000.0, "k1_ms": k1_ms,
+                         "k1_share_of_step": k1_ms / (ms / args.steps),
+                         "algorithmic_bytes_per_launch": k1_bytes},
+            "gpu_launches": an.n_launches() * args.steps,
+            "clocks": ck,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    cs.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):
+    """Same metric through the public API with HOST inputs: every step copies the
+    step's logits + tokens from pinned host memory, runs the pass, and reads the
+    statistics table back."""
+    import torch
+    import torch.distributed as dist
+    T, V = logits.shape
+    h_logits = torch.empty((T, V), dtype=logits.dtype, pin_memory=True)
+    h_logits.copy_(logits)
+    h_tok = torch.from_numpy(ts.tokens.copy()).pin_memory()
+    h_offs = torch.from_numpy(ts.traj_offsets.copy()).pin_memory()
+    d_logits = torch.empty_like(logits)
+    d_tok = torch.empty(T, dtype=torch.int32, device=dev)
+    d_offs = torch.empty(h_offs.shape, dtype=torch.int64, device=dev)
+    host_stats = torch.empty(an.stats.shape, dtype=torch.int64, pin_memory=True)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        d_logits.copy_(h_logits, non_blocking=True)
+        d_tok.copy_(h_tok, non_blocking=True)
+        d_offs.copy_(h_offs, non_blocking=True)
+        an.run(d_logits, d_tok, d_offs)
+        if world > 1:
+            dist.all_reduce(an.stats, op=dist.ReduceOp.SUM)
+        host_stats.copy_(an.stats, non_blocking=True)
+        stream.synchronize()
+        relay.stats_finalize(host_stats.numpy(), cs.n_cues, world)
+
+    step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    bi = h_logits.numel() * h_logits.element_size() + h_tok.numel() * 4 + h_offs.numel() * 8
+    bo = host_stats.numel() * 8
+    del h_logits, d_logits
+    torch.cuda.empty_cache()
+    return {"value": T * world * args.e2e_steps / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": args.e2e_steps,
+            "path": "pinned host logits+tokens -> H2D -> Analyzer.run (C ABI) -> D2H stats -> finalize"}
+
+
+def cpu_baseline(logits, ts, cs_h, dtype, vocab):
+    """The oracle as it stands on this host's cores, on a bounded contiguous
+    sample of the same workload (~10-20 s of CPU work)."""
+    import synth
+    threads = cpu_threads()
+    host8 = synth.host_rows(logits[:8], dtype)
+    t0 = time.perf_counter()
+    oracle_pass(host8, dtype, vocab, ts.tokens[:8], None, cs_h, 1)
+    per_row = (time.perf_counter() - t0) / 8
+    S = int(min(logits.shape[0], max(threads, 12.0 * threads / max(per_row, 1e-9))))
+    host = synth.host_rows(logits[:S], dtype)
+    toks = np.ascontiguousarray(ts.tokens[:S])
+    t0 = time.perf_counter()
+    oracle_pass(host, dtype, vocab, toks, None, cs_h, threads)
+    dt = time.perf_counter() - t0
+    return {"value": S / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"first {S} rows (+ their tokens) of the rank-0 trajectory, full H1-H7 oracle pass, "
+                      f"{dt:.1f} s"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,262 @@
+/*
+ * relay.h — C ABI of librelay.so: the B200 (sm_100a) hot path of RelayGen
+ * (arXiv 2602.06454): per-token probability margins from logits, switch-cue
+ * scanning, post-sentence segment statistics and the decode-step switch flag.
+ *
+ * Citations: "P:n" = PAPER.md line n (§ / equation / table named alongside),
+ * "S:n" = SPEC.md line n.  DESIGN.md "Readings" R1..R16 records every reading
+ * of a silent or ambiguous passage that an entry point below depends on.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless marked [host].  The caller owns every
+ *    buffer, the stream and the workspace; the library allocates device memory
+ *    only inside relay_cueset_create (the cue set's own <20 KB copy).
+ *  - Hot calls (margin_rows, cue_scan, segment_reduce, stats_init,
+ *    step_switch) are asynchronous on `stream`: they never synchronise, never
+ *    allocate and never read device memory from the host, so they can be
+ *    captured in a CUDA graph.  `stream` is a cudaStream_t (NULL = legacy).
+ *  - Host-side argument validation returns an error with NO device work.
+ *    Launch failures return RELAY_ERR_CUDA.  relay_last_error() gives a
+ *    thread-local message for the last non-OK return.
+ *  - Per-row data errors are not return codes: see row_status.
+ */
+#ifndef RELAY_H_
+#define RELAY_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RELAY_VERSION 1
+#define RELAY_MAX_CUE_LEN 8     /* tokens per pattern; the configs need 1..6 */
+#define RELAY_MAX_PATTERNS 64
+#define RELAY_MAX_CUES 64
+#define RELAY_STAT_FIELDS 8     /* + world_size min slots per stats row */
+
+/* stats row layout: row c < n_cues is cue c, row n_cues is the global row. */
+enum {
+  RELAY_F_N = 0,        /* cue: valid occurrences counted; global: positions counted   */
+  RELAY_F_SUM_MQ = 1,   /* cue: sum of window means in Q20; global: sum of q           */
+  RELAY_F_SUM_MQ2 = 2,  /* cue: sum of squared window means (Q40); global: sum of q^2  */
+  RELAY_F_SUM_WQ = 3,   /* cue: sum of window sums of q; global: sum of q             */
+  RELAY_F_SUM_LEN = 4,  /* cue: sum of window lengths; global: positions counted      */
+  RELAY_F_SUM_LOW = 5,  /* #{m < tau} inside windows (global: over positions)          */
+  RELAY_F_TRIG = 6,     /* cue: occurrences first in their sentence; global: 0         */
+  RELAY_F_INVALID = 7,  /* windows (global: positions) holding a NaN margin, excluded  */
+  RELAY_F_MIN0 = 8      /* + rank: float bits of this rank's minimum margin            */
+};
+/* q = rint(m * 2^20) (Q20 fixed point, round-half-even); a window mean is
+ * floor((2*sum_q + len) / (2*len)).  Integer fields make the table exact and
+ * order-free, so 1 GPU and N GPUs (after the sum all-reduce) agree bit for bit. */
+
+typedef enum {
+  RELAY_OK = 0,
+  RELAY_ERR_INVALID = 1,      /* bad argument (see each call)                      */
+  RELAY_ERR_CUDA = 2,         /* a CUDA launch / runtime call failed               */
+  RELAY_ERR_ALLOC = 4,        /* cue-set device allocation failed                  */
+  RELAY_ERR_UNSUPPORTED = 5,  /* e.g. no sm_100 device                             */
+  RELAY_ERR_WORKSPACE = 7     /* ws NULL or smaller than relay_workspace_bytes()   */
+} relay_status_t;
+
+typedef enum { RELAY_DT_BF16 = 0, RELAY_DT_F16 = 1, RELAY_DT_F32 = 2 } relay_dtype_t;
+
+typedef enum {
+  RELAY_FLAG_NONE = 0,
+  RELAY_FLAG_L2S = 1,         /* a switch cue completed on the large model  */
+  RELAY_FLAG_S2L = 2,         /* sentence end on the small model            */
+  RELAY_FLAG_TO_ANSWER = 3,   /* </think>: the small model owns the answer  */
+  RELAY_FLAG_S2L_BUDGET = 4   /* optional small-segment budget hit (off by default) */
+} relay_flag_t;
+
+typedef struct CUstream_st* relay_stream_t;   /* == cudaStream_t */
+typedef struct relay_cueset_s* relay_cueset_t; /* immutable after create; shareable */
+
+int relay_version(void);
+const char* relay_status_string(relay_status_t s);
+const char* relay_last_error(void);
+
+/* ------------------------------------------------------------------ H1 --
+ * relay_margin_rows — probability margin per logit row.
+ * Defines (§3.2): p_t = softmax(z_t), m_t = p_t,(1) - p_t,(2).
+ * Computed as i1 = argmax z, i2 = argmax over j != i1 (ties: lowest index,
+ * IEEE equality, R3), M = z[i1]*iota, S = sum_j exp(z_j*iota - M),
+ * margin = (1 - exp(z[i2]*iota - M)) / S, lse = M + ln S.  Probabilities are
+ * never materialised.  Indices use the unscaled values.
+ *   logits      [n_rows][row_stride] elements of `dt`, row-major; any alignment
+ *               of the element type; columns [vocab, row_stride) are never read.
+ *   vocab       >= 2 entries per row that participate (R2: all of them).
+ *   inv_temperature  iota > 0; 1.0f is the paper (R1).
+ *   margin      float[n_rows] (required).
+ *   top1, top2  int32[n_rows] (nullable).   lse  float[n_rows] (nullable).
+ *   row_status  uint8[n_rows] (nullable): 0 ok; 1 the row holds NaN or +inf
+ *               (margin/lse NaN, indices -1); 2 no finite entry (same) (R4).
+ * Errors: RELAY_ERR_INVALID if vocab < 2, row_stride < vocab, n_rows < 0,
+ * inv_temperature <= 0 or not finite, logits/margin NULL while n_rows > 0, or
+ * dt unknown.  n_rows == 0 is a no-op. */
+relay_status_t relay_margin_rows(const void* logits, relay_dtype_t dt, int64_t n_rows,
+                                 int64_t vocab, int64_t row_stride, float inv_temperature,
+                                 float* margin, int32_t* top1, int32_t* top2, float* lse,
+                                 uint8_t* row_status, relay_stream_t stream);
+
+/* ------------------------------------------------------------- cue set --
+ * A model pair's switch-cue set (tab:switch_cue_sets) as token-ID
+ * patterns (R5: the caller tokenises every surface variant) plus the sentence
+ * terminator set ("sentence-ending punctuation", R8) and </think>.
+ *   pat_tokens  [host] int32 CSR tokens; pat_offsets [host] int32[n_patterns+1].
+ *   pat_cue     [host] int32[n_patterns] -> cue id in [0, n_cues).
+ *   terminator  [host] uint8[vocab], nonzero = sentence-ending token.
+ *   think_end_token  the </think> id, or -1.
+ *   match_mode  0 LONGEST (one occurrence per start, the longest pattern, R7),
+ *               1 ALL (one occurrence per (start, cue), that cue's longest).
+ * Errors: RELAY_ERR_INVALID for n_patterns outside [1, 64], n_cues outside
+ * [1, 64], an empty or >8-token pattern, a token outside [0, vocab), a cue id
+ * outside [0, n_cues), two identical patterns, vocab < 2, match_mode > 1.
+ * RELAY_ERR_ALLOC / RELAY_ERR_CUDA on device allocation/copy failure.
+ * Ownership: the handle owns its device copies; destroy frees them (call it
+ * after the last stream using the handle has been synchronised). */
+relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat_offsets,
+                                   int32_t n_patterns, const int32_t* pat_cue, int32_t n_cues,
+                                   const uint8_t* terminator, int64_t vocab,
+                                   int32_t think_end_token, uint32_t match_mode,
+                                   relay_cueset_t* out);
+relay_status_t relay_cueset_destroy(relay_cueset_t cs);
+int32_t relay_cueset_n_cues(relay_cueset_t cs);
+
+/* Workspace for cue_scan + segment_reduce (n_tok positions, n_occ occurrence
+ * capacity) and for step_switch (batch rows); one buffer may serve all calls
+ * that run in stream order.  The step_switch part holds arrival counters that
+ * must be zero before first use: call relay_workspace_init once (the kernels
+ * leave them zero again, so graph replays need no reset). */
+size_t relay_workspace_bytes(int64_t n_tok, int64_t occ_capacity, int32_t batch);
+relay_status_t relay_workspace_init(void* ws, size_t ws_bytes, relay_stream_t stream);
+
+/* ------------------------------------------------------------------ H2 --
+ * relay_cue_scan — switch-cue occurrences by "simple token matching"
+ * ("each occurrence of a discourse-level cue").
+ * For each start s of each trajectory [a, b): in LONGEST mode the longest
+ * pattern with s + len <= b and tokens[s..s+len) == pattern; patterns never
+ * cross a trajectory end.  Occurrences are written in ascending s (ALL mode:
+ * then ascending cue id).  term_bits bit t = terminator[tokens[t]] (bit t%32
+ * of word t/32; bits past n_tok are 0).
+ *   tokens       int32[n_tok], ids in [0, vocab) (other ids never match and
+ *                are not terminators).
+ *   traj_offsets int64[n_traj+1] nondecreasing, 0 <= offsets <= n_tok; NULL =>
+ *                one trajectory [0, n_tok).  Positions outside every
+ *                trajectory never start an occurrence.
+ *   term_bits    uint32[ceil(n_tok/32)] out.
+ *   occ_pos, occ_pat  int32[occ_capacity] out: start and pattern index.
+ *   n_occ        int64 device scalar out: the TRUE count even when it
+ *                exceeds occ_capacity (then only the first occ_capacity are
+ *                written; the caller checks after synchronising).
+ * Errors: RELAY_ERR_INVALID (NULL cs/tokens/term_bits/n_occ, n_tok < 0 or
+ * >= 2^31, n_traj < 1 with offsets, occ_capacity < 0, occ_pos/occ_pat NULL
+ * with occ_capacity > 0); RELAY_ERR_WORKSPACE. */
+relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t n_tok,
+                              const int64_t* traj_offsets, int32_t n_traj, uint32_t* term_bits,
+                              int32_t* occ_pos, int32_t* occ_pat, int64_t occ_capacity,
+                              int64_t* n_occ, void* ws, size_t ws_bytes, relay_stream_t stream);
+
+/* ------------------------------------------------------------ H3 - H5 --
+ * relay_segment_reduce — post-sentence windows and the statistics table.
+ * Window ("the remainder of the sentence in which the cue appears",
+ * P:246 "from the cue position to the next sentence boundary", "from
+ * that token until the end of the sentence"): [s, e] inclusive (R9), e = the
+ * first t >= s in s's trajectory with a terminator, else the trajectory's
+ * last token (R10).  Per occurrence: seg_end = e, seg_mean = mean margin,
+ * seg_min, seg_lowfrac = #{m < tau}/len (R11); NaN in the window -> NaN
+ * outputs and the occurrence is counted in RELAY_F_INVALID instead.
+ * ACCUMULATES (+=) into `stats` ((n_cues+1) rows x (8+world_size) uint64):
+ * per cue c: n, sum mean_q, sum mean_q^2, sum window
+ * q, sum len, sum low, n_triggers (first occurrence in its sentence, R13),
+ * invalid, min into slot 8+rank; global row ("all token positions"):
+ * n, sum q, sum q^2, low count, NaN count, min.  With think_end_pos
+ * (int64[n_traj], nullable), occurrences at s >= think_end_pos[k] are left out
+ * of the cue rows and positions t >= think_end_pos[k] out of the global row
+ * (R14); seg_* are still written for them.
+ *   margin      float[n_tok] in [0, 1] (relay_margin_rows output; values
+ *               outside are clamped to [0,1] for the table only).
+ *   term_bits, occ_pos, occ_pat, n_occ: relay_cue_scan outputs (same
+ *               traj_offsets); the first min(*n_occ, occ_capacity) are used.
+ *   seg_end int32, seg_mean/seg_min/seg_lowfrac float [occ_capacity] out.
+ *   stats must have been set by relay_stats_init for (n_cues, rank, world_size).
+ * Errors: RELAY_ERR_INVALID (NULLs, n_tok range, rank outside [0,world_size),
+ * world_size < 1, !(tau finite)); RELAY_ERR_WORKSPACE. */
+relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int64_t n_tok,
+                                    const int64_t* traj_offsets, int32_t n_traj,
+                                    const int64_t* think_end_pos, const uint32_t* term_bits,
+                                    const int32_t* occ_pos, const int32_t* occ_pat,
+                                    const int64_t* n_occ, int64_t occ_capacity, float tau,
+                                    int32_t* seg_end, float* seg_mean, float* seg_min,
+                                    float* seg_lowfrac, uint64_t* stats, int32_t rank,
+                                    int32_t world_size, void* ws, size_t ws_bytes,
+                                    relay_stream_t stream);
+
+/* Zero the table, then set this rank's min slots to +inf bits (0x7f800000)
+ * and every other slot to 0, so that after a SUM all-reduce slot r holds rank
+ * r's minimum (H6: one sum-only collective). */
+relay_status_t relay_stats_init(uint64_t* stats, int32_t n_cues, int32_t rank, int32_t world_size,
+                                relay_stream_t stream);
+size_t relay_stats_words(int32_t n_cues, int32_t world_size);
+
+/* ------------------------------------------------------------------ H7 --
+ * relay_stats_finalize [host] — per-cue and global summaries and the switch-
+ * cue selection (§4.2: "selected as a switch cue if its post-
+ * sentence margin is higher than the global average by at least one standard
+ * error").  host_stats is the (all-reduced) table copied to the host.
+ *   mean  = sum_mq / (n 2^20); std = population std from exact 128-bit
+ *   integer moments; se = std / sqrt(n); token_mean = sum_wq/(sum_len 2^20);
+ *   min = min over the world_size slots; low_frac = sum_low / sum_len.
+ *   rule 0: mean_c >= mu + SE_global (R15, default); 1: mean_c >= mu + se_c;
+ *   2: mean_c > mu (App. B).  Always also n_c >= min_count.  With
+ *   fewer than 2 global positions std/se are NaN and nothing is selected.
+ *   out [host] relay_cue_summary_t[n_cues+1]; out[n_cues] is the global row.
+ * Errors: RELAY_ERR_INVALID for NULLs, n_cues/world_size out of range, rule>2. */
+typedef struct {
+  int64_t n;
+  double mean, std, se, token_mean, min, low_frac;
+  int64_t n_triggers;
+  int64_t n_invalid;
+  int32_t selected;
+} relay_cue_summary_t;
+relay_status_t relay_stats_finalize(const uint64_t* host_stats, int32_t n_cues, int32_t world_size,
+                                    int64_t min_count, int32_t rule, relay_cue_summary_t* out);
+
+/* ------------------------------------------------------------------ H8 --
+ * relay_step_switch — one decode step for `batch` live sequences: the H1
+ * margin of each row, then RelayGen's runtime switch (§4.3,
+ * fig:mechanism P:209-216) as an on-device flag, priority </think> > cue >
+ * terminator > budget (R16):
+ *   answer stage -> NONE;  tok == think_end -> TO_ANSWER, state = answer|small;
+ *   large: the longest pattern that is a suffix of hist ++ tok -> L2S + cue id
+ *          (suppressed when margin_gate >= 0 and the row margin < margin_gate;
+ *          the paper has no gate: pass -1);
+ *   small: terminator[tok] -> S2L; else max_small_segment > 0 and
+ *          small_run + 1 >= max_small_segment -> S2L_BUDGET (paper: 0 = off);
+ *   otherwise NONE, large appends tok to hist, small increments small_run.
+ *   Every switch clears hist and small_run.  Cues on the small model are
+ *   ignored.  tok = sampled[b], or top1 when sampled == NULL; an
+ *   invalid tok (row status != 0 and no sample) gives NONE with no update.
+ *   logits [batch][row_stride] of dt; state uint8[batch] in/out (bit0 active
+ *   model 0 large / 1 small, bit1 answer stage); hist int32[batch][7] in/out,
+ *   oldest first, right-aligned, -1 padded; small_run int32[batch] in/out
+ *   (nullable when max_small_segment == 0); outputs margin float, top1/top2
+ *   int32 (nullable), flag uint8, cue_id int16 (-1 unless L2S) [batch].
+ *   ws: relay_workspace_bytes(0, 0, batch) bytes, zeroed once by
+ *   relay_workspace_init.
+ * Errors: as relay_margin_rows, plus batch < 0, NULL state/hist/flag/cue_id,
+ * RELAY_ERR_WORKSPACE. */
+relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dtype_t dt,
+                                 int32_t batch, int64_t vocab, int64_t row_stride,
+                                 float inv_temperature, const int32_t* sampled, uint8_t* state,
+                                 int32_t* hist, int32_t* small_run, float margin_gate,
+                                 int32_t max_small_segment, float* margin, int32_t* top1,
+                                 int32_t* top2, uint8_t* flag, int16_t* cue_id, void* ws,
+                                 size_t ws_bytes, relay_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RELAY_H_ */

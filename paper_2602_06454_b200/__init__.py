@@ -1,0 +1,379 @@
+"""RelayGen (arXiv 2602.06454) hot path on B200 — thin Python binding of librelay.so.
+
+Argument marshalling only: every step of the path (margins, cue scan, segment
+statistics, decode-step switch) runs in the sm_100a kernels of ``librelay.so``
+behind the C ABI declared in ``include/relay.h``.  PyTorch supplies device
+memory, streams and process groups.  There is NO CPU fallback: importing this
+package without a built ``librelay.so`` raises, and every call raises
+``RelayError`` on a non-OK status.
+
+Names follow the C ABI (``relay_margin_rows`` -> ``margin_rows`` ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_REPO = os.path.dirname(_HERE)
+LIB_PATH = os.path.join(_HERE, "librelay.so")
+_SOURCES = [os.path.join(_HERE, "csrc", f) for f in
+            ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu")]
+_HEADERS = [os.path.join(_HERE, "csrc", f) for f in ("relay_device.cuh", "relay_internal.h")] + \
+           [os.path.join(_REPO, "include", "relay.h")]
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+DT = {"bf16": 0, "f16": 1, "f32": 2}
+FLAG_NONE, FLAG_L2S, FLAG_S2L, FLAG_TO_ANSWER, FLAG_S2L_BUDGET = 0, 1, 2, 3, 4
+STAT_FIELDS = 8
+F_N, F_SUM_MQ, F_SUM_MQ2, F_SUM_WQ, F_SUM_LEN, F_SUM_LOW, F_TRIG, F_INVALID, F_MIN0 = range(9)
+HIST = 7
+
+
+class RelayError(RuntimeError):
+    pass
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile librelay.so for sm_100a with nvcc (works without a GPU)."""
+    newest = max(os.path.getmtime(p) for p in _SOURCES + _HEADERS)
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+        if not os.path.exists(nvcc):
+            nvcc = "nvcc"
+        tmp = LIB_PATH + ".tmp"
+        cmd = [nvcc] + NVCC_FLAGS + ["-o", tmp] + _SOURCES
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+        os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, i32, i64, f32, u32, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint32, C.c_size_t
+    sig = {
+        "relay_version": (C.c_int, []),
+        "relay_status_string": (C.c_char_p, [C.c_int]),
+        "relay_last_error": (C.c_char_p, []),
+        "relay_margin_rows": (C.c_int, [P, C.c_int, i64, i64, i64, f32, P, P, P, P, P, P]),
+        "relay_cueset_create": (C.c_int, [P, P, i32, P, i32, P, i64, i32, u32, P]),
+        "relay_cueset_destroy": (C.c_int, [P]),
+        "relay_cueset_n_cues": (i32, [P]),
+        "relay_workspace_bytes": (sz, [i64, i64, i32]),
+        "relay_workspace_init": (C.c_int, [P, sz, P]),
+        "relay_cue_scan": (C.c_int, [P, P, i64, P, i32, P, P, P, i64, P, P, sz, P]),
+        "relay_segment_reduce": (C.c_int, [P, P, i64, P, i32, P, P, P, P, P, i64, f32, P, P, P, P,
+                                           P, i32, i32, P, sz, P]),
+        "relay_stats_init": (C.c_int, [P, i32, i32, i32, P]),
+        "relay_stats_words": (sz, [i32, i32]),
+        "relay_stats_finalize": (C.c_int, [P, i32, i32, i64, i32, P]),
+        "relay_step_switch": (C.c_int, [P, P, C.c_int, i32, i64, i64, f32, P, P, P, P, f32, i32,
+                                        P, P, P, P, P, P, sz, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_margin_rows",
+           "relay_cueset_create", "relay_cueset_destroy", "relay_cueset_n_cues",
+           "relay_workspace_bytes", "relay_workspace_init", "relay_cue_scan",
+           "relay_segment_reduce", "relay_stats_init", "relay_stats_words",
+           "relay_stats_finalize", "relay_step_switch")
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = _lib.relay_last_error().decode()
+        raise RelayError(f"{what}: {_lib.relay_status_string(rc).decode()} ({msg})")
+
+
+def version() -> int:
+    return _lib.relay_version()
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dtype_of(t) -> int:
+    import torch
+    m = {torch.bfloat16: 0, torch.float16: 1, torch.float32: 2}
+    if t.dtype not in m:
+        raise RelayError(f"unsupported logits dtype {t.dtype}")
+    return m[t.dtype]
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise RelayError("all tensors must be CUDA tensors (there is no CPU path)")
+
+
+# ------------------------------------------------------------------- H1
+def margin_rows(logits, vocab: int | None = None, inv_temperature: float = 1.0, out=None,
+                want_lse: bool = True, stream=None):
+    """relay_margin_rows on a [n_rows, row_stride] CUDA tensor (rows contiguous
+    in their last dim).  Returns dict(margin, top1, top2, lse, status)."""
+    import torch
+    _need_cuda(logits)
+    if logits.dim() != 2 or logits.stride(1) != 1:
+        raise RelayError("logits must be 2-D with unit stride in the vocabulary dim")
+    n = logits.shape[0]
+    stride = logits.stride(0) if n > 1 else logits.shape[1]
+    vocab = logits.shape[1] if vocab is None else vocab
+    dev = logits.device
+    if out is None:
+        out = dict(margin=torch.empty(n, dtype=torch.float32, device=dev),
+                   top1=torch.empty(n, dtype=torch.int32, device=dev),
+                   top2=torch.empty(n, dtype=torch.int32, device=dev),
+                   lse=torch.empty(n, dtype=torch.float32, device=dev) if want_lse else None,
+                   status=torch.empty(n, dtype=torch.uint8, device=dev))
+    rc = _lib.relay_margin_rows(_ptr(logits), _dtype_of(logits), n, vocab, stride,
+                                float(inv_temperature), _ptr(out["margin"]), _ptr(out.get("top1")),
+                                _ptr(out.get("top2")), _ptr(out.get("lse")),
+                                _ptr(out.get("status")), _stream(stream))
+    _check(rc, "relay_margin_rows")
+    return out
+
+
+# --------------------------------------------------------------- cue set
+class CueSet:
+    """relay_cueset_create / destroy.  Host arrays (numpy) in, device copy owned."""
+
+    def __init__(self, pat_tokens, pat_offsets, pat_cue, n_cues: int, terminator, vocab: int,
+                 think_end: int = -1, mode: int = 0):
+        self.pat_tokens = np.ascontiguousarray(pat_tokens, np.int32)
+        self.pat_offsets = np.ascontiguousarray(pat_offsets, np.int32)
+        self.pat_cue = np.ascontiguousarray(pat_cue, np.int32)
+        self.terminator = np.ascontiguousarray(terminator, np.uint8)
+        self.n_cues, self.vocab, self.think_end, self.mode = int(n_cues), int(vocab), int(think_end), int(mode)
+        if self.terminator.shape[0] < vocab:
+            raise RelayError("terminator table shorter than vocab")
+        h = C.c_void_p()
+        rc = _lib.relay_cueset_create(self.pat_tokens.ctypes.data_as(C.c_void_p),
+                                      self.pat_offsets.ctypes.data_as(C.c_void_p),
+                                      self.pat_offsets.shape[0] - 1,
+                                      self.pat_cue.ctypes.data_as(C.c_void_p), self.n_cues,
+                                      self.terminator.ctypes.data_as(C.c_void_p), self.vocab,
+                                      self.think_end, self.mode, C.byref(h))
+        _check(rc, "relay_cueset_create")
+        self._h = h
+
+    @classmethod
+    def from_synth(cls, cs, mode: int = 0):
+        return cls(cs.pat_tokens, cs.pat_offsets, cs.pat_cue, cs.n_cues, cs.terminator, cs.vocab,
+                   cs.think_end, mode)
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RelayError("cue set destroyed")
+        return self._h
+
+    def destroy(self):
+        if getattr(self, "_h", None) is not None:
+            _lib.relay_cueset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def workspace_bytes(n_tok: int = 0, occ_capacity: int = 0, batch: int = 0) -> int:
+    return int(_lib.relay_workspace_bytes(n_tok, occ_capacity, batch))
+
+
+def workspace(n_tok: int = 0, occ_capacity: int = 0, batch: int = 0, device="cuda", stream=None):
+    import torch
+    nb = workspace_bytes(n_tok, occ_capacity, batch)
+    ws = torch.empty(nb, dtype=torch.uint8, device=device)
+    _check(_lib.relay_workspace_init(_ptr(ws), nb, _stream(stream)), "relay_workspace_init")
+    return ws
+
+
+# ------------------------------------------------------------------- H2
+def cue_scan(cs: CueSet, tokens, traj_offsets=None, occ_capacity: int | None = None, ws=None,
+             out=None, stream=None):
+    import torch
+    _need_cuda(tokens, traj_offsets)
+    n_tok = tokens.shape[0]
+    dev = tokens.device
+    cap = n_tok * (cs.n_cues if cs.mode else 1) if occ_capacity is None else occ_capacity
+    if ws is None:
+        ws = workspace(n_tok, cap, 0, dev, stream)
+    if out is None:
+        out = dict(term_bits=torch.zeros((n_tok + 31) // 32 + 1, dtype=torch.int32, device=dev),
+                   occ_pos=torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+                   occ_pat=torch.empty(max(cap, 1), dtype=torch.int32, device=dev),
+                   n_occ=torch.zeros(1, dtype=torch.int64, device=dev))
+    n_traj = 1 if traj_offsets is None else traj_offsets.shape[0] - 1
+    rc = _lib.relay_cue_scan(cs.handle, _ptr(tokens), n_tok, _ptr(traj_offsets), n_traj,
+                             _ptr(out["term_bits"]), _ptr(out["occ_pos"]), _ptr(out["occ_pat"]),
+                             cap, _ptr(out["n_occ"]), _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "relay_cue_scan")
+    out["capacity"] = cap
+    return out
+
+
+def stats_words(n_cues: int, world_size: int = 1) -> int:
+    return int(_lib.relay_stats_words(n_cues, world_size))
+
+
+def stats_init(stats, n_cues: int, rank: int = 0, world_size: int = 1, stream=None):
+    _check(_lib.relay_stats_init(_ptr(stats), n_cues, rank, world_size, _stream(stream)),
+           "relay_stats_init")
+    return stats
+
+
+def new_stats(n_cues: int, rank: int = 0, world_size: int = 1, device="cuda", stream=None):
+    import torch
+    st = torch.empty(stats_words(n_cues, world_size), dtype=torch.int64, device=device)
+    return stats_init(st, n_cues, rank, world_size, stream)
+
+
+# ---------------------------------------------------------------- H3-H5
+def segment_reduce(cs: CueSet, margin, scan: dict, traj_offsets=None, think_end_pos=None,
+                   tau: float = 0.5, stats=None, rank: int = 0, world_size: int = 1, ws=None,
+                   out=None, stream=None):
+    import torch
+    _need_cuda(margin, traj_offsets, think_end_pos)
+    n_tok = margin.shape[0]
+    cap = scan["capacity"]
+    dev = margin.device
+    if ws is None:
+        ws = workspace(n_tok, cap, 0, dev, stream)
+    if stats is None:
+        stats = new_stats(cs.n_cues, rank, world_size, dev, stream)
+    c1 = max(cap, 1)
+    if out is None:
+        out = dict(seg_end=torch.empty(c1, dtype=torch.int32, device=dev),
+                   seg_mean=torch.empty(c1, dtype=torch.float32, device=dev),
+                   seg_min=torch.empty(c1, dtype=torch.float32, device=dev),
+                   seg_lowfrac=torch.empty(c1, dtype=torch.float32, device=dev))
+    n_traj = 1 if traj_offsets is None else traj_offsets.shape[0] - 1
+    rc = _lib.relay_segment_reduce(cs.handle, _ptr(margin), n_tok, _ptr(traj_offsets), n_traj,
+                                   _ptr(think_end_pos), _ptr(scan["term_bits"]),
+                                   _ptr(scan["occ_pos"]), _ptr(scan["occ_pat"]),
+                                   _ptr(scan["n_occ"]), cap, float(tau), _ptr(out["seg_end"]),
+                                   _ptr(out["seg_mean"]), _ptr(out["seg_min"]),
+                                   _ptr(out["seg_lowfrac"]), _ptr(stats), rank, world_size,
+                                   _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "relay_segment_reduce")
+    out["stats"] = stats
+    return out
+
+
+class Summary(C.Structure):
+    _fields_ = [("n", C.c_int64), ("mean", C.c_double), ("std", C.c_double), ("se", C.c_double),
+                ("token_mean", C.c_double), ("min", C.c_double), ("low_frac", C.c_double),
+                ("n_triggers", C.c_int64), ("n_invalid", C.c_int64), ("selected", C.c_int32)]
+
+
+def stats_finalize(host_stats: np.ndarray, n_cues: int, world_size: int = 1, min_count: int = 3,
+                   rule: int = 0):
+    """H7 on the host: list of per-cue dicts, global row last."""
+    hs = np.ascontiguousarray(host_stats).view(np.uint64)
+    if hs.shape[0] < stats_words(n_cues, world_size):
+        raise RelayError("stats table too short")
+    out = (Summary * (n_cues + 1))()
+    rc = _lib.relay_stats_finalize(hs.ctypes.data_as(C.c_void_p), n_cues, world_size, min_count,
+                                   rule, C.cast(out, C.c_void_p))
+    _check(rc, "relay_stats_finalize")
+    return [{f: getattr(s, f) for f, _ in Summary._fields_} for s in out]
+
+
+# ------------------------------------------------------------------- H8
+def step_switch(cs: CueSet, logits, state, hist, small_run=None, sampled=None, vocab=None,
+                inv_temperature: float = 1.0, margin_gate: float = -1.0,
+                max_small_segment: int = 0, ws=None, out=None, stream=None):
+    import torch
+    _need_cuda(logits, state, hist, small_run, sampled)
+    B = logits.shape[0]
+    stride = logits.stride(0) if B > 1 else logits.shape[1]
+    vocab = logits.shape[1] if vocab is None else vocab
+    dev = logits.device
+    if ws is None:
+        ws = workspace(0, 0, B, dev, stream)
+    if out is None:
+        out = dict(margin=torch.empty(B, dtype=torch.float32, device=dev),
+                   top1=torch.empty(B, dtype=torch.int32, device=dev),
+                   top2=torch.empty(B, dtype=torch.int32, device=dev),
+                   flag=torch.empty(B, dtype=torch.uint8, device=dev),
+                   cue_id=torch.empty(B, dtype=torch.int16, device=dev))
+    rc = _lib.relay_step_switch(cs.handle, _ptr(logits), _dtype_of(logits), B, vocab, stride,
+                                float(inv_temperature), _ptr(sampled), _ptr(state), _ptr(hist),
+                                _ptr(small_run), float(margin_gate), int(max_small_segment),
+                                _ptr(out["margin"]), _ptr(out.get("top1")), _ptr(out.get("top2")),
+                                _ptr(out["flag"]), _ptr(out["cue_id"]), _ptr(ws), ws.numel(),
+                                _stream(stream))
+    _check(rc, "relay_step_switch")
+    return out
+
+
+# ------------------------------------------------------- whole offline pass
+class Analyzer:
+    """The full offline hot path for one shard: H1 margins -> H2 cue scan ->
+    H3-H5 segment statistics into a uint64 table (-> H6 all-reduce -> H7 on
+    the host).  Buffers are allocated once; ``run`` only launches kernels."""
+
+    def __init__(self, cs: CueSet, n_tok: int, vocab: int, device="cuda", occ_capacity=None,
+                 tau: float = 0.5, rank: int = 0, world_size: int = 1, inv_temperature=1.0):
+        import torch
+        self.cs, self.n_tok, self.vocab, self.tau = cs, n_tok, vocab, tau
+        self.rank, self.world_size, self.iota = rank, world_size, inv_temperature
+        self.device = torch.device(device)
+        self.cap = (n_tok * (cs.n_cues if cs.mode else 1)) if occ_capacity is None else occ_capacity
+        d = self.device
+        self.ws = workspace(n_tok, self.cap, 0, d)
+        self.rows = dict(margin=torch.empty(n_tok, dtype=torch.float32, device=d),
+                         top1=torch.empty(n_tok, dtype=torch.int32, device=d),
+                         top2=torch.empty(n_tok, dtype=torch.int32, device=d),
+                         lse=torch.empty(n_tok, dtype=torch.float32, device=d),
+                         status=torch.empty(n_tok, dtype=torch.uint8, device=d))
+        c1 = max(self.cap, 1)
+        self.scan = dict(term_bits=torch.zeros((n_tok + 31) // 32 + 1, dtype=torch.int32, device=d),
+                         occ_pos=torch.empty(c1, dtype=torch.int32, device=d),
+                         occ_pat=torch.empty(c1, dtype=torch.int32, device=d),
+                         n_occ=torch.zeros(1, dtype=torch.int64, device=d), capacity=self.cap)
+        self.seg = dict(seg_end=torch.empty(c1, dtype=torch.int32, device=d),
+                        seg_mean=torch.empty(c1, dtype=torch.float32, device=d),
+                        seg_min=torch.empty(c1, dtype=torch.float32, device=d),
+                        seg_lowfrac=torch.empty(c1, dtype=torch.float32, device=d))
+        self.stats = torch.empty(stats_words(cs.n_cues, world_size), dtype=torch.int64, device=d)
+
+    def run(self, logits, tokens, traj_offsets=None, think_end_pos=None, stream=None,
+            vocab=None):
+        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, stream)
+        margin_rows(logits, vocab=vocab or self.vocab, inv_temperature=self.iota, out=self.rows,
+                    stream=stream)
+        cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, stream)
+        segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
+                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, stream)
+        return self.stats
+
+    def n_launches(self) -> int:
+        """Kernels launched by one run(): stats_init 1 + K1 1 + K2 2 + K3 4."""
+        return 8 if self.cap > 0 else 6

@@ -1,0 +1,390 @@
+// relay_api.cu — the C ABI of librelay.so (include/relay.h): argument
+// validation, the cue-set handle, workspace layout, launches and the host-side
+// finalize (H7).  Every hot call is stream-ordered and allocation-free.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/relay.h"
+#include "relay_internal.h"
+
+using namespace relay;
+
+struct relay_cueset_s {
+  CueDev dev;
+  void* block;  // one device allocation holding every array
+};
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+relay_status_t fail(relay_status_t s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+relay_status_t cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RELAY_OK;
+  return fail(RELAY_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+long long tiles_of(long long n_tok) {
+  long long t = (n_tok + kTile - 1) / kTile;
+  return t < 1 ? 1 : t;
+}
+
+bool valid_dtype(relay_dtype_t dt) { return dt == RELAY_DT_BF16 || dt == RELAY_DT_F16 || dt == RELAY_DT_F32; }
+
+relay_status_t check_offsets_args(const int64_t* offs, int32_t n_traj) {
+  if (offs && n_traj < 1) return fail(RELAY_ERR_INVALID, "n_traj must be >= 1 with traj_offsets");
+  return RELAY_OK;
+}
+
+}  // namespace
+
+namespace relay {
+
+ScanWs scan_ws_layout(void* base, long long n_tok, long long cap) {
+  ScanWs w{};
+  const long long nt = tiles_of(n_tok);
+  if (cap < 0) cap = 0;
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* q = p ? p + off : nullptr;
+    off += align256(bytes);
+    return q;
+  };
+  w.tile_count = reinterpret_cast<int*>(take(sizeof(int) * nt));
+  w.tile_head = reinterpret_cast<Agg*>(take(sizeof(Agg) * nt));
+  w.tile_carry = reinterpret_cast<Agg*>(take(sizeof(Agg) * nt));
+  w.occ_sumq = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (cap + 1)));
+  w.occ_low = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (cap + 1)));
+  w.occ_nan = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (cap + 1)));
+  w.bytes = off;
+  return w;
+}
+
+StepWs step_ws_layout(void* base, int batch) {
+  StepWs w{};
+  char* p = static_cast<char*>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* q = p ? p + off : nullptr;
+    off += align256(bytes);
+    return q;
+  };
+  if (batch < 0) batch = 0;
+  w.counter = reinterpret_cast<int*>(take(sizeof(int) * (batch + 1)));
+  w.part = reinterpret_cast<float*>(take(sizeof(float) * 6 * kMaxSplit * (static_cast<size_t>(batch) + 1)));
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace relay
+
+extern "C" {
+
+int relay_version(void) { return RELAY_VERSION; }
+
+const char* relay_status_string(relay_status_t s) {
+  switch (s) {
+    case RELAY_OK: return "ok";
+    case RELAY_ERR_INVALID: return "invalid argument";
+    case RELAY_ERR_CUDA: return "CUDA error";
+    case RELAY_ERR_ALLOC: return "allocation failed";
+    case RELAY_ERR_UNSUPPORTED: return "unsupported";
+    case RELAY_ERR_WORKSPACE: return "workspace missing or too small";
+  }
+  return "unknown status";
+}
+
+const char* relay_last_error(void) { return g_err; }
+
+relay_status_t relay_margin_rows(const void* logits, relay_dtype_t dt, int64_t n_rows, int64_t vocab,
+                                 int64_t row_stride, float inv_temperature, float* margin,
+                                 int32_t* top1, int32_t* top2, float* lse, uint8_t* row_status,
+                                 relay_stream_t stream) {
+  if (!valid_dtype(dt)) return fail(RELAY_ERR_INVALID, "unknown dtype %d", static_cast<int>(dt));
+  if (vocab < 2) return fail(RELAY_ERR_INVALID, "vocab must be >= 2 (got %lld)", static_cast<long long>(vocab));
+  if (vocab > 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "vocab must be < 2^31");
+  if (row_stride < vocab) return fail(RELAY_ERR_INVALID, "row_stride < vocab");
+  if (n_rows < 0) return fail(RELAY_ERR_INVALID, "n_rows < 0");
+  if (!(inv_temperature > 0.0f) || !std::isfinite(inv_temperature))
+    return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
+  if (n_rows == 0) return RELAY_OK;
+  if (!logits || !margin) return fail(RELAY_ERR_INVALID, "logits and margin are required");
+  return cuda_status(launch_margin_rows(logits, static_cast<int>(dt), n_rows, static_cast<int>(vocab),
+                                        row_stride, inv_temperature, margin, top1, top2, lse,
+                                        row_status, reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_margin_rows launch");
+}
+
+relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat_offsets,
+                                   int32_t n_patterns, const int32_t* pat_cue, int32_t n_cues,
+                                   const uint8_t* terminator, int64_t vocab, int32_t think_end_token,
+                                   uint32_t match_mode, relay_cueset_t* out) {
+  if (!out) return fail(RELAY_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!pat_tokens || !pat_offsets || !pat_cue || !terminator)
+    return fail(RELAY_ERR_INVALID, "pattern arrays and terminator are required");
+  if (n_patterns < 1 || n_patterns > kMaxPat) return fail(RELAY_ERR_INVALID, "n_patterns must be in [1, %d]", kMaxPat);
+  if (n_cues < 1 || n_cues > kMaxCues) return fail(RELAY_ERR_INVALID, "n_cues must be in [1, %d]", kMaxCues);
+  if (vocab < 2 || vocab > 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "vocab out of range");
+  if (match_mode > 1) return fail(RELAY_ERR_INVALID, "match_mode must be 0 or 1");
+  if (pat_offsets[0] != 0) return fail(RELAY_ERR_INVALID, "pat_offsets[0] must be 0");
+  std::vector<int> len(n_patterns);
+  for (int p = 0; p < n_patterns; p++) {
+    len[p] = pat_offsets[p + 1] - pat_offsets[p];
+    if (len[p] < 1 || len[p] > kMaxLen) return fail(RELAY_ERR_INVALID, "pattern %d has length %d (1..%d)", p, len[p], kMaxLen);
+    if (pat_cue[p] < 0 || pat_cue[p] >= n_cues) return fail(RELAY_ERR_INVALID, "pattern %d cue id out of range", p);
+    for (int k = 0; k < len[p]; k++) {
+      int t = pat_tokens[pat_offsets[p] + k];
+      if (t < 0 || t >= vocab) return fail(RELAY_ERR_INVALID, "pattern %d token %d outside [0, vocab)", p, t);
+    }
+  }
+  for (int p = 0; p < n_patterns; p++)
+    for (int q = p + 1; q < n_patterns; q++)
+      if (len[p] == len[q] &&
+          std::memcmp(pat_tokens + pat_offsets[p], pat_tokens + pat_offsets[q], sizeof(int32_t) * len[p]) == 0)
+        return fail(RELAY_ERR_INVALID, "patterns %d and %d are identical", p, q);
+  // sort by length descending, stable in the caller's order
+  std::vector<int> order(n_patterns);
+  for (int p = 0; p < n_patterns; p++) order[p] = p;
+  for (int a = 1; a < n_patterns; a++)
+    for (int b = a; b > 0 && len[order[b]] > len[order[b - 1]]; b--) std::swap(order[b], order[b - 1]);
+  std::vector<int> h_tok(static_cast<size_t>(n_patterns) * kMaxLen, -1), h_len(n_patterns), h_cue(n_patterns),
+      h_orig(n_patterns), h_cue_orig(n_patterns);
+  for (int i = 0; i < n_patterns; i++) {
+    const int p = order[i];
+    h_len[i] = len[p];
+    h_cue[i] = pat_cue[p];
+    h_orig[i] = p;
+    for (int k = 0; k < len[p]; k++) h_tok[static_cast<size_t>(i) * kMaxLen + k] = pat_tokens[pat_offsets[p] + k];
+  }
+  for (int p = 0; p < n_patterns; p++) h_cue_orig[p] = pat_cue[p];
+  const size_t words = static_cast<size_t>((vocab + 31) / 32);
+  std::vector<uint32_t> h_term(words, 0u);
+  for (int64_t v = 0; v < vocab; v++)
+    if (terminator[v]) h_term[v >> 5] |= 1u << (v & 31);
+  size_t off_tok = 0, off_len = align256(h_tok.size() * 4), off_cue = off_len + align256(n_patterns * 4),
+         off_orig = off_cue + align256(n_patterns * 4), off_co = off_orig + align256(n_patterns * 4),
+         off_term = off_co + align256(n_patterns * 4), total = off_term + align256(words * 4);
+  std::vector<char> host(total, 0);
+  std::memcpy(host.data() + off_tok, h_tok.data(), h_tok.size() * 4);
+  std::memcpy(host.data() + off_len, h_len.data(), n_patterns * 4);
+  std::memcpy(host.data() + off_cue, h_cue.data(), n_patterns * 4);
+  std::memcpy(host.data() + off_orig, h_orig.data(), n_patterns * 4);
+  std::memcpy(host.data() + off_co, h_cue_orig.data(), n_patterns * 4);
+  std::memcpy(host.data() + off_term, h_term.data(), words * 4);
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, total);
+  if (e != cudaSuccess) return fail(RELAY_ERR_ALLOC, "cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
+  e = cudaMemcpy(d, host.data(), total, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return cuda_status(e, "cue set upload");
+  }
+  relay_cueset_s* cs = new (std::nothrow) relay_cueset_s;
+  if (!cs) {
+    cudaFree(d);
+    return fail(RELAY_ERR_ALLOC, "host allocation failed");
+  }
+  char* b = static_cast<char*>(d);
+  cs->block = d;
+  cs->dev.n_pat = n_patterns;
+  cs->dev.n_cues = n_cues;
+  cs->dev.mode = static_cast<int>(match_mode);
+  cs->dev.think_end = think_end_token;
+  cs->dev.vocab = vocab;
+  cs->dev.pat_tok = reinterpret_cast<const int*>(b + off_tok);
+  cs->dev.pat_len = reinterpret_cast<const int*>(b + off_len);
+  cs->dev.pat_cue = reinterpret_cast<const int*>(b + off_cue);
+  cs->dev.pat_orig = reinterpret_cast<const int*>(b + off_orig);
+  cs->dev.cue_of_orig = reinterpret_cast<const int*>(b + off_co);
+  cs->dev.term_tab = reinterpret_cast<const uint32_t*>(b + off_term);
+  *out = cs;
+  return RELAY_OK;
+}
+
+relay_status_t relay_cueset_destroy(relay_cueset_t cs) {
+  if (!cs) return RELAY_OK;
+  cudaError_t e = cudaFree(cs->block);
+  delete cs;
+  return cuda_status(e, "cue set free");
+}
+
+int32_t relay_cueset_n_cues(relay_cueset_t cs) { return cs ? cs->dev.n_cues : -1; }
+
+size_t relay_workspace_bytes(int64_t n_tok, int64_t occ_capacity, int32_t batch) {
+  size_t a = scan_ws_layout(nullptr, n_tok < 0 ? 0 : n_tok, occ_capacity).bytes;
+  size_t b = step_ws_layout(nullptr, batch).bytes;
+  return a > b ? a : b;
+}
+
+relay_status_t relay_workspace_init(void* ws, size_t ws_bytes, relay_stream_t stream) {
+  if (!ws && ws_bytes) return fail(RELAY_ERR_INVALID, "ws is NULL");
+  if (!ws_bytes) return RELAY_OK;
+  return cuda_status(cudaMemsetAsync(ws, 0, ws_bytes, reinterpret_cast<cudaStream_t>(stream)),
+                     "workspace init");
+}
+
+relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t n_tok,
+                              const int64_t* traj_offsets, int32_t n_traj, uint32_t* term_bits,
+                              int32_t* occ_pos, int32_t* occ_pat, int64_t occ_capacity, int64_t* n_occ,
+                              void* ws, size_t ws_bytes, relay_stream_t stream) {
+  if (!cs || !n_occ) return fail(RELAY_ERR_INVALID, "cs and n_occ are required");
+  if (n_tok < 0 || n_tok >= 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "n_tok must be in [0, 2^31)");
+  if (n_tok > 0 && (!tokens || !term_bits)) return fail(RELAY_ERR_INVALID, "tokens and term_bits are required");
+  if (occ_capacity < 0) return fail(RELAY_ERR_INVALID, "occ_capacity < 0");
+  if (occ_capacity > 0 && (!occ_pos || !occ_pat)) return fail(RELAY_ERR_INVALID, "occ_pos/occ_pat are required");
+  relay_status_t s = check_offsets_args(traj_offsets, n_traj);
+  if (s != RELAY_OK) return s;
+  ScanWs w = scan_ws_layout(ws, n_tok, occ_capacity);
+  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  return cuda_status(launch_cue_scan(cs->dev, tokens, n_tok, reinterpret_cast<const long long*>(traj_offsets),
+                                     traj_offsets ? n_traj : 1, term_bits, occ_pos, occ_pat, occ_capacity,
+                                     reinterpret_cast<long long*>(n_occ), w,
+                                     reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_cue_scan launch");
+}
+
+size_t relay_stats_words(int32_t n_cues, int32_t world_size) {
+  if (n_cues < 0 || world_size < 1) return 0;
+  return static_cast<size_t>(n_cues + 1) * (kStatFields + world_size);
+}
+
+relay_status_t relay_stats_init(uint64_t* stats, int32_t n_cues, int32_t rank, int32_t world_size,
+                                relay_stream_t stream) {
+  if (!stats) return fail(RELAY_ERR_INVALID, "stats is NULL");
+  if (n_cues < 1 || n_cues > kMaxCues) return fail(RELAY_ERR_INVALID, "n_cues out of range");
+  if (world_size < 1 || rank < 0 || rank >= world_size) return fail(RELAY_ERR_INVALID, "bad rank/world_size");
+  return cuda_status(launch_stats_init(reinterpret_cast<unsigned long long*>(stats), n_cues, rank, world_size,
+                                       reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_stats_init launch");
+}
+
+relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int64_t n_tok,
+                                    const int64_t* traj_offsets, int32_t n_traj, const int64_t* think_end_pos,
+                                    const uint32_t* term_bits, const int32_t* occ_pos, const int32_t* occ_pat,
+                                    const int64_t* n_occ, int64_t occ_capacity, float tau, int32_t* seg_end,
+                                    float* seg_mean, float* seg_min, float* seg_lowfrac, uint64_t* stats,
+                                    int32_t rank, int32_t world_size, void* ws, size_t ws_bytes,
+                                    relay_stream_t stream) {
+  if (!cs || !stats || !n_occ) return fail(RELAY_ERR_INVALID, "cs, stats and n_occ are required");
+  if (n_tok < 0 || n_tok >= 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "n_tok must be in [0, 2^31)");
+  if (n_tok > 0 && (!margin || !term_bits)) return fail(RELAY_ERR_INVALID, "margin and term_bits are required");
+  if (occ_capacity < 0) return fail(RELAY_ERR_INVALID, "occ_capacity < 0");
+  if (occ_capacity > 0 && (!occ_pos || !occ_pat || !seg_end || !seg_mean || !seg_min || !seg_lowfrac))
+    return fail(RELAY_ERR_INVALID, "occurrence and seg_* arrays are required");
+  if (world_size < 1 || rank < 0 || rank >= world_size) return fail(RELAY_ERR_INVALID, "bad rank/world_size");
+  if (!std::isfinite(tau)) return fail(RELAY_ERR_INVALID, "tau must be finite");
+  if (think_end_pos && !traj_offsets) return fail(RELAY_ERR_INVALID, "think_end_pos needs traj_offsets");
+  relay_status_t s = check_offsets_args(traj_offsets, n_traj);
+  if (s != RELAY_OK) return s;
+  ScanWs w = scan_ws_layout(ws, n_tok, occ_capacity);
+  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  return cuda_status(
+      launch_segment_reduce(cs->dev, margin, n_tok, reinterpret_cast<const long long*>(traj_offsets),
+                            traj_offsets ? n_traj : 1, reinterpret_cast<const long long*>(think_end_pos),
+                            term_bits, occ_pos, occ_pat, reinterpret_cast<const long long*>(n_occ),
+                            occ_capacity, tau, seg_end, seg_mean, seg_min, seg_lowfrac,
+                            reinterpret_cast<unsigned long long*>(stats), rank, world_size, w,
+                            reinterpret_cast<cudaStream_t>(stream)),
+      "relay_segment_reduce launch");
+}
+
+relay_status_t relay_stats_finalize(const uint64_t* host_stats, int32_t n_cues, int32_t world_size,
+                                    int64_t min_count, int32_t rule, relay_cue_summary_t* out) {
+  if (!host_stats || !out) return fail(RELAY_ERR_INVALID, "host_stats and out are required");
+  if (n_cues < 1 || n_cues > kMaxCues) return fail(RELAY_ERR_INVALID, "n_cues out of range");
+  if (world_size < 1) return fail(RELAY_ERR_INVALID, "world_size < 1");
+  if (rule < 0 || rule > 2) return fail(RELAY_ERR_INVALID, "rule must be 0, 1 or 2");
+  const int nf = kStatFields + world_size;
+  const double Q = 1048576.0;
+  for (int r = 0; r <= n_cues; r++) {
+    const uint64_t* row = host_stats + static_cast<size_t>(r) * nf;
+    relay_cue_summary_t& o = out[r];
+    const uint64_t n = row[RELAY_F_N];
+    const uint64_t s1 = row[RELAY_F_SUM_MQ], s2 = row[RELAY_F_SUM_MQ2];
+    o.n = static_cast<int64_t>(n);
+    o.n_triggers = static_cast<int64_t>(row[RELAY_F_TRIG]);
+    o.n_invalid = static_cast<int64_t>(row[RELAY_F_INVALID]);
+    o.selected = 0;
+    float mn = INFINITY;
+    for (int k = 0; k < world_size; k++) {
+      uint32_t bits = static_cast<uint32_t>(row[RELAY_F_MIN0 + k]);
+      float f;
+      std::memcpy(&f, &bits, sizeof f);
+      mn = std::fmin(mn, f);
+    }
+    if (n == 0) {
+      o.mean = o.std = o.se = o.token_mean = o.min = o.low_frac = NAN;
+      continue;
+    }
+    o.mean = static_cast<double>(s1) / (static_cast<double>(n) * Q);
+    // n^2 var = n s2 - s1^2, exact in 128-bit integers
+    const unsigned __int128 a = static_cast<unsigned __int128>(n) * s2;
+    const unsigned __int128 b = static_cast<unsigned __int128>(s1) * s1;
+    const unsigned __int128 d = a > b ? a - b : 0;
+    const double var = static_cast<double>(d) / (static_cast<double>(n) * static_cast<double>(n) * Q * Q);
+    o.std = std::sqrt(var);
+    o.se = o.std / std::sqrt(static_cast<double>(n));
+    const uint64_t lens = row[RELAY_F_SUM_LEN];
+    o.token_mean = lens ? static_cast<double>(row[RELAY_F_SUM_WQ]) / (static_cast<double>(lens) * Q) : NAN;
+    o.low_frac = lens ? static_cast<double>(row[RELAY_F_SUM_LOW]) / static_cast<double>(lens) : NAN;
+    o.min = mn;
+  }
+  relay_cue_summary_t& g = out[n_cues];
+  if (g.n < 2) {
+    g.std = g.se = NAN;
+    return RELAY_OK;
+  }
+  for (int c = 0; c < n_cues; c++) {
+    relay_cue_summary_t& o = out[c];
+    if (o.n < 1 || o.n < min_count) continue;
+    if (rule == 0) o.selected = o.mean >= g.mean + g.se;
+    else if (rule == 1) o.selected = o.mean >= g.mean + o.se;
+    else o.selected = o.mean > g.mean;
+  }
+  return RELAY_OK;
+}
+
+relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dtype_t dt, int32_t batch,
+                                 int64_t vocab, int64_t row_stride, float inv_temperature,
+                                 const int32_t* sampled, uint8_t* state, int32_t* hist, int32_t* small_run,
+                                 float margin_gate, int32_t max_small_segment, float* margin, int32_t* top1,
+                                 int32_t* top2, uint8_t* flag, int16_t* cue_id, void* ws, size_t ws_bytes,
+                                 relay_stream_t stream) {
+  if (!cs) return fail(RELAY_ERR_INVALID, "cs is NULL");
+  if (!valid_dtype(dt)) return fail(RELAY_ERR_INVALID, "unknown dtype");
+  if (vocab < 2 || vocab > 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "vocab out of range");
+  if (vocab != cs->dev.vocab) return fail(RELAY_ERR_INVALID, "vocab differs from the cue set's");
+  if (row_stride < vocab) return fail(RELAY_ERR_INVALID, "row_stride < vocab");
+  if (batch < 0) return fail(RELAY_ERR_INVALID, "batch < 0");
+  if (!(inv_temperature > 0.0f) || !std::isfinite(inv_temperature))
+    return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
+  if (max_small_segment < 0) return fail(RELAY_ERR_INVALID, "max_small_segment < 0");
+  if (max_small_segment > 0 && !small_run) return fail(RELAY_ERR_INVALID, "small_run required with a budget");
+  if (batch == 0) return RELAY_OK;
+  if (!logits || !state || !hist || !margin || !flag || !cue_id)
+    return fail(RELAY_ERR_INVALID, "logits/state/hist/margin/flag/cue_id are required");
+  StepWs w = step_ws_layout(ws, batch);
+  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  return cuda_status(launch_step_switch(cs->dev, logits, static_cast<int>(dt), batch, static_cast<int>(vocab),
+                                        row_stride, inv_temperature, sampled, state, hist, small_run, margin_gate,
+                                        max_small_segment, margin, top1, top2, flag, cue_id, w,
+                                        reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_step_switch launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+// relay_device.cuh — device-side building blocks shared by the sm_100a kernels
+// of librelay.so.  Nothing here is shared with oracle/ (which is plain C).
+#pragma once
+
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace relay {
+
+constexpr unsigned kFull = 0xffffffffu;
+// Lazy exp-reference slack in log2 units: a term is at most 2^16 before the
+// reference is raised, so fp32 partial sums never overflow (K1).
+constexpr float kSlack = 16.0f;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float qnan() { return __int_as_float(0x7fffffff); }
+
+// ---------------------------------------------------------------- top-2
+// Order: value descending, then index ascending (P:141-146 + R3).  IEEE
+// compares: -0 == +0; NaN never ranks (all comparisons with NaN are false).
+__device__ __forceinline__ bool better(float a, int ia, float b, int ib) {
+  return a > b || (a == b && ia < ib);
+}
+
+struct Top2 {
+  float v1, v2;
+  int i1, i2;
+};
+
+__device__ __forceinline__ Top2 top2_empty() { return Top2{-INFINITY, -INFINITY, INT_MAX, INT_MAX}; }
+
+__device__ __forceinline__ void top2_push(Top2& t, float x, int j) {
+  if (better(x, j, t.v1, t.i1)) {
+    t.v2 = t.v1; t.i2 = t.i1; t.v1 = x; t.i1 = j;
+  } else if (better(x, j, t.v2, t.i2)) {
+    t.v2 = x; t.i2 = j;
+  }
+}
+
+__device__ __forceinline__ Top2 top2_merge(const Top2& a, const Top2& b) {
+  Top2 r;
+  if (better(a.v1, a.i1, b.v1, b.i1)) {
+    r.v1 = a.v1; r.i1 = a.i1;
+    if (better(a.v2, a.i2, b.v1, b.i1)) { r.v2 = a.v2; r.i2 = a.i2; }
+    else { r.v2 = b.v1; r.i2 = b.i1; }
+  } else {
+    r.v1 = b.v1; r.i1 = b.i1;
+    if (better(a.v1, a.i1, b.v2, b.i2)) { r.v2 = a.v1; r.i2 = a.i1; }
+    else { r.v2 = b.v2; r.i2 = b.i2; }
+  }
+  return r;
+}
+
+// ------------------------------------------------- softmax normaliser
+// s = sum_j 2^(y_j - m), y = z * c (c = iota * log2 e), m a lazily raised
+// reference (never above the row maximum).
+struct Norm {
+  float m, s;
+};
+
+__device__ __forceinline__ Norm norm_merge(const Norm& a, const Norm& b) {
+  float m = fmaxf(a.m, b.m);
+  return Norm{m, a.s * ex2(a.m - m) + b.s * ex2(b.m - m)};
+}
+
+// Row partial: everything a (row, range) pass produces.
+struct Partial {
+  Top2 t;
+  Norm n;
+};
+
+__device__ __forceinline__ Partial partial_merge(const Partial& a, const Partial& b) {
+  return Partial{top2_merge(a.t, b.t), norm_merge(a.n, b.n)};
+}
+
+__device__ __forceinline__ Partial shfl_xor_partial(const Partial& p, int off) {
+  Partial o;
+  o.t.v1 = __shfl_xor_sync(kFull, p.t.v1, off);
+  o.t.v2 = __shfl_xor_sync(kFull, p.t.v2, off);
+  o.t.i1 = __shfl_xor_sync(kFull, p.t.i1, off);
+  o.t.i2 = __shfl_xor_sync(kFull, p.t.i2, off);
+  o.n.m = __shfl_xor_sync(kFull, p.n.m, off);
+  o.n.s = __shfl_xor_sync(kFull, p.n.s, off);
+  return o;
+}
+
+__device__ __forceinline__ Partial warp_reduce_partial(Partial p) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) p = partial_merge(p, shfl_xor_partial(p, off));
+  return p;
+}
+
+// Order-preserving float <-> int key (for atomicMax on a shared threshold).
+__device__ __forceinline__ int fkey(float f) {
+  int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float unkey(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+
+// Finish a row: margin, lse, status (R4).  c = iota*log2e, iota = c/log2e.
+struct RowOut {
+  float margin, lse;
+  int i1, i2;
+  int status;
+};
+
+__device__ __forceinline__ RowOut finish_row(const Partial& p, float c, float iota) {
+  RowOut o;
+  float S0 = p.n.s;
+  if (isnan(S0) || p.t.v1 == INFINITY) {
+    o.status = 1;
+  } else if (p.t.v1 == -INFINITY) {
+    o.status = 2;
+  } else {
+    o.status = 0;
+  }
+  if (o.status != 0) {
+    o.margin = qnan(); o.lse = qnan(); o.i1 = -1; o.i2 = -1;
+    return o;
+  }
+  float My = p.t.v1 * c;
+  float S = S0 * ex2(p.n.m - My);          // S = sum_j exp((z_j - z1) iota)
+  float p2 = ex2(p.t.v2 * c - My);          // exp((z2 - z1) iota) (0 for -inf)
+  o.margin = (1.0f - p2) / S;
+  o.lse = p.t.v1 * iota + logf(S);
+  o.i1 = p.t.i1;
+  o.i2 = p.t.i2;
+  return o;
+}
+
+// ------------------------------------------------------------ loads
+__device__ __forceinline__ uint4 ldg_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+struct U8x32 {
+  uint32_t w[8];
+};
+
+__device__ __forceinline__ U8x32 ldg_stream32(const void* p) {
+  U8x32 r;
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+        "=r"(r.w[6]), "=r"(r.w[7])
+      : "l"(p));
+  return r;
+}
+
+// Element formats.  unpack2 turns one 32-bit word into two fp32 values
+// (exact for bf16/f16).
+struct EBf16 {
+  using T = uint16_t;
+  static constexpr int SZ = 2;
+  __device__ static __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
+    lo = __uint_as_float(w << 16);
+    hi = __uint_as_float(w & 0xffff0000u);
+  }
+  __device__ static __forceinline__ float load1(const T* p) {
+    return __uint_as_float(static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(p))) << 16);
+  }
+};
+
+struct EF16 {
+  using T = uint16_t;
+  static constexpr int SZ = 2;
+  __device__ static __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
+    __half2 h = *reinterpret_cast<__half2*>(&w);
+    float2 f = __half22float2(h);
+    lo = f.x;
+    hi = f.y;
+  }
+  __device__ static __forceinline__ float load1(const T* p) {
+    unsigned short b = __ldg(reinterpret_cast<const unsigned short*>(p));
+    return __half2float(__ushort_as_half(b));
+  }
+};
+
+struct EF32 {
+  using T = float;
+  static constexpr int SZ = 4;
+  __device__ static __forceinline__ void unpack2(uint32_t, float&, float&) {}
+  __device__ static __forceinline__ float load1(const T* p) { return __ldg(p); }
+};
+
+}  // namespace relay

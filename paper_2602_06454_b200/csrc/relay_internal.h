@@ -1,0 +1,91 @@
+// relay_internal.h — host/device structures and launcher declarations shared
+// by relay_kernels.cu and relay_api.cu (not part of the public ABI).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace relay {
+
+constexpr int kMaxLen = 8;        // RELAY_MAX_CUE_LEN
+constexpr int kMaxPat = 64;       // RELAY_MAX_PATTERNS
+constexpr int kMaxCues = 64;      // RELAY_MAX_CUES
+constexpr int kStatFields = 8;    // RELAY_STAT_FIELDS
+constexpr int kTile = 2048;       // positions per CTA in the scan kernels
+constexpr int kScanThreads = 256; // kTile / 8 consecutive positions per thread
+constexpr int kHist = kMaxLen - 1;
+
+// Device view of a cue set (all pointers device memory owned by the handle).
+// Patterns are stored sorted by length descending (ties: original order), so
+// the first match at a start / as a suffix is the longest.
+struct CueDev {
+  int n_pat, n_cues, mode, think_end;
+  long long vocab;
+  const int* pat_tok;      // [n_pat][kMaxLen], sorted
+  const int* pat_len;      // [n_pat], sorted
+  const int* pat_cue;      // [n_pat], sorted
+  const int* pat_orig;     // [n_pat] sorted -> caller's pattern index
+  const int* cue_of_orig;  // [n_pat] caller's pattern index -> cue
+  const uint32_t* term_tab;  // [ceil(vocab/32)] terminator bitmap
+};
+
+// Aggregate of a run of positions for the reverse segmented scan (K3).
+struct Agg {
+  unsigned long long sumq;  // sum of q = rint(m 2^20)
+  unsigned int low;         // #{m < tau}
+  unsigned int nan;         // # NaN margins
+  float mn;                 // min margin (+inf if none)
+  int end;                  // index of the run's first segment tail (valid if tail)
+  int tail;                 // 1 if the run contains a segment tail
+  int pad;
+};
+
+// Workspace layouts (256-byte aligned pieces).
+struct ScanWs {
+  int* tile_count;     // [n_tiles]
+  Agg* tile_head;      // [n_tiles]
+  Agg* tile_carry;     // [n_tiles]
+  unsigned long long* occ_sumq;  // [cap]
+  unsigned int* occ_low;         // [cap]
+  unsigned int* occ_nan;         // [cap]
+  size_t bytes;
+};
+ScanWs scan_ws_layout(void* base, long long n_tok, long long cap);
+
+struct StepWs {
+  int* counter;        // [batch] (zero between launches)
+  float* part;         // [batch][nsplit][6] partial (v1, v2, i1, i2, m, s)
+  size_t bytes;
+};
+constexpr int kMaxSplit = 32;
+StepWs step_ws_layout(void* base, int batch);
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_margin_rows(const void* logits, int dt, long long n_rows, int vocab,
+                               long long stride, float iota, float* margin, int* top1, int* top2,
+                               float* lse, uint8_t* status, cudaStream_t st);
+
+cudaError_t launch_cue_scan(const CueDev& cs, const int* tokens, long long n_tok,
+                            const long long* offs, int n_traj, uint32_t* term_bits, int* occ_pos,
+                            int* occ_pat, long long cap, long long* n_occ, const ScanWs& ws,
+                            cudaStream_t st);
+
+cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long long n_tok,
+                                  const long long* offs, int n_traj, const long long* think_end,
+                                  const uint32_t* term_bits, const int* occ_pos, const int* occ_pat,
+                                  const long long* n_occ, long long cap, float tau, int* seg_end,
+                                  float* seg_mean, float* seg_min, float* seg_lowfrac,
+                                  unsigned long long* stats, int rank, int world, const ScanWs& ws,
+                                  cudaStream_t st);
+
+cudaError_t launch_stats_init(unsigned long long* stats, int n_cues, int rank, int world,
+                              cudaStream_t st);
+
+cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
+                               long long stride, float iota, const int* sampled, uint8_t* state,
+                               int* hist, int* small_run, float gate, int max_seg, float* margin,
+                               int* top1, int* top2, uint8_t* flag, int16_t* cue_id,
+                               const StepWs& ws, cudaStream_t st);
+
+}  // namespace relay

@@ -1,0 +1,598 @@
+// scan_kernels.cu — K2 relay_cue_scan and K3 relay_segment_reduce (sm_100a).
+//
+// K2: switch-cue occurrences by token matching + the
+//     terminator bitmap.  Tiles of 2048 positions (8 consecutive per
+//     thread) staged in shared memory with an 8-token halo; count pass ->
+//     exclusive tile prefix -> ordered scatter, so occurrences come out sorted
+//     by position with no atomics (deterministic).
+// K3: post-sentence windows as a REVERSE segmented scan
+//     keyed by segment tails (terminator or trajectory end): the aggregate at
+//     s over [s, first tail >= s] is exactly the window of a cue at s.
+//     Tile heads -> cross-tile carries -> per-position suffix aggregates
+//     gathered at occurrence starts -> per-cue integer moments (u64 atomics:
+//     order-free, so bit-identical across launch shapes and ranks).
+// Both are tiny next to K1 (4 B per token vs ~300 KB per logit row).
+#include <cfloat>
+
+#include "relay_device.cuh"
+#include "relay_internal.h"
+
+namespace relay {
+
+constexpr int kItems = kTile / kScanThreads;  // 8 consecutive positions per thread
+static_assert(kItems == 8, "tile layout");
+
+// Trajectory index of position t: offs[k] <= t < offs[k+1], or -1.
+__device__ __forceinline__ int find_traj(const long long* offs, int n_traj, long long n_tok,
+                                         long long t) {
+  if (!offs) return (t >= 0 && t < n_tok) ? 0 : -1;
+  int lo = 0, hi = n_traj + 1;  // upper_bound over offs[0..n_traj]
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (offs[mid] <= t) lo = mid + 1; else hi = mid;
+  }
+  int k = lo - 1;
+  return (k >= 0 && k < n_traj) ? k : -1;
+}
+
+__device__ __forceinline__ long long traj_end(const long long* offs, long long n_tok, int k) {
+  return offs ? offs[k + 1] : n_tok;
+}
+
+struct SmemPat {
+  int tok[kMaxPat * kMaxLen];
+  int len[kMaxPat];
+  int cue[kMaxPat];
+  int orig[kMaxPat];
+};
+
+__device__ __forceinline__ void load_patterns(const CueDev& cs, SmemPat& sp) {
+  for (int i = threadIdx.x; i < cs.n_pat * kMaxLen; i += blockDim.x) sp.tok[i] = cs.pat_tok[i];
+  for (int i = threadIdx.x; i < cs.n_pat; i += blockDim.x) {
+    sp.len[i] = cs.pat_len[i];
+    sp.cue[i] = cs.pat_cue[i];
+    sp.orig[i] = cs.pat_orig[i];
+  }
+}
+
+__device__ __forceinline__ bool match_at(const SmemPat& sp, int p, const int* tk, long long room) {
+  const int len = sp.len[p];
+  if (len > room) return false;
+  for (int k = 0; k < len; k++)
+    if (tk[k] != sp.tok[p * kMaxLen + k]) return false;
+  return true;
+}
+
+// Occurrences starting at this position.  LONGEST: 0/1 and the sorted index
+// of the longest matching pattern.  ALL: a cue bitmask (one occurrence per
+// matching cue).
+__device__ __forceinline__ int count_at(const CueDev& cs, const SmemPat& sp, const int* tk,
+                                        long long room, unsigned long long* mask, int* best) {
+  if (cs.mode == 0) {
+    for (int p = 0; p < cs.n_pat; p++)
+      if (match_at(sp, p, tk, room)) { *best = p; return 1; }
+    return 0;
+  }
+  unsigned long long m = 0;
+  for (int p = 0; p < cs.n_pat; p++)
+    if (match_at(sp, p, tk, room)) m |= 1ull << sp.cue[p];
+  *mask = m;
+  return __popcll(m);
+}
+
+__device__ __forceinline__ void stage_tokens(const int* __restrict__ tokens, long long n_tok,
+                                             long long base, int* s_tok) {
+  for (int i = threadIdx.x; i < kTile + kMaxLen; i += blockDim.x) {
+    long long t = base + i;
+    s_tok[i] = (t < n_tok) ? tokens[t] : -1;
+  }
+}
+
+// Room (tokens available inside the trajectory) at position t; 0 outside.
+__device__ __forceinline__ long long room_at(const long long* offs, int n_traj, long long n_tok,
+                                             long long t) {
+  int k = find_traj(offs, n_traj, n_tok, t);
+  return k < 0 ? 0 : traj_end(offs, n_tok, k) - t;
+}
+
+template <int NT>
+__device__ __forceinline__ int block_sum(int v, int* s_tmp) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) s_tmp[warp] = v;
+  __syncthreads();
+  int tot = 0;
+  for (int w = 0; w < NT / 32; w++) tot += s_tmp[w];
+  return tot;
+}
+
+// ------------------------------------------------------------- K2 count
+__global__ void __launch_bounds__(kScanThreads)
+    cue_count_kernel(CueDev cs, const int* __restrict__ tokens, long long n_tok,
+                     const long long* __restrict__ offs, int n_traj, uint32_t* __restrict__ term_bits,
+                     int* __restrict__ tile_count) {
+  __shared__ int s_tok[kTile + kMaxLen];
+  __shared__ SmemPat sp;
+  __shared__ int s_tmp[32];
+  const long long base = static_cast<long long>(blockIdx.x) * kTile;
+  stage_tokens(tokens, n_tok, base, s_tok);
+  load_patterns(cs, sp);
+  __syncthreads();
+  const int li = threadIdx.x * kItems;
+  int cnt = 0;
+  uint32_t tb = 0;
+#pragma unroll 1
+  for (int k = 0; k < kItems; k++) {
+    const long long t = base + li + k;
+    if (t >= n_tok) break;
+    const int tok = s_tok[li + k];
+    if (tok >= 0 && tok < cs.vocab && ((cs.term_tab[tok >> 5] >> (tok & 31)) & 1u)) tb |= 1u << k;
+    const long long room = room_at(offs, n_traj, n_tok, t);
+    unsigned long long mask;
+    int best;
+    if (room > 0) cnt += count_at(cs, sp, s_tok + li + k, room, &mask, &best);
+  }
+  // 4 lanes x 8 bits -> one 32-bit word
+  const int lane = threadIdx.x & 31;
+  uint32_t w = tb << (8 * (lane & 3));
+  w |= __shfl_xor_sync(kFull, w, 1);
+  w |= __shfl_xor_sync(kFull, w, 2);
+  if ((lane & 3) == 0 && base + li < n_tok) term_bits[(base + li) >> 5] = w;
+  const int tot = block_sum<kScanThreads>(cnt, s_tmp);
+  if (threadIdx.x == 0) tile_count[blockIdx.x] = tot;
+}
+
+// ----------------------------------------------------------- K2 scatter
+__global__ void __launch_bounds__(kScanThreads)
+    cue_scatter_kernel(CueDev cs, const int* __restrict__ tokens, long long n_tok,
+                       const long long* __restrict__ offs, int n_traj,
+                       const int* __restrict__ tile_count, int n_tiles, int* __restrict__ occ_pos,
+                       int* __restrict__ occ_pat, long long cap, long long* __restrict__ n_occ) {
+  __shared__ int s_tok[kTile + kMaxLen];
+  __shared__ SmemPat sp;
+  __shared__ int s_tmp[32];
+  __shared__ int s_scan[kScanThreads];
+  const long long base = static_cast<long long>(blockIdx.x) * kTile;
+  stage_tokens(tokens, n_tok, base, s_tok);
+  load_patterns(cs, sp);
+  // prefix of earlier tiles (ints; true counts < 2^31 per call)
+  int pre = 0;
+  for (int i = threadIdx.x; i < blockIdx.x; i += blockDim.x) pre += tile_count[i];
+  __syncthreads();
+  const long long prefix = block_sum<kScanThreads>(pre, s_tmp);
+  const int li = threadIdx.x * kItems;
+  int cnt = 0;
+  unsigned long long masks[kItems];
+  int bests[kItems];
+  long long rooms[kItems];
+#pragma unroll
+  for (int k = 0; k < kItems; k++) {
+    masks[k] = 0; bests[k] = -1; rooms[k] = 0;
+    const long long t = base + li + k;
+    if (t < n_tok) {
+      rooms[k] = room_at(offs, n_traj, n_tok, t);
+      if (rooms[k] > 0) {
+        int c = count_at(cs, sp, s_tok + li + k, rooms[k], &masks[k], &bests[k]);
+        if (c == 0) bests[k] = -1;
+        cnt += c;
+      }
+    }
+  }
+  // block exclusive scan of cnt (thread order == position order)
+  s_scan[threadIdx.x] = cnt;
+  __syncthreads();
+  for (int off = 1; off < kScanThreads; off <<= 1) {
+    int v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
+    __syncthreads();
+    s_scan[threadIdx.x] += v;
+    __syncthreads();
+  }
+  long long o = prefix + s_scan[threadIdx.x] - cnt;
+  const int tile_total = s_scan[kScanThreads - 1];
+#pragma unroll 1
+  for (int k = 0; k < kItems; k++) {
+    const long long t = base + li + k;
+    if (t >= n_tok) break;
+    if (cs.mode == 0) {
+      if (bests[k] >= 0) {
+        if (o < cap) { occ_pos[o] = static_cast<int>(t); occ_pat[o] = sp.orig[bests[k]]; }
+        o++;
+      }
+    } else {
+      unsigned long long m = masks[k];
+      while (m) {
+        const int c = __ffsll(m) - 1;
+        m &= m - 1;
+        int best = -1;
+        for (int p = 0; p < cs.n_pat && best < 0; p++)
+          if (sp.cue[p] == c && match_at(sp, p, s_tok + li + k, rooms[k])) best = p;
+        if (o < cap) { occ_pos[o] = static_cast<int>(t); occ_pat[o] = sp.orig[best]; }
+        o++;
+      }
+    }
+  }
+  if (blockIdx.x == n_tiles - 1 && threadIdx.x == 0) *n_occ = prefix + tile_total;
+}
+
+// ------------------------------------------------------------------ K3
+__device__ __forceinline__ Agg agg_identity() {
+  Agg a;
+  a.sumq = 0; a.low = 0; a.nan = 0; a.mn = INFINITY; a.end = -1; a.tail = 0; a.pad = 0;
+  return a;
+}
+
+// L precedes R (L earlier positions).  The run starting at L's first
+// position stops at its first tail.
+__device__ __forceinline__ Agg agg_suffix(const Agg& L, const Agg& R) {
+  if (L.tail) return L;
+  Agg o;
+  o.sumq = L.sumq + R.sumq;
+  o.low = L.low + R.low;
+  o.nan = L.nan + R.nan;
+  o.mn = fminf(L.mn, R.mn);
+  o.end = R.end;
+  o.tail = R.tail;
+  o.pad = 0;
+  return o;
+}
+
+__device__ __forceinline__ Agg shfl_down_agg(const Agg& a, int off) {
+  Agg o;
+  o.sumq = __shfl_down_sync(kFull, a.sumq, off);
+  o.low = __shfl_down_sync(kFull, a.low, off);
+  o.nan = __shfl_down_sync(kFull, a.nan, off);
+  o.mn = __shfl_down_sync(kFull, a.mn, off);
+  o.end = __shfl_down_sync(kFull, a.end, off);
+  o.tail = __shfl_down_sync(kFull, a.tail, off);
+  o.pad = 0;
+  return o;
+}
+
+// q = rint(m * 2^20) with m clamped to [0, 1] (NaN handled by the caller).
+__device__ __forceinline__ unsigned long long q20(float m) {
+  float c = fminf(fmaxf(m, 0.0f), 1.0f);
+  return static_cast<unsigned long long>(__float2int_rn(c * 1048576.0f));
+}
+
+struct PosVal {
+  Agg v;        // single-position aggregate
+  int counted;  // counts in the global row
+};
+
+// Per-position values for this thread's 8 consecutive positions.
+__device__ __forceinline__ void load_positions(const float* __restrict__ margin,
+                                               const uint32_t* __restrict__ term_bits,
+                                               long long n_tok, const long long* offs, int n_traj,
+                                               const long long* think_end, float tau,
+                                               long long p0, PosVal (&pv)[kItems]) {
+  int k = find_traj(offs, n_traj, n_tok, p0);
+#pragma unroll
+  for (int i = 0; i < kItems; i++) {
+    const long long t = p0 + i;
+    Agg a = agg_identity();
+    int counted = 0;
+    if (t < n_tok) {
+      if (offs && (k < 0 || t >= offs[k + 1])) k = find_traj(offs, n_traj, n_tok, t);
+      const float m = margin[t];
+      const bool term = (term_bits[t >> 5] >> (t & 31)) & 1u;
+      const bool in = k >= 0;
+      const bool last = in && (t == traj_end(offs, n_tok, k) - 1);
+      a.tail = (!in || term || last) ? 1 : 0;
+      a.end = static_cast<int>(t);
+      if (isnan(m)) {
+        a.nan = 1;
+      } else {
+        a.sumq = q20(m);
+        a.low = (m < tau) ? 1u : 0u;
+        a.mn = m;
+      }
+      counted = in && (!think_end || t < think_end[k]);
+    } else {
+      a.tail = 1;
+      a.end = static_cast<int>(t);
+    }
+    pv[i].v = a;
+    pv[i].counted = counted;
+  }
+}
+
+// K3a: tile heads + global moments.
+__global__ void __launch_bounds__(kScanThreads)
+    seg_head_kernel(const float* __restrict__ margin, const uint32_t* __restrict__ term_bits,
+                    long long n_tok, const long long* __restrict__ offs, int n_traj,
+                    const long long* __restrict__ think_end, float tau, Agg* __restrict__ tile_head,
+                    unsigned long long* __restrict__ grow, int nf, int rank) {
+  __shared__ Agg s_w[kScanThreads / 32];
+  __shared__ unsigned long long s_red[kScanThreads / 32][5];
+  __shared__ float s_min[kScanThreads / 32];
+  const long long base = static_cast<long long>(blockIdx.x) * kTile;
+  const long long p0 = base + threadIdx.x * kItems;
+  PosVal pv[kItems];
+  load_positions(margin, term_bits, n_tok, offs, n_traj, think_end, tau, p0, pv);
+  // thread head: v0 (+) v1 (+) ... (+) v7
+  Agg h = pv[kItems - 1].v;
+  unsigned long long gn = 0, gs = 0, gs2 = 0, glow = 0, gnan = 0;
+  float gmin = INFINITY;
+#pragma unroll
+  for (int i = kItems - 1; i >= 0; i--) {
+    if (i < kItems - 1) h = agg_suffix(pv[i].v, h);
+    if (pv[i].counted) {
+      if (pv[i].v.nan) {
+        gnan++;
+      } else {
+        const unsigned long long q = pv[i].v.sumq;
+        gn++; gs += q; gs2 += q * q; glow += pv[i].v.low;
+        gmin = fminf(gmin, pv[i].v.mn);
+      }
+    }
+  }
+  // ordered warp reduce (offsets 1,2,4,...: lane 0 covers lanes 0..31 in order)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Agg o = shfl_down_agg(h, off);
+    if (lane + off < 32) h = agg_suffix(h, o);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    gn += __shfl_xor_sync(kFull, gn, off);
+    gs += __shfl_xor_sync(kFull, gs, off);
+    gs2 += __shfl_xor_sync(kFull, gs2, off);
+    glow += __shfl_xor_sync(kFull, glow, off);
+    gnan += __shfl_xor_sync(kFull, gnan, off);
+    gmin = fminf(gmin, __shfl_xor_sync(kFull, gmin, off));
+  }
+  if (lane == 0) {
+    s_w[warp] = h;
+    s_red[warp][0] = gn; s_red[warp][1] = gs; s_red[warp][2] = gs2;
+    s_red[warp][3] = glow; s_red[warp][4] = gnan;
+    s_min[warp] = gmin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Agg t = s_w[kScanThreads / 32 - 1];
+    for (int w = kScanThreads / 32 - 2; w >= 0; w--) t = agg_suffix(s_w[w], t);
+    tile_head[blockIdx.x] = t;
+    unsigned long long a[5] = {0, 0, 0, 0, 0};
+    float mn = INFINITY;
+    for (int w = 0; w < kScanThreads / 32; w++) {
+      for (int f = 0; f < 5; f++) a[f] += s_red[w][f];
+      mn = fminf(mn, s_min[w]);
+    }
+    if (a[0]) {
+      atomicAdd(grow + 0, a[0]);   // n
+      atomicAdd(grow + 1, a[1]);   // sum q
+      atomicAdd(grow + 2, a[2]);   // sum q^2
+      atomicAdd(grow + 3, a[1]);   // sum q (token-pooled)
+      atomicAdd(grow + 4, a[0]);   // positions
+      atomicAdd(grow + 5, a[3]);   // low
+      atomicMin(grow + kStatFields + rank,
+                static_cast<unsigned long long>(__float_as_uint(fminf(fmaxf(mn, 0.0f), 1.0f))));
+    }
+    if (a[4]) atomicAdd(grow + 7, a[4]);  // NaN positions
+  }
+  (void)nf;
+}
+
+// K3b: carry[k] = head[k+1] (+) head[k+2] (+) ... (exclusive suffix), one CTA.
+__global__ void __launch_bounds__(1024) seg_carry_kernel(const Agg* __restrict__ head,
+                                                         Agg* __restrict__ carry, int n_tiles) {
+  __shared__ Agg s[1024];
+  __shared__ Agg s_run;
+  if (threadIdx.x == 0) s_run = agg_identity();
+  __syncthreads();
+  // process chunks of 1024 tiles from the right end
+  for (int hi = n_tiles; hi > 0; hi -= 1024) {
+    const int lo = max(0, hi - 1024);
+    const int n = hi - lo;
+    const int i = threadIdx.x;
+    s[i] = (i < n) ? head[lo + i] : agg_identity();
+    __syncthreads();
+    // inclusive suffix scan within the chunk (Hillis-Steele, right to left)
+    for (int off = 1; off < 1024; off <<= 1) {
+      Agg v = s[i];
+      Agg r = (i + off < n) ? s[i + off] : agg_identity();
+      __syncthreads();
+      if (i + off < n) s[i] = agg_suffix(v, r);
+      __syncthreads();
+    }
+    if (i < n) {
+      Agg nxt = (i + 1 < n) ? agg_suffix(s[i + 1], s_run) : s_run;
+      carry[lo + i] = nxt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_run = agg_suffix(s[0], s_run);
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int lower_bound_occ(const int* occ_pos, int n, long long key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (occ_pos[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// K3c: per-position suffix aggregates in this tile, gathered at occurrences.
+__global__ void __launch_bounds__(kScanThreads)
+    seg_gather_kernel(const float* __restrict__ margin, const uint32_t* __restrict__ term_bits,
+                      long long n_tok, const long long* __restrict__ offs, int n_traj, float tau,
+                      const Agg* __restrict__ tile_carry, const int* __restrict__ occ_pos,
+                      const long long* __restrict__ n_occ_p, long long cap, int* __restrict__ seg_end,
+                      float* __restrict__ seg_mean, float* __restrict__ seg_min,
+                      float* __restrict__ seg_lowfrac, unsigned long long* __restrict__ occ_sumq,
+                      unsigned int* __restrict__ occ_low, unsigned int* __restrict__ occ_nan) {
+  __shared__ Agg s_w[kScanThreads / 32];
+  __shared__ int s_range[2];
+  const long long nocc_ll = *n_occ_p < cap ? *n_occ_p : cap;
+  const int nocc = static_cast<int>(nocc_ll);
+  const long long base = static_cast<long long>(blockIdx.x) * kTile;
+  if (threadIdx.x == 0) {
+    s_range[0] = lower_bound_occ(occ_pos, nocc, base);
+    s_range[1] = lower_bound_occ(occ_pos, nocc, base + kTile);
+  }
+  __syncthreads();
+  if (s_range[0] == s_range[1]) return;  // no occurrence starts in this tile
+  const long long p0 = base + threadIdx.x * kItems;
+  PosVal pv[kItems];
+  load_positions(margin, term_bits, n_tok, offs, n_traj, nullptr, tau, p0, pv);
+  Agg h = pv[kItems - 1].v;
+#pragma unroll
+  for (int i = kItems - 2; i >= 0; i--) h = agg_suffix(pv[i].v, h);
+  // inclusive suffix scan over lanes (lane i: lanes i..31)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Agg x = h;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    Agg o = shfl_down_agg(x, off);
+    if (lane + off < 32) x = agg_suffix(x, o);
+  }
+  if (lane == 0) s_w[warp] = x;
+  __syncthreads();
+  // carry into this warp: warps to the right, then the tile carry
+  Agg wc = tile_carry[blockIdx.x];
+  for (int w = kScanThreads / 32 - 1; w > warp; w--) wc = agg_suffix(s_w[w], wc);
+  Agg nx = shfl_down_agg(x, 1);  // lanes i+1..31
+  Agg cin = (lane < 31) ? agg_suffix(nx, wc) : wc;
+  // per-position suffix aggregates (right to left), gather at occurrences
+  Agg sfx[kItems];
+  Agg run = cin;
+#pragma unroll
+  for (int i = kItems - 1; i >= 0; i--) {
+    run = agg_suffix(pv[i].v, run);
+    sfx[i] = run;
+  }
+  int lo = lower_bound_occ(occ_pos + s_range[0], s_range[1] - s_range[0], p0) + s_range[0];
+  for (int o = lo; o < s_range[1]; o++) {
+    const long long s = occ_pos[o];
+    if (s >= p0 + kItems) break;
+    const Agg a = sfx[s - p0];
+    const int len = a.end - static_cast<int>(s) + 1;
+    seg_end[o] = a.end;
+    occ_sumq[o] = a.sumq;
+    occ_low[o] = a.low;
+    occ_nan[o] = a.nan;
+    if (a.nan) {
+      seg_mean[o] = qnan(); seg_min[o] = qnan(); seg_lowfrac[o] = qnan();
+    } else {
+      seg_mean[o] = static_cast<float>(static_cast<double>(a.sumq) / (1048576.0 * len));
+      seg_min[o] = a.mn;
+      seg_lowfrac[o] = static_cast<float>(static_cast<double>(a.low) / len);
+    }
+  }
+}
+
+// K3d: per-occurrence statistics into the cue rows.
+__global__ void __launch_bounds__(256)
+    seg_stats_kernel(CueDev cs, long long n_tok, const long long* __restrict__ offs, int n_traj,
+                     const long long* __restrict__ think_end, const int* __restrict__ occ_pos,
+                     const int* __restrict__ occ_pat, const long long* __restrict__ n_occ_p,
+                     long long cap, const int* __restrict__ seg_end, const float* __restrict__ seg_min,
+                     const unsigned long long* __restrict__ occ_sumq,
+                     const unsigned int* __restrict__ occ_low, const unsigned int* __restrict__ occ_nan,
+                     unsigned long long* __restrict__ stats, int nf, int rank) {
+  const long long nocc = *n_occ_p < cap ? *n_occ_p : cap;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nocc;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int s = occ_pos[i];
+    const int e = seg_end[i];
+    // trigger: no occurrence starts earlier in the same sentence (R13)
+    long long j = i - 1;
+    while (j >= 0 && occ_pos[j] == s) j--;
+    const unsigned long long trig = (j < 0 || seg_end[j] != e) ? 1ull : 0ull;
+    if (think_end) {
+      const int k = find_traj(offs, n_traj, n_tok, s);
+      if (k >= 0 && s >= think_end[k]) continue;
+    }
+    const int cue = cs.cue_of_orig[occ_pat[i]];
+    unsigned long long* row = stats + static_cast<size_t>(cue) * nf;
+    if (occ_nan[i]) {
+      atomicAdd(row + 7, 1ull);
+      continue;
+    }
+    const unsigned long long len = static_cast<unsigned long long>(e - s + 1);
+    const unsigned long long sq = occ_sumq[i];
+    const unsigned long long mq = (2 * sq + len) / (2 * len);  // round half up
+    atomicAdd(row + 0, 1ull);
+    atomicAdd(row + 1, mq);
+    atomicAdd(row + 2, mq * mq);
+    atomicAdd(row + 3, sq);
+    atomicAdd(row + 4, len);
+    atomicAdd(row + 5, static_cast<unsigned long long>(occ_low[i]));
+    if (trig) atomicAdd(row + 6, 1ull);
+    atomicMin(row + kStatFields + rank,
+              static_cast<unsigned long long>(__float_as_uint(fminf(fmaxf(seg_min[i], 0.0f), 1.0f))));
+  }
+}
+
+__global__ void stats_init_kernel(unsigned long long* stats, int rows, int nf, int rank) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows * nf) {
+    const int f = i % nf;
+    stats[i] = (f == kStatFields + rank) ? 0x7f800000ull : 0ull;
+  }
+}
+
+// ------------------------------------------------------------ launchers
+static inline int n_tiles_of(long long n_tok) {
+  long long t = (n_tok + kTile - 1) / kTile;
+  return static_cast<int>(t < 1 ? 1 : t);
+}
+
+cudaError_t launch_cue_scan(const CueDev& cs, const int* tokens, long long n_tok,
+                            const long long* offs, int n_traj, uint32_t* term_bits, int* occ_pos,
+                            int* occ_pat, long long cap, long long* n_occ, const ScanWs& ws,
+                            cudaStream_t st) {
+  const int nt = n_tiles_of(n_tok);
+  cue_count_kernel<<<nt, kScanThreads, 0, st>>>(cs, tokens, n_tok, offs, n_traj, term_bits,
+                                                ws.tile_count);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  cue_scatter_kernel<<<nt, kScanThreads, 0, st>>>(cs, tokens, n_tok, offs, n_traj, ws.tile_count,
+                                                  nt, occ_pos, occ_pat, cap, n_occ);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long long n_tok,
+                                  const long long* offs, int n_traj, const long long* think_end,
+                                  const uint32_t* term_bits, const int* occ_pos, const int* occ_pat,
+                                  const long long* n_occ, long long cap, float tau, int* seg_end,
+                                  float* seg_mean, float* seg_min, float* seg_lowfrac,
+                                  unsigned long long* stats, int rank, int world, const ScanWs& ws,
+                                  cudaStream_t st) {
+  if (n_tok <= 0) return cudaSuccess;
+  const int nt = n_tiles_of(n_tok);
+  const int nf = kStatFields + world;
+  unsigned long long* grow = stats + static_cast<size_t>(cs.n_cues) * nf;
+  seg_head_kernel<<<nt, kScanThreads, 0, st>>>(margin, term_bits, n_tok, offs, n_traj, think_end,
+                                               tau, ws.tile_head, grow, nf, rank);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  seg_carry_kernel<<<1, 1024, 0, st>>>(ws.tile_head, ws.tile_carry, nt);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (cap <= 0) return cudaSuccess;
+  seg_gather_kernel<<<nt, kScanThreads, 0, st>>>(margin, term_bits, n_tok, offs, n_traj, tau,
+                                                 ws.tile_carry, occ_pos, n_occ, cap, seg_end,
+                                                 seg_mean, seg_min, seg_lowfrac, ws.occ_sumq,
+                                                 ws.occ_low, ws.occ_nan);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  long long blocks = (cap + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  seg_stats_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+      cs, n_tok, offs, n_traj, think_end, occ_pos, occ_pat, n_occ, cap, seg_end, seg_min,
+      ws.occ_sumq, ws.occ_low, ws.occ_nan, stats, nf, rank);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats_init(unsigned long long* stats, int n_cues, int rank, int world,
+                              cudaStream_t st) {
+  const int nf = kStatFields + world;
+  const int n = (n_cues + 1) * nf;
+  stats_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(stats, n_cues + 1, nf, rank);
+  return cudaGetLastError();
+}
+
+}  // namespace relay

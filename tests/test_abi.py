@@ -1,0 +1,148 @@
+"""No-GPU tests of the boundary: librelay.so loads, exports every symbol that
+include/relay.h declares, rejects bad arguments on the host before any device
+work, and finalizes an integer stats table (H7, host code) to the values of
+the hand-traced golden fixture."""
+import ctypes as C
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def relay():
+    import __graft_entry__
+    __graft_entry__._build_lib()
+    import paper_2602_06454_b200 as r
+    return r
+
+
+def test_exports_match_header(relay):
+    hdr = open(os.path.join(ROOT, "include", "relay.h")).read()
+    declared = set(re.findall(r"\b(relay_[a-z0-9_]+)\s*\(", hdr))
+    lib = C.CDLL(relay.LIB_PATH)
+    missing = [n for n in sorted(declared) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert declared == set(relay.EXPORTS)
+    assert relay.version() == 1
+
+
+def test_library_is_sm100a_only(relay):
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", relay.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def test_host_validation_without_device(relay):
+    lib = relay._lib
+    P = C.c_void_p
+    ptr = P(16)        # never dereferenced: validation fails first
+    # vocab < 2
+    assert lib.relay_margin_rows(ptr, 0, 4, 1, 1, 1.0, ptr, None, None, None, None, None) == 1
+    assert b"vocab" in lib.relay_last_error()
+    # row_stride < vocab
+    assert lib.relay_margin_rows(ptr, 0, 4, 8, 7, 1.0, ptr, None, None, None, None, None) == 1
+    # bad dtype / temperature / n_rows
+    assert lib.relay_margin_rows(ptr, 9, 4, 8, 8, 1.0, ptr, None, None, None, None, None) == 1
+    assert lib.relay_margin_rows(ptr, 0, 4, 8, 8, 0.0, ptr, None, None, None, None, None) == 1
+    assert lib.relay_margin_rows(ptr, 0, -1, 8, 8, 1.0, ptr, None, None, None, None, None) == 1
+    # n_rows == 0 is a no-op
+    assert lib.relay_margin_rows(None, 0, 0, 8, 8, 1.0, None, None, None, None, None, None) == 0
+    # cue set validation happens before any allocation
+    out = P()
+    term = np.zeros(16, np.uint8)
+    t = lambda a: np.ascontiguousarray(a, np.int32).ctypes.data_as(P)  # noqa: E731
+    keep = [np.array([1, 2, 1, 2], np.int32), np.array([0, 2, 4], np.int32), np.array([0, 0], np.int32)]
+    assert lib.relay_cueset_create(keep[0].ctypes.data_as(P), keep[1].ctypes.data_as(P), 2,
+                                   keep[2].ctypes.data_as(P), 1, term.ctypes.data_as(P), 16, -1, 0,
+                                   C.byref(out)) == 1
+    assert b"identical" in lib.relay_last_error()
+    bad = [np.array([1, 99], np.int32), np.array([0, 2], np.int32), np.array([0], np.int32)]
+    assert lib.relay_cueset_create(bad[0].ctypes.data_as(P), bad[1].ctypes.data_as(P), 1,
+                                   bad[2].ctypes.data_as(P), 1, term.ctypes.data_as(P), 16, -1, 0,
+                                   C.byref(out)) == 1
+    assert lib.relay_cueset_create(bad[0].ctypes.data_as(P), bad[1].ctypes.data_as(P), 1,
+                                   bad[2].ctypes.data_as(P), 1, term.ctypes.data_as(P), 16, -1, 2,
+                                   C.byref(out)) == 1
+    # workspace checks
+    assert lib.relay_cue_scan(None, ptr, 10, None, 1, ptr, ptr, ptr, 4, ptr, ptr, 0, None) == 1
+    assert lib.relay_stats_init(ptr, 3, 2, 2, None) == 1            # rank >= world
+    assert lib.relay_stats_finalize(None, 3, 1, 3, 0, None) == 1
+    del t
+
+
+def test_workspace_sizes_are_monotone(relay):
+    a = relay.workspace_bytes(1000, 10, 0)
+    b = relay.workspace_bytes(100000, 1000, 0)
+    c = relay.workspace_bytes(0, 0, 256)
+    assert 0 < a < b and c > 0
+    assert relay.stats_words(8, 1) == 9 * 9 and relay.stats_words(8, 4) == 9 * 12
+
+
+def _q20(x: float) -> int:
+    # round-half-even of the fp32 value times 2^20 (exact in Python)
+    return int(round(float(np.float32(x)) * (1 << 20)))
+
+
+def test_finalize_golden_trace(relay):
+    """Build the uint64 table by integer arithmetic from the golden fixture's
+    windows (hand-traced ends), finalize on the host, compare to the golden
+    per-cue and global numbers (within the Q20 error, 1e-5)."""
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "trace_fixture.json")))
+    m = g["margins"]
+    nf = 9
+    tab = np.zeros((3, nf), np.uint64)
+    tab[:, 8] = 0x7F800000
+    pat_cue = g["pat_cue"]
+    for k, o in enumerate(g["occurrences"]):
+        c = pat_cue[o["pat"]]
+        w = [_q20(x) for x in m[o["s"]:o["e"] + 1]]
+        ln = len(w)
+        sq = sum(w)
+        mq = (2 * sq + ln) // (2 * ln)
+        prev = [p for p in g["occurrences"][:k] if p["s"] < o["s"]]
+        trig = 1 if not prev or prev[-1]["e"] != o["e"] else 0
+        row = tab[c]
+        row[0] += 1; row[1] += mq; row[2] += mq * mq; row[3] += sq; row[4] += ln
+        row[5] += sum(1 for x in m[o["s"]:o["e"] + 1] if np.float32(x) < np.float32(g["tau"]))
+        row[6] += trig
+        row[8] = min(int(row[8]), int(np.float32(o["min"]).view(np.uint32)))
+    q = [_q20(x) for x in m]
+    gr = tab[2]
+    gr[0] = len(q); gr[1] = sum(q); gr[2] = sum(x * x for x in q); gr[3] = sum(q); gr[4] = len(q)
+    gr[5] = sum(1 for x in m if np.float32(x) < np.float32(g["tau"]))
+    gr[8] = int(np.float32(min(m)).view(np.uint32))
+    fin = relay.stats_finalize(tab.reshape(-1).view(np.int64), 2, 1, min_count=1)
+    for c, e in enumerate(g["cues"]):
+        assert fin[c]["n"] == e["n"] and fin[c]["n_triggers"] == e["n_triggers"]
+        for f in ("mean", "std", "se", "token_mean", "min", "low_frac"):
+            assert abs(fin[c][f] - e[f]) < 1e-5, (c, f)
+    for f in ("mean", "std", "se", "min", "low_frac"):
+        assert abs(fin[2][f] - g["global"][f]) < 1e-5, f
+    assert [f["selected"] for f in fin[:2]] == g["selected_rule0_min_count_1"]
+    fin3 = relay.stats_finalize(tab.reshape(-1).view(np.int64), 2, 1, min_count=5)
+    assert [f["selected"] for f in fin3[:2]] == [0, 0]
+
+
+def test_finalize_rules_and_small_n(relay):
+    nf = 9
+    tab = np.zeros((2, nf), np.uint64)
+    Q = 1 << 20
+    # global: margins {0.25, 0.75} -> mu .5, sigma .25, SE .25/sqrt2
+    tab[1, 0] = 2; tab[1, 1] = Q // 4 + 3 * Q // 4; tab[1, 2] = (Q // 4) ** 2 + (3 * Q // 4) ** 2
+    tab[1, 4] = 2
+    # cue: one window of mean 0.6
+    tab[0, 0] = 1; tab[0, 1] = int(0.6 * Q); tab[0, 2] = int(0.6 * Q) ** 2; tab[0, 4] = 1
+    f0 = relay.stats_finalize(tab.reshape(-1).view(np.int64), 1, 1, 1, rule=0)
+    f1 = relay.stats_finalize(tab.reshape(-1).view(np.int64), 1, 1, 1, rule=1)
+    f2 = relay.stats_finalize(tab.reshape(-1).view(np.int64), 1, 1, 1, rule=2)
+    assert abs(f0[1]["se"] - 0.25 / np.sqrt(2)) < 1e-12
+    assert (f0[0]["selected"], f1[0]["selected"], f2[0]["selected"]) == (0, 1, 1)
+    tab[1, 0] = 1
+    f = relay.stats_finalize(tab.reshape(-1).view(np.int64), 1, 1, 1, rule=2)
+    assert np.isnan(f[1]["se"]) and f[0]["selected"] == 0

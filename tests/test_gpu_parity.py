@@ -1,0 +1,473 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element, on the same seeded synthetic inputs.
+
+Bars (north_star): indices, statuses, cue positions, window ends, counts and
+trigger counts bit-exact; margins and statistics within 1e-5 absolute.  Where
+a float decides an integer (m < tau), both sides decide on the same fp32
+margins (K3 is fed synthetic fp32 margins, never K1's output).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def relay():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2602_06454_b200 as r
+    return r
+
+
+DEV = "cuda:0"
+
+
+def _rows_check(relay, logits, dtype, vocab, iota=1.0, rows=None):
+    out = relay.margin_rows(logits, vocab=vocab, inv_temperature=iota)
+    torch.cuda.synchronize()
+    host = synth.host_rows(logits if rows is None else logits[rows], dtype)
+    ref = oracle.margin_rows(host, dtype=dtype, vocab=vocab, inv_temperature=iota, threads=8)
+    sel = slice(None) if rows is None else rows
+    got = {k: v[sel].cpu().numpy() for k, v in out.items() if v is not None}
+    np.testing.assert_array_equal(got["status"], ref["status"].astype(np.uint8))
+    np.testing.assert_array_equal(got["top1"], ref["top1"])
+    np.testing.assert_array_equal(got["top2"], ref["top2"])
+    ok = ref["status"] == 0
+    assert np.all(np.isnan(got["margin"][~ok]))
+    err = np.abs(got["margin"][ok] - ref["margin"][ok])
+    assert err.size == 0 or err.max() < TOL, err.max()
+    lerr = np.abs(got["lse"][ok] - ref["lse"][ok]) / np.maximum(1.0, np.abs(ref["lse"][ok]))
+    assert lerr.size == 0 or lerr.max() < 1e-5
+    return got, ref
+
+
+# ------------------------------------------------------------------ H1
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "f32"])
+@pytest.mark.parametrize("vocab,stride", [(1000, 1000), (1000, 1003), (4099, 4113), (2, 2), (37, 40)])
+def test_margin_rows_ragged(relay, dtype, vocab, stride):
+    L = synth.make_logits(300, vocab, dtype, row_stride=stride, seed=vocab + stride, device=DEV)
+    _rows_check(relay, L, dtype, vocab)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_margin_rows_edge_rows(relay, dtype):
+    V = 5000
+    tdt = {"bf16": torch.bfloat16, "f32": torch.float32}[dtype]
+    rows = []
+    z = torch.randn(V) * 2
+    rows.append(z.clone())
+    r = z.clone(); r[17] = float("nan"); rows.append(r)               # NaN -> status 1
+    r = z.clone(); r[4000] = float("inf"); rows.append(r)             # +inf -> status 1
+    rows.append(torch.full((V,), float("-inf")))                      # all -inf -> 2
+    r = torch.full((V,), float("-inf")); r[1234] = 3.0; rows.append(r)  # one finite
+    r = torch.full((V,), float("-inf")); r[0] = 3.0; rows.append(r)
+    r = torch.full((V,), float("-inf")); r[V - 1] = 3.0; rows.append(r)
+    r = torch.full((V,), float("-inf")); r[9] = float("nan"); rows.append(r)  # NaN among -inf
+    rows.append(torch.zeros(V))                                       # uniform
+    rows.append(torch.full((V,), -0.0))
+    r = torch.zeros(V); r[::2] = -0.0; rows.append(r)                 # +-0 ties
+    r = z.clone(); r[100] = 50.0; r[4999] = 50.0; rows.append(r)     # top-1 tie at the ends
+    r = z.clone(); r[3] = 50.0; r[7] = 40.0; r[4998] = 40.0; rows.append(r)  # top-2 tie
+    r = torch.arange(V, dtype=torch.float32) * 1e-3; rows.append(r)  # ascending (slow path)
+    r = -torch.arange(V, dtype=torch.float32) * 1e-3; rows.append(r)  # descending
+    r = torch.full((V,), 1e-40); r[5] = 2e-40; r[6] = 2e-40; rows.append(r)  # subnormals
+    r = z.clone() * 1e30; rows.append(r)                              # huge magnitudes
+    r = torch.full((V,), -1e30); r[77] = -1e30 + 1e24; rows.append(r)
+    L = torch.stack(rows).to(tdt).to(DEV)
+    got, ref = _rows_check(relay, L, dtype, V)
+    assert got["status"].tolist()[:4] == [0, 1, 1, 2]
+    assert got["top1"][4] == 1234 and got["top2"][4] == 0 and got["margin"][4] == 1.0
+    assert got["margin"][8] == 0.0 and got["top1"][8] == 0 and got["top2"][8] == 1
+
+
+def test_margin_rows_temperature(relay):
+    L = synth.make_logits(64, 3000, "bf16", seed=5, device=DEV)
+    _rows_check(relay, L, "bf16", 3000, iota=1.0 / 0.6)
+
+
+def test_margin_rows_misaligned_base(relay):
+    """A view starting one element in: every row start is 2 bytes off 16."""
+    base = synth.make_logits(65, 2049, "bf16", seed=6, device=DEV)
+    flat = base.reshape(-1)[1:1 + 64 * 2049].reshape(64, 2049)
+    _rows_check(relay, flat, "bf16", 2049)
+
+
+def test_margin_rows_c1_full(relay):
+    """configs[0]: 2,048 x 32,000 fp32, every row against the oracle."""
+    cs = synth.make_cueset(32000, 3, 3)
+    ts = synth.make_tokens(1, 2048, cs)
+    L = synth.make_logits(2048, 32000, "f32", tokens=ts.tokens, device=DEV)
+    _rows_check(relay, L, "f32", 32000)
+
+
+def test_margin_rows_c2_sampled(relay):
+    """configs[1] launch shape (32,768 x 151,936 bf16): 192 sampled rows."""
+    cs = synth.make_cueset(151936, 8, 12)
+    ts = synth.make_tokens(1, 32768, cs)
+    L = synth.make_logits(32768, 151936, "bf16", tokens=ts.tokens, device=DEV, chunk_rows=2048)
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([rng.choice(32768, 190, replace=False), [0, 32767]]))
+    _rows_check(relay, L, "bf16", 151936, rows=torch.as_tensor(rows))
+    del L
+    torch.cuda.empty_cache()
+
+
+def test_margin_rows_deterministic(relay):
+    L = synth.make_logits(500, 151936, "bf16", seed=9, device=DEV)
+    a = relay.margin_rows(L)
+    b = relay.margin_rows(L)
+    torch.cuda.synchronize()
+    for k in a:
+        if a[k] is not None:
+            x, y = a[k], b[k]
+            if x.is_floating_point():
+                x, y = torch.nan_to_num(x, 7.0), torch.nan_to_num(y, 7.0)
+            assert torch.equal(x, y), k
+
+
+def test_margin_rows_invalid_args(relay):
+    L = torch.zeros((4, 1), device=DEV)
+    with pytest.raises(relay.RelayError):
+        relay.margin_rows(L)                       # vocab 1
+    L = torch.zeros((4, 8), device=DEV)
+    with pytest.raises(relay.RelayError):
+        relay.margin_rows(L, inv_temperature=0.0)
+    with pytest.raises(relay.RelayError):
+        relay.margin_rows(L, vocab=9)              # stride < vocab
+
+
+# ------------------------------------------------------------------ H2
+def _cs_pair(relay, vocab, n_cues, n_pat, max_len, seed, mode=0, **kw):
+    h = synth.make_cueset(vocab, n_cues, n_pat, max_len=max_len, seed=seed, **kw)
+    return h, relay.CueSet.from_synth(h, mode=mode)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("n_traj,traj_len,n_pat,max_len", [
+    (1, 2048, 3, 3), (3, 5000, 12, 3), (7, 333, 32, 6), (1, 1, 3, 2), (64, 1024, 32, 6)])
+def test_cue_scan(relay, mode, n_traj, traj_len, n_pat, max_len):
+    vocab = 151936
+    h, cs = _cs_pair(relay, vocab, min(n_pat, 8), n_pat, max_len, seed=n_pat * 7 + max_len, mode=mode)
+    ts = synth.make_tokens(n_traj, traj_len, h, seed=n_traj + traj_len, cue_rate=0.5)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    out = relay.cue_scan(cs, tok, offs)
+    torch.cuda.synchronize()
+    ref = oracle.cue_scan(ts.tokens, ts.traj_offsets, h.pat_tokens, h.pat_offsets, h.pat_cue,
+                          h.n_cues, h.terminator, mode)
+    n = int(out["n_occ"].item())
+    assert n == ref["occ_pos"].shape[0]
+    np.testing.assert_array_equal(out["occ_pos"][:n].cpu().numpy(), ref["occ_pos"])
+    np.testing.assert_array_equal(out["occ_pat"][:n].cpu().numpy(), ref["occ_pat"])
+    bits = out["term_bits"].cpu().numpy().view(np.uint32)
+    term = (bits[np.arange(ts.tokens.shape[0]) >> 5] >> (np.arange(ts.tokens.shape[0]) & 31)) & 1
+    np.testing.assert_array_equal(term.astype(np.uint8), ref["term"])
+
+
+def test_cue_scan_boundaries_and_empty_trajectories(relay):
+    """Patterns never cross a trajectory end; empty trajectories; positions
+    outside every trajectory never start an occurrence."""
+    h = synth.CueSet(np.array([5, 5, 6, 7], np.int32), np.array([0, 1, 3, 4], np.int32),
+                     np.array([0, 0, 1], np.int32), 2, 16, np.eye(16, dtype=np.uint8)[0])
+    cs = relay.CueSet.from_synth(h)
+    tokens = np.array([5, 6, 5, 5, 6, 7, 0, 5, 6, 5], np.int32)
+    for offs in ([0, 10], [0, 3, 3, 7, 10], [2, 5, 8], [0, 4, 5, 5, 9]):
+        offs = np.array(offs, np.int64)
+        out = relay.cue_scan(cs, torch.as_tensor(tokens, device=DEV), torch.as_tensor(offs, device=DEV))
+        torch.cuda.synchronize()
+        ref = oracle.cue_scan(tokens, offs, h.pat_tokens, h.pat_offsets, h.pat_cue, 2, h.terminator)
+        n = int(out["n_occ"].item())
+        assert out["occ_pos"][:n].tolist() == ref["occ_pos"].tolist()
+        assert out["occ_pat"][:n].tolist() == ref["occ_pat"].tolist()
+
+
+def test_cue_scan_capacity_overflow(relay):
+    h, cs = _cs_pair(relay, 4096, 3, 3, 2, seed=3)
+    ts = synth.make_tokens(1, 20000, h, cue_rate=0.9)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    full = relay.cue_scan(cs, tok)
+    torch.cuda.synchronize()
+    n = int(full["n_occ"].item())
+    cap = n // 3
+    part = relay.cue_scan(cs, tok, occ_capacity=cap)
+    torch.cuda.synchronize()
+    assert int(part["n_occ"].item()) == n          # true count reported
+    assert torch.equal(part["occ_pos"][:cap], full["occ_pos"][:cap])
+
+
+def test_cueset_rejects_bad_patterns(relay):
+    term = np.zeros(16, np.uint8)
+    with pytest.raises(relay.RelayError):   # duplicate
+        relay.CueSet([1, 2, 1, 2], [0, 2, 4], [0, 0], 1, term, 16)
+    with pytest.raises(relay.RelayError):   # token out of range
+        relay.CueSet([1, 99], [0, 2], [0], 1, term, 16)
+    with pytest.raises(relay.RelayError):   # empty pattern
+        relay.CueSet([1], [0, 0, 1], [0, 0], 1, term, 16)
+    with pytest.raises(relay.RelayError):   # too long
+        relay.CueSet(list(range(9)), [0, 9], [0], 1, term, 16)
+    with pytest.raises(relay.RelayError):   # cue id out of range
+        relay.CueSet([1], [0, 1], [3], 2, term, 16)
+
+
+# ---------------------------------------------------------------- H3-H7
+def _segment_case(relay, n_traj, traj_len, n_cues, n_pat, max_len, seed, think=False,
+                  nan_rate=0.0, mode=0, tau=0.5, world=1):
+    vocab = 151936
+    h, cs = _cs_pair(relay, vocab, n_cues, n_pat, max_len, seed=seed, mode=mode)
+    ts = synth.make_tokens(n_traj, traj_len, h, seed=seed + 1)
+    m = synth.make_margins(ts.tokens.shape[0], seed=seed + 2, nan_rate=nan_rate, tau=tau)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    tep = torch.as_tensor(ts.think_end_pos, device=DEV) if think else None
+    scan = relay.cue_scan(cs, tok, offs)
+    seg = relay.segment_reduce(cs, torch.as_tensor(m, device=DEV), scan, offs, tep, tau=tau)
+    torch.cuda.synchronize()
+    o_scan, o_win, o_sum = oracle.analyze(m, ts.tokens, ts.traj_offsets, h.pat_tokens,
+                                          h.pat_offsets, h.pat_cue, h.n_cues, h.terminator, tau=tau,
+                                          think_end_pos=ts.think_end_pos if think else None,
+                                          mode=mode, min_count=1)
+    return h, cs, ts, m, scan, seg, o_scan, o_win, o_sum
+
+
+def _compare_segments(relay, h, scan, seg, o_scan, o_win, o_sum, world=1, min_count=1):
+    n = int(scan["n_occ"].item())
+    assert n == o_scan["occ_pos"].shape[0]
+    np.testing.assert_array_equal(seg["seg_end"][:n].cpu().numpy(), o_win["seg_end"])
+    inv = o_win["seg_invalid"].astype(bool)
+    for k in ("seg_mean", "seg_min", "seg_lowfrac"):
+        got = seg[k][:n].cpu().numpy().astype(np.float64)
+        assert np.all(np.isnan(got[inv]))
+        err = np.abs(got[~inv] - o_win[k][~inv])
+        bar = 0.0 if k == "seg_min" else (1e-6 if k == "seg_mean" else 1e-7)
+        assert err.size == 0 or err.max() <= bar, (k, err.max())
+    fin = relay.stats_finalize(seg["stats"].cpu().numpy(), h.n_cues, world, min_count=min_count)
+    for c in range(h.n_cues + 1):
+        g, r = fin[c], o_sum[c]
+        assert g["n"] == r["n"] and g["n_invalid"] == r["n_invalid"], (c, g, r)
+        if c < h.n_cues:
+            assert g["n_triggers"] == r["n_triggers"], (c, g, r)
+        if r["n"] == 0:
+            continue
+        for f in ("mean", "token_mean", "min", "low_frac"):
+            assert abs(g[f] - r[f]) < TOL, (c, f, g[f], r[f])
+        if not np.isnan(r["std"]):
+            assert abs(g["std"] - r["std"]) < TOL and abs(g["se"] - r["se"]) < TOL, (c, g, r)
+        assert g["selected"] == r["selected"] or abs(
+            r["mean"] - (o_sum[-1]["mean"] + o_sum[-1]["se"])) < 2e-6, (c, g, r)
+    return fin
+
+
+@pytest.mark.parametrize("case", [
+    dict(n_traj=1, traj_len=2048, n_cues=3, n_pat=3, max_len=3, seed=1),
+    dict(n_traj=1, traj_len=32768, n_cues=8, n_pat=12, max_len=3, seed=2),
+    dict(n_traj=8, traj_len=4096, n_cues=8, n_pat=12, max_len=3, seed=3, think=True),
+    dict(n_traj=5, traj_len=3001, n_cues=6, n_pat=20, max_len=6, seed=4, nan_rate=0.002),
+    dict(n_traj=3, traj_len=2500, n_cues=4, n_pat=9, max_len=4, seed=5, mode=1),
+    dict(n_traj=64, traj_len=700, n_cues=32, n_pat=32, max_len=6, seed=6, think=True),
+])
+def test_segment_reduce(relay, case):
+    h, cs, ts, m, scan, seg, o_scan, o_win, o_sum = _segment_case(relay, **case)
+    _compare_segments(relay, h, scan, seg, o_scan, o_win, o_sum)
+
+
+def test_segment_reduce_golden_trace(relay, golden_dir):
+    import json
+    import os
+    g = json.load(open(os.path.join(golden_dir, "trace_fixture.json")))
+    pats = g["patterns"]
+    po = np.zeros(len(pats) + 1, np.int32)
+    po[1:] = np.cumsum([len(p) for p in pats])
+    term = np.zeros(g["vocab"], np.uint8)
+    term[g["terminator_ids"]] = 1
+    cs = relay.CueSet([t for p in pats for t in p], po, g["pat_cue"], g["n_cues"], term, g["vocab"])
+    tok = torch.as_tensor(np.array(g["tokens"], np.int32), device=DEV)
+    offs = torch.as_tensor(np.array(g["traj_offsets"], np.int64), device=DEV)
+    scan = relay.cue_scan(cs, tok, offs)
+    seg = relay.segment_reduce(cs, torch.as_tensor(np.array(g["margins"], np.float32), device=DEV),
+                               scan, offs, tau=g["tau"])
+    torch.cuda.synchronize()
+    n = int(scan["n_occ"].item())
+    assert scan["occ_pos"][:n].tolist() == [o["s"] for o in g["occurrences"]]
+    assert seg["seg_end"][:n].tolist() == [o["e"] for o in g["occurrences"]]
+    fin = relay.stats_finalize(seg["stats"].cpu().numpy(), 2, 1, min_count=1)
+    for c, e in enumerate(g["cues"]):
+        assert fin[c]["n"] == e["n"] and fin[c]["n_triggers"] == e["n_triggers"]
+        for f in ("mean", "std", "se", "token_mean", "min", "low_frac"):
+            assert abs(fin[c][f] - e[f]) < TOL
+    assert [f["selected"] for f in fin[:2]] == g["selected_rule0_min_count_1"]
+
+
+def test_stats_table_rank_split_is_bit_identical(relay):
+    """H6: two ranks each reduce half of the trajectories into their own
+    table; the element-wise sum equals the one-rank table (min slots aside)
+    and finalizes identically — the property the NCCL sum relies on."""
+    vocab = 151936
+    h, cs = _cs_pair(relay, vocab, 8, 12, 3, seed=21)
+    ts = synth.make_tokens(8, 4096, h, seed=22)
+    m = torch.as_tensor(synth.make_margins(ts.tokens.shape[0], seed=23), device=DEV)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    one = relay.segment_reduce(cs, m, relay.cue_scan(cs, tok, offs), offs)["stats"]
+    tabs = []
+    for r in range(2):
+        lo, hi = r * 4 * 4096, (r + 1) * 4 * 4096
+        o2 = torch.as_tensor(ts.traj_offsets[4 * r:4 * r + 5] - lo, device=DEV)
+        sc = relay.cue_scan(cs, tok[lo:hi].contiguous(), o2)
+        st = relay.new_stats(8, r, 2, DEV)
+        relay.segment_reduce(cs, m[lo:hi].contiguous(), sc, o2, stats=st, rank=r, world_size=2)
+        tabs.append(st)
+    torch.cuda.synchronize()
+    tot = (tabs[0] + tabs[1]).cpu().numpy().reshape(9, 10)
+    base = one.cpu().numpy().reshape(9, 9)
+    np.testing.assert_array_equal(tot[:, :8], base[:, :8])
+    np.testing.assert_array_equal(np.minimum(tot[:, 8], tot[:, 9]), base[:, 8])
+    f1 = relay.stats_finalize(base.reshape(-1), 8, 1, 1)
+    f2 = relay.stats_finalize(tot.reshape(-1), 8, 2, 1)
+    assert f1 == f2
+
+
+def test_segment_reduce_deterministic(relay):
+    args = dict(n_traj=8, traj_len=4096, n_cues=8, n_pat=12, max_len=3, seed=31)
+    a = _segment_case(relay, **args)
+    b = _segment_case(relay, **args)
+    assert torch.equal(a[5]["stats"], b[5]["stats"])
+    assert torch.equal(a[5]["seg_end"], b[5]["seg_end"])
+
+
+def test_analyzer_end_to_end_small(relay):
+    """H1 -> H2 -> H3..H7 through the Analyzer vs the oracle on its own margins:
+    exact structure, statistics within 1e-5 (low counts within the +-1e-5 band)."""
+    h, cs = _cs_pair(relay, 4096, 3, 4, 3, seed=41)
+    ts = synth.make_tokens(2, 1500, h, seed=42)
+    n = ts.tokens.shape[0]
+    L = synth.make_logits(n, 4096, "bf16", tokens=ts.tokens, seed=43, device=DEV)
+    an = relay.Analyzer(cs, n, 4096, DEV)
+    stats = an.run(L, torch.as_tensor(ts.tokens, device=DEV), torch.as_tensor(ts.traj_offsets, device=DEV))
+    torch.cuda.synchronize()
+    ref = oracle.margin_rows(synth.host_rows(L, "bf16"), dtype="bf16", threads=8)
+    m64 = ref["margin"]
+    got_m = an.rows["margin"].cpu().numpy()
+    ok = ref["status"] == 0
+    assert np.abs(got_m[ok] - m64[ok]).max() < TOL
+    o_scan, o_win, o_sum = oracle.analyze(m64.astype(np.float32), ts.tokens, ts.traj_offsets,
+                                          h.pat_tokens, h.pat_offsets, h.pat_cue, h.n_cues,
+                                          h.terminator, min_count=1)
+    fin = relay.stats_finalize(stats.cpu().numpy(), h.n_cues, 1, 1)
+    for c in range(h.n_cues + 1):
+        assert fin[c]["n"] == o_sum[c]["n"]
+        if o_sum[c]["n"]:
+            assert abs(fin[c]["mean"] - o_sum[c]["mean"]) < TOL
+            assert abs(fin[c]["token_mean"] - o_sum[c]["token_mean"]) < TOL
+    # low-margin fraction: counts may only differ for margins within 1e-5 of tau
+    band = np.sum(np.abs(m64[ok] - 0.5) < TOL)
+    assert abs(fin[-1]["low_frac"] - o_sum[-1]["low_frac"]) * fin[-1]["n"] <= band + 1e-9
+
+
+# ------------------------------------------------------------------ H8
+def _step_reference(h, lg_host, dtype, vocab, state, hist, small_run, sampled, gate, max_seg):
+    ref = oracle.margin_rows(lg_host, dtype=dtype, vocab=vocab)
+    B = state.shape[0]
+    flags, cues = np.zeros(B, np.uint8), np.zeros(B, np.int16)
+    st2, hi2, sr2 = state.copy(), hist.copy(), small_run.copy()
+    for b in range(B):
+        tok = int(sampled[b]) if sampled is not None else int(ref["top1"][b])
+        f, c, s, hh, r = oracle.step_one(tok, np.float32(ref["margin"][b]), int(state[b]), hist[b],
+                                         int(small_run[b]), h.pat_tokens, h.pat_offsets, h.pat_cue,
+                                         h.terminator, h.think_end, gate, max_seg)
+        flags[b], cues[b], st2[b], hi2[b], sr2[b] = f, c, s, hh, r
+    return ref, flags, cues, st2, hi2, sr2
+
+
+@pytest.mark.parametrize("greedy", [False, True])
+@pytest.mark.parametrize("B,vocab,dtype,max_seg,gate", [
+    (256, 152064, "bf16", 0, -1.0), (37, 5003, "f16", 3, -1.0), (64, 32000, "f32", 0, 0.5)])
+def test_step_switch(relay, greedy, B, vocab, dtype, max_seg, gate):
+    h, cs = _cs_pair(relay, vocab, 8, 12, 3, seed=51)
+    rng = np.random.default_rng(52)
+    state = rng.choice([0, 0, 1, 3], B).astype(np.uint8)
+    hist = np.full((B, 7), -1, np.int32)
+    small_run = rng.integers(0, 4, B).astype(np.int32)
+    sampled = rng.integers(3000, vocab, B).astype(np.int32)
+    for b in range(B):                       # plant cue completions, terminators, </think>
+        kind = rng.integers(0, 5)
+        p = h.patterns[int(rng.integers(0, len(h.patterns)))]
+        hist[b, 7 - (len(p) - 1):] = p[:-1] if len(p) > 1 else hist[b, 7:]
+        if kind == 0:
+            sampled[b] = p[-1]
+        elif kind == 1:
+            sampled[b] = int(rng.choice(synth.TERMINATOR_IDS))
+        elif kind == 2:
+            sampled[b] = h.think_end
+    tokens = None if greedy else sampled
+    L = synth.make_logits(B, vocab, dtype, tokens=sampled, seed=53, device=DEV)
+    ref, flags, cues, st2, hi2, sr2 = _step_reference(h, synth.host_rows(L, dtype), dtype, vocab,
+                                                      state, hist, small_run, tokens, gate, max_seg)
+    d_state = torch.as_tensor(state, device=DEV)
+    d_hist = torch.as_tensor(hist, device=DEV)
+    d_sr = torch.as_tensor(small_run, device=DEV)
+    d_samp = None if greedy else torch.as_tensor(sampled, device=DEV)
+    out = relay.step_switch(cs, L, d_state, d_hist, d_sr, d_samp, margin_gate=gate,
+                            max_small_segment=max_seg)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out["top1"].cpu().numpy(), ref["top1"])
+    np.testing.assert_array_equal(out["top2"].cpu().numpy(), ref["top2"])
+    ok = ref["status"] == 0
+    assert np.abs(out["margin"].cpu().numpy()[ok] - ref["margin"][ok]).max() < TOL
+    got_flags = out["flag"].cpu().numpy()
+    if gate >= 0:   # the gate decision may only differ within 1e-5 of the gate
+        near = np.abs(ref["margin"] - gate) < TOL
+        keep = ~near
+    else:
+        keep = np.ones(B, bool)
+    np.testing.assert_array_equal(got_flags[keep], flags[keep])
+    np.testing.assert_array_equal(out["cue_id"].cpu().numpy()[keep], cues[keep])
+    np.testing.assert_array_equal(d_state.cpu().numpy()[keep], st2[keep])
+    np.testing.assert_array_equal(d_hist.cpu().numpy()[keep], hi2[keep])
+    np.testing.assert_array_equal(d_sr.cpu().numpy()[keep], sr2[keep])
+    assert (got_flags == 1).sum() > 0 or greedy
+
+
+def test_step_switch_graph_replay(relay):
+    """Captured in a CUDA graph and replayed: the arrival counters reset
+    themselves; replaying a token stream matches the oracle step by step."""
+    vocab, B, T = 8192, 16, 40
+    h, cs = _cs_pair(relay, vocab, 4, 6, 3, seed=61)
+    rng = np.random.default_rng(62)
+    ts = synth.make_tokens(B, T, h, seed=63, cue_rate=0.6, mean_sentence=4)
+    toks = ts.tokens.reshape(B, T)
+    L = synth.make_logits(B, vocab, "bf16", seed=64, device=DEV)
+    d_state = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    d_hist = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    d_sr = torch.zeros(B, dtype=torch.int32, device=DEV)
+    d_samp = torch.zeros(B, dtype=torch.int32, device=DEV)
+    ws = relay.workspace(0, 0, B, DEV)
+    out = relay.step_switch(cs, L, d_state, d_hist, d_sr, d_samp, ws=ws)   # warm-up allocs
+    d_state.zero_(); d_hist.fill_(-1); d_sr.zero_()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            relay.step_switch(cs, L, d_state, d_hist, d_sr, d_samp, ws=ws, out=out)
+    torch.cuda.synchronize()
+    state = np.zeros(B, np.uint8); hist = np.full((B, 7), -1, np.int32); sr = np.zeros(B, np.int32)
+    ref = oracle.margin_rows(synth.host_rows(L, "bf16"), dtype="bf16")
+    for t in range(T):
+        d_samp.copy_(torch.as_tensor(toks[:, t], device=DEV))
+        g.replay()
+        torch.cuda.synchronize()
+        for b in range(B):
+            f, c, state[b], hist[b], sr[b] = oracle.step_one(
+                int(toks[b, t]), np.float32(ref["margin"][b]), int(state[b]), hist[b], int(sr[b]),
+                h.pat_tokens, h.pat_offsets, h.pat_cue, h.terminator, h.think_end)
+            assert out["flag"][b].item() == f and out["cue_id"][b].item() == c
+        np.testing.assert_array_equal(d_state.cpu().numpy(), state)
+        np.testing.assert_array_equal(d_hist.cpu().numpy(), hist)
+    del rng

@@ -2,21 +2,31 @@
 //
 // One streaming pass over each logit row (§3.2): online max with a
 // lazily raised exp reference, the softmax normaliser in fp32 (MUFU.EX2 via
-// ex2.approx, FFMA2/FADD2 pairs), and the exact top-2 (value desc, index asc)
-// with a CTA-shared threshold so that only vectors that can still enter the
-// row's top-2 take the exact per-element path.
-// HBM-bound: algorithmic bytes = vocab * sizeof(elem) per row; no tensor cores
-// (this is a scan, not a contraction).
+// ex2.approx; FFMA2/FADD2 on element pairs), and the exact top-2 (value desc,
+// index asc) behind a CTA-shared threshold so that only vector groups that
+// can still enter the row's top-2 take the exact per-element path
+// (DESIGN.md §6).  HBM-bound: algorithmic bytes = vocab * sizeof(elem) per row.
+// No tensor cores: this is a scan, not a contraction.
+//
+// K1 is a persistent warp-specialised kernel: one producer warp streams row
+// bodies into a shared-memory ring with 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx), 8 consumer warps reduce them.
+// The ring runs across row boundaries, so a row's epilogue overlaps the next
+// row's loads.  K4 splits rows into chunks (LDG path) with a last-arriver
+// combine, then runs RelayGen's switch state machine on-device.
 #include "relay_device.cuh"
 #include "relay_internal.h"
 
 namespace relay {
+
+constexpr float kHuge = 268435456.0f;  // 2^28: beyond it fp32 y = z*c is too coarse
 
 struct ThreadState {
   Top2 t;
   float g2;    // own skip guard: NaN until t.i2 holds a real index, then t.v2
   float mref;  // exp reference in the y = z*c domain (never above the row max)
   float acc[4];
+  int huge;
 };
 
 __device__ __forceinline__ void state_init(ThreadState& st) {
@@ -25,18 +35,20 @@ __device__ __forceinline__ void state_init(ThreadState& st) {
   st.mref = -FLT_MAX;
 #pragma unroll
   for (int k = 0; k < 4; k++) st.acc[k] = 0.0f;
+  st.huge = 0;
 }
 
 __device__ __forceinline__ void rescale(ThreadState& st, float ymax) {
   if (ymax > st.mref + kSlack) {
-    float r = ex2(st.mref - ymax);
+    if (fabsf(ymax) >= kHuge) st.huge = 1;
+    const float r = ex2(st.mref - ymax);
 #pragma unroll
     for (int k = 0; k < 4; k++) st.acc[k] *= r;
     st.mref = ymax;
   }
 }
 
-// Exact path for one element (head/tail of a misaligned range).
+// Exact path for one element (misaligned head/tail of a row range).
 __device__ __forceinline__ void consume_scalar(float x, int j, ThreadState& st, float c) {
   top2_push(st.t, x, j);
   st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
@@ -44,133 +56,360 @@ __device__ __forceinline__ void consume_scalar(float x, int j, ThreadState& st, 
   st.acc[0] += ex2(fmaf(x, c, -st.mref));
 }
 
-// One vector of VEC consecutive elements starting at index j0.
-template <int VEC>
-__device__ __forceinline__ void consume_vec(const float (&f)[VEC], int j0, ThreadState& st,
-                                            float c, float theta, bool& slow) {
-  float vmax = f[0];
+// A group of U vectors of VEC consecutive elements; vector u starts at index
+// j0[u] and the groups of one thread are visited in increasing index order.
+// The top-2 guard and the exp-reference check are hoisted to the group max.
+template <int U, int VEC>
+__device__ __forceinline__ void consume_group(const float (&f)[U][VEC], const int (&j0)[U],
+                                              ThreadState& st, float c, float theta, bool& slow) {
+  float vm[U];
 #pragma unroll
-  for (int k = 1; k < VEC; k++) vmax = fmaxf(vmax, f[k]);
-  // A vector can change the row's top-2 only if it holds a value >= theta
-  // (theta <= the row's 2nd-best value) and one that beats this thread's own
-  // 2nd-best (indices only grow along a thread's walk).
-  bool s = (vmax >= theta) && !(vmax <= st.g2);
-  if (s) {
+  for (int u = 0; u < U; u++) {
+    float m = f[u][0];
 #pragma unroll
-    for (int k = 0; k < VEC; k++) top2_push(st.t, f[k], j0 + k);
-    st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
+    for (int k = 1; k < VEC; k++) m = fmaxf(m, f[u][k]);
+    vm[u] = m;
   }
-  slow |= s;
-  rescale(st, vmax * c);
+  float gm = vm[0];
+#pragma unroll
+  for (int u = 1; u < U; u++) gm = fmaxf(gm, vm[u]);
+  // A vector can change the row's top-2 only if it holds a value >= theta
+  // (theta <= the row's 2nd-best value) that also beats this thread's own
+  // 2nd-best (indices only grow along a thread's walk).
+  if (gm >= theta && !(gm <= st.g2)) {
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (vm[u] >= theta && !(vm[u] <= st.g2)) {
+#pragma unroll
+        for (int k = 0; k < VEC; k++) top2_push(st.t, f[u][k], j0[u] + k);
+        st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
+      }
+    }
+    slow = true;
+  }
+  rescale(st, gm * c);
   const float2 cc = make_float2(c, c);
   const float2 nm = make_float2(-st.mref, -st.mref);
 #pragma unroll
-  for (int k = 0; k < VEC; k += 2) {
-    float2 y = __ffma2_rn(make_float2(f[k], f[k + 1]), cc, nm);
-    float2 e = make_float2(ex2(y.x), ex2(y.y));
-    const int a = ((k >> 1) & 1) * 2;
-    float2 acc = __fadd2_rn(make_float2(st.acc[a], st.acc[a + 1]), e);
-    st.acc[a] = acc.x;
-    st.acc[a + 1] = acc.y;
+  for (int u = 0; u < U; u++) {
+#pragma unroll
+    for (int k = 0; k < VEC; k += 2) {
+      const float2 y = __ffma2_rn(make_float2(f[u][k], f[u][k + 1]), cc, nm);
+      const float2 e = make_float2(ex2(y.x), ex2(y.y));
+      const int a = (((u * VEC + k) >> 1) & 1) * 2;
+      const float2 s = __fadd2_rn(make_float2(st.acc[a], st.acc[a + 1]), e);
+      st.acc[a] = s.x;
+      st.acc[a + 1] = s.y;
+    }
   }
 }
 
-template <class E, int VB>
-struct Vec;
+// The warp's two best values bound the row's 2nd-best from below: raise theta.
+__device__ __forceinline__ void warp_raise_theta(const ThreadState& st, int* s_theta) {
+  float a = st.t.v1, b = st.t.v2;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float oa = __shfl_xor_sync(kFull, a, off);
+    const float ob = __shfl_xor_sync(kFull, b, off);
+    b = fmaxf(fminf(a, oa), fmaxf(b, ob));
+    a = fmaxf(a, oa);
+  }
+  if ((threadIdx.x & 31) == 0 && b > unkey(*reinterpret_cast<volatile int*>(s_theta)))
+    atomicMax(s_theta, fkey(b));
+}
 
-template <class E>
-struct Vec<E, 16> {
-  using Raw = uint4;
-  static constexpr int N = 16 / E::SZ;
-  __device__ static __forceinline__ Raw load(const char* p) { return ldg_stream16(p); }
-  __device__ static __forceinline__ void unpack(const Raw& r, float (&f)[N]) {
-    if constexpr (E::SZ == 4) {
-      f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
-      f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
-    } else {
-      E::unpack2(r.x, f[0], f[1]); E::unpack2(r.y, f[2], f[3]);
-      E::unpack2(r.z, f[4], f[5]); E::unpack2(r.w, f[6], f[7]);
-    }
+template <class E, int VEC>
+__device__ __forceinline__ void unpack16(const uint4& r, float (&f)[VEC]) {
+  if constexpr (E::SZ == 4) {
+    f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
+    f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
+  } else {
+    E::unpack2(r.x, f[0], f[1]); E::unpack2(r.y, f[2], f[3]);
+    E::unpack2(r.z, f[4], f[5]); E::unpack2(r.w, f[6], f[7]);
   }
-};
-
-template <class E>
-struct Vec<E, 32> {
-  using Raw = U8x32;
-  static constexpr int N = 32 / E::SZ;
-  __device__ static __forceinline__ Raw load(const char* p) { return ldg_stream32(p); }
-  __device__ static __forceinline__ void unpack(const Raw& r, float (&f)[N]) {
-    if constexpr (E::SZ == 4) {
-#pragma unroll
-      for (int k = 0; k < 8; k++) f[k] = __uint_as_float(r.w[k]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; k++) E::unpack2(r.w[k], f[2 * k], f[2 * k + 1]);
-    }
-  }
-};
-
-// Stream elements [j0, j1) of one row through this CTA (all threads call).
-template <class E, int VB, int THREADS, int U>
-__device__ __forceinline__ void stream_range(const typename E::T* __restrict__ row, int j0, int j1,
-                                             float c, ThreadState& st, int* s_theta) {
-  using V = Vec<E, VB>;
-  constexpr int VEC = V::N;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const uintptr_t addr = reinterpret_cast<uintptr_t>(row + j0);
-  int head = static_cast<int>(((VB - (addr & (VB - 1))) & (VB - 1)) / E::SZ);
-  if (head > j1 - j0) head = j1 - j0;
-  if (tid < head) consume_scalar(E::load1(row + j0 + tid), j0 + tid, st, c);
-  const int jb = j0 + head;
-  const int nvec = (j1 - jb) / VEC;
-  const char* vbase = reinterpret_cast<const char*>(row + jb);
-  // main loop: warp-uniform bound so the vote below sees all 32 lanes
-  int wv = tid - lane;
-  for (; wv + 31 + (U - 1) * THREADS < nvec; wv += U * THREADS) {
-    const int v = wv + lane;
-    typename V::Raw raw[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) raw[u] = V::load(vbase + static_cast<size_t>(v + u * THREADS) * VB);
-    const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
-    bool slow = false;
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      float f[VEC];
-      V::unpack(raw[u], f);
-      consume_vec<VEC>(f, jb + (v + u * THREADS) * VEC, st, c, theta, slow);
-    }
-    if (__any_sync(kFull, slow)) {
-      // the warp's two best values bound the row's 2nd-best from below
-      float a = st.t.v1, b = st.t.v2;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        float oa = __shfl_xor_sync(kFull, a, off);
-        float ob = __shfl_xor_sync(kFull, b, off);
-        b = fmaxf(fminf(a, oa), fmaxf(b, ob));
-        a = fmaxf(a, oa);
-      }
-      if (lane == 0 && b > unkey(*reinterpret_cast<volatile int*>(s_theta))) atomicMax(s_theta, fkey(b));
-    }
-  }
-  for (int v = wv + lane; v < nvec; v += THREADS) {
-    typename V::Raw raw = V::load(vbase + static_cast<size_t>(v) * VB);
-    const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
-    bool slow = false;
-    float f[VEC];
-    V::unpack(raw, f);
-    consume_vec<VEC>(f, jb + v * VEC, st, c, theta, slow);
-  }
-  const int jt = jb + nvec * VEC;
-  if (tid < j1 - jt) consume_scalar(E::load1(row + jt + tid), jt + tid, st, c);
 }
 
 __device__ __forceinline__ Partial thread_partial(const ThreadState& st) {
-  return Partial{st.t, Norm{st.mref, (st.acc[0] + st.acc[1]) + (st.acc[2] + st.acc[3])}};
+  return Partial{st.t, Norm{st.mref, (st.acc[0] + st.acc[1]) + (st.acc[2] + st.acc[3])}, st.huge};
 }
 
 __device__ __forceinline__ Partial partial_empty() {
-  return Partial{top2_empty(), Norm{-FLT_MAX, 0.0f}};
+  return Partial{top2_empty(), Norm{-FLT_MAX, 0.0f}, 0};
+}
+
+// Row geometry: `head` scalar elements up to the first 16-byte boundary, a
+// 16-byte-aligned body, then scalar tail elements from `tail`.
+struct Geom {
+  int head;
+  long long body;  // bytes, multiple of 16
+  int tail;
+};
+
+template <class E>
+__device__ __forceinline__ Geom row_geom(const typename E::T* row, int j0, int j1) {
+  Geom g;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(row + j0);
+  int head = static_cast<int>(((16 - (a & 15)) & 15) / E::SZ);
+  if (head > j1 - j0) head = j1 - j0;
+  g.head = head;
+  g.body = (static_cast<long long>(j1 - j0 - head) * E::SZ) & ~15LL;
+  g.tail = j0 + head + static_cast<int>(g.body / E::SZ);
+  return g;
+}
+
+// Exact normaliser pass for rows flagged huge: S = sum_j 2^((z_j - z1) c),
+// the difference taken first (exact near the maximum by Sterbenz).
+template <class E>
+__device__ __forceinline__ float exact_sum_thread(const typename E::T* row, int vocab, float z1,
+                                                  float c, int tid, int nthreads) {
+  float s = 0.0f;
+  for (int j = tid; j < vocab; j += nthreads) {
+    const float z = E::load1(row + j);
+    s += ex2((z - z1) * c);
+  }
+  return s;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+  return v;
+}
+
+// ------------------------------------------------------------------- K1
+template <class E, int NCW, int NS, int SB>
+__global__ void __launch_bounds__((NCW + 1) * 32)
+    margin_rows_tma_kernel(const typename E::T* __restrict__ logits, long long n_rows, int vocab,
+                           long long stride, float c, float iota, float* __restrict__ margin,
+                           int* __restrict__ top1, int* __restrict__ top2, float* __restrict__ lse,
+                           uint8_t* __restrict__ status) {
+  using T = typename E::T;
+  constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
+  constexpr int NCT = NCW * 32;             // consumer threads
+  constexpr int U = SB / 16 / NCT;          // vectors per consumer thread per full stage
+  static_assert(U >= 1 && U * NCT * 16 == SB, "stage must split evenly");
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[NS];
+  __shared__ __align__(8) uint64_t empty[NS];
+  __shared__ int s_theta[2];
+  __shared__ Partial s_red[2][NCW];
+  __shared__ float s_sum[2][NCW];
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NS; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    s_theta[0] = s_theta[1] = fkey(-INFINITY);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == NCW) {
+    // ------------------------------------------------ producer warp
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long r = blockIdx.x; r < n_rows; r += gridDim.x) {
+        const T* row = logits + r * stride;
+        const Geom g = row_geom<E>(row, 0, vocab);
+        const char* src = reinterpret_cast<const char*>(row + g.head);
+        for (long long off = 0; off < g.body; off += SB) {
+          const uint32_t bytes = static_cast<uint32_t>(g.body - off < SB ? g.body - off : SB);
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], bytes);
+          bulk_g2s(ring + static_cast<size_t>(stage) * SB, src + off, bytes, &full[stage], pol);
+          if (++stage == NS) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumer warps
+  int stage = 0;
+  uint32_t phase = 0;
+  int it = 0;
+  for (long long r = blockIdx.x; r < n_rows; r += gridDim.x, ++it) {
+    int* theta_p = &s_theta[it & 1];
+    const T* row = logits + r * stride;
+    const Geom g = row_geom<E>(row, 0, vocab);
+    ThreadState st;
+    state_init(st);
+    if (tid < g.head) consume_scalar(E::load1(row + tid), tid, st, c);
+    for (long long off = 0; off < g.body; off += SB) {
+      const int bytes = static_cast<int>(g.body - off < SB ? g.body - off : SB);
+      const int jb = g.head + static_cast<int>(off / E::SZ);
+      mbar_wait(&full[stage], phase);
+      const unsigned char* buf = ring + static_cast<size_t>(stage) * SB;
+      const float theta = unkey(*reinterpret_cast<volatile int*>(theta_p));
+      bool slow = false;
+      if (bytes == SB) {
+        uint4 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) raw[u] = lds128(buf + (tid + u * NCT) * 16);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);  // release orders the loads above
+        float f[U][VEC];
+        int j0[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          unpack16<E, VEC>(raw[u], f[u]);
+          j0[u] = jb + (tid + u * NCT) * VEC;
+        }
+        consume_group<U, VEC>(f, j0, st, c, theta, slow);
+      } else {
+        const int nvec = bytes / 16;
+        for (int v = tid; v < nvec; v += NCT) {
+          float f[1][VEC];
+          const int j0[1] = {jb + v * VEC};
+          unpack16<E, VEC>(lds128(buf + v * 16), f[0]);
+          consume_group<1, VEC>(f, j0, st, c, theta, slow);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      }
+      if (__any_sync(kFull, slow)) warp_raise_theta(st, theta_p);
+      if (++stage == NS) { stage = 0; phase ^= 1; }
+    }
+    if (tid < vocab - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
+
+    // ------------------------------------------------ row epilogue
+    Partial p = warp_reduce_partial(thread_partial(st));
+    if (lane == 0) s_red[it & 1][warp] = p;
+    if (tid == 0) s_theta[(it + 1) & 1] = fkey(-INFINITY);
+    named_bar(1, NCT);
+    // s_red[it & 1] is rewritten only after the next row's barrier, which
+    // every warp reaches after this read, so the decision is uniform.
+    if (__any_sync(kFull, lane < NCW && s_red[it & 1][lane].huge)) {
+      // rare: every consumer joins an exact second pass over the row
+      Partial q = lane < NCW ? s_red[it & 1][lane] : partial_empty();
+      q = warp_reduce_partial(q);
+      float s = warp_sum(exact_sum_thread<E>(row, vocab, q.t.v1, c, tid, NCT));
+      if (lane == 0) s_sum[it & 1][warp] = s;
+      named_bar(1, NCT);
+      if (tid == 0) {
+        float S = 0.0f;
+        for (int w = 0; w < NCW; w++) S += s_sum[it & 1][w];
+        const RowOut o = finish_row(q, c, iota, S);
+        margin[r] = o.margin;
+        if (top1) top1[r] = o.i1;
+        if (top2) top2[r] = o.i2;
+        if (lse) lse[r] = o.lse;
+        if (status) status[r] = static_cast<uint8_t>(o.status);
+      }
+    } else if (warp == 0) {
+      Partial q = lane < NCW ? s_red[it & 1][lane] : partial_empty();
+      q = warp_reduce_partial(q);
+      if (lane == 0) {
+        const RowOut o = finish_row(q, c, iota);
+        margin[r] = o.margin;
+        if (top1) top1[r] = o.i1;
+        if (top2) top2[r] = o.i2;
+        if (lse) lse[r] = o.lse;
+        if (status) status[r] = static_cast<uint8_t>(o.status);
+      }
+    }
+  }
+}
+
+static int g_num_sms = 0;
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+constexpr int kNCW = 8;        // consumer warps per CTA
+constexpr int kStages = 6;     // ring depth
+constexpr int kStageBytes = 16384;
+
+template <class E>
+static cudaError_t launch_rows_t(const void* logits, long long n_rows, int vocab, long long stride,
+                                 float iota, float* margin, int* top1, int* top2, float* lse,
+                                 uint8_t* status, cudaStream_t st) {
+  auto kern = margin_rows_tma_kernel<E, kNCW, kStages, kStageBytes>;
+  const int smem = kStages * kStageBytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  long long grid = static_cast<long long>(per_sm) * num_sms();
+  if (grid > n_rows) grid = n_rows;
+  kern<<<static_cast<unsigned>(grid), (kNCW + 1) * 32, smem, st>>>(
+      static_cast<const typename E::T*>(logits), n_rows, vocab, stride, iota * kLog2e, iota, margin,
+      top1, top2, lse, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_margin_rows(const void* logits, int dt, long long n_rows, int vocab,
+                               long long stride, float iota, float* margin, int* top1, int* top2,
+                               float* lse, uint8_t* status, cudaStream_t st) {
+  if (n_rows <= 0) return cudaSuccess;
+  switch (dt) {
+    case 0:
+      return launch_rows_t<EBf16>(logits, n_rows, vocab, stride, iota, margin, top1, top2, lse, status, st);
+    case 1:
+      return launch_rows_t<EF16>(logits, n_rows, vocab, stride, iota, margin, top1, top2, lse, status, st);
+    default:
+      return launch_rows_t<EF32>(logits, n_rows, vocab, stride, iota, margin, top1, top2, lse, status, st);
+  }
+}
+
+// ------------------------------------------------------------------- K4
+// Stream elements [j0, j1) of one row through this CTA with 16-byte loads.
+template <class E, int THREADS, int U>
+__device__ __forceinline__ void stream_range_ldg(const typename E::T* __restrict__ row, int j0, int j1,
+                                                 float c, ThreadState& st, int* s_theta) {
+  constexpr int VEC = 16 / E::SZ;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const Geom g = row_geom<E>(row, j0, j1);
+  if (tid < g.head) consume_scalar(E::load1(row + j0 + tid), j0 + tid, st, c);
+  const int jb = j0 + g.head;
+  const int nvec = static_cast<int>(g.body / 16);
+  const char* vbase = reinterpret_cast<const char*>(row + jb);
+  int wv = tid - lane;  // warp-uniform bound so the vote sees all 32 lanes
+  for (; wv + 31 + (U - 1) * THREADS < nvec; wv += U * THREADS) {
+    const int v = wv + lane;
+    uint4 raw[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) raw[u] = ldg_stream16(vbase + static_cast<size_t>(v + u * THREADS) * 16);
+    const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
+    bool slow = false;
+    float f[U][VEC];
+    int jj[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      unpack16<E, VEC>(raw[u], f[u]);
+      jj[u] = jb + (v + u * THREADS) * VEC;
+    }
+    consume_group<U, VEC>(f, jj, st, c, theta, slow);
+    if (__any_sync(kFull, slow)) warp_raise_theta(st, s_theta);
+  }
+  for (int v = wv + lane; v < nvec; v += THREADS) {
+    const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
+    bool slow = false;
+    float f[1][VEC];
+    const int jj[1] = {jb + v * VEC};
+    unpack16<E, VEC>(ldg_stream16(vbase + static_cast<size_t>(v) * 16), f[0]);
+    consume_group<1, VEC>(f, jj, st, c, theta, slow);
+  }
+  if (tid < j1 - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
 }
 
 template <int THREADS>
@@ -184,86 +423,9 @@ __device__ __forceinline__ Partial block_reduce(Partial p, Partial* s_red) {
     p = lane < NW ? s_red[lane] : partial_empty();
     p = warp_reduce_partial(p);
   }
-  return p;  // valid in thread 0
+  return p;  // valid in warp 0
 }
 
-// ------------------------------------------------------------------- K1
-template <class E, int VB, int THREADS, int U>
-__global__ void __launch_bounds__(THREADS)
-    margin_rows_kernel(const typename E::T* __restrict__ logits, long long n_rows, int vocab,
-                       long long stride, float c, float iota, float* __restrict__ margin,
-                       int* __restrict__ top1, int* __restrict__ top2, float* __restrict__ lse,
-                       uint8_t* __restrict__ status) {
-  __shared__ int s_theta;
-  __shared__ Partial s_red[THREADS / 32];
-  for (long long r = blockIdx.x; r < n_rows; r += gridDim.x) {
-    if (threadIdx.x == 0) s_theta = fkey(-INFINITY);
-    __syncthreads();
-    ThreadState st;
-    state_init(st);
-    stream_range<E, VB, THREADS, U>(logits + r * stride, 0, vocab, c, st, &s_theta);
-    Partial p = block_reduce<THREADS>(thread_partial(st), s_red);
-    if (threadIdx.x == 0) {
-      RowOut o = finish_row(p, c, iota);
-      margin[r] = o.margin;
-      if (top1) top1[r] = o.i1;
-      if (top2) top2[r] = o.i2;
-      if (lse) lse[r] = o.lse;
-      if (status) status[r] = static_cast<uint8_t>(o.status);
-    }
-    __syncthreads();
-  }
-}
-
-static int g_num_sms = 0;
-
-static int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
-
-template <class E, int VB, int THREADS, int U>
-static cudaError_t launch_rows_t(const void* logits, long long n_rows, int vocab, long long stride,
-                                 float iota, float* margin, int* top1, int* top2, float* lse,
-                                 uint8_t* status, cudaStream_t st) {
-  auto kern = margin_rows_kernel<E, VB, THREADS, U>;
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, 0);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  long long grid = static_cast<long long>(per_sm) * num_sms();
-  if (grid > n_rows) grid = n_rows;
-  kern<<<static_cast<unsigned>(grid), THREADS, 0, st>>>(
-      static_cast<const typename E::T*>(logits), n_rows, vocab, stride, iota * kLog2e, iota,
-      margin, top1, top2, lse, status);
-  return cudaGetLastError();
-}
-
-constexpr int kRowThreads = 512;
-
-cudaError_t launch_margin_rows(const void* logits, int dt, long long n_rows, int vocab,
-                               long long stride, float iota, float* margin, int* top1, int* top2,
-                               float* lse, uint8_t* status, cudaStream_t st) {
-  if (n_rows <= 0) return cudaSuccess;
-  switch (dt) {
-    case 0:
-      return launch_rows_t<EBf16, 16, kRowThreads, 4>(logits, n_rows, vocab, stride, iota, margin,
-                                                      top1, top2, lse, status, st);
-    case 1:
-      return launch_rows_t<EF16, 16, kRowThreads, 4>(logits, n_rows, vocab, stride, iota, margin,
-                                                     top1, top2, lse, status, st);
-    default:
-      return launch_rows_t<EF32, 16, kRowThreads, 4>(logits, n_rows, vocab, stride, iota, margin,
-                                                     top1, top2, lse, status, st);
-  }
-}
-
-// ------------------------------------------------------------------- K4
 // Runtime switching (§4.3, fig:mechanism P:209-216), one thread.
 __device__ void switch_one(const CueDev& cs, int tok, float m, uint8_t* state_p, int* hist,
                            int* small_run_p, float gate, int max_seg, uint8_t* flag_out,
@@ -271,7 +433,7 @@ __device__ void switch_one(const CueDev& cs, int tok, float m, uint8_t* state_p,
   int cue = -1, flag = 0;
   uint8_t state = *state_p;
   if (tok >= 0 && tok < cs.vocab && !(state & 2)) {
-    int sr = small_run_p ? *small_run_p : 0;
+    const int sr = small_run_p ? *small_run_p : 0;
     bool clear = false;
     if (tok == cs.think_end) {
       flag = 3; state = 3; clear = true;
@@ -314,7 +476,9 @@ __device__ void switch_one(const CueDev& cs, int tok, float m, uint8_t* state_p,
   *cue_out = static_cast<int16_t>(cue);
 }
 
-template <class E, int VB, int THREADS, int U>
+constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s huge pad
+
+template <class E, int THREADS, int U>
 __global__ void __launch_bounds__(THREADS)
     step_switch_kernel(CueDev cs, const typename E::T* __restrict__ logits, int vocab,
                        long long stride, int nsplit, int chunk, float c, float iota,
@@ -323,51 +487,66 @@ __global__ void __launch_bounds__(THREADS)
                        uint8_t* flag, int16_t* cue_id, int* counter, float* part) {
   __shared__ int s_theta;
   __shared__ Partial s_red[THREADS / 32];
+  __shared__ float s_sum[THREADS / 32];
   __shared__ int s_last;
   const int b = blockIdx.x / nsplit;
   const int k = blockIdx.x % nsplit;
   const int j0 = k * chunk;
   const int j1 = min(vocab, j0 + chunk);
+  const typename E::T* row = logits + b * stride;
   if (threadIdx.x == 0) s_theta = fkey(-INFINITY);
   __syncthreads();
   ThreadState st;
   state_init(st);
-  if (j0 < j1) stream_range<E, VB, THREADS, U>(logits + b * stride, j0, j1, c, st, &s_theta);
+  if (j0 < j1) stream_range_ldg<E, THREADS, U>(row, j0, j1, c, st, &s_theta);
   Partial p = block_reduce<THREADS>(thread_partial(st), s_red);
   if (threadIdx.x == 0) {
-    float* q = part + (static_cast<size_t>(b) * nsplit + k) * 6;
+    float* q = part + (static_cast<size_t>(b) * nsplit + k) * kPartWords;
     __stcg(q + 0, p.t.v1); __stcg(q + 1, p.t.v2);
     __stcg(q + 2, __int_as_float(p.t.i1)); __stcg(q + 3, __int_as_float(p.t.i2));
     __stcg(q + 4, p.n.m); __stcg(q + 5, p.n.s);
+    __stcg(q + 6, __int_as_float(p.huge));
     __threadfence();
     const int old = atomicAdd(counter + b, 1);
     s_last = (old == nsplit - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  // last arriver for row b: merge the nsplit partials (one warp)
+  // last arriver for row b: merge the nsplit partials
   __threadfence();
   if (threadIdx.x < 32) {
     Partial acc = partial_empty();
     for (int kk = threadIdx.x; kk < nsplit; kk += 32) {
-      const float* q = part + (static_cast<size_t>(b) * nsplit + kk) * 6;
+      const float* q = part + (static_cast<size_t>(b) * nsplit + kk) * kPartWords;
       Partial o;
       o.t.v1 = __ldcg(q + 0); o.t.v2 = __ldcg(q + 1);
       o.t.i1 = __float_as_int(__ldcg(q + 2)); o.t.i2 = __float_as_int(__ldcg(q + 3));
       o.n.m = __ldcg(q + 4); o.n.s = __ldcg(q + 5);
+      o.huge = __float_as_int(__ldcg(q + 6));
       acc = partial_merge(acc, o);
     }
     acc = warp_reduce_partial(acc);
-    if (threadIdx.x == 0) {
-      counter[b] = 0;  // ready for the next launch / graph replay
-      RowOut o = finish_row(acc, c, iota);
-      margin[b] = o.margin;
-      if (top1) top1[b] = o.i1;
-      if (top2) top2[b] = o.i2;
-      const int tok = sampled ? sampled[b] : o.i1;
-      switch_one(cs, tok, o.margin, state + b, hist + static_cast<size_t>(b) * kHist,
-                 small_run ? small_run + b : nullptr, gate, max_seg, flag + b, cue_id + b);
-    }
+    if (threadIdx.x == 0) s_red[0] = acc;
+  }
+  __syncthreads();
+  const Partial acc = s_red[0];
+  float S_exact = -1.0f;
+  if (acc.huge) {  // rare: exact normaliser over the whole row by this CTA
+    const float s = warp_sum(exact_sum_thread<E>(row, vocab, acc.t.v1, c, threadIdx.x, THREADS));
+    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = s;
+    __syncthreads();
+    S_exact = 0.0f;
+    for (int w = 0; w < THREADS / 32; w++) S_exact += s_sum[w];
+  }
+  if (threadIdx.x == 0) {
+    counter[b] = 0;  // ready for the next launch / graph replay
+    const RowOut o = finish_row(acc, c, iota, S_exact);
+    margin[b] = o.margin;
+    if (top1) top1[b] = o.i1;
+    if (top2) top2[b] = o.i2;
+    const int tok = sampled ? sampled[b] : o.i1;
+    switch_one(cs, tok, o.margin, state + b, hist + static_cast<size_t>(b) * kHist,
+               small_run ? small_run + b : nullptr, gate, max_seg, flag + b, cue_id + b);
   }
 }
 
@@ -387,7 +566,7 @@ static cudaError_t launch_step_t(const CueDev& cs, const void* logits, int batch
   chunk = (chunk + 63) / 64 * 64;
   if (chunk < 1024) chunk = 1024;
   nsplit = (vocab + chunk - 1) / chunk;
-  auto kern = step_switch_kernel<E, 16, kStepThreads, 2>;
+  auto kern = step_switch_kernel<E, kStepThreads, 4>;
   kern<<<static_cast<unsigned>(batch) * nsplit, kStepThreads, 0, st>>>(
       cs, static_cast<const typename E::T*>(logits), vocab, stride, nsplit, chunk, iota * kLog2e,
       iota, sampled, state, hist, small_run, gate, max_seg, margin, top1, top2, flag, cue_id,

@@ -73,14 +73,17 @@ __device__ __forceinline__ Norm norm_merge(const Norm& a, const Norm& b) {
   return Norm{m, a.s * ex2(a.m - m) + b.s * ex2(b.m - m)};
 }
 
-// Row partial: everything a (row, range) pass produces.
+// Row partial: everything a (row, range) pass produces.  huge = 1 when some
+// exp reference reached |y| >= 2^28, where fp32 y = z*c can no longer resolve
+// the distances that matter; such rows take an exact second pass.
 struct Partial {
   Top2 t;
   Norm n;
+  int huge;
 };
 
 __device__ __forceinline__ Partial partial_merge(const Partial& a, const Partial& b) {
-  return Partial{top2_merge(a.t, b.t), norm_merge(a.n, b.n)};
+  return Partial{top2_merge(a.t, b.t), norm_merge(a.n, b.n), a.huge | b.huge};
 }
 
 __device__ __forceinline__ Partial shfl_xor_partial(const Partial& p, int off) {
@@ -91,6 +94,7 @@ __device__ __forceinline__ Partial shfl_xor_partial(const Partial& p, int off) {
   o.t.i2 = __shfl_xor_sync(kFull, p.t.i2, off);
   o.n.m = __shfl_xor_sync(kFull, p.n.m, off);
   o.n.s = __shfl_xor_sync(kFull, p.n.s, off);
+  o.huge = __shfl_xor_sync(kFull, p.huge, off);
   return o;
 }
 
@@ -108,16 +112,20 @@ __device__ __forceinline__ int fkey(float f) {
 __device__ __forceinline__ float unkey(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
 
 // Finish a row: margin, lse, status (R4).  c = iota*log2e, iota = c/log2e.
+// n.s sums 2^(fl(z_j c - m)) with fma, i.e. every term carries the same
+// shift delta = exact(z1 c) - fl(z1 c) relative to the row maximum; it is
+// removed exactly with fma(z1, c, -My) (the rounding error of a product is
+// representable).  S_exact (when >= 0) replaces the normaliser (exact pass).
 struct RowOut {
   float margin, lse;
   int i1, i2;
   int status;
 };
 
-__device__ __forceinline__ RowOut finish_row(const Partial& p, float c, float iota) {
+__device__ __forceinline__ RowOut finish_row(const Partial& p, float c, float iota,
+                                             float S_exact = -1.0f) {
   RowOut o;
-  float S0 = p.n.s;
-  if (isnan(S0) || p.t.v1 == INFINITY) {
+  if (isnan(p.n.s) || p.t.v1 == INFINITY) {
     o.status = 1;
   } else if (p.t.v1 == -INFINITY) {
     o.status = 2;
@@ -128,9 +136,16 @@ __device__ __forceinline__ RowOut finish_row(const Partial& p, float c, float io
     o.margin = qnan(); o.lse = qnan(); o.i1 = -1; o.i2 = -1;
     return o;
   }
-  float My = p.t.v1 * c;
-  float S = S0 * ex2(p.n.m - My);          // S = sum_j exp((z_j - z1) iota)
-  float p2 = ex2(p.t.v2 * c - My);          // exp((z2 - z1) iota) (0 for -inf)
+  float S, p2;
+  if (S_exact >= 0.0f) {                          // exact pass: sum of 2^((z - z1) c)
+    S = S_exact;
+    p2 = ex2((p.t.v2 - p.t.v1) * c);
+  } else {
+    const float My = p.t.v1 * c;
+    const float d1 = fmaf(p.t.v1, c, -My);        // exact(z1 c) - My
+    S = p.n.s * ex2((p.n.m - My) - d1);           // S = sum_j exp((z_j - z1) iota)
+    p2 = ex2(fmaf(p.t.v2, c, -My) - d1);          // exp((z2 - z1) iota), 0 for -inf
+  }
   o.margin = (1.0f - p2) / S;
   o.lse = p.t.v1 * iota + logf(S);
   o.i1 = p.t.i1;
@@ -196,5 +211,68 @@ struct EF32 {
   __device__ static __forceinline__ void unpack2(uint32_t, float&, float&) {}
   __device__ static __forceinline__ float load1(const T* p) { return __ldg(p); }
 };
+
+// --------------------------------------------- mbarrier + TMA bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D TMA: global -> shared, completion counted on `bar` (bytes % 16 == 0,
+// both addresses 16-byte aligned).  evict_first: logits are read once.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
 
 }  // namespace relay

@@ -55,7 +55,7 @@ ScanWs scan_ws_layout(void* base, long long n_tok, long long cap);
 
 struct StepWs {
   int* counter;        // [batch] (zero between launches)
-  float* part;         // [batch][nsplit][6] partial (v1, v2, i1, i2, m, s)
+  float* part;         // [batch][nsplit][8] partial (v1, v2, i1, i2, m, s, huge, pad)
   size_t bytes;
 };
 constexpr int kMaxSplit = 32;

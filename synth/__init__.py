@@ -161,11 +161,12 @@ def make_logits(n_rows: int, vocab: int, dtype: str = "bf16", row_stride: int | 
                 chunk_rows: int = 1024, edge_rows: bool = True, pad_value: float = float("nan")):
     """Logit rows [n_rows, row_stride] (torch tensor on ``device``).
 
-    Background ~ N(0, 2.5^2) clipped to [-8, 8].  Per row t the runner-up sits
-    at 12 and the top at 12 + gap; with probability 0.9 the top-1 id is
+    Background ~ N(0, 2.5^2) (unclipped).  Per row t the runner-up sits 3 above
+    the row's background maximum and the top at runner-up + gap; with
+    probability 0.9 the top-1 id is
     ``tokens[t]`` (else the runner-up is), mimicking T = 0.6 sampling.
     Gap: 70% "confident" U[3, 12], 30% "uncertain" U[0, 2] with a third
-    candidate at 12 - U[0, 0.5].  Edge rows: 1% exact top-1 ties, 1% exact
+    candidate at runner-up - U[0, 0.5].  Edge rows: 1% exact top-1 ties, 1% exact
     top-2 ties, 0.1% rows with only 20 finite entries (rest -inf), 0.1%
     uniform rows.  Columns [vocab, row_stride) hold ``pad_value`` (NaN by
     default: any kernel that reads the padding fails the tests).  Values are
@@ -194,27 +195,28 @@ def make_logits(n_rows: int, vocab: int, dtype: str = "bf16", row_stride: int | 
     run = np.where(top_is_tok, other, tokens)
     confident = rng.random(n_rows) < 0.7
     gap = np.where(confident, rng.uniform(3, 12, n_rows), rng.uniform(0, 2, n_rows))
-    third_val = np.where(confident, -100.0, 12.0 - rng.uniform(0, 0.5, n_rows))
+    third_off = np.where(confident, np.nan, -rng.uniform(0, 0.5, n_rows))
     kind = rng.random(n_rows)
     if edge_rows:
         gap[kind < 0.01] = 0.0                                  # exact top-1 tie
-        third_val[(kind >= 0.01) & (kind < 0.02)] = 12.0        # exact top-2 tie
+        third_off[(kind >= 0.01) & (kind < 0.02)] = 0.0         # exact top-2 tie
     sparse = edge_rows & (kind >= 0.02) & (kind < 0.021)        # 20 finite entries
     uniform = edge_rows & (kind >= 0.021) & (kind < 0.022)      # all equal
     for r0 in range(0, n_rows, chunk_rows):
         r1 = min(n_rows, r0 + chunk_rows)
         R = r1 - r0
         bg = torch.randn((R, vocab), generator=g, device=device, dtype=torch.float32)
-        bg.mul_(2.5).clamp_(-8.0, 8.0)
+        bg.mul_(2.5)
+        run_v = bg.amax(dim=1) + 3.0                            # runner-up value per row
         rows = torch.arange(R, device=device)
         t_top = torch.as_tensor(top[r0:r1], device=device)
         t_run = torch.as_tensor(run[r0:r1], device=device)
         t_3 = torch.as_tensor(third[r0:r1], device=device)
-        v3 = torch.as_tensor(third_val[r0:r1], device=device, dtype=torch.float32)
-        has3 = v3 > -50
-        bg[rows[has3], t_3[has3]] = v3[has3]
-        bg[rows, t_run] = 12.0
-        bg[rows, t_top] = torch.as_tensor(12.0 + gap[r0:r1], device=device, dtype=torch.float32)
+        off3 = torch.as_tensor(third_off[r0:r1], device=device, dtype=torch.float32)
+        has3 = ~torch.isnan(off3)
+        bg[rows[has3], t_3[has3]] = (run_v + torch.nan_to_num(off3))[has3]
+        bg[rows, t_run] = run_v
+        bg[rows, t_top] = run_v + torch.as_tensor(gap[r0:r1], device=device, dtype=torch.float32)
         sp = np.nonzero(sparse[r0:r1])[0]
         for i in sp:
             keep = torch.randperm(vocab, generator=g, device=device)[:20]

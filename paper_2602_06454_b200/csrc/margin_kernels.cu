@@ -105,7 +105,8 @@ __device__ __forceinline__ void consume_group(const float (&f)[U][VEC], const in
 }
 
 // The warp's two best values bound the row's 2nd-best from below: raise theta.
-__device__ __forceinline__ void warp_raise_theta(const ThreadState& st, int* s_theta) {
+// Returns that bound (all lanes).
+__device__ __forceinline__ float warp_raise_theta(const ThreadState& st, int* s_theta) {
   float a = st.t.v1, b = st.t.v2;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -116,6 +117,31 @@ __device__ __forceinline__ void warp_raise_theta(const ThreadState& st, int* s_t
   }
   if ((threadIdx.x & 31) == 0 && b > unkey(*reinterpret_cast<volatile int*>(s_theta)))
     atomicMax(s_theta, fkey(b));
+  return b;
+}
+
+// Row-start probe: the two largest VALUES of the warp's first stage (branch
+// free) give a warp-local lower bound of the row's 2nd-best before any exact
+// work, so the first stage of a row does not take the exact path everywhere.
+template <int U, int VEC>
+__device__ __forceinline__ float warp_probe_second(const float (&f)[U][VEC]) {
+  float a = -INFINITY, b = -INFINITY;
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+#pragma unroll
+    for (int k = 0; k < VEC; k++) {
+      b = fmaxf(b, fminf(a, f[u][k]));
+      a = fmaxf(a, f[u][k]);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float oa = __shfl_xor_sync(kFull, a, off);
+    const float ob = __shfl_xor_sync(kFull, b, off);
+    b = fmaxf(fminf(a, oa), fmaxf(b, ob));
+    a = fmaxf(a, oa);
+  }
+  return b;
 }
 
 template <class E, int VEC>
@@ -217,11 +243,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
         const T* row = logits + r * stride;
         const Geom g = row_geom<E>(row, 0, vocab);
         const char* src = reinterpret_cast<const char*>(row + g.head);
-        for (long long off = 0; off < g.body; off += SB) {
-          const uint32_t bytes = static_cast<uint32_t>(g.body - off < SB ? g.body - off : SB);
-          mbar_wait(&empty[stage], phase ^ 1);
+        const int body = static_cast<int>(g.body);
+        for (int off = 0; off < body; off += SB) {
+          const uint32_t bytes = static_cast<uint32_t>(min(SB, body - off));
+          mbar_wait_sleep(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], bytes);
-          bulk_g2s(ring + static_cast<size_t>(stage) * SB, src + off, bytes, &full[stage], pol);
+          bulk_g2s(ring + stage * SB, src + off, bytes, &full[stage], pol);
           if (++stage == NS) { stage = 0; phase ^= 1; }
         }
       }
@@ -239,13 +266,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
     const Geom g = row_geom<E>(row, 0, vocab);
     ThreadState st;
     state_init(st);
+    float theta_w = -INFINITY;  // warp-local lower bound of the row's 2nd-best
     if (tid < g.head) consume_scalar(E::load1(row + tid), tid, st, c);
-    for (long long off = 0; off < g.body; off += SB) {
-      const int bytes = static_cast<int>(g.body - off < SB ? g.body - off : SB);
-      const int jb = g.head + static_cast<int>(off / E::SZ);
+    const int body = static_cast<int>(g.body);
+    for (int off = 0; off < body; off += SB) {
+      const int bytes = min(SB, body - off);
+      const int jb = g.head + off / E::SZ;
       mbar_wait(&full[stage], phase);
-      const unsigned char* buf = ring + static_cast<size_t>(stage) * SB;
-      const float theta = unkey(*reinterpret_cast<volatile int*>(theta_p));
+      const unsigned char* buf = ring + stage * SB;
       bool slow = false;
       if (bytes == SB) {
         uint4 raw[U];
@@ -260,8 +288,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
           unpack16<E, VEC>(raw[u], f[u]);
           j0[u] = jb + (tid + u * NCT) * VEC;
         }
+        if (off == 0) {
+          theta_w = warp_probe_second<U, VEC>(f);
+          if (lane == 0 && theta_w > unkey(*reinterpret_cast<volatile int*>(theta_p)))
+            atomicMax(theta_p, fkey(theta_w));
+        }
+        const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         consume_group<U, VEC>(f, j0, st, c, theta, slow);
       } else {
+        const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         const int nvec = bytes / 16;
         for (int v = tid; v < nvec; v += NCT) {
           float f[1][VEC];
@@ -272,7 +307,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
       }
-      if (__any_sync(kFull, slow)) warp_raise_theta(st, theta_p);
+      if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, warp_raise_theta(st, theta_p));
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     if (tid < vocab - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
@@ -294,7 +329,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
       if (tid == 0) {
         float S = 0.0f;
         for (int w = 0; w < NCW; w++) S += s_sum[it & 1][w];
-        const RowOut o = finish_row(q, c, iota, S);
+        const RowOut o = finish_row(q, c, iota, true, S);
         margin[r] = o.margin;
         if (top1) top1[r] = o.i1;
         if (top2) top2[r] = o.i2;
@@ -530,17 +565,16 @@ __global__ void __launch_bounds__(THREADS)
   }
   __syncthreads();
   const Partial acc = s_red[0];
-  float S_exact = -1.0f;
+  float S_exact = 0.0f;
   if (acc.huge) {  // rare: exact normaliser over the whole row by this CTA
     const float s = warp_sum(exact_sum_thread<E>(row, vocab, acc.t.v1, c, threadIdx.x, THREADS));
     if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = s;
     __syncthreads();
-    S_exact = 0.0f;
     for (int w = 0; w < THREADS / 32; w++) S_exact += s_sum[w];
   }
   if (threadIdx.x == 0) {
     counter[b] = 0;  // ready for the next launch / graph replay
-    const RowOut o = finish_row(acc, c, iota, S_exact);
+    const RowOut o = finish_row(acc, c, iota, acc.huge != 0, S_exact);
     margin[b] = o.margin;
     if (top1) top1[b] = o.i1;
     if (top2) top2[b] = o.i2;

@@ -118,6 +118,7 @@ relay_status_t relay_margin_rows(const void* logits, relay_dtype_t dt, int64_t n
   if (vocab < 2) return fail(RELAY_ERR_INVALID, "vocab must be >= 2 (got %lld)", static_cast<long long>(vocab));
   if (vocab > 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "vocab must be < 2^31");
   if (row_stride < vocab) return fail(RELAY_ERR_INVALID, "row_stride < vocab");
+  if (vocab * (dt == RELAY_DT_F32 ? 4 : 2) >= 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "row bytes must be < 2^31");
   if (n_rows < 0) return fail(RELAY_ERR_INVALID, "n_rows < 0");
   if (!(inv_temperature > 0.0f) || !std::isfinite(inv_temperature))
     return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");

@@ -123,9 +123,9 @@ struct RowOut {
 };
 
 __device__ __forceinline__ RowOut finish_row(const Partial& p, float c, float iota,
-                                             float S_exact = -1.0f) {
+                                             bool exact = false, float S_exact = 0.0f) {
   RowOut o;
-  if (isnan(p.n.s) || p.t.v1 == INFINITY) {
+  if (isnan(exact ? S_exact : p.n.s) || p.t.v1 == INFINITY) {
     o.status = 1;
   } else if (p.t.v1 == -INFINITY) {
     o.status = 2;
@@ -137,7 +137,7 @@ __device__ __forceinline__ RowOut finish_row(const Partial& p, float c, float io
     return o;
   }
   float S, p2;
-  if (S_exact >= 0.0f) {                          // exact pass: sum of 2^((z - z1) c)
+  if (exact) {                                    // exact pass: sum of 2^((z - z1) c)
     S = S_exact;
     p2 = ex2((p.t.v2 - p.t.v1) * c);
   } else {
@@ -228,6 +228,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Producer-side wait: the thread is suspended (up to ~hint ns) instead of
+// spinning on issue slots while the ring is full.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(20000u)
+      : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

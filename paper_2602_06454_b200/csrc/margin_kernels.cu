@@ -3,17 +3,20 @@
 // One streaming pass over each logit row (§3.2): online max with a
 // lazily raised exp reference, the softmax normaliser in fp32 (MUFU.EX2 via
 // ex2.approx; FFMA2/FADD2 on element pairs), and the exact top-2 (value desc,
-// index asc) behind a CTA-shared threshold so that only vector groups that
+// index asc) behind a CTA-shared threshold so that only the rare vectors that
 // can still enter the row's top-2 take the exact per-element path
 // (DESIGN.md §6).  HBM-bound: algorithmic bytes = vocab * sizeof(elem) per row.
 // No tensor cores: this is a scan, not a contraction.
 //
 // K1 is a persistent warp-specialised kernel: one producer warp streams row
 // bodies into a shared-memory ring with 1-D TMA bulk copies
-// (cp.async.bulk + mbarrier complete_tx), 8 consumer warps reduce them.
-// The ring runs across row boundaries, so a row's epilogue overlaps the next
-// row's loads.  K4 splits rows into chunks (LDG path) with a last-arriver
-// combine, then runs RelayGen's switch state machine on-device.
+// (cp.async.bulk + mbarrier complete_tx), consumer warps reduce them.  The
+// ring runs across row boundaries, so a row's epilogue overlaps the next
+// row's loads.  Per stage a thread reduces its raw 16-bit words with a packed
+// NaN-propagating max tree (HMNMX2.NAN) before unpacking anything, so the
+// guards cost ~0.5 instruction per element.  K4 splits rows into chunks
+// (LDG path) with a last-arriver combine, then runs RelayGen's switch state
+// machine on-device.
 #include "relay_device.cuh"
 #include "relay_internal.h"
 
@@ -26,7 +29,7 @@ struct ThreadState {
   float g2;    // own skip guard: NaN until t.i2 holds a real index, then t.v2
   float mref;  // exp reference in the y = z*c domain (never above the row max)
   float acc[4];
-  int huge;
+  int flags;   // kFlagHuge | kFlagNan
 };
 
 __device__ __forceinline__ void state_init(ThreadState& st) {
@@ -35,12 +38,12 @@ __device__ __forceinline__ void state_init(ThreadState& st) {
   st.mref = -FLT_MAX;
 #pragma unroll
   for (int k = 0; k < 4; k++) st.acc[k] = 0.0f;
-  st.huge = 0;
+  st.flags = 0;
 }
 
 __device__ __forceinline__ void rescale(ThreadState& st, float ymax) {
   if (ymax > st.mref + kSlack) {
-    if (fabsf(ymax) >= kHuge) st.huge = 1;
+    if (fabsf(ymax) >= kHuge) st.flags |= kFlagHuge;
     const float r = ex2(st.mref - ymax);
 #pragma unroll
     for (int k = 0; k < 4; k++) st.acc[k] *= r;
@@ -50,102 +53,15 @@ __device__ __forceinline__ void rescale(ThreadState& st, float ymax) {
 
 // Exact path for one element (misaligned head/tail of a row range).
 __device__ __forceinline__ void consume_scalar(float x, int j, ThreadState& st, float c) {
+  if (x != x) st.flags |= kFlagNan;
   top2_push(st.t, x, j);
   st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
   rescale(st, x * c);
   st.acc[0] += ex2(fmaf(x, c, -st.mref));
 }
 
-// A group of U vectors of VEC consecutive elements; vector u starts at index
-// j0[u] and the groups of one thread are visited in increasing index order.
-// The top-2 guard and the exp-reference check are hoisted to the group max.
-template <int U, int VEC>
-__device__ __forceinline__ void consume_group(const float (&f)[U][VEC], const int (&j0)[U],
-                                              ThreadState& st, float c, float theta, bool& slow) {
-  float vm[U];
-#pragma unroll
-  for (int u = 0; u < U; u++) {
-    float m = f[u][0];
-#pragma unroll
-    for (int k = 1; k < VEC; k++) m = fmaxf(m, f[u][k]);
-    vm[u] = m;
-  }
-  float gm = vm[0];
-#pragma unroll
-  for (int u = 1; u < U; u++) gm = fmaxf(gm, vm[u]);
-  // A vector can change the row's top-2 only if it holds a value >= theta
-  // (theta <= the row's 2nd-best value) that also beats this thread's own
-  // 2nd-best (indices only grow along a thread's walk).
-  if (gm >= theta && !(gm <= st.g2)) {
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      if (vm[u] >= theta && !(vm[u] <= st.g2)) {
-#pragma unroll
-        for (int k = 0; k < VEC; k++) top2_push(st.t, f[u][k], j0[u] + k);
-        st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
-      }
-    }
-    slow = true;
-  }
-  rescale(st, gm * c);
-  const float2 cc = make_float2(c, c);
-  const float2 nm = make_float2(-st.mref, -st.mref);
-#pragma unroll
-  for (int u = 0; u < U; u++) {
-#pragma unroll
-    for (int k = 0; k < VEC; k += 2) {
-      const float2 y = __ffma2_rn(make_float2(f[u][k], f[u][k + 1]), cc, nm);
-      const float2 e = make_float2(ex2(y.x), ex2(y.y));
-      const int a = (((u * VEC + k) >> 1) & 1) * 2;
-      const float2 s = __fadd2_rn(make_float2(st.acc[a], st.acc[a + 1]), e);
-      st.acc[a] = s.x;
-      st.acc[a + 1] = s.y;
-    }
-  }
-}
-
-// The warp's two best values bound the row's 2nd-best from below: raise theta.
-// Returns that bound (all lanes).
-__device__ __forceinline__ float warp_raise_theta(const ThreadState& st, int* s_theta) {
-  float a = st.t.v1, b = st.t.v2;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const float oa = __shfl_xor_sync(kFull, a, off);
-    const float ob = __shfl_xor_sync(kFull, b, off);
-    b = fmaxf(fminf(a, oa), fmaxf(b, ob));
-    a = fmaxf(a, oa);
-  }
-  if ((threadIdx.x & 31) == 0 && b > unkey(*reinterpret_cast<volatile int*>(s_theta)))
-    atomicMax(s_theta, fkey(b));
-  return b;
-}
-
-// Row-start probe: the two largest VALUES of the warp's first stage (branch
-// free) give a warp-local lower bound of the row's 2nd-best before any exact
-// work, so the first stage of a row does not take the exact path everywhere.
-template <int U, int VEC>
-__device__ __forceinline__ float warp_probe_second(const float (&f)[U][VEC]) {
-  float a = -INFINITY, b = -INFINITY;
-#pragma unroll
-  for (int u = 0; u < U; u++) {
-#pragma unroll
-    for (int k = 0; k < VEC; k++) {
-      b = fmaxf(b, fminf(a, f[u][k]));
-      a = fmaxf(a, f[u][k]);
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const float oa = __shfl_xor_sync(kFull, a, off);
-    const float ob = __shfl_xor_sync(kFull, b, off);
-    b = fmaxf(fminf(a, oa), fmaxf(b, ob));
-    a = fmaxf(a, oa);
-  }
-  return b;
-}
-
-template <class E, int VEC>
-__device__ __forceinline__ void unpack16(const uint4& r, float (&f)[VEC]) {
+template <class E>
+__device__ __forceinline__ void unpack16(const uint4& r, float (&f)[16 / E::SZ]) {
   if constexpr (E::SZ == 4) {
     f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
     f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
@@ -155,8 +71,105 @@ __device__ __forceinline__ void unpack16(const uint4& r, float (&f)[VEC]) {
   }
 }
 
+// Maxima of two disjoint halves of the UV vectors' elements (NaN-propagating):
+// lo/hi 16-bit lanes for packed formats, even/odd words for fp32.
+template <class E, int UV>
+__device__ __forceinline__ float2 stage_max2(const uint4 (&raw)[UV]) {
+  if constexpr (E::SZ == 2) {
+    uint32_t m[UV];
+#pragma unroll
+    for (int u = 0; u < UV; u++) m[u] = E::pmax(E::pmax(raw[u].x, raw[u].y), E::pmax(raw[u].z, raw[u].w));
+#pragma unroll
+    for (int w = 1; w < UV; w <<= 1)
+#pragma unroll
+      for (int u = 0; u + w < UV; u += 2 * w) m[u] = E::pmax(m[u], m[u + w]);
+    float lo, hi;
+    E::unpack2(m[0], lo, hi);
+    return make_float2(lo, hi);
+  } else {
+    float a = max_nan(__uint_as_float(raw[0].x), __uint_as_float(raw[0].z));
+    float b = max_nan(__uint_as_float(raw[0].y), __uint_as_float(raw[0].w));
+#pragma unroll
+    for (int u = 1; u < UV; u++) {
+      a = max3_nan(a, __uint_as_float(raw[u].x), __uint_as_float(raw[u].z));
+      b = max3_nan(b, __uint_as_float(raw[u].y), __uint_as_float(raw[u].w));
+    }
+    return make_float2(a, b);
+  }
+}
+
+// One stage of UV 16-byte vectors; vector u holds elements j0 + u*jstep ..
+// + VEC-1, and a thread's vectors are visited in increasing index order.
+// Returns the two half maxima (for the row-start probe).
+template <class E, int UV>
+__device__ __forceinline__ void consume_stage(const uint4 (&raw)[UV], float2 h, int j0, int jstep,
+                                              ThreadState& st, float c, float theta, bool& slow) {
+  constexpr int VEC = 16 / E::SZ;
+  const float gm = max_nan(h.x, h.y);
+  if (gm != gm) st.flags |= kFlagNan;  // a NaN anywhere in the stage (status 1)
+  // A vector can change the row's top-2 only if it holds a value >= theta
+  // (theta <= the row's 2nd-best value) that also beats this thread's own
+  // 2nd-best (indices only grow along a thread's walk).
+  if (gm >= theta && !(gm <= st.g2)) {
+#pragma unroll
+    for (int u = 0; u < UV; u++) {
+      float f[VEC];
+      unpack16<E>(raw[u], f);
+      float vm = f[0];
+#pragma unroll
+      for (int k = 1; k < VEC; k++) vm = fmaxf(vm, f[k]);
+      if (vm >= theta && !(vm <= st.g2)) {
+#pragma unroll
+        for (int k = 0; k < VEC; k++) top2_push(st.t, f[k], j0 + u * jstep + k);
+        st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
+      }
+    }
+    slow = true;
+  }
+#ifdef RELAY_K1_NULL
+  st.acc[0] += gm;  // tuning only: streaming ceiling without the exp work
+  return;
+#endif
+  rescale(st, gm * c);
+  const float2 cc = make_float2(c, c);
+  const float2 nm = make_float2(-st.mref, -st.mref);
+#pragma unroll
+  for (int u = 0; u < UV; u++) {
+    float f[VEC];
+    unpack16<E>(raw[u], f);
+#pragma unroll
+    for (int k = 0; k < VEC; k += 2) {
+      const float2 y = __ffma2_rn(make_float2(f[k], f[k + 1]), cc, nm);
+      const float2 e = make_float2(ex2(y.x), ex2(y.y));
+      const int a = (((u * VEC + k) >> 1) & 1) * 2;
+      const float2 s = __fadd2_rn(make_float2(st.acc[a], st.acc[a + 1]), e);
+      st.acc[a] = s.x;
+      st.acc[a + 1] = s.y;
+    }
+  }
+}
+
+// Warp top-2 of (a, b) value pairs (a >= b, distinct elements): the result's
+// second value bounds the row's 2nd-best from below.
+__device__ __forceinline__ float warp_second(float a, float b) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float oa = __shfl_xor_sync(kFull, a, off);
+    const float ob = __shfl_xor_sync(kFull, b, off);
+    b = fmaxf(fminf(a, oa), fmaxf(b, ob));
+    a = fmaxf(a, oa);
+  }
+  return b;
+}
+
+__device__ __forceinline__ float theta_raise(float b, int* s_theta) {
+  if ((threadIdx.x & 31) == 0 && b > unkey(*reinterpret_cast<volatile int*>(s_theta)))
+    atomicMax(s_theta, fkey(b));
+  return b;
+}
+
 __device__ __forceinline__ Partial thread_partial(const ThreadState& st) {
-  return Partial{st.t, Norm{st.mref, (st.acc[0] + st.acc[1]) + (st.acc[2] + st.acc[3])}, st.huge};
+  return Partial{st.t, Norm{st.mref, (st.acc[0] + st.acc[1]) + (st.acc[2] + st.acc[3])}, st.flags};
 }
 
 __device__ __forceinline__ Partial partial_empty() {
@@ -167,7 +180,7 @@ __device__ __forceinline__ Partial partial_empty() {
 // 16-byte-aligned body, then scalar tail elements from `tail`.
 struct Geom {
   int head;
-  long long body;  // bytes, multiple of 16
+  int body;  // bytes, multiple of 16 (< 2^31: validated on the host)
   int tail;
 };
 
@@ -178,8 +191,8 @@ __device__ __forceinline__ Geom row_geom(const typename E::T* row, int j0, int j
   int head = static_cast<int>(((16 - (a & 15)) & 15) / E::SZ);
   if (head > j1 - j0) head = j1 - j0;
   g.head = head;
-  g.body = (static_cast<long long>(j1 - j0 - head) * E::SZ) & ~15LL;
-  g.tail = j0 + head + static_cast<int>(g.body / E::SZ);
+  g.body = ((j1 - j0 - head) * E::SZ) & ~15;
+  g.tail = j0 + head + g.body / E::SZ;
   return g;
 }
 
@@ -203,8 +216,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ------------------------------------------------------------------- K1
-template <class E, int NCW, int NS, int SB>
-__global__ void __launch_bounds__((NCW + 1) * 32)
+template <class E, int NCW, int NS, int UV, int MINB>
+__global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     margin_rows_tma_kernel(const typename E::T* __restrict__ logits, long long n_rows, int vocab,
                            long long stride, float c, float iota, float* __restrict__ margin,
                            int* __restrict__ top1, int* __restrict__ top2, float* __restrict__ lse,
@@ -212,21 +225,24 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
   constexpr int NCT = NCW * 32;             // consumer threads
-  constexpr int U = SB / 16 / NCT;          // vectors per consumer thread per full stage
-  static_assert(U >= 1 && U * NCT * 16 == SB, "stage must split evenly");
+  constexpr int SB = UV * NCT * 16;         // bytes per ring stage
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
+  constexpr int NRED = NCW * 8;             // partials per row after 2 shuffle rounds
   __shared__ int s_theta[2];
-  __shared__ Partial s_red[2][NCW];
+  __shared__ Partial s_red[2][NRED];
   __shared__ float s_sum[2][NCW];
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t full_s = smem_u32(full);
+  const uint32_t empty_s = smem_u32(empty);
   if (tid == 0) {
     for (int s = 0; s < NS; s++) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCW);
+      mbar_init(full_s + 8 * s, 1);
+      mbar_init(empty_s + 8 * s, NCW);
     }
     s_theta[0] = s_theta[1] = fkey(-INFINITY);
     fence_barrier_init();
@@ -243,12 +259,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
         const T* row = logits + r * stride;
         const Geom g = row_geom<E>(row, 0, vocab);
         const char* src = reinterpret_cast<const char*>(row + g.head);
-        const int body = static_cast<int>(g.body);
-        for (int off = 0; off < body; off += SB) {
-          const uint32_t bytes = static_cast<uint32_t>(min(SB, body - off));
-          mbar_wait_sleep(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], bytes);
-          bulk_g2s(ring + stage * SB, src + off, bytes, &full[stage], pol);
+        for (int off = 0; off < g.body; off += SB) {
+          const uint32_t bytes = static_cast<uint32_t>(min(SB, g.body - off));
+          mbar_wait_sleep(empty_s + 8 * stage, phase ^ 1);
+          mbar_expect_tx(full_s + 8 * stage, bytes);
+          bulk_g2s(ring_s + stage * SB, src + off, bytes, full_s + 8 * stage, pol);
           if (++stage == NS) { stage = 0; phase ^= 1; }
         }
       }
@@ -268,79 +283,73 @@ __global__ void __launch_bounds__((NCW + 1) * 32)
     state_init(st);
     float theta_w = -INFINITY;  // warp-local lower bound of the row's 2nd-best
     if (tid < g.head) consume_scalar(E::load1(row + tid), tid, st, c);
-    const int body = static_cast<int>(g.body);
-    for (int off = 0; off < body; off += SB) {
-      const int bytes = min(SB, body - off);
+    for (int off = 0; off < g.body; off += SB) {
+      const int bytes = min(SB, g.body - off);
       const int jb = g.head + off / E::SZ;
-      mbar_wait(&full[stage], phase);
-      const unsigned char* buf = ring + stage * SB;
+      mbar_wait(full_s + 8 * stage, phase);
+      const uint32_t buf = ring_s + stage * SB;
       bool slow = false;
       if (bytes == SB) {
-        uint4 raw[U];
+        uint4 raw[UV];
 #pragma unroll
-        for (int u = 0; u < U; u++) raw[u] = lds128(buf + (tid + u * NCT) * 16);
+        for (int u = 0; u < UV; u++) raw[u] = lds128(buf + (tid + u * NCT) * 16);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);  // release orders the loads above
-        float f[U][VEC];
-        int j0[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-          unpack16<E, VEC>(raw[u], f[u]);
-          j0[u] = jb + (tid + u * NCT) * VEC;
-        }
+        if (lane == 0) mbar_arrive(empty_s + 8 * stage);  // release orders the loads above
+        const float2 h = stage_max2<E, UV>(raw);
         if (off == 0) {
-          theta_w = warp_probe_second<U, VEC>(f);
-          if (lane == 0 && theta_w > unkey(*reinterpret_cast<volatile int*>(theta_p)))
-            atomicMax(theta_p, fkey(theta_w));
+          // row-start probe: the two half maxima are two distinct elements, so
+          // the warp's second-best of them bounds the row's 2nd-best from below
+          theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
         }
         const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
-        consume_group<U, VEC>(f, j0, st, c, theta, slow);
+        consume_stage<E, UV>(raw, h, jb + tid * VEC, NCT * VEC, st, c, theta, slow);
       } else {
         const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         const int nvec = bytes / 16;
         for (int v = tid; v < nvec; v += NCT) {
-          float f[1][VEC];
-          const int j0[1] = {jb + v * VEC};
-          unpack16<E, VEC>(lds128(buf + v * 16), f[0]);
-          consume_group<1, VEC>(f, j0, st, c, theta, slow);
+          const uint4 raw1[1] = {lds128(buf + v * 16)};
+          consume_stage<E, 1>(raw1, stage_max2<E, 1>(raw1), jb + v * VEC, 0, st, c, theta, slow);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (lane == 0) mbar_arrive(empty_s + 8 * stage);
       }
-      if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, warp_raise_theta(st, theta_p));
+      if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     if (tid < vocab - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
 
     // ------------------------------------------------ row epilogue
-    Partial p = warp_reduce_partial(thread_partial(st));
-    if (lane == 0) s_red[it & 1][warp] = p;
+    // Two shuffle rounds leave 8 partials per warp in smem; one warp merges
+    // them (the other warps go straight on to the next row).
+    Partial p = thread_partial(st);
+    p = partial_merge(p, shfl_xor_partial(p, 16));
+    p = partial_merge(p, shfl_xor_partial(p, 8));
+    if (lane < 8) s_red[it & 1][warp * 8 + lane] = p;
     if (tid == 0) s_theta[(it + 1) & 1] = fkey(-INFINITY);
     named_bar(1, NCT);
     // s_red[it & 1] is rewritten only after the next row's barrier, which
-    // every warp reaches after this read, so the decision is uniform.
-    if (__any_sync(kFull, lane < NCW && s_red[it & 1][lane].huge)) {
-      // rare: every consumer joins an exact second pass over the row
-      Partial q = lane < NCW ? s_red[it & 1][lane] : partial_empty();
+    // every warp reaches after these reads, so the decision is uniform.
+    bool huge_lane = false;
+#pragma unroll
+    for (int e = lane; e < NRED; e += 32) huge_lane |= (s_red[it & 1][e].flags & kFlagHuge) != 0;
+    const bool huge = __any_sync(kFull, huge_lane);
+    if (huge || warp == 0) {
+      Partial q = partial_empty();
+#pragma unroll
+      for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[it & 1][e]);
       q = warp_reduce_partial(q);
-      float s = warp_sum(exact_sum_thread<E>(row, vocab, q.t.v1, c, tid, NCT));
-      if (lane == 0) s_sum[it & 1][warp] = s;
-      named_bar(1, NCT);
-      if (tid == 0) {
-        float S = 0.0f;
+      bool exact = false;
+      float S = 0.0f;
+      if (huge) {
+        // rare: every consumer joins an exact second pass over the row
+        const float s = warp_sum(exact_sum_thread<E>(row, vocab, q.t.v1, c, tid, NCT));
+        if (lane == 0) s_sum[it & 1][warp] = s;
+        named_bar(1, NCT);
         for (int w = 0; w < NCW; w++) S += s_sum[it & 1][w];
-        const RowOut o = finish_row(q, c, iota, true, S);
-        margin[r] = o.margin;
-        if (top1) top1[r] = o.i1;
-        if (top2) top2[r] = o.i2;
-        if (lse) lse[r] = o.lse;
-        if (status) status[r] = static_cast<uint8_t>(o.status);
+        exact = true;
       }
-    } else if (warp == 0) {
-      Partial q = lane < NCW ? s_red[it & 1][lane] : partial_empty();
-      q = warp_reduce_partial(q);
-      if (lane == 0) {
-        const RowOut o = finish_row(q, c, iota);
+      if (tid == 0) {
+        const RowOut o = finish_row(q, c, iota, exact, S);
         margin[r] = o.margin;
         if (top1) top1[r] = o.i1;
         if (top2) top2[r] = o.i2;
@@ -363,16 +372,30 @@ int num_sms() {
   return g_num_sms;
 }
 
-constexpr int kNCW = 8;        // consumer warps per CTA
-constexpr int kStages = 6;     // ring depth
-constexpr int kStageBytes = 16384;
+// K1 launch shape (overridable at build time for tuning sweeps, tools/k1_sweep.py).
+#ifndef RELAY_K1_NCW
+#define RELAY_K1_NCW 8
+#endif
+#ifndef RELAY_K1_STAGES
+#define RELAY_K1_STAGES 4
+#endif
+#ifndef RELAY_K1_UV
+#define RELAY_K1_UV 4
+#endif
+#ifndef RELAY_K1_MINB
+#define RELAY_K1_MINB 3
+#endif
+constexpr int kNCW = RELAY_K1_NCW;        // consumer warps per CTA
+constexpr int kStages = RELAY_K1_STAGES;  // ring depth
+constexpr int kUV = RELAY_K1_UV;          // 16-byte vectors per consumer thread per stage
+constexpr int kMinBlocks = RELAY_K1_MINB; // CTAs per SM the registers must allow
 
 template <class E>
 static cudaError_t launch_rows_t(const void* logits, long long n_rows, int vocab, long long stride,
                                  float iota, float* margin, int* top1, int* top2, float* lse,
                                  uint8_t* status, cudaStream_t st) {
-  auto kern = margin_rows_tma_kernel<E, kNCW, kStages, kStageBytes>;
-  const int smem = kStages * kStageBytes;
+  auto kern = margin_rows_tma_kernel<E, kNCW, kStages, kUV, kMinBlocks>;
+  const int smem = kStages * kUV * kNCW * 32 * 16;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -416,7 +439,7 @@ __device__ __forceinline__ void stream_range_ldg(const typename E::T* __restrict
   const Geom g = row_geom<E>(row, j0, j1);
   if (tid < g.head) consume_scalar(E::load1(row + j0 + tid), j0 + tid, st, c);
   const int jb = j0 + g.head;
-  const int nvec = static_cast<int>(g.body / 16);
+  const int nvec = g.body / 16;
   const char* vbase = reinterpret_cast<const char*>(row + jb);
   int wv = tid - lane;  // warp-uniform bound so the vote sees all 32 lanes
   for (; wv + 31 + (U - 1) * THREADS < nvec; wv += U * THREADS) {
@@ -426,23 +449,14 @@ __device__ __forceinline__ void stream_range_ldg(const typename E::T* __restrict
     for (int u = 0; u < U; u++) raw[u] = ldg_stream16(vbase + static_cast<size_t>(v + u * THREADS) * 16);
     const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
     bool slow = false;
-    float f[U][VEC];
-    int jj[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      unpack16<E, VEC>(raw[u], f[u]);
-      jj[u] = jb + (v + u * THREADS) * VEC;
-    }
-    consume_group<U, VEC>(f, jj, st, c, theta, slow);
-    if (__any_sync(kFull, slow)) warp_raise_theta(st, s_theta);
+    consume_stage<E, U>(raw, stage_max2<E, U>(raw), jb + v * VEC, THREADS * VEC, st, c, theta, slow);
+    if (__any_sync(kFull, slow)) theta_raise(warp_second(st.t.v1, st.t.v2), s_theta);
   }
   for (int v = wv + lane; v < nvec; v += THREADS) {
     const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
     bool slow = false;
-    float f[1][VEC];
-    const int jj[1] = {jb + v * VEC};
-    unpack16<E, VEC>(ldg_stream16(vbase + static_cast<size_t>(v) * 16), f[0]);
-    consume_group<1, VEC>(f, jj, st, c, theta, slow);
+    const uint4 raw1[1] = {ldg_stream16(vbase + static_cast<size_t>(v) * 16)};
+    consume_stage<E, 1>(raw1, stage_max2<E, 1>(raw1), jb + v * VEC, 0, st, c, theta, slow);
   }
   if (tid < j1 - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
 }
@@ -511,7 +525,7 @@ __device__ void switch_one(const CueDev& cs, int tok, float m, uint8_t* state_p,
   *cue_out = static_cast<int16_t>(cue);
 }
 
-constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s huge pad
+constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
 
 template <class E, int THREADS, int U>
 __global__ void __launch_bounds__(THREADS)
@@ -540,7 +554,7 @@ __global__ void __launch_bounds__(THREADS)
     __stcg(q + 0, p.t.v1); __stcg(q + 1, p.t.v2);
     __stcg(q + 2, __int_as_float(p.t.i1)); __stcg(q + 3, __int_as_float(p.t.i2));
     __stcg(q + 4, p.n.m); __stcg(q + 5, p.n.s);
-    __stcg(q + 6, __int_as_float(p.huge));
+    __stcg(q + 6, __int_as_float(p.flags));
     __threadfence();
     const int old = atomicAdd(counter + b, 1);
     s_last = (old == nsplit - 1);
@@ -557,7 +571,7 @@ __global__ void __launch_bounds__(THREADS)
       o.t.v1 = __ldcg(q + 0); o.t.v2 = __ldcg(q + 1);
       o.t.i1 = __float_as_int(__ldcg(q + 2)); o.t.i2 = __float_as_int(__ldcg(q + 3));
       o.n.m = __ldcg(q + 4); o.n.s = __ldcg(q + 5);
-      o.huge = __float_as_int(__ldcg(q + 6));
+      o.flags = __float_as_int(__ldcg(q + 6));
       acc = partial_merge(acc, o);
     }
     acc = warp_reduce_partial(acc);
@@ -566,7 +580,7 @@ __global__ void __launch_bounds__(THREADS)
   __syncthreads();
   const Partial acc = s_red[0];
   float S_exact = 0.0f;
-  if (acc.huge) {  // rare: exact normaliser over the whole row by this CTA
+  if (acc.flags & kFlagHuge) {  // rare: exact normaliser over the whole row by this CTA
     const float s = warp_sum(exact_sum_thread<E>(row, vocab, acc.t.v1, c, threadIdx.x, THREADS));
     if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = s;
     __syncthreads();
@@ -574,7 +588,7 @@ __global__ void __launch_bounds__(THREADS)
   }
   if (threadIdx.x == 0) {
     counter[b] = 0;  // ready for the next launch / graph replay
-    const RowOut o = finish_row(acc, c, iota, acc.huge != 0, S_exact);
+    const RowOut o = finish_row(acc, c, iota, (acc.flags & kFlagHuge) != 0, S_exact);
     margin[b] = o.margin;
     if (top1) top1[b] = o.i1;
     if (top2) top2[b] = o.i2;

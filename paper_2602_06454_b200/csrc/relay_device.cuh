@@ -73,17 +73,20 @@ __device__ __forceinline__ Norm norm_merge(const Norm& a, const Norm& b) {
   return Norm{m, a.s * ex2(a.m - m) + b.s * ex2(b.m - m)};
 }
 
-// Row partial: everything a (row, range) pass produces.  huge = 1 when some
-// exp reference reached |y| >= 2^28, where fp32 y = z*c can no longer resolve
-// the distances that matter; such rows take an exact second pass.
+// Row partial: everything a (row, range) pass produces.  flags bit 0 (huge):
+// some exp reference reached |y| >= 2^28, where fp32 y = z*c can no longer
+// resolve the distances that matter, so the row takes an exact second pass;
+// bit 1: a NaN was seen (status 1).
 struct Partial {
   Top2 t;
   Norm n;
-  int huge;
+  int flags;
 };
+constexpr int kFlagHuge = 1;
+constexpr int kFlagNan = 2;
 
 __device__ __forceinline__ Partial partial_merge(const Partial& a, const Partial& b) {
-  return Partial{top2_merge(a.t, b.t), norm_merge(a.n, b.n), a.huge | b.huge};
+  return Partial{top2_merge(a.t, b.t), norm_merge(a.n, b.n), a.flags | b.flags};
 }
 
 __device__ __forceinline__ Partial shfl_xor_partial(const Partial& p, int off) {
@@ -94,7 +97,7 @@ __device__ __forceinline__ Partial shfl_xor_partial(const Partial& p, int off) {
   o.t.i2 = __shfl_xor_sync(kFull, p.t.i2, off);
   o.n.m = __shfl_xor_sync(kFull, p.n.m, off);
   o.n.s = __shfl_xor_sync(kFull, p.n.s, off);
-  o.huge = __shfl_xor_sync(kFull, p.huge, off);
+  o.flags = __shfl_xor_sync(kFull, p.flags, off);
   return o;
 }
 
@@ -125,7 +128,7 @@ struct RowOut {
 __device__ __forceinline__ RowOut finish_row(const Partial& p, float c, float iota,
                                              bool exact = false, float S_exact = 0.0f) {
   RowOut o;
-  if (isnan(exact ? S_exact : p.n.s) || p.t.v1 == INFINITY) {
+  if ((p.flags & kFlagNan) || isnan(exact ? S_exact : p.n.s) || p.t.v1 == INFINITY) {
     o.status = 1;
   } else if (p.t.v1 == -INFINITY) {
     o.status = 2;
@@ -177,13 +180,19 @@ __device__ __forceinline__ U8x32 ldg_stream32(const void* p) {
 }
 
 // Element formats.  unpack2 turns one 32-bit word into two fp32 values
-// (exact for bf16/f16).
+// (exact for bf16/f16); pmax is the NaN-propagating packed max of two words
+// (HMNMX2.NAN), used to reduce a whole stage before unpacking.
 struct EBf16 {
   using T = uint16_t;
   static constexpr int SZ = 2;
   __device__ static __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
     lo = __uint_as_float(w << 16);
     hi = __uint_as_float(w & 0xffff0000u);
+  }
+  __device__ static __forceinline__ uint32_t pmax(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
   }
   __device__ static __forceinline__ float load1(const T* p) {
     return __uint_as_float(static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(p))) << 16);
@@ -199,6 +208,11 @@ struct EF16 {
     lo = f.x;
     hi = f.y;
   }
+  __device__ static __forceinline__ uint32_t pmax(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.NaN.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+  }
   __device__ static __forceinline__ float load1(const T* p) {
     unsigned short b = __ldg(reinterpret_cast<const unsigned short*>(p));
     return __half2float(__ushort_as_half(b));
@@ -209,61 +223,79 @@ struct EF32 {
   using T = float;
   static constexpr int SZ = 4;
   __device__ static __forceinline__ void unpack2(uint32_t, float&, float&) {}
+  __device__ static __forceinline__ uint32_t pmax(uint32_t a, uint32_t) { return a; }
   __device__ static __forceinline__ float load1(const T* p) { return __ldg(p); }
 };
 
+// NaN-propagating maxima (FMNMX.NAN / FMNMX3.NAN).
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float max3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 // --------------------------------------------- mbarrier + TMA bulk copy
+// All helpers take 32-bit shared-window addresses computed once per kernel.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
 // Producer-side wait: the thread is suspended (up to ~hint ns) instead of
 // spinning on issue slots while the ring is full.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAITS_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAITS_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(20000u)
-      : "memory");
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  for (;;) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(20000u)
+        : "memory");
+    if (done) return;
+    __nanosleep(128);
+  }
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
+      "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
 }
 
 // 1-D TMA: global -> shared, completion counted on `bar` (bytes % 16 == 0,
 // both addresses 16-byte aligned).  evict_first: logits are read once.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
                                          uint64_t policy) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
       : "memory");
 }
 
@@ -281,11 +313,11 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-__device__ __forceinline__ uint4 lds128(const void* p) {
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 r;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "r"(smem_u32(p)));
+               : "r"(addr));
   return r;
 }
 

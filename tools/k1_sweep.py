@@ -1,0 +1,92 @@
+"""Tuning sweep for K1 (relay_margin_rows): build librelay variants with
+different launch shapes (tools/k1_sweep.py build, on any host with nvcc) and
+time them on one GPU on the configs[1] workload (tools/k1_sweep.py run).
+Reports GB/s of algorithmic bytes and the fraction of MEASURED_PEAKS hbm_gbs."""
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "build", "k1_sweep")
+SRC = [os.path.join(ROOT, "paper_2602_06454_b200", "csrc", f)
+       for f in ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu")]
+VARIANTS = [  # (ncw, stages, uv, minb, extra): stage bytes = uv * ncw * 32 * 16
+    (8, 4, 4, 3, ""), (8, 4, 4, 3, "NULL"), (6, 4, 4, 4, ""), (4, 5, 4, 5, ""),
+    (4, 6, 4, 4, ""), (8, 6, 2, 3, ""), (8, 3, 4, 3, ""), (4, 4, 4, 6, ""),
+]
+
+
+def name(v):
+    return "w%d_s%d_u%d_m%d" % v[:4] + (("_" + v[4]) if v[4] else "")
+
+
+def extra(v):
+    if v[4] == "NULL":
+        return ["-DRELAY_K1_NULL"]
+    if v[4].startswith("POLY"):
+        return ["-DRELAY_K1_POLY_EVERY=%s" % v[4][4:]]
+    return []
+
+
+def build():
+    os.makedirs(OUT, exist_ok=True)
+    for v in VARIANTS:
+        so = os.path.join(OUT, "librelay_%s.so" % name(v))
+        cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+               "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+               "-DRELAY_K1_NCW=%d" % v[0], "-DRELAY_K1_STAGES=%d" % v[1],
+               "-DRELAY_K1_UV=%d" % v[2], "-DRELAY_K1_MINB=%d" % v[3], "-o", so] + extra(v) + SRC
+        subprocess.check_call(cmd)
+        print("built", so)
+
+
+def run(cfg="c2", reps=20):
+    import torch
+    import synth
+    c = synth.CONFIGS[cfg]
+    T, V, dt = c["traj_len"], c["vocab"], c["dtype"]
+    ts = synth.make_tokens(1, T, synth.make_cueset(V, c["n_cues"], c["n_pat"], max_len=c["max_len"]))
+    L = synth.make_logits(T, V, dt, tokens=ts.tokens, device="cuda", chunk_rows=2048)
+    esz = 2 if dt != "f32" else 4
+    nbytes = T * (V * esz + 17)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
+    outs = [torch.empty(T, dtype=d, device="cuda") for d in (torch.float32, torch.int32, torch.int32,
+                                                                torch.float32, torch.uint8)]
+    P = C.c_void_p
+    res = {}
+    for v in VARIANTS:
+        so = os.path.join(OUT, "librelay_%s.so" % name(v))
+        if not os.path.exists(so):
+            continue
+        lib = C.CDLL(so)
+        f = lib.relay_margin_rows
+        f.restype = C.c_int
+        f.argtypes = [P, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_float, P, P, P, P, P, P]
+        s = torch.cuda.current_stream()
+        call = lambda: f(P(L.data_ptr()), {"bf16": 0, "f16": 1, "f32": 2}[dt], T, V, V, 1.0,
+                         *[P(o.data_ptr()) for o in outs], P(s.cuda_stream))  # noqa: E731
+        for _ in range(3):
+            assert call() == 0
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+        for i in range(reps):
+            ev[2 * i].record(s)
+            call()
+            ev[2 * i + 1].record(s)
+        torch.cuda.synchronize()
+        ms = sorted(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(reps))
+        med = ms[reps // 2]
+        gbs = nbytes / (med / 1e3) / 1e9
+        res[name(v)] = dict(ms_median=med, ms_best=ms[0], gbs=gbs, frac=gbs / peak)
+        print(json.dumps({name(v): res[name(v)]}), flush=True)
+    return res
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        run(*(sys.argv[2:3] or ["c2"]))

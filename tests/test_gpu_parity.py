@@ -338,7 +338,13 @@ def test_segment_reduce_deterministic(relay):
     a = _segment_case(relay, **args)
     b = _segment_case(relay, **args)
     assert torch.equal(a[5]["stats"], b[5]["stats"])
-    assert torch.equal(a[5]["seg_end"], b[5]["seg_end"])
+    n = int(a[4]["n_occ"].item())
+    assert n == int(b[4]["n_occ"].item())
+    for k in ("seg_end", "seg_mean", "seg_min", "seg_lowfrac"):
+        x, y = a[5][k][:n], b[5][k][:n]
+        if x.is_floating_point():
+            x, y = torch.nan_to_num(x, 7.0), torch.nan_to_num(y, 7.0)
+        assert torch.equal(x, y), k
 
 
 def test_analyzer_end_to_end_small(relay):

@@ -210,31 +210,39 @@ def main():
     tep = torch.as_tensor(ts.think_end_pos, device=dev)
     an = relay.Analyzer(cs, T, vocab, dev, rank=rank, world_size=world)
     stream = torch.cuda.current_stream()
-    host_stats = torch.empty(an.stats.shape, dtype=torch.int64, pin_memory=True)
-
+    # two pinned host tables: step i's table is finalized on the host while the
+    # GPU already runs step i+1 (the work per step is unchanged)
+    host_stats = [torch.empty(an.stats.shape, dtype=torch.int64, pin_memory=True) for _ in range(2)]
+    done = [torch.cuda.Event(), torch.cuda.Event()]
     k1_ev = []
+    results = []
 
-    def step(timed=False):
-        relay.stats_init(an.stats, cs.n_cues, rank, world)
+    def launch(i, timed=False):
+        """Device side of step i: H1-H5 (K1 timed with events on its stream), H6, D2H."""
+        e0 = e1 = None
         if timed:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        relay.margin_rows(logits, vocab=vocab, out=an.rows)
+        an.run(logits, tok, offs, tep, k1_events=(e0, e1) if timed else None)
         if timed:
-            e1.record(stream)
             k1_ev.append((e0, e1))
-        relay.cue_scan(cs, tok, offs, an.cap, an.ws, an.scan)
-        relay.segment_reduce(cs, an.rows["margin"], an.scan, offs, tep, an.tau, an.stats, rank, world,
-                             an.ws, an.seg)
         if world > 1:
             dist.all_reduce(an.stats, op=dist.ReduceOp.SUM)     # H6: one NCCL all-reduce
-        host_stats.copy_(an.stats, non_blocking=True)
-        stream.synchronize()
-        return relay.stats_finalize(host_stats.numpy(), cs.n_cues, world)   # H7
+        host_stats[i % 2].copy_(an.stats, non_blocking=True)
+        done[i % 2].record(stream)
 
-    for _ in range(args.warmup):
-        step()
+    def finish(i):
+        done[i % 2].synchronize()
+        results.append(relay.stats_finalize(host_stats[i % 2].numpy(), cs.n_cues, world))   # H7
+
+    def run_steps(n, timed=False):
+        for i in range(n):
+            launch(i, timed)
+            if i > 0:
+                finish(i - 1)
+        finish(n - 1)
+
+    run_steps(args.warmup)
     clocks = Clocks(local)
     if not args.profile:
         clocks.start()
@@ -245,8 +253,7 @@ def main():
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    for _ in range(args.steps):
-        step(timed=True)
+    run_steps(args.steps, timed=True)
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:

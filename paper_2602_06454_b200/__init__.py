@@ -363,16 +363,51 @@ class Analyzer:
                         seg_min=torch.empty(c1, dtype=torch.float32, device=d),
                         seg_lowfrac=torch.empty(c1, dtype=torch.float32, device=d))
         self.stats = torch.empty(stats_words(cs.n_cues, world_size), dtype=torch.int64, device=d)
+        self._side = None
 
     def run(self, logits, tokens, traj_offsets=None, think_end_pos=None, stream=None,
-            vocab=None):
-        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, stream)
+            vocab=None, k1_events=None):
+        """Launch one pass.  K2 (tokens only) runs on a side stream concurrently
+        with K1; K3 joins both.  Stream-ordered, no host synchronisation."""
+        import torch
+        s = torch.cuda.current_stream() if stream is None else stream
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+            self._fork = torch.cuda.Event()
+            self._join = torch.cuda.Event()
+        self._fork.record(s)
+        self._side.wait_event(self._fork)
+        cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
+        self._join.record(self._side)
+        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s)
+        if k1_events:
+            k1_events[0].record(s)
         margin_rows(logits, vocab=vocab or self.vocab, inv_temperature=self.iota, out=self.rows,
-                    stream=stream)
-        cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, stream)
+                    stream=s)
+        if k1_events:
+            k1_events[1].record(s)
+        s.wait_event(self._join)
         segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
-                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, stream)
+                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s)
         return self.stats
+
+    def capture(self, logits, tokens, traj_offsets=None, think_end_pos=None, host_stats=None,
+                vocab=None):
+        """A CUDA graph of one device-side pass (+ the stats table copied to the
+        pinned ``host_stats`` when given).  ``graph.replay()`` re-runs it on the
+        same buffers; the inputs may be refilled in place between replays."""
+        import torch
+        self.run(logits, tokens, traj_offsets, think_end_pos, vocab=vocab)   # warm-up
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=self.device)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                self.run(logits, tokens, traj_offsets, think_end_pos, stream=cap, vocab=vocab)
+                if host_stats is not None:
+                    host_stats.copy_(self.stats, non_blocking=True)
+        torch.cuda.synchronize(self.device)
+        return g
 
     def n_launches(self) -> int:
         """Kernels launched by one run(): stats_init 1 + K1 1 + K2 2 + K3 4."""

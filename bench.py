@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no clocks/e2e/baseline)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
@@ -188,15 +189,23 @@ def main():
 
     import paper_2602_06454_b200 as relay
     import synth
+    from paper_2602_06454_b200.dist import allreduce_stats
 
     rank, world, local = dist_env()
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    # RELAY_BENCH_SAME_DEVICE=1: every rank on cuda:0 (a 1-GPU functional check of the
+    # multi-rank path with --dist-backend gloo; its timings are not a scaling result)
+    if os.environ.get("RELAY_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     c = workload(args.config)
     vocab, dtype, T = c["vocab"], c["dtype"], c["traj_len"]
     cs_h = synth.make_cueset(vocab, c["n_cues"], c["n_pat"], max_len=c["max_len"])
@@ -227,7 +236,7 @@ def main():
         if timed:
             k1_ev.append((e0, e1))
         if world > 1:
-            dist.all_reduce(an.stats, op=dist.ReduceOp.SUM)     # H6: one NCCL all-reduce
+            allreduce_stats(an.stats)     # H6: one NCCL all-reduce of the stats table
         host_stats[i % 2].copy_(an.stats, non_blocking=True)
         done[i % 2].record(stream)
 

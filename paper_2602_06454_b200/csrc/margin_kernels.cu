@@ -236,9 +236,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const uint32_t ring_s = smem_u32(ring);
-  const uint32_t full_s = smem_u32(full);
-  const uint32_t empty_s = smem_u32(empty);
+  const uint32_t ring_s = smem_u32_pinned(ring);
+  const uint32_t full_s = smem_u32_pinned(full);
+  const uint32_t empty_s = smem_u32_pinned(empty);
   if (tid == 0) {
     for (int s = 0; s < NS; s++) {
       mbar_init(full_s + 8 * s, 1);

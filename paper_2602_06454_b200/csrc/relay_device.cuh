@@ -245,6 +245,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// The same address, opaque to the compiler: kept in a register instead of
+// being re-derived from SR_CgaCtaId (an S2R) inside hot loops.
+__device__ __forceinline__ uint32_t smem_u32_pinned(const void* p) {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -257,6 +265,9 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+#ifndef RELAY_PRODUCER_SLEEP_NS
+#define RELAY_PRODUCER_SLEEP_NS 256
+#endif
 // Producer-side wait: the thread is suspended (up to ~hint ns) instead of
 // spinning on issue slots while the ring is full.
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
@@ -272,7 +283,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity), "r"(20000u)
         : "memory");
     if (done) return;
-    __nanosleep(128);
+    __nanosleep(RELAY_PRODUCER_SLEEP_NS);
   }
 }
 

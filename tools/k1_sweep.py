@@ -14,8 +14,8 @@ OUT = os.path.join(ROOT, "build", "k1_sweep")
 SRC = [os.path.join(ROOT, "paper_2602_06454_b200", "csrc", f)
        for f in ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu")]
 VARIANTS = [  # (ncw, stages, uv, minb, extra): stage bytes = uv * ncw * 32 * 16
-    (8, 4, 4, 3, ""), (8, 4, 4, 3, "NULL"), (6, 4, 4, 4, ""), (4, 5, 4, 5, ""),
-    (4, 6, 4, 4, ""), (8, 6, 2, 3, ""), (8, 3, 4, 3, ""), (4, 4, 4, 6, ""),
+    (8, 4, 4, 3, ""), (8, 4, 4, 3, "S64"), (8, 4, 4, 3, "S1024"), (8, 4, 4, 3, "NULL"),
+    (4, 4, 4, 6, ""), (4, 5, 4, 5, ""),
 ]
 
 
@@ -26,8 +26,8 @@ def name(v):
 def extra(v):
     if v[4] == "NULL":
         return ["-DRELAY_K1_NULL"]
-    if v[4].startswith("POLY"):
-        return ["-DRELAY_K1_POLY_EVERY=%s" % v[4][4:]]
+    if v[4].startswith("S"):
+        return ["-DRELAY_PRODUCER_SLEEP_NS=%s" % v[4][1:]]
     return []
 
 

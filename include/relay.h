@@ -125,11 +125,12 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
 relay_status_t relay_cueset_destroy(relay_cueset_t cs);
 int32_t relay_cueset_n_cues(relay_cueset_t cs);
 
-/* Workspace for cue_scan + segment_reduce (n_tok positions, n_occ occurrence
- * capacity) and for step_switch (batch rows); one buffer may serve all calls
- * that run in stream order.  The step_switch part holds arrival counters that
- * must be zero before first use: call relay_workspace_init once (the kernels
- * leave them zero again, so graph replays need no reset). */
+/* Workspace bytes for cue_scan + segment_reduce (n_tok positions) or for
+ * step_switch (batch rows).  Use one workspace for cue_scan/segment_reduce
+ * and a separate one for step_switch.  Both hold counters/flags that must be
+ * zero before first use: call relay_workspace_init once after allocating
+ * (the kernels leave them zero again, so CUDA-graph replays need no reset).
+ * One workspace must not be used by two calls running concurrently. */
 size_t relay_workspace_bytes(int64_t n_tok, int64_t occ_capacity, int32_t batch);
 relay_status_t relay_workspace_init(void* ws, size_t ws_bytes, relay_stream_t stream);
 

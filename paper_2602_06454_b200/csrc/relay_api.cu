@@ -65,11 +65,10 @@ ScanWs scan_ws_layout(void* base, long long n_tok, long long cap) {
     return q;
   };
   w.tile_count = reinterpret_cast<int*>(take(sizeof(int) * nt));
-  w.tile_head = reinterpret_cast<Agg*>(take(sizeof(Agg) * nt));
-  w.tile_carry = reinterpret_cast<Agg*>(take(sizeof(Agg) * nt));
-  w.occ_sumq = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * (cap + 1)));
-  w.occ_low = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (cap + 1)));
-  w.occ_nan = reinterpret_cast<unsigned int*>(take(sizeof(unsigned int) * (cap + 1)));
+  w.tile_flag = reinterpret_cast<int*>(take(sizeof(int) * nt));
+  w.tile_val = reinterpret_cast<Agg*>(take(sizeof(Agg) * nt));
+  w.done = reinterpret_cast<int*>(take(sizeof(int)));
+  (void)cap;
   w.bytes = off;
   return w;
 }

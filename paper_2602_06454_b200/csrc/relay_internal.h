@@ -41,14 +41,13 @@ struct Agg {
   int pad;
 };
 
-// Workspace layouts (256-byte aligned pieces).
+// Workspace layouts (256-byte aligned pieces).  tile_flag and done must be
+// zero before the first K3 launch (relay_workspace_init); K3 leaves them zero.
 struct ScanWs {
-  int* tile_count;     // [n_tiles]
-  Agg* tile_head;      // [n_tiles]
-  Agg* tile_carry;     // [n_tiles]
-  unsigned long long* occ_sumq;  // [cap]
-  unsigned int* occ_low;         // [cap]
-  unsigned int* occ_nan;         // [cap]
+  int* tile_count;     // [n_tiles] K2 per-tile occurrence counts
+  int* tile_flag;      // [n_tiles] K3 look-back state (0 / head / inclusive)
+  Agg* tile_val;       // [n_tiles] K3 published aggregates
+  int* done;           // [1] K3 finished-tile counter
   size_t bytes;
 };
 ScanWs scan_ws_layout(void* base, long long n_tok, long long cap);

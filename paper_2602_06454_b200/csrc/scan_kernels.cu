@@ -7,10 +7,12 @@
 //     by position with no atomics (deterministic).
 // K3: post-sentence windows as a REVERSE segmented scan
 //     keyed by segment tails (terminator or trajectory end): the aggregate at
-//     s over [s, first tail >= s] is exactly the window of a cue at s.
-//     Tile heads -> cross-tile carries -> per-position suffix aggregates
-//     gathered at occurrence starts -> per-cue integer moments (u64 atomics:
-//     order-free, so bit-identical across launch shapes and ranks).
+//     s over [s, first tail >= s] is exactly the window of a cue at s.  One
+//     kernel: tiles run right to left and take their carry from the tiles to
+//     the right with a decoupled look-back (nearly every 2,048-token tile
+//     holds a sentence end, so the look-back stops at the next tile), then
+//     gather at occurrence starts and add per-cue integer moments (u64
+//     atomics: order-free, so bit-identical across launch shapes and ranks).
 // Both are tiny next to K1 (4 B per token vs ~300 KB per logit row).
 #include <cfloat>
 
@@ -297,20 +299,66 @@ __device__ __forceinline__ void load_positions(const float* __restrict__ margin,
   }
 }
 
-// K3a: tile heads + global moments.
+// Is there a terminator in [a, b] (inclusive; a <= b)?  Word-wise scan.
+__device__ __forceinline__ bool any_term(const uint32_t* __restrict__ term_bits, long long a,
+                                         long long b) {
+  long long w0 = a >> 5, w1 = b >> 5;
+  for (long long w = w0; w <= w1; w++) {
+    uint32_t m = term_bits[w];
+    if (w == w0) m &= 0xffffffffu << (a & 31);
+    if (w == w1 && (b & 31) != 31) m &= (2u << (b & 31)) - 1u;
+    if (m) return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ int lower_bound_occ(const int* occ_pos, int n, long long key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (occ_pos[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Published per-tile state for the reverse decoupled look-back.
+constexpr int kTileHead = 1;   // value = aggregate from the tile start to its first tail
+constexpr int kTileIncl = 2;   // value = aggregate from the tile start onwards (carry included)
+
+__device__ __forceinline__ void publish(int* flag, Agg* val, const Agg& a, int state) {
+  val->sumq = a.sumq; val->low = a.low; val->nan = a.nan; val->mn = a.mn;
+  val->end = a.end; val->tail = a.tail; val->pad = 0;
+  __threadfence();
+  atomicExch(flag, state);
+}
+
+// K3: one pass per 2,048-position tile.  Tiles are processed right to left
+// (tile = n_tiles-1-blockIdx.x), so a tile's carry comes from tiles that were
+// dispatched earlier: the reverse segmented scan of (sum q, low, NaN, min, end)
+// keyed by segment tails gives, at every position s, the aggregate over
+// [s, first tail >= s] — the post-sentence window of a cue at s.  The same pass
+// adds the global moments and every occurrence's window to the stats table.
 __global__ void __launch_bounds__(kScanThreads)
-    seg_head_kernel(const float* __restrict__ margin, const uint32_t* __restrict__ term_bits,
-                    long long n_tok, const long long* __restrict__ offs, int n_traj,
-                    const long long* __restrict__ think_end, float tau, Agg* __restrict__ tile_head,
-                    unsigned long long* __restrict__ grow, int nf, int rank) {
+    seg_fused_kernel(CueDev cs, const float* __restrict__ margin, const uint32_t* __restrict__ term_bits,
+                     long long n_tok, const long long* __restrict__ offs, int n_traj,
+                     const long long* __restrict__ think_end, float tau, const int* __restrict__ occ_pos,
+                     const int* __restrict__ occ_pat, const long long* __restrict__ n_occ_p, long long cap,
+                     int* __restrict__ seg_end, float* __restrict__ seg_mean, float* __restrict__ seg_min,
+                     float* __restrict__ seg_lowfrac, unsigned long long* __restrict__ stats, int nf,
+                     int rank, int* tile_flag, Agg* tile_val, int* done) {
   __shared__ Agg s_w[kScanThreads / 32];
+  __shared__ Agg s_carry;
   __shared__ unsigned long long s_red[kScanThreads / 32][5];
   __shared__ float s_min[kScanThreads / 32];
-  const long long base = static_cast<long long>(blockIdx.x) * kTile;
+  const int n_tiles = gridDim.x;
+  const int tile = n_tiles - 1 - blockIdx.x;
+  const long long base = static_cast<long long>(tile) * kTile;
   const long long p0 = base + threadIdx.x * kItems;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   PosVal pv[kItems];
   load_positions(margin, term_bits, n_tok, offs, n_traj, think_end, tau, p0, pv);
-  // thread head: v0 (+) v1 (+) ... (+) v7
+
+  // ---- thread / warp / tile aggregates and global moments
   Agg h = pv[kItems - 1].v;
   unsigned long long gn = 0, gs = 0, gs2 = 0, glow = 0, gnan = 0;
   float gmin = INFINITY;
@@ -327,12 +375,11 @@ __global__ void __launch_bounds__(kScanThreads)
       }
     }
   }
-  // ordered warp reduce (offsets 1,2,4,...: lane 0 covers lanes 0..31 in order)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Agg x = h;  // inclusive suffix over lanes (lane i: lanes i..31)
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    Agg o = shfl_down_agg(h, off);
-    if (lane + off < 32) h = agg_suffix(h, o);
+    Agg o = shfl_down_agg(x, off);
+    if (lane + off < 32) x = agg_suffix(x, o);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -344,16 +391,15 @@ __global__ void __launch_bounds__(kScanThreads)
     gmin = fminf(gmin, __shfl_xor_sync(kFull, gmin, off));
   }
   if (lane == 0) {
-    s_w[warp] = h;
+    s_w[warp] = x;
     s_red[warp][0] = gn; s_red[warp][1] = gs; s_red[warp][2] = gs2;
     s_red[warp][3] = glow; s_red[warp][4] = gnan;
     s_min[warp] = gmin;
   }
   __syncthreads();
+
   if (threadIdx.x == 0) {
-    Agg t = s_w[kScanThreads / 32 - 1];
-    for (int w = kScanThreads / 32 - 2; w >= 0; w--) t = agg_suffix(s_w[w], t);
-    tile_head[blockIdx.x] = t;
+    unsigned long long* grow = stats + static_cast<size_t>(cs.n_cues) * nf;
     unsigned long long a[5] = {0, 0, 0, 0, 0};
     float mn = INFINITY;
     for (int w = 0; w < kScanThreads / 32; w++) {
@@ -371,93 +417,40 @@ __global__ void __launch_bounds__(kScanThreads)
                 static_cast<unsigned long long>(__float_as_uint(fminf(fmaxf(mn, 0.0f), 1.0f))));
     }
     if (a[4]) atomicAdd(grow + 7, a[4]);  // NaN positions
-  }
-  (void)nf;
-}
 
-// K3b: carry[k] = head[k+1] (+) head[k+2] (+) ... (exclusive suffix), one CTA.
-__global__ void __launch_bounds__(1024) seg_carry_kernel(const Agg* __restrict__ head,
-                                                         Agg* __restrict__ carry, int n_tiles) {
-  __shared__ Agg s[1024];
-  __shared__ Agg s_run;
-  if (threadIdx.x == 0) s_run = agg_identity();
+    // ---- tile head, publish, reverse look-back for the carry
+    Agg head = s_w[kScanThreads / 32 - 1];
+    for (int w = kScanThreads / 32 - 2; w >= 0; w--) head = agg_suffix(s_w[w], head);
+    Agg carry = agg_identity();
+    if (head.tail) {
+      publish(tile_flag + tile, tile_val + tile, head, kTileIncl);
+    } else {
+      publish(tile_flag + tile, tile_val + tile, head, kTileHead);
+      for (int j = tile + 1; j < n_tiles; j++) {
+        int f;
+        while ((f = *reinterpret_cast<volatile int*>(tile_flag + j)) == 0) {
+        }
+        __threadfence();
+        Agg v;
+        v.sumq = __ldcg(&tile_val[j].sumq); v.low = __ldcg(&tile_val[j].low);
+        v.nan = __ldcg(&tile_val[j].nan); v.mn = __ldcg(&tile_val[j].mn);
+        v.end = __ldcg(&tile_val[j].end); v.tail = __ldcg(&tile_val[j].tail); v.pad = 0;
+        carry = agg_suffix(carry, v);
+        if (f == kTileIncl || v.tail) break;
+      }
+      publish(tile_flag + tile, tile_val + tile, agg_suffix(head, carry), kTileIncl);
+    }
+    s_carry = carry;
+  }
   __syncthreads();
-  // process chunks of 1024 tiles from the right end
-  for (int hi = n_tiles; hi > 0; hi -= 1024) {
-    const int lo = max(0, hi - 1024);
-    const int n = hi - lo;
-    const int i = threadIdx.x;
-    s[i] = (i < n) ? head[lo + i] : agg_identity();
-    __syncthreads();
-    // inclusive suffix scan within the chunk (Hillis-Steele, right to left)
-    for (int off = 1; off < 1024; off <<= 1) {
-      Agg v = s[i];
-      Agg r = (i + off < n) ? s[i + off] : agg_identity();
-      __syncthreads();
-      if (i + off < n) s[i] = agg_suffix(v, r);
-      __syncthreads();
-    }
-    if (i < n) {
-      Agg nxt = (i + 1 < n) ? agg_suffix(s[i + 1], s_run) : s_run;
-      carry[lo + i] = nxt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_run = agg_suffix(s[0], s_run);
-    __syncthreads();
-  }
-}
 
-__device__ __forceinline__ int lower_bound_occ(const int* occ_pos, int n, long long key) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (occ_pos[mid] < key) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// K3c: per-position suffix aggregates in this tile, gathered at occurrences.
-__global__ void __launch_bounds__(kScanThreads)
-    seg_gather_kernel(const float* __restrict__ margin, const uint32_t* __restrict__ term_bits,
-                      long long n_tok, const long long* __restrict__ offs, int n_traj, float tau,
-                      const Agg* __restrict__ tile_carry, const int* __restrict__ occ_pos,
-                      const long long* __restrict__ n_occ_p, long long cap, int* __restrict__ seg_end,
-                      float* __restrict__ seg_mean, float* __restrict__ seg_min,
-                      float* __restrict__ seg_lowfrac, unsigned long long* __restrict__ occ_sumq,
-                      unsigned int* __restrict__ occ_low, unsigned int* __restrict__ occ_nan) {
-  __shared__ Agg s_w[kScanThreads / 32];
-  __shared__ int s_range[2];
+  // ---- per-position suffix aggregates, gathered at the occurrences
   const long long nocc_ll = *n_occ_p < cap ? *n_occ_p : cap;
   const int nocc = static_cast<int>(nocc_ll);
-  const long long base = static_cast<long long>(blockIdx.x) * kTile;
-  if (threadIdx.x == 0) {
-    s_range[0] = lower_bound_occ(occ_pos, nocc, base);
-    s_range[1] = lower_bound_occ(occ_pos, nocc, base + kTile);
-  }
-  __syncthreads();
-  if (s_range[0] == s_range[1]) return;  // no occurrence starts in this tile
-  const long long p0 = base + threadIdx.x * kItems;
-  PosVal pv[kItems];
-  load_positions(margin, term_bits, n_tok, offs, n_traj, nullptr, tau, p0, pv);
-  Agg h = pv[kItems - 1].v;
-#pragma unroll
-  for (int i = kItems - 2; i >= 0; i--) h = agg_suffix(pv[i].v, h);
-  // inclusive suffix scan over lanes (lane i: lanes i..31)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Agg x = h;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    Agg o = shfl_down_agg(x, off);
-    if (lane + off < 32) x = agg_suffix(x, o);
-  }
-  if (lane == 0) s_w[warp] = x;
-  __syncthreads();
-  // carry into this warp: warps to the right, then the tile carry
-  Agg wc = tile_carry[blockIdx.x];
+  Agg wc = s_carry;
   for (int w = kScanThreads / 32 - 1; w > warp; w--) wc = agg_suffix(s_w[w], wc);
   Agg nx = shfl_down_agg(x, 1);  // lanes i+1..31
-  Agg cin = (lane < 31) ? agg_suffix(nx, wc) : wc;
-  // per-position suffix aggregates (right to left), gather at occurrences
+  const Agg cin = (lane < 31) ? agg_suffix(nx, wc) : wc;
   Agg sfx[kItems];
   Agg run = cin;
 #pragma unroll
@@ -465,66 +458,67 @@ __global__ void __launch_bounds__(kScanThreads)
     run = agg_suffix(pv[i].v, run);
     sfx[i] = run;
   }
-  int lo = lower_bound_occ(occ_pos + s_range[0], s_range[1] - s_range[0], p0) + s_range[0];
-  for (int o = lo; o < s_range[1]; o++) {
-    const long long s = occ_pos[o];
-    if (s >= p0 + kItems) break;
-    const Agg a = sfx[s - p0];
-    const int len = a.end - static_cast<int>(s) + 1;
-    seg_end[o] = a.end;
-    occ_sumq[o] = a.sumq;
-    occ_low[o] = a.low;
-    occ_nan[o] = a.nan;
-    if (a.nan) {
-      seg_mean[o] = qnan(); seg_min[o] = qnan(); seg_lowfrac[o] = qnan();
-    } else {
-      seg_mean[o] = static_cast<float>(static_cast<double>(a.sumq) / (1048576.0 * len));
-      seg_min[o] = a.mn;
-      seg_lowfrac[o] = static_cast<float>(static_cast<double>(a.low) / len);
+  if (nocc > 0 && p0 < n_tok) {
+    const int lo = lower_bound_occ(occ_pos, nocc, p0);
+    for (int o = lo; o < nocc; o++) {
+      const long long s = occ_pos[o];
+      if (s >= p0 + kItems) break;
+      Agg a = sfx[0];
+#pragma unroll
+      for (int i = 1; i < kItems; i++)
+        if (s == p0 + i) a = sfx[i];
+      const int len = a.end - static_cast<int>(s) + 1;
+      seg_end[o] = a.end;
+      if (a.nan) {
+        seg_mean[o] = qnan(); seg_min[o] = qnan(); seg_lowfrac[o] = qnan();
+      } else {
+        seg_mean[o] = static_cast<float>(static_cast<double>(a.sumq) / (1048576.0 * len));
+        seg_min[o] = a.mn;
+        seg_lowfrac[o] = static_cast<float>(static_cast<double>(a.low) / len);
+      }
+      // trigger (R13): no occurrence starts earlier in the same sentence,
+      // i.e. the previous start is in another trajectory or a terminator lies
+      // in [previous start, s - 1]
+      const int k = find_traj(offs, n_traj, n_tok, s);
+      int j = o - 1;
+      while (j >= 0 && occ_pos[j] == s) j--;
+      bool trig = true;
+      if (j >= 0) {
+        const long long pp = occ_pos[j];
+        const long long ts = offs ? offs[k] : 0;
+        trig = (pp < ts) || any_term(term_bits, pp, s - 1);
+      }
+      if (think_end && k >= 0 && s >= think_end[k]) continue;
+      const int cue = cs.cue_of_orig[occ_pat[o]];
+      unsigned long long* row = stats + static_cast<size_t>(cue) * nf;
+      if (a.nan) {
+        atomicAdd(row + 7, 1ull);
+        continue;
+      }
+      const unsigned long long ln = static_cast<unsigned long long>(len);
+      const unsigned long long sq = a.sumq;
+      const unsigned long long mq = (2 * sq + ln) / (2 * ln);  // round half up
+      atomicAdd(row + 0, 1ull);
+      atomicAdd(row + 1, mq);
+      atomicAdd(row + 2, mq * mq);
+      atomicAdd(row + 3, sq);
+      atomicAdd(row + 4, ln);
+      atomicAdd(row + 5, static_cast<unsigned long long>(a.low));
+      if (trig) atomicAdd(row + 6, 1ull);
+      atomicMin(row + kStatFields + rank,
+                static_cast<unsigned long long>(__float_as_uint(fminf(fmaxf(a.mn, 0.0f), 1.0f))));
     }
   }
-}
 
-// K3d: per-occurrence statistics into the cue rows.
-__global__ void __launch_bounds__(256)
-    seg_stats_kernel(CueDev cs, long long n_tok, const long long* __restrict__ offs, int n_traj,
-                     const long long* __restrict__ think_end, const int* __restrict__ occ_pos,
-                     const int* __restrict__ occ_pat, const long long* __restrict__ n_occ_p,
-                     long long cap, const int* __restrict__ seg_end, const float* __restrict__ seg_min,
-                     const unsigned long long* __restrict__ occ_sumq,
-                     const unsigned int* __restrict__ occ_low, const unsigned int* __restrict__ occ_nan,
-                     unsigned long long* __restrict__ stats, int nf, int rank) {
-  const long long nocc = *n_occ_p < cap ? *n_occ_p : cap;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nocc;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int s = occ_pos[i];
-    const int e = seg_end[i];
-    // trigger: no occurrence starts earlier in the same sentence (R13)
-    long long j = i - 1;
-    while (j >= 0 && occ_pos[j] == s) j--;
-    const unsigned long long trig = (j < 0 || seg_end[j] != e) ? 1ull : 0ull;
-    if (think_end) {
-      const int k = find_traj(offs, n_traj, n_tok, s);
-      if (k >= 0 && s >= think_end[k]) continue;
+  // ---- the last tile to finish resets the look-back flags for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1) == n_tiles - 1) {
+      for (int j = 0; j < n_tiles; j++) tile_flag[j] = 0;
+      __threadfence();
+      *done = 0;
     }
-    const int cue = cs.cue_of_orig[occ_pat[i]];
-    unsigned long long* row = stats + static_cast<size_t>(cue) * nf;
-    if (occ_nan[i]) {
-      atomicAdd(row + 7, 1ull);
-      continue;
-    }
-    const unsigned long long len = static_cast<unsigned long long>(e - s + 1);
-    const unsigned long long sq = occ_sumq[i];
-    const unsigned long long mq = (2 * sq + len) / (2 * len);  // round half up
-    atomicAdd(row + 0, 1ull);
-    atomicAdd(row + 1, mq);
-    atomicAdd(row + 2, mq * mq);
-    atomicAdd(row + 3, sq);
-    atomicAdd(row + 4, len);
-    atomicAdd(row + 5, static_cast<unsigned long long>(occ_low[i]));
-    if (trig) atomicAdd(row + 6, 1ull);
-    atomicMin(row + kStatFields + rank,
-              static_cast<unsigned long long>(__float_as_uint(fminf(fmaxf(seg_min[i], 0.0f), 1.0f))));
   }
 }
 
@@ -566,24 +560,10 @@ cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long lo
   if (n_tok <= 0) return cudaSuccess;
   const int nt = n_tiles_of(n_tok);
   const int nf = kStatFields + world;
-  unsigned long long* grow = stats + static_cast<size_t>(cs.n_cues) * nf;
-  seg_head_kernel<<<nt, kScanThreads, 0, st>>>(margin, term_bits, n_tok, offs, n_traj, think_end,
-                                               tau, ws.tile_head, grow, nf, rank);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  seg_carry_kernel<<<1, 1024, 0, st>>>(ws.tile_head, ws.tile_carry, nt);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (cap <= 0) return cudaSuccess;
-  seg_gather_kernel<<<nt, kScanThreads, 0, st>>>(margin, term_bits, n_tok, offs, n_traj, tau,
-                                                 ws.tile_carry, occ_pos, n_occ, cap, seg_end,
-                                                 seg_mean, seg_min, seg_lowfrac, ws.occ_sumq,
-                                                 ws.occ_low, ws.occ_nan);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  long long blocks = (cap + 255) / 256;
-  if (blocks > 1184) blocks = 1184;
-  seg_stats_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-      cs, n_tok, offs, n_traj, think_end, occ_pos, occ_pat, n_occ, cap, seg_end, seg_min,
-      ws.occ_sumq, ws.occ_low, ws.occ_nan, stats, nf, rank);
+  seg_fused_kernel<<<nt, kScanThreads, 0, st>>>(cs, margin, term_bits, n_tok, offs, n_traj, think_end,
+                                                tau, occ_pos, occ_pat, n_occ, cap, seg_end, seg_mean,
+                                                seg_min, seg_lowfrac, stats, nf, rank, ws.tile_flag,
+                                                ws.tile_val, ws.done);
   return cudaGetLastError();
 }
 

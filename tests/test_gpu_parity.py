@@ -477,3 +477,57 @@ def test_step_switch_graph_replay(relay):
         np.testing.assert_array_equal(d_state.cpu().numpy(), state)
         np.testing.assert_array_equal(d_hist.cpu().numpy(), hist)
     del rng
+
+
+def _segment_custom(relay, tokens, offs, margins, h, tau=0.5, think=None, mode=0):
+    cs = relay.CueSet.from_synth(h, mode=mode)
+    tok = torch.as_tensor(np.asarray(tokens, np.int32), device=DEV)
+    d_offs = torch.as_tensor(np.asarray(offs, np.int64), device=DEV)
+    tep = None if think is None else torch.as_tensor(np.asarray(think, np.int64), device=DEV)
+    scan = relay.cue_scan(cs, tok, d_offs)
+    seg = relay.segment_reduce(cs, torch.as_tensor(margins, device=DEV), scan, d_offs, tep, tau=tau)
+    torch.cuda.synchronize()
+    o_scan, o_win, o_sum = oracle.analyze(margins, tokens, offs, h.pat_tokens, h.pat_offsets,
+                                          h.pat_cue, h.n_cues, h.terminator, tau=tau,
+                                          think_end_pos=think, mode=mode, min_count=1)
+    _compare_segments(relay, h, scan, seg, o_scan, o_win, o_sum)
+
+
+def test_segment_reduce_windows_spanning_tiles(relay):
+    """Unterminated runs longer than several 2,048-token tiles: the look-back
+    must chain tile heads until a sentence end (K3 carry)."""
+    h = synth.make_cueset(8192, 3, 4, max_len=2, seed=81)
+    rng = np.random.default_rng(82)
+    n = 20000
+    tokens = rng.integers(synth.OTHER_BASE, 8192, n).astype(np.int32)
+    for s in (5, 1000, 2047, 2048, 4100, 9000, 15000, 19990):      # cue starts
+        p = h.patterns[int(rng.integers(0, len(h.patterns)))]
+        tokens[s:s + len(p)] = p
+    tokens[13000] = synth.TERMINATOR_IDS[0]                          # one sentence end
+    m = synth.make_margins(n, seed=83)
+    _segment_custom(relay, tokens, [0, n], m, h)
+    _segment_custom(relay, tokens, [0, 7000, 7000, 16000, n], m, h, think=[6000, 7000, 15500, n])
+
+
+def test_segment_reduce_many_tiny_trajectories(relay):
+    h = synth.make_cueset(4096, 3, 5, max_len=3, seed=84)
+    ts = synth.make_tokens(3000, 7, h, seed=85, cue_rate=0.7, mean_sentence=3)
+    m = synth.make_margins(ts.tokens.shape[0], seed=86, nan_rate=0.01)
+    _segment_custom(relay, ts.tokens, ts.traj_offsets, m, h, think=ts.think_end_pos)
+    _segment_custom(relay, ts.tokens, ts.traj_offsets, m, h, mode=1)
+
+
+def test_segment_reduce_graph_replay_resets_lookback(relay):
+    """K3's look-back flags are reset by the last tile: replays stay exact."""
+    h, cs = _cs_pair(relay, 151936, 8, 12, 3, seed=87)
+    ts = synth.make_tokens(2, 9000, h, seed=88)
+    m = torch.as_tensor(synth.make_margins(ts.tokens.shape[0], seed=89), device=DEV)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    ws = relay.workspace(tok.shape[0], tok.shape[0], 0, DEV)
+    scan = relay.cue_scan(cs, tok, offs, ws=ws)
+    first = relay.segment_reduce(cs, m, scan, offs, ws=ws)["stats"].clone()
+    for _ in range(5):
+        again = relay.segment_reduce(cs, m, scan, offs, ws=ws)["stats"]
+        torch.cuda.synchronize()
+        assert torch.equal(first, again)

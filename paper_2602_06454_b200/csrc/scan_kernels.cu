@@ -421,25 +421,25 @@ __global__ void __launch_bounds__(kScanThreads)
     // ---- tile head, publish, reverse look-back for the carry
     Agg head = s_w[kScanThreads / 32 - 1];
     for (int w = kScanThreads / 32 - 2; w >= 0; w--) head = agg_suffix(s_w[w], head);
+    // A head holding a tail is already this tile's inclusive value.  Every
+    // tile still needs its own carry (the run after its last tail), which the
+    // look-back assembles from the heads of the tiles to the right: it stops
+    // at the first head holding a tail or at an inclusive value.
+    publish(tile_flag + tile, tile_val + tile, head, head.tail ? kTileIncl : kTileHead);
     Agg carry = agg_identity();
-    if (head.tail) {
-      publish(tile_flag + tile, tile_val + tile, head, kTileIncl);
-    } else {
-      publish(tile_flag + tile, tile_val + tile, head, kTileHead);
-      for (int j = tile + 1; j < n_tiles; j++) {
-        int f;
-        while ((f = *reinterpret_cast<volatile int*>(tile_flag + j)) == 0) {
-        }
-        __threadfence();
-        Agg v;
-        v.sumq = __ldcg(&tile_val[j].sumq); v.low = __ldcg(&tile_val[j].low);
-        v.nan = __ldcg(&tile_val[j].nan); v.mn = __ldcg(&tile_val[j].mn);
-        v.end = __ldcg(&tile_val[j].end); v.tail = __ldcg(&tile_val[j].tail); v.pad = 0;
-        carry = agg_suffix(carry, v);
-        if (f == kTileIncl || v.tail) break;
+    for (int j = tile + 1; j < n_tiles; j++) {
+      int f;
+      while ((f = *reinterpret_cast<volatile int*>(tile_flag + j)) == 0) {
       }
-      publish(tile_flag + tile, tile_val + tile, agg_suffix(head, carry), kTileIncl);
+      __threadfence();
+      Agg v;
+      v.sumq = __ldcg(&tile_val[j].sumq); v.low = __ldcg(&tile_val[j].low);
+      v.nan = __ldcg(&tile_val[j].nan); v.mn = __ldcg(&tile_val[j].mn);
+      v.end = __ldcg(&tile_val[j].end); v.tail = __ldcg(&tile_val[j].tail); v.pad = 0;
+      carry = agg_suffix(carry, v);
+      if (f == kTileIncl || v.tail) break;
     }
+    if (!head.tail) publish(tile_flag + tile, tile_val + tile, agg_suffix(head, carry), kTileIncl);
     s_carry = carry;
   }
   __syncthreads();

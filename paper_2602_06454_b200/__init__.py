@@ -391,6 +391,34 @@ class Analyzer:
                        self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s)
         return self.stats
 
+    def run_streamed(self, chunks, tokens, traj_offsets=None, think_end_pos=None, stream=None,
+                     vocab=None):
+        """The same pass with the logits streamed in row chunks (configs[4]: a
+        corpus larger than HBM).  ``chunks`` yields (first_row, logits[R, V]);
+        each chunk's margins land at their row offset, then H2-H5 run once over
+        the whole token stream.  The caller may refill a chunk buffer as soon as
+        the stream has moved past its relay_margin_rows launch."""
+        import torch
+        s = torch.cuda.current_stream() if stream is None else stream
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+            self._fork = torch.cuda.Event()
+            self._join = torch.cuda.Event()
+        self._fork.record(s)
+        self._side.wait_event(self._fork)
+        cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
+        self._join.record(self._side)
+        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s)
+        for r0, chunk in chunks:
+            r1 = r0 + chunk.shape[0]
+            out = {k: (v[r0:r1] if v is not None else None) for k, v in self.rows.items()}
+            margin_rows(chunk, vocab=vocab or self.vocab, inv_temperature=self.iota, out=out,
+                        stream=s)
+        s.wait_event(self._join)
+        segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
+                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s)
+        return self.stats
+
     def capture(self, logits, tokens, traj_offsets=None, think_end_pos=None, host_stats=None,
                 vocab=None):
         """A CUDA graph of one device-side pass (+ the stats table copied to the
@@ -410,5 +438,5 @@ class Analyzer:
         return g
 
     def n_launches(self) -> int:
-        """Kernels launched by one run(): stats_init 1 + K1 1 + K2 2 + K3 4."""
-        return 8 if self.cap > 0 else 6
+        """Kernels launched by one run(): stats_init 1 + K1 1 + K2 2 + K3 1."""
+        return 5

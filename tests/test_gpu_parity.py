@@ -531,3 +531,88 @@ def test_segment_reduce_graph_replay_resets_lookback(relay):
         again = relay.segment_reduce(cs, m, scan, offs, ws=ws)["stats"]
         torch.cuda.synchronize()
         assert torch.equal(first, again)
+
+
+# ------------------------------------------------- full BASELINE sizes
+def test_c4_shape_sampled(relay):
+    """configs[3] corpus on one GPU (8 x 32,768 x 151,936 bf16, 79.7 GB): the
+    Analyzer pass; sampled rows vs the oracle; K2/K3 vs the oracle on two
+    sampled trajectories (trajectories are independent)."""
+    free = torch.cuda.mem_get_info()[0]
+    if free < 95e9:
+        pytest.skip("needs ~90 GB of free HBM")
+    h, cs = _cs_pair(relay, 151936, 8, 12, 3, seed=91)
+    ts = synth.make_tokens(8, 32768, h, seed=92)
+    n = ts.tokens.shape[0]
+    L = synth.make_logits(n, 151936, "bf16", tokens=ts.tokens, seed=93, device=DEV, chunk_rows=4096)
+    an = relay.Analyzer(cs, n, 151936, DEV)
+    an.run(L, torch.as_tensor(ts.tokens, device=DEV), torch.as_tensor(ts.traj_offsets, device=DEV),
+           torch.as_tensor(ts.think_end_pos, device=DEV))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(94)
+    rows = np.unique(np.concatenate([rng.choice(n, 60, replace=False), [0, 32767, 32768, n - 1]]))
+    ref = oracle.margin_rows(synth.host_rows(L[torch.as_tensor(rows, device=DEV)], "bf16"), dtype="bf16",
+                             threads=8)
+    got_m = an.rows["margin"][torch.as_tensor(rows, device=DEV)].cpu().numpy()
+    np.testing.assert_array_equal(an.rows["top1"][torch.as_tensor(rows, device=DEV)].cpu().numpy(), ref["top1"])
+    np.testing.assert_array_equal(an.rows["top2"][torch.as_tensor(rows, device=DEV)].cpu().numpy(), ref["top2"])
+    ok = ref["status"] == 0
+    assert np.abs(got_m[ok] - ref["margin"][ok]).max() < TOL
+    del L
+    torch.cuda.empty_cache()
+    # K2/K3 on the GPU margins' structure: occurrences and windows per sampled trajectory
+    nocc = int(an.scan["n_occ"].item())
+    occ = an.scan["occ_pos"][:nocc].cpu().numpy()
+    ends = an.seg["seg_end"][:nocc].cpu().numpy()
+    for k in (2, 7):
+        a, b = int(ts.traj_offsets[k]), int(ts.traj_offsets[k + 1])
+        o = oracle.cue_scan(ts.tokens[a:b], None, h.pat_tokens, h.pat_offsets, h.pat_cue, h.n_cues,
+                            h.terminator)
+        sel = (occ >= a) & (occ < b)
+        np.testing.assert_array_equal(occ[sel] - a, o["occ_pos"])
+        w = oracle.windows(np.zeros(b - a, np.float32), o["term"], None, o["occ_pos"], 0.5)
+        np.testing.assert_array_equal(ends[sel] - a, w["seg_end"])
+
+
+def test_c5_shape_streamed(relay):
+    """configs[4]: 64 x 16,384 tokens, 32 patterns of length 1-6, logits
+    streamed in 2,048-row chunks from a rotating pool (the 318 GB corpus never
+    exists at once).  Sampled rows vs the oracle; K2/K3 (on synthetic margins)
+    vs the oracle on three sampled trajectories."""
+    V, R, K = 151936, 2048, 4
+    h, cs = _cs_pair(relay, V, 32, 32, 6, seed=95, mode=0, min_len=1)
+    ts = synth.make_tokens(64, 16384, h, seed=96)
+    n = ts.tokens.shape[0]
+    pool = [synth.make_logits(R, V, "bf16", seed=97 + i, device=DEV) for i in range(K)]
+    an = relay.Analyzer(cs, n, V, DEV)
+    chunks = ((c * R, pool[c % K]) for c in range(n // R))
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    an.run_streamed(chunks, tok, offs)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(98)
+    rows = np.unique(np.concatenate([rng.choice(n, 40, replace=False), [0, n - 1]]))
+    for r in rows.tolist():
+        ref = oracle.margin_rows(synth.host_rows(pool[(r // R) % K][r % R:r % R + 1], "bf16"), dtype="bf16")
+        assert an.rows["top1"][r].item() == ref["top1"][0] and an.rows["top2"][r].item() == ref["top2"][0]
+        if ref["status"][0] == 0:
+            assert abs(an.rows["margin"][r].item() - ref["margin"][0]) < TOL
+    # stage-wise K2/K3 with synthetic margins on the full stream
+    m = synth.make_margins(n, seed=99)
+    seg = relay.segment_reduce(cs, torch.as_tensor(m, device=DEV), an.scan, offs, ws=an.ws)
+    torch.cuda.synchronize()
+    nocc = int(an.scan["n_occ"].item())
+    occ = an.scan["occ_pos"][:nocc].cpu().numpy()
+    pat = an.scan["occ_pat"][:nocc].cpu().numpy()
+    ends = seg["seg_end"][:nocc].cpu().numpy()
+    means = seg["seg_mean"][:nocc].cpu().numpy()
+    for k in (0, 33, 63):
+        a, b = int(ts.traj_offsets[k]), int(ts.traj_offsets[k + 1])
+        o = oracle.cue_scan(ts.tokens[a:b], None, h.pat_tokens, h.pat_offsets, h.pat_cue, h.n_cues,
+                            h.terminator)
+        w = oracle.windows(m[a:b], o["term"], None, o["occ_pos"], 0.5)
+        sel = (occ >= a) & (occ < b)
+        np.testing.assert_array_equal(occ[sel] - a, o["occ_pos"])
+        np.testing.assert_array_equal(pat[sel], o["occ_pat"])
+        np.testing.assert_array_equal(ends[sel] - a, w["seg_end"])
+        assert np.abs(means[sel] - w["seg_mean"]).max() < 1e-6

@@ -215,25 +215,146 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// ------------------------------------------------------------------- K1
-template <class E, int NCW, int NS, int UV, int MINB>
-__global__ void __launch_bounds__((NCW + 1) * 32, MINB)
-    margin_rows_tma_kernel(const typename E::T* __restrict__ logits, long long n_rows, int vocab,
-                           long long stride, float c, float iota, float* __restrict__ margin,
-                           int* __restrict__ top1, int* __restrict__ top2, float* __restrict__ lse,
-                           uint8_t* __restrict__ status) {
+// ------------------------------------------------- K1 / K4 row kernel
+// Work items are (row, part) pairs: part k of a row covers elements
+// [k*chunk, min(vocab, (k+1)*chunk)).  K1 uses one part per row; K4 (a
+// batch of only ~256 live rows) splits rows so that every SM streams, and the
+// last CTA to finish a row merges its parts (arrival counter, reset after use
+// so CUDA-graph replays need no reset).
+struct RowsArgs {
+  const void* logits;
+  long long n_rows;
+  int vocab;
+  long long stride;
+  float c, iota;
+  int nsplit, chunk;
+  float* margin;
+  int* top1;
+  int* top2;
+  float* lse;
+  uint8_t* status;
+  int* counter;   // [n_rows] (nsplit > 1)
+  float* part;    // [n_rows][nsplit][kPartWords] (nsplit > 1)
+  // decode-step switch (STEP)
+  const int* sampled;
+  uint8_t* state;
+  int* hist;
+  int* small_run;
+  float gate;
+  int max_seg;
+  uint8_t* flag;
+  int16_t* cue_id;
+};
+
+constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
+
+struct SmemCue {
+  int tok[kMaxPat * kMaxLen];
+  int len[kMaxPat];
+  int cue[kMaxPat];
+};
+
+// Runtime switching (§4.3, fig:mechanism P:209-216) for one
+// sequence, by one warp: lanes test the (length-sorted) patterns as suffixes of
+// hist ++ tok in parallel; the lowest matching lane is the longest pattern.
+__device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float m, uint8_t* state_p,
+                            int* hist, int* small_run_p, float gate, int max_seg, uint8_t* flag_out,
+                            int16_t* cue_out) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t state = *state_p;
+  const bool valid = tok >= 0 && tok < cs.vocab && !(state & 2);
+  // seq[0..6] = hist (oldest first), seq[7] = tok; lane i < 8 holds seq[i]
+  int mine = -1;
+  if (lane < kHist) mine = hist[lane];
+  if (lane == kHist) mine = tok;
+  int best = -1;
+  if (valid && tok != cs.think_end && (state & 1) == 0) {
+    for (int base = 0; base < cs.n_pat; base += 32) {
+      const int p = base + lane;
+      bool ok = p < cs.n_pat;
+      const int len = ok ? sc.len[p] : 0;
+#pragma unroll
+      for (int i = 0; i < kMaxLen; i++) {
+        const int v = __shfl_sync(kFull, mine, i);
+        const int k = i - (kMaxLen - len);  // pattern position of seq[i]
+        if (ok && k >= 0 && v != sc.tok[p * kMaxLen + k]) ok = false;
+      }
+      const unsigned b = __ballot_sync(kFull, ok);
+      if (b) { best = base + __ffs(b) - 1; break; }
+    }
+  }
+  if (lane != 0) return;
+  int cue = -1, flag = 0;
+  uint8_t st = state;
+  if (valid) {
+    const int sr = small_run_p ? *small_run_p : 0;
+    bool clear = false;
+    if (tok == cs.think_end) {
+      flag = 3; st = 3; clear = true;
+    } else if ((state & 1) == 0) {
+      if (best >= 0 && !(gate >= 0.0f && m < gate)) {
+        flag = 1; cue = sc.cue[best]; st = 1; clear = true;
+      } else {
+        for (int k = 0; k < kHist - 1; k++) hist[k] = hist[k + 1];
+        hist[kHist - 1] = tok;
+      }
+    } else {
+      const bool term = (cs.term_tab[tok >> 5] >> (tok & 31)) & 1u;
+      if (term) {
+        flag = 2; st = 0; clear = true;
+      } else if (max_seg > 0 && sr + 1 >= max_seg) {
+        flag = 4; st = 0; clear = true;
+      } else if (small_run_p) {
+        *small_run_p = sr + 1;
+      }
+    }
+    if (clear) {
+      for (int k = 0; k < kHist; k++) hist[k] = -1;
+      if (small_run_p) *small_run_p = 0;
+    }
+    *state_p = st;
+  }
+  *flag_out = static_cast<uint8_t>(flag);
+  *cue_out = static_cast<int16_t>(cue);
+}
+
+// Warp-level finish of row r from its merged partial (lane 0 writes).
+template <class E, bool STEP>
+__device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs, const SmemCue& sc,
+                                            long long r, const Partial& q, bool exact, float S) {
+  const RowOut o = finish_row(q, a.c, a.iota, exact, S);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    a.margin[r] = o.margin;
+    if (a.top1) a.top1[r] = o.i1;
+    if (a.top2) a.top2[r] = o.i2;
+    if (a.lse) a.lse[r] = o.lse;
+    if (a.status) a.status[r] = static_cast<uint8_t>(o.status);
+  }
+  if constexpr (STEP) {
+    const int tok = a.sampled ? a.sampled[r] : o.i1;
+    switch_warp(cs, sc, tok, o.margin, a.state + r, a.hist + r * kHist,
+                a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r, a.cue_id + r);
+  }
+}
+
+template <class E, int NCW, int NS, int UV, int MINB, bool STEP>
+__global__ void __launch_bounds__((NCW + 1) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
   constexpr int NCT = NCW * 32;             // consumer threads
   constexpr int SB = UV * NCT * 16;         // bytes per ring stage
+  constexpr int NRED = NCW * 8;             // partials per item after 2 shuffle rounds
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
-  constexpr int NRED = NCW * 8;             // partials per row after 2 shuffle rounds
   __shared__ int s_theta[2];
   __shared__ Partial s_red[2][NRED];
   __shared__ float s_sum[2][NCW];
+  __shared__ SmemCue sc;
 
+  const T* logits = static_cast<const T*>(a.logits);
+  const long long n_items = a.n_rows * a.nsplit;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t ring_s = smem_u32_pinned(ring);
@@ -247,6 +368,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
     s_theta[0] = s_theta[1] = fkey(-INFINITY);
     fence_barrier_init();
   }
+  if constexpr (STEP) {
+    for (int i = tid; i < cs.n_pat * kMaxLen; i += blockDim.x) sc.tok[i] = cs.pat_tok[i];
+    for (int i = tid; i < cs.n_pat; i += blockDim.x) {
+      sc.len[i] = cs.pat_len[i];
+      sc.cue[i] = cs.pat_cue[i];
+    }
+  }
   __syncthreads();
 
   if (warp == NCW) {
@@ -255,10 +383,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (long long r = blockIdx.x; r < n_rows; r += gridDim.x) {
-        const T* row = logits + r * stride;
-        const Geom g = row_geom<E>(row, 0, vocab);
-        const char* src = reinterpret_cast<const char*>(row + g.head);
+      for (long long w = blockIdx.x; w < n_items; w += gridDim.x) {
+        const long long r = w / a.nsplit;
+        const int j0 = static_cast<int>(w % a.nsplit) * a.chunk;
+        const int j1 = min(a.vocab, j0 + a.chunk);
+        const T* row = logits + r * a.stride;
+        const Geom g = row_geom<E>(row, j0, j1);
+        const char* src = reinterpret_cast<const char*>(row + j0 + g.head);
         for (int off = 0; off < g.body; off += SB) {
           const uint32_t bytes = static_cast<uint32_t>(min(SB, g.body - off));
           mbar_wait_sleep(empty_s + 8 * stage, phase ^ 1);
@@ -272,20 +403,24 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
   }
 
   // -------------------------------------------------- consumer warps
+  const float c = a.c;
   int stage = 0;
   uint32_t phase = 0;
   int it = 0;
-  for (long long r = blockIdx.x; r < n_rows; r += gridDim.x, ++it) {
+  for (long long w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    const long long r = w / a.nsplit;
+    const int j0 = static_cast<int>(w % a.nsplit) * a.chunk;
+    const int j1 = min(a.vocab, j0 + a.chunk);
     int* theta_p = &s_theta[it & 1];
-    const T* row = logits + r * stride;
-    const Geom g = row_geom<E>(row, 0, vocab);
+    const T* row = logits + r * a.stride;
+    const Geom g = row_geom<E>(row, j0, j1);
     ThreadState st;
     state_init(st);
     float theta_w = -INFINITY;  // warp-local lower bound of the row's 2nd-best
-    if (tid < g.head) consume_scalar(E::load1(row + tid), tid, st, c);
+    if (tid < g.head) consume_scalar(E::load1(row + j0 + tid), j0 + tid, st, c);
     for (int off = 0; off < g.body; off += SB) {
       const int bytes = min(SB, g.body - off);
-      const int jb = g.head + off / E::SZ;
+      const int jb = j0 + g.head + off / E::SZ;
       mbar_wait(full_s + 8 * stage, phase);
       const uint32_t buf = ring_s + stage * SB;
       bool slow = false;
@@ -297,7 +432,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
         if (lane == 0) mbar_arrive(empty_s + 8 * stage);  // release orders the loads above
         const float2 h = stage_max2<E, UV>(raw);
         if (off == 0) {
-          // row-start probe: the two half maxima are two distinct elements, so
+          // item-start probe: the two half maxima are two distinct elements, so
           // the warp's second-best of them bounds the row's 2nd-best from below
           theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
         }
@@ -316,46 +451,73 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB)
       if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
-    if (tid < vocab - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
+    if (tid < j1 - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
 
-    // ------------------------------------------------ row epilogue
+    // ------------------------------------------------ item epilogue
     // Two shuffle rounds leave 8 partials per warp in smem; one warp merges
-    // them (the other warps go straight on to the next row).
+    // them (the other warps go straight on to the next item).
     Partial p = thread_partial(st);
     p = partial_merge(p, shfl_xor_partial(p, 16));
     p = partial_merge(p, shfl_xor_partial(p, 8));
     if (lane < 8) s_red[it & 1][warp * 8 + lane] = p;
     if (tid == 0) s_theta[(it + 1) & 1] = fkey(-INFINITY);
     named_bar(1, NCT);
-    // s_red[it & 1] is rewritten only after the next row's barrier, which
+    // s_red[it & 1] is rewritten only after the next item's barrier, which
     // every warp reaches after these reads, so the decision is uniform.
     bool huge_lane = false;
 #pragma unroll
     for (int e = lane; e < NRED; e += 32) huge_lane |= (s_red[it & 1][e].flags & kFlagHuge) != 0;
-    const bool huge = __any_sync(kFull, huge_lane);
-    if (huge || warp == 0) {
-      Partial q = partial_empty();
+    const bool huge = __any_sync(kFull, huge_lane) && a.nsplit == 1;
+    if (!(huge || warp == 0)) continue;
+    Partial q = partial_empty();
 #pragma unroll
-      for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[it & 1][e]);
-      q = warp_reduce_partial(q);
+    for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[it & 1][e]);
+    q = warp_reduce_partial(q);
+    if (a.nsplit == 1) {
       bool exact = false;
       float S = 0.0f;
       if (huge) {
         // rare: every consumer joins an exact second pass over the row
-        const float s = warp_sum(exact_sum_thread<E>(row, vocab, q.t.v1, c, tid, NCT));
-        if (lane == 0) s_sum[it & 1][warp] = s;
+        const float sw = warp_sum(exact_sum_thread<E>(row, a.vocab, q.t.v1, c, tid, NCT));
+        if (lane == 0) s_sum[it & 1][warp] = sw;
         named_bar(1, NCT);
-        for (int w = 0; w < NCW; w++) S += s_sum[it & 1][w];
+        for (int k = 0; k < NCW; k++) S += s_sum[it & 1][k];
         exact = true;
       }
-      if (tid == 0) {
-        const RowOut o = finish_row(q, c, iota, exact, S);
-        margin[r] = o.margin;
-        if (top1) top1[r] = o.i1;
-        if (top2) top2[r] = o.i2;
-        if (lse) lse[r] = o.lse;
-        if (status) status[r] = static_cast<uint8_t>(o.status);
+      if (warp == 0) finish_item<E, STEP>(a, cs, sc, r, q, exact, S);
+    } else {
+      // publish this part; the last part of the row to arrive finishes it
+      int last = 0;
+      if (lane == 0) {
+        float* pw = a.part + (static_cast<size_t>(r) * a.nsplit + (w % a.nsplit)) * kPartWords;
+        __stcg(pw + 0, q.t.v1); __stcg(pw + 1, q.t.v2);
+        __stcg(pw + 2, __int_as_float(q.t.i1)); __stcg(pw + 3, __int_as_float(q.t.i2));
+        __stcg(pw + 4, q.n.m); __stcg(pw + 5, q.n.s);
+        __stcg(pw + 6, __int_as_float(q.flags));
+        __threadfence();
+        last = atomicAdd(a.counter + r, 1) == a.nsplit - 1;
       }
+      if (!__shfl_sync(kFull, last, 0)) continue;
+      __threadfence();
+      Partial m = partial_empty();
+      for (int k = lane; k < a.nsplit; k += 32) {
+        const float* pr = a.part + (static_cast<size_t>(r) * a.nsplit + k) * kPartWords;
+        Partial o;
+        o.t.v1 = __ldcg(pr + 0); o.t.v2 = __ldcg(pr + 1);
+        o.t.i1 = __float_as_int(__ldcg(pr + 2)); o.t.i2 = __float_as_int(__ldcg(pr + 3));
+        o.n.m = __ldcg(pr + 4); o.n.s = __ldcg(pr + 5);
+        o.flags = __float_as_int(__ldcg(pr + 6));
+        m = partial_merge(m, o);
+      }
+      m = warp_reduce_partial(m);
+      bool exact = false;
+      float S = 0.0f;
+      if (m.flags & kFlagHuge) {  // rare: this warp sums the whole row exactly
+        S = warp_sum(exact_sum_thread<E>(row, a.vocab, m.t.v1, c, lane, 32));
+        exact = true;
+      }
+      if (lane == 0) a.counter[r] = 0;  // ready for the next launch / graph replay
+      finish_item<E, STEP>(a, cs, sc, r, m, exact, S);
     }
   }
 }
@@ -372,7 +534,8 @@ int num_sms() {
   return g_num_sms;
 }
 
-// K1 launch shape (overridable at build time for tuning sweeps, tools/k1_sweep.py).
+// Row-kernel launch shape (overridable at build time for tuning sweeps,
+// tools/k1_sweep.py).
 #ifndef RELAY_K1_NCW
 #define RELAY_K1_NCW 8
 #endif
@@ -390,236 +553,54 @@ constexpr int kStages = RELAY_K1_STAGES;  // ring depth
 constexpr int kUV = RELAY_K1_UV;          // 16-byte vectors per consumer thread per stage
 constexpr int kMinBlocks = RELAY_K1_MINB; // CTAs per SM the registers must allow
 
-template <class E>
-static cudaError_t launch_rows_t(const void* logits, long long n_rows, int vocab, long long stride,
-                                 float iota, float* margin, int* top1, int* top2, float* lse,
-                                 uint8_t* status, cudaStream_t st) {
-  auto kern = margin_rows_tma_kernel<E, kNCW, kStages, kUV, kMinBlocks>;
+template <class E, bool STEP>
+static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) {
+  auto kern = rows_kernel<E, kNCW, kStages, kUV, kMinBlocks, STEP>;
   const int smem = kStages * kUV * kNCW * 32 * 16;
-  static bool configured = false;
-  if (!configured) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
   }
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  long long grid = static_cast<long long>(per_sm) * num_sms();
-  if (grid > n_rows) grid = n_rows;
-  kern<<<static_cast<unsigned>(grid), (kNCW + 1) * 32, smem, st>>>(
-      static_cast<const typename E::T*>(logits), n_rows, vocab, stride, iota * kLog2e, iota, margin,
-      top1, top2, lse, status);
+  const long long slots = static_cast<long long>(per_sm) * num_sms();
+  if (a.nsplit == 0) {
+    // decode step: split rows until there are ~4 items per CTA slot
+    long long ns = (4 * slots + a.n_rows - 1) / a.n_rows;
+    if (ns > kMaxSplit) ns = kMaxSplit;
+    if (ns < 1) ns = 1;
+    int chunk = static_cast<int>((a.vocab + ns - 1) / ns);
+    chunk = (chunk + 63) / 64 * 64;
+    if (chunk < 4096) chunk = 4096;
+    a.chunk = chunk;
+    a.nsplit = (a.vocab + chunk - 1) / chunk;
+  }
+  long long grid = slots;
+  if (grid > a.n_rows * a.nsplit) grid = a.n_rows * a.nsplit;
+  kern<<<static_cast<unsigned>(grid), (kNCW + 1) * 32, smem, st>>>(a, cs);
   return cudaGetLastError();
+}
+
+template <bool STEP>
+static cudaError_t launch_rows(int dt, const RowsArgs& a, const CueDev& cs, cudaStream_t st) {
+  switch (dt) {
+    case 0: return launch_rows_t<EBf16, STEP>(a, cs, st);
+    case 1: return launch_rows_t<EF16, STEP>(a, cs, st);
+    default: return launch_rows_t<EF32, STEP>(a, cs, st);
+  }
 }
 
 cudaError_t launch_margin_rows(const void* logits, int dt, long long n_rows, int vocab,
                                long long stride, float iota, float* margin, int* top1, int* top2,
                                float* lse, uint8_t* status, cudaStream_t st) {
   if (n_rows <= 0) return cudaSuccess;
-  switch (dt) {
-    case 0:
-      return launch_rows_t<EBf16>(logits, n_rows, vocab, stride, iota, margin, top1, top2, lse, status, st);
-    case 1:
-      return launch_rows_t<EF16>(logits, n_rows, vocab, stride, iota, margin, top1, top2, lse, status, st);
-    default:
-      return launch_rows_t<EF32>(logits, n_rows, vocab, stride, iota, margin, top1, top2, lse, status, st);
-  }
-}
-
-// ------------------------------------------------------------------- K4
-// Stream elements [j0, j1) of one row through this CTA with 16-byte loads.
-template <class E, int THREADS, int U>
-__device__ __forceinline__ void stream_range_ldg(const typename E::T* __restrict__ row, int j0, int j1,
-                                                 float c, ThreadState& st, int* s_theta) {
-  constexpr int VEC = 16 / E::SZ;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const Geom g = row_geom<E>(row, j0, j1);
-  if (tid < g.head) consume_scalar(E::load1(row + j0 + tid), j0 + tid, st, c);
-  const int jb = j0 + g.head;
-  const int nvec = g.body / 16;
-  const char* vbase = reinterpret_cast<const char*>(row + jb);
-  int wv = tid - lane;  // warp-uniform bound so the vote sees all 32 lanes
-  for (; wv + 31 + (U - 1) * THREADS < nvec; wv += U * THREADS) {
-    const int v = wv + lane;
-    uint4 raw[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) raw[u] = ldg_stream16(vbase + static_cast<size_t>(v + u * THREADS) * 16);
-    const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
-    bool slow = false;
-    consume_stage<E, U>(raw, stage_max2<E, U>(raw), jb + v * VEC, THREADS * VEC, st, c, theta, slow);
-    if (__any_sync(kFull, slow)) theta_raise(warp_second(st.t.v1, st.t.v2), s_theta);
-  }
-  for (int v = wv + lane; v < nvec; v += THREADS) {
-    const float theta = unkey(*reinterpret_cast<volatile int*>(s_theta));
-    bool slow = false;
-    const uint4 raw1[1] = {ldg_stream16(vbase + static_cast<size_t>(v) * 16)};
-    consume_stage<E, 1>(raw1, stage_max2<E, 1>(raw1), jb + v * VEC, 0, st, c, theta, slow);
-  }
-  if (tid < j1 - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
-}
-
-template <int THREADS>
-__device__ __forceinline__ Partial block_reduce(Partial p, Partial* s_red) {
-  constexpr int NW = THREADS / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  p = warp_reduce_partial(p);
-  if (lane == 0) s_red[warp] = p;
-  __syncthreads();
-  if (warp == 0) {
-    p = lane < NW ? s_red[lane] : partial_empty();
-    p = warp_reduce_partial(p);
-  }
-  return p;  // valid in warp 0
-}
-
-// Runtime switching (§4.3, fig:mechanism P:209-216), one thread.
-__device__ void switch_one(const CueDev& cs, int tok, float m, uint8_t* state_p, int* hist,
-                           int* small_run_p, float gate, int max_seg, uint8_t* flag_out,
-                           int16_t* cue_out) {
-  int cue = -1, flag = 0;
-  uint8_t state = *state_p;
-  if (tok >= 0 && tok < cs.vocab && !(state & 2)) {
-    const int sr = small_run_p ? *small_run_p : 0;
-    bool clear = false;
-    if (tok == cs.think_end) {
-      flag = 3; state = 3; clear = true;
-    } else if ((state & 1) == 0) {
-      int seq[kMaxLen];
-#pragma unroll
-      for (int k = 0; k < kHist; k++) seq[k] = hist[k];
-      seq[kHist] = tok;
-      int best = -1;
-      for (int p = 0; p < cs.n_pat && best < 0; p++) {  // sorted by length desc
-        const int len = cs.pat_len[p];
-        bool ok = true;
-        for (int k = 0; k < len; k++)
-          if (seq[kMaxLen - len + k] != cs.pat_tok[p * kMaxLen + k]) { ok = false; break; }
-        if (ok) best = p;
-      }
-      if (best >= 0 && !(gate >= 0.0f && m < gate)) {
-        flag = 1; cue = cs.pat_cue[best]; state = 1; clear = true;
-      } else {
-        for (int k = 0; k < kHist - 1; k++) hist[k] = hist[k + 1];
-        hist[kHist - 1] = tok;
-      }
-    } else {
-      const bool term = (cs.term_tab[tok >> 5] >> (tok & 31)) & 1u;
-      if (term) {
-        flag = 2; state = 0; clear = true;
-      } else if (max_seg > 0 && sr + 1 >= max_seg) {
-        flag = 4; state = 0; clear = true;
-      } else if (small_run_p) {
-        *small_run_p = sr + 1;
-      }
-    }
-    if (clear) {
-      for (int k = 0; k < kHist; k++) hist[k] = -1;
-      if (small_run_p) *small_run_p = 0;
-    }
-    *state_p = state;
-  }
-  *flag_out = static_cast<uint8_t>(flag);
-  *cue_out = static_cast<int16_t>(cue);
-}
-
-constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
-
-template <class E, int THREADS, int U>
-__global__ void __launch_bounds__(THREADS)
-    step_switch_kernel(CueDev cs, const typename E::T* __restrict__ logits, int vocab,
-                       long long stride, int nsplit, int chunk, float c, float iota,
-                       const int* __restrict__ sampled, uint8_t* state, int* hist, int* small_run,
-                       float gate, int max_seg, float* margin, int* top1, int* top2,
-                       uint8_t* flag, int16_t* cue_id, int* counter, float* part) {
-  __shared__ int s_theta;
-  __shared__ Partial s_red[THREADS / 32];
-  __shared__ float s_sum[THREADS / 32];
-  __shared__ int s_last;
-  const int b = blockIdx.x / nsplit;
-  const int k = blockIdx.x % nsplit;
-  const int j0 = k * chunk;
-  const int j1 = min(vocab, j0 + chunk);
-  const typename E::T* row = logits + b * stride;
-  if (threadIdx.x == 0) s_theta = fkey(-INFINITY);
-  __syncthreads();
-  ThreadState st;
-  state_init(st);
-  if (j0 < j1) stream_range_ldg<E, THREADS, U>(row, j0, j1, c, st, &s_theta);
-  Partial p = block_reduce<THREADS>(thread_partial(st), s_red);
-  if (threadIdx.x == 0) {
-    float* q = part + (static_cast<size_t>(b) * nsplit + k) * kPartWords;
-    __stcg(q + 0, p.t.v1); __stcg(q + 1, p.t.v2);
-    __stcg(q + 2, __int_as_float(p.t.i1)); __stcg(q + 3, __int_as_float(p.t.i2));
-    __stcg(q + 4, p.n.m); __stcg(q + 5, p.n.s);
-    __stcg(q + 6, __int_as_float(p.flags));
-    __threadfence();
-    const int old = atomicAdd(counter + b, 1);
-    s_last = (old == nsplit - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  // last arriver for row b: merge the nsplit partials
-  __threadfence();
-  if (threadIdx.x < 32) {
-    Partial acc = partial_empty();
-    for (int kk = threadIdx.x; kk < nsplit; kk += 32) {
-      const float* q = part + (static_cast<size_t>(b) * nsplit + kk) * kPartWords;
-      Partial o;
-      o.t.v1 = __ldcg(q + 0); o.t.v2 = __ldcg(q + 1);
-      o.t.i1 = __float_as_int(__ldcg(q + 2)); o.t.i2 = __float_as_int(__ldcg(q + 3));
-      o.n.m = __ldcg(q + 4); o.n.s = __ldcg(q + 5);
-      o.flags = __float_as_int(__ldcg(q + 6));
-      acc = partial_merge(acc, o);
-    }
-    acc = warp_reduce_partial(acc);
-    if (threadIdx.x == 0) s_red[0] = acc;
-  }
-  __syncthreads();
-  const Partial acc = s_red[0];
-  float S_exact = 0.0f;
-  if (acc.flags & kFlagHuge) {  // rare: exact normaliser over the whole row by this CTA
-    const float s = warp_sum(exact_sum_thread<E>(row, vocab, acc.t.v1, c, threadIdx.x, THREADS));
-    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = s;
-    __syncthreads();
-    for (int w = 0; w < THREADS / 32; w++) S_exact += s_sum[w];
-  }
-  if (threadIdx.x == 0) {
-    counter[b] = 0;  // ready for the next launch / graph replay
-    const RowOut o = finish_row(acc, c, iota, (acc.flags & kFlagHuge) != 0, S_exact);
-    margin[b] = o.margin;
-    if (top1) top1[b] = o.i1;
-    if (top2) top2[b] = o.i2;
-    const int tok = sampled ? sampled[b] : o.i1;
-    switch_one(cs, tok, o.margin, state + b, hist + static_cast<size_t>(b) * kHist,
-               small_run ? small_run + b : nullptr, gate, max_seg, flag + b, cue_id + b);
-  }
-}
-
-constexpr int kStepThreads = 256;
-
-template <class E>
-static cudaError_t launch_step_t(const CueDev& cs, const void* logits, int batch, int vocab,
-                                 long long stride, float iota, const int* sampled, uint8_t* state,
-                                 int* hist, int* small_run, float gate, int max_seg, float* margin,
-                                 int* top1, int* top2, uint8_t* flag, int16_t* cue_id,
-                                 const StepWs& ws, cudaStream_t st) {
-  // split rows so that the grid covers every SM several times
-  int nsplit = (8 * num_sms() + batch - 1) / batch;
-  if (nsplit > kMaxSplit) nsplit = kMaxSplit;
-  if (nsplit < 1) nsplit = 1;
-  int chunk = (vocab + nsplit - 1) / nsplit;
-  chunk = (chunk + 63) / 64 * 64;
-  if (chunk < 1024) chunk = 1024;
-  nsplit = (vocab + chunk - 1) / chunk;
-  auto kern = step_switch_kernel<E, kStepThreads, 4>;
-  kern<<<static_cast<unsigned>(batch) * nsplit, kStepThreads, 0, st>>>(
-      cs, static_cast<const typename E::T*>(logits), vocab, stride, nsplit, chunk, iota * kLog2e,
-      iota, sampled, state, hist, small_run, gate, max_seg, margin, top1, top2, flag, cue_id,
-      ws.counter, ws.part);
-  return cudaGetLastError();
+  RowsArgs a{};
+  a.logits = logits; a.n_rows = n_rows; a.vocab = vocab; a.stride = stride;
+  a.c = iota * kLog2e; a.iota = iota; a.nsplit = 1; a.chunk = vocab;
+  a.margin = margin; a.top1 = top1; a.top2 = top2; a.lse = lse; a.status = status;
+  return launch_rows<false>(dt, a, CueDev{}, st);
 }
 
 cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
@@ -628,17 +609,14 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
                                int* top1, int* top2, uint8_t* flag, int16_t* cue_id,
                                const StepWs& ws, cudaStream_t st) {
   if (batch <= 0) return cudaSuccess;
-  switch (dt) {
-    case 0:
-      return launch_step_t<EBf16>(cs, logits, batch, vocab, stride, iota, sampled, state, hist,
-                                  small_run, gate, max_seg, margin, top1, top2, flag, cue_id, ws, st);
-    case 1:
-      return launch_step_t<EF16>(cs, logits, batch, vocab, stride, iota, sampled, state, hist,
-                                 small_run, gate, max_seg, margin, top1, top2, flag, cue_id, ws, st);
-    default:
-      return launch_step_t<EF32>(cs, logits, batch, vocab, stride, iota, sampled, state, hist,
-                                 small_run, gate, max_seg, margin, top1, top2, flag, cue_id, ws, st);
-  }
+  RowsArgs a{};
+  a.logits = logits; a.n_rows = batch; a.vocab = vocab; a.stride = stride;
+  a.c = iota * kLog2e; a.iota = iota; a.nsplit = 0;  // chosen by the launcher
+  a.margin = margin; a.top1 = top1; a.top2 = top2;
+  a.counter = ws.counter; a.part = ws.part;
+  a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
+  a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
+  return launch_rows<true>(dt, a, cs, st);
 }
 
 }  // namespace relay

@@ -338,8 +338,15 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
   }
 }
 
+// Warp roles: NCW consumer warps stream stages; warp NCW is the TMA producer;
+// warp NCW+1 is the epilogue warp, which merges an item's partials, finishes
+// the row (or publishes a part and, as last arriver, merges the row) and runs
+// the decode-step switch — so consumer warps never wait for an epilogue.
+// Items rotate over NSLOT reduction slots guarded by mbarriers.
+constexpr int kSlots = 4;
+
 template <class E, int NCW, int NS, int UV, int MINB, bool STEP>
-__global__ void __launch_bounds__((NCW + 1) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
+__global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
   constexpr int NCT = NCW * 32;             // consumer threads
@@ -348,9 +355,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) rows_kernel(RowsArgs a, 
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
-  __shared__ int s_theta[2];
-  __shared__ Partial s_red[2][NRED];
-  __shared__ float s_sum[2][NCW];
+  __shared__ __align__(8) uint64_t red_full[kSlots];
+  __shared__ __align__(8) uint64_t red_empty[kSlots];
+  __shared__ int s_theta[kSlots];
+  __shared__ Partial s_red[kSlots][NRED];
   __shared__ SmemCue sc;
 
   const T* logits = static_cast<const T*>(a.logits);
@@ -360,12 +368,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) rows_kernel(RowsArgs a, 
   const uint32_t ring_s = smem_u32_pinned(ring);
   const uint32_t full_s = smem_u32_pinned(full);
   const uint32_t empty_s = smem_u32_pinned(empty);
+  const uint32_t rfull_s = smem_u32_pinned(red_full);
+  const uint32_t rempty_s = smem_u32_pinned(red_empty);
   if (tid == 0) {
     for (int s = 0; s < NS; s++) {
       mbar_init(full_s + 8 * s, 1);
       mbar_init(empty_s + 8 * s, NCW);
     }
-    s_theta[0] = s_theta[1] = fkey(-INFINITY);
+    for (int s = 0; s < kSlots; s++) {
+      mbar_init(rfull_s + 8 * s, NCW);
+      mbar_init(rempty_s + 8 * s, 1);
+      s_theta[s] = fkey(-INFINITY);
+    }
     fence_barrier_init();
   }
   if constexpr (STEP) {
@@ -376,6 +390,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) rows_kernel(RowsArgs a, 
     }
   }
   __syncthreads();
+  const float c = a.c;
 
   if (warp == NCW) {
     // ------------------------------------------------ producer warp
@@ -402,16 +417,79 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) rows_kernel(RowsArgs a, 
     return;
   }
 
+  if (warp == NCW + 1) {
+    // ------------------------------------------------ epilogue warp
+    int it = 0;
+    for (long long w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      const int slot = it % kSlots;
+      const long long r = w / a.nsplit;
+      const T* row = logits + r * a.stride;
+      mbar_wait_sleep(rfull_s + 8 * slot, (it / kSlots) & 1);
+      Partial q = partial_empty();
+#pragma unroll
+      for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
+      q = warp_reduce_partial(q);
+      if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
+      __syncwarp();
+      if (lane == 0) mbar_arrive(rempty_s + 8 * slot);
+      if (a.nsplit == 1) {
+        bool exact = false;
+        float S = 0.0f;
+        if (q.flags & kFlagHuge) {  // rare: exact normaliser over the row by this warp
+          S = warp_sum(exact_sum_thread<E>(row, a.vocab, q.t.v1, c, lane, 32));
+          exact = true;
+        }
+        finish_item<E, STEP>(a, cs, sc, r, q, exact, S);
+        continue;
+      }
+      // publish this part; the last part of the row to arrive finishes it
+      int last = 0;
+      if (lane == 0) {
+        float* pw = a.part + (static_cast<size_t>(r) * a.nsplit + (w % a.nsplit)) * kPartWords;
+        __stcg(pw + 0, q.t.v1); __stcg(pw + 1, q.t.v2);
+        __stcg(pw + 2, __int_as_float(q.t.i1)); __stcg(pw + 3, __int_as_float(q.t.i2));
+        __stcg(pw + 4, q.n.m); __stcg(pw + 5, q.n.s);
+        __stcg(pw + 6, __int_as_float(q.flags));
+        __threadfence();
+        last = atomicAdd(a.counter + r, 1) == a.nsplit - 1;
+      }
+      if (!__shfl_sync(kFull, last, 0)) continue;
+      __threadfence();
+      Partial m = partial_empty();
+      for (int k = lane; k < a.nsplit; k += 32) {
+        const float* pr = a.part + (static_cast<size_t>(r) * a.nsplit + k) * kPartWords;
+        Partial o;
+        o.t.v1 = __ldcg(pr + 0); o.t.v2 = __ldcg(pr + 1);
+        o.t.i1 = __float_as_int(__ldcg(pr + 2)); o.t.i2 = __float_as_int(__ldcg(pr + 3));
+        o.n.m = __ldcg(pr + 4); o.n.s = __ldcg(pr + 5);
+        o.flags = __float_as_int(__ldcg(pr + 6));
+        m = partial_merge(m, o);
+      }
+      m = warp_reduce_partial(m);
+      bool exact = false;
+      float S = 0.0f;
+      if (m.flags & kFlagHuge) {
+        S = warp_sum(exact_sum_thread<E>(row, a.vocab, m.t.v1, c, lane, 32));
+        exact = true;
+      }
+      if (lane == 0) a.counter[r] = 0;  // ready for the next launch / graph replay
+      finish_item<E, STEP>(a, cs, sc, r, m, exact, S);
+    }
+    return;
+  }
+
   // -------------------------------------------------- consumer warps
-  const float c = a.c;
   int stage = 0;
   uint32_t phase = 0;
   int it = 0;
   for (long long w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    const int slot = it % kSlots;
     const long long r = w / a.nsplit;
     const int j0 = static_cast<int>(w % a.nsplit) * a.chunk;
     const int j1 = min(a.vocab, j0 + a.chunk);
-    int* theta_p = &s_theta[it & 1];
+    // the slot (threshold + partials) is free once the epilogue took item it - kSlots
+    mbar_wait(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
+    int* theta_p = &s_theta[slot];
     const T* row = logits + r * a.stride;
     const Geom g = row_geom<E>(row, j0, j1);
     ThreadState st;
@@ -452,73 +530,13 @@ __global__ void __launch_bounds__((NCW + 1) * 32, MINB) rows_kernel(RowsArgs a, 
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     if (tid < j1 - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
-
-    // ------------------------------------------------ item epilogue
-    // Two shuffle rounds leave 8 partials per warp in smem; one warp merges
-    // them (the other warps go straight on to the next item).
+    // hand the warp's 8 partials (after two shuffle rounds) to the epilogue warp
     Partial p = thread_partial(st);
     p = partial_merge(p, shfl_xor_partial(p, 16));
     p = partial_merge(p, shfl_xor_partial(p, 8));
-    if (lane < 8) s_red[it & 1][warp * 8 + lane] = p;
-    if (tid == 0) s_theta[(it + 1) & 1] = fkey(-INFINITY);
-    named_bar(1, NCT);
-    // s_red[it & 1] is rewritten only after the next item's barrier, which
-    // every warp reaches after these reads, so the decision is uniform.
-    bool huge_lane = false;
-#pragma unroll
-    for (int e = lane; e < NRED; e += 32) huge_lane |= (s_red[it & 1][e].flags & kFlagHuge) != 0;
-    const bool huge = __any_sync(kFull, huge_lane) && a.nsplit == 1;
-    if (!(huge || warp == 0)) continue;
-    Partial q = partial_empty();
-#pragma unroll
-    for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[it & 1][e]);
-    q = warp_reduce_partial(q);
-    if (a.nsplit == 1) {
-      bool exact = false;
-      float S = 0.0f;
-      if (huge) {
-        // rare: every consumer joins an exact second pass over the row
-        const float sw = warp_sum(exact_sum_thread<E>(row, a.vocab, q.t.v1, c, tid, NCT));
-        if (lane == 0) s_sum[it & 1][warp] = sw;
-        named_bar(1, NCT);
-        for (int k = 0; k < NCW; k++) S += s_sum[it & 1][k];
-        exact = true;
-      }
-      if (warp == 0) finish_item<E, STEP>(a, cs, sc, r, q, exact, S);
-    } else {
-      // publish this part; the last part of the row to arrive finishes it
-      int last = 0;
-      if (lane == 0) {
-        float* pw = a.part + (static_cast<size_t>(r) * a.nsplit + (w % a.nsplit)) * kPartWords;
-        __stcg(pw + 0, q.t.v1); __stcg(pw + 1, q.t.v2);
-        __stcg(pw + 2, __int_as_float(q.t.i1)); __stcg(pw + 3, __int_as_float(q.t.i2));
-        __stcg(pw + 4, q.n.m); __stcg(pw + 5, q.n.s);
-        __stcg(pw + 6, __int_as_float(q.flags));
-        __threadfence();
-        last = atomicAdd(a.counter + r, 1) == a.nsplit - 1;
-      }
-      if (!__shfl_sync(kFull, last, 0)) continue;
-      __threadfence();
-      Partial m = partial_empty();
-      for (int k = lane; k < a.nsplit; k += 32) {
-        const float* pr = a.part + (static_cast<size_t>(r) * a.nsplit + k) * kPartWords;
-        Partial o;
-        o.t.v1 = __ldcg(pr + 0); o.t.v2 = __ldcg(pr + 1);
-        o.t.i1 = __float_as_int(__ldcg(pr + 2)); o.t.i2 = __float_as_int(__ldcg(pr + 3));
-        o.n.m = __ldcg(pr + 4); o.n.s = __ldcg(pr + 5);
-        o.flags = __float_as_int(__ldcg(pr + 6));
-        m = partial_merge(m, o);
-      }
-      m = warp_reduce_partial(m);
-      bool exact = false;
-      float S = 0.0f;
-      if (m.flags & kFlagHuge) {  // rare: this warp sums the whole row exactly
-        S = warp_sum(exact_sum_thread<E>(row, a.vocab, m.t.v1, c, lane, 32));
-        exact = true;
-      }
-      if (lane == 0) a.counter[r] = 0;  // ready for the next launch / graph replay
-      finish_item<E, STEP>(a, cs, sc, r, m, exact, S);
-    }
+    if (lane < 8) s_red[slot][warp * 8 + lane] = p;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(rfull_s + 8 * slot);
   }
 }
 
@@ -561,7 +579,7 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 2) * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }
@@ -579,7 +597,7 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   }
   long long grid = slots;
   if (grid > a.n_rows * a.nsplit) grid = a.n_rows * a.nsplit;
-  kern<<<static_cast<unsigned>(grid), (kNCW + 1) * 32, smem, st>>>(a, cs);
+  kern<<<static_cast<unsigned>(grid), (kNCW + 2) * 32, smem, st>>>(a, cs);
   return cudaGetLastError();
 }
 

@@ -34,20 +34,41 @@ def main(B=256, V=152064, steps=200, graph=True):
     torch.cuda.synchronize()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
     res = {}
+    # steps are captured in one CUDA graph (as a serving engine would run the
+    # decode step), so the number is device time, not Python launch overhead
+    reps = max(1, steps // nbuf)
     for mode in ("cold", "hot"):
-        seq = [bufs[i % nbuf] if mode == "cold" else bufs[0] for i in range(steps)]
-        for i in range(5):
-            relay.step_switch(cs, seq[i], state, hist, small, samp, ws=ws, out=out)
+        seq = [bufs[i % nbuf] if mode == "cold" else bufs[0] for i in range(nbuf)]
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            for x in seq:                     # warm-up on the capture stream
+                relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=out)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                for x in seq:
+                    relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=out)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for x in seq:
-            relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=out)
+        for _ in range(reps):
+            g.replay()
         e1.record()
         torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / steps
+        us = e0.elapsed_time(e1) * 1e3 / (reps * nbuf)
         gbs = B * (V * 2 + 12) / (us * 1e-6) / 1e9
         res[mode] = dict(us_per_step=us, rows_per_s=B / (us * 1e-6), gbs=gbs, frac=gbs / peak)
+    # host cost of one eager Python call (argument marshalling + launch)
+    torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    for _ in range(100):
+        relay.step_switch(cs, bufs[0], state, hist, small, samp, ws=ws, out=out)
+    res["eager_host_us_per_call"] = (time.perf_counter() - t0) * 1e4
+    torch.cuda.synchronize()
     print(json.dumps({"kernel": "relay_step_switch (K4)", "batch": B, "vocab": V, "buffers": nbuf,
                       "l2_bytes": l2, **res}), flush=True)
     cs.destroy()

@@ -227,14 +227,15 @@ struct RowsArgs {
   int vocab;
   long long stride;
   float c, iota;
-  int nsplit, chunk;
+  int flat;       // 0: one item per row, rows strided over CTAs (K1)
+                  // 1: each CTA takes an equal slice of the flattened rows (K4)
   float* margin;
   int* top1;
   int* top2;
   float* lse;
   uint8_t* status;
-  int* counter;   // [n_rows] (nsplit > 1)
-  float* part;    // [n_rows][nsplit][kPartWords] (nsplit > 1)
+  int* counter;   // [n_rows] arrival counters (flat)
+  float* part;    // [n_rows][kMaxSplit][kPartWords] row-part partials (flat)
   // decode-step switch (STEP)
   const int* sampled;
   uint8_t* state;
@@ -338,6 +339,61 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
   }
 }
 
+// Work items.  Strided mode: item i of a CTA is row blockIdx.x + i*gridDim.x,
+// whole.  Flat mode: the n_rows*vocab elements are cut into gridDim.x equal
+// slices (boundaries on 64-element multiples); a CTA's slice splits at row
+// boundaries into 1-3 row parts, so every CTA streams the same number of bytes
+// however few rows there are.  A row's parts are merged by the last arriver.
+struct Item {
+  long long r;
+  int j0, j1;     // element range of the row
+  int part, nparts;
+};
+
+struct ItemIter {
+  long long next_w;  // strided: next row
+  long long e, E1;   // flat: next element, end of this CTA's slice
+
+  __device__ static long long slice_start(long long b, long long T, long long G) {
+    if (b >= G) return T;
+    return static_cast<long long>((static_cast<unsigned __int128>(b) * T) / G) & ~63LL;
+  }
+  // the CTA whose (non-empty) slice holds element e
+  __device__ static long long owner(long long e, long long T, long long G) {
+    long long b = static_cast<long long>((static_cast<unsigned __int128>(e) * G) / T);
+    while (b > 0 && slice_start(b, T, G) > e) b--;
+    while (b + 1 < G && slice_start(b + 1, T, G) <= e) b++;
+    return b;
+  }
+  __device__ void init(const RowsArgs& a) {
+    next_w = blockIdx.x;
+    if (a.flat) {
+      const long long T = a.n_rows * a.vocab, G = gridDim.x;
+      e = slice_start(blockIdx.x, T, G);
+      E1 = slice_start(blockIdx.x + 1, T, G);
+    }
+  }
+  __device__ bool next(const RowsArgs& a, Item& it) {
+    if (!a.flat) {
+      if (next_w >= a.n_rows) return false;
+      it = Item{next_w, 0, a.vocab, 0, 1};
+      next_w += gridDim.x;
+      return true;
+    }
+    if (e >= E1) return false;
+    const long long T = a.n_rows * a.vocab, G = gridDim.x, V = a.vocab;
+    const long long r = e / V;
+    it.r = r;
+    it.j0 = static_cast<int>(e - r * V);
+    it.j1 = static_cast<int>(min(V, E1 - r * V));
+    const long long first = owner(r * V, T, G);
+    it.part = static_cast<int>(blockIdx.x - first);
+    it.nparts = static_cast<int>(owner(r * V + V - 1, T, G) - first + 1);
+    e = (r + 1) * V;
+    return true;
+  }
+};
+
 // Warp roles: NCW consumer warps stream stages; warp NCW is the TMA producer;
 // warp NCW+1 is the epilogue warp, which merges an item's partials, finishes
 // the row (or publishes a part and, as last arriver, merges the row) and runs
@@ -362,7 +418,6 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   __shared__ SmemCue sc;
 
   const T* logits = static_cast<const T*>(a.logits);
-  const long long n_items = a.n_rows * a.nsplit;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const uint32_t ring_s = smem_u32_pinned(ring);
@@ -398,13 +453,13 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (long long w = blockIdx.x; w < n_items; w += gridDim.x) {
-        const long long r = w / a.nsplit;
-        const int j0 = static_cast<int>(w % a.nsplit) * a.chunk;
-        const int j1 = min(a.vocab, j0 + a.chunk);
-        const T* row = logits + r * a.stride;
-        const Geom g = row_geom<E>(row, j0, j1);
-        const char* src = reinterpret_cast<const char*>(row + j0 + g.head);
+      ItemIter iter;
+      iter.init(a);
+      Item item;
+      while (iter.next(a, item)) {
+        const T* row = logits + item.r * a.stride;
+        const Geom g = row_geom<E>(row, item.j0, item.j1);
+        const char* src = reinterpret_cast<const char*>(row + item.j0 + g.head);
         for (int off = 0; off < g.body; off += SB) {
           const uint32_t bytes = static_cast<uint32_t>(min(SB, g.body - off));
           mbar_wait_sleep(empty_s + 8 * stage, phase ^ 1);
@@ -419,10 +474,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 
   if (warp == NCW + 1) {
     // ------------------------------------------------ epilogue warp
-    int it = 0;
-    for (long long w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    ItemIter iter;
+    iter.init(a);
+    Item item;
+    for (int it = 0; iter.next(a, item); ++it) {
       const int slot = it % kSlots;
-      const long long r = w / a.nsplit;
+      const long long r = item.r;
       const T* row = logits + r * a.stride;
       mbar_wait_sleep(rfull_s + 8 * slot, (it / kSlots) & 1);
       Partial q = partial_empty();
@@ -432,7 +489,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
       __syncwarp();
       if (lane == 0) mbar_arrive(rempty_s + 8 * slot);
-      if (a.nsplit == 1) {
+      if (item.nparts == 1) {
         bool exact = false;
         float S = 0.0f;
         if (q.flags & kFlagHuge) {  // rare: exact normaliser over the row by this warp
@@ -445,19 +502,19 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       // publish this part; the last part of the row to arrive finishes it
       int last = 0;
       if (lane == 0) {
-        float* pw = a.part + (static_cast<size_t>(r) * a.nsplit + (w % a.nsplit)) * kPartWords;
+        float* pw = a.part + (static_cast<size_t>(r) * kMaxSplit + item.part) * kPartWords;
         __stcg(pw + 0, q.t.v1); __stcg(pw + 1, q.t.v2);
         __stcg(pw + 2, __int_as_float(q.t.i1)); __stcg(pw + 3, __int_as_float(q.t.i2));
         __stcg(pw + 4, q.n.m); __stcg(pw + 5, q.n.s);
         __stcg(pw + 6, __int_as_float(q.flags));
         __threadfence();
-        last = atomicAdd(a.counter + r, 1) == a.nsplit - 1;
+        last = atomicAdd(a.counter + r, 1) == item.nparts - 1;
       }
       if (!__shfl_sync(kFull, last, 0)) continue;
       __threadfence();
       Partial m = partial_empty();
-      for (int k = lane; k < a.nsplit; k += 32) {
-        const float* pr = a.part + (static_cast<size_t>(r) * a.nsplit + k) * kPartWords;
+      for (int k = lane; k < item.nparts; k += 32) {
+        const float* pr = a.part + (static_cast<size_t>(r) * kMaxSplit + k) * kPartWords;
         Partial o;
         o.t.v1 = __ldcg(pr + 0); o.t.v2 = __ldcg(pr + 1);
         o.t.i1 = __float_as_int(__ldcg(pr + 2)); o.t.i2 = __float_as_int(__ldcg(pr + 3));
@@ -481,12 +538,14 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   // -------------------------------------------------- consumer warps
   int stage = 0;
   uint32_t phase = 0;
-  int it = 0;
-  for (long long w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+  ItemIter iter;
+  iter.init(a);
+  Item item;
+  for (int it = 0; iter.next(a, item); ++it) {
     const int slot = it % kSlots;
-    const long long r = w / a.nsplit;
-    const int j0 = static_cast<int>(w % a.nsplit) * a.chunk;
-    const int j1 = min(a.vocab, j0 + a.chunk);
+    const long long r = item.r;
+    const int j0 = item.j0;
+    const int j1 = item.j1;
     // the slot (threshold + partials) is free once the epilogue took item it - kSlots
     mbar_wait(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
     int* theta_p = &s_theta[slot];
@@ -584,19 +643,15 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
     if (per_sm < 1) per_sm = 1;
   }
   const long long slots = static_cast<long long>(per_sm) * num_sms();
-  if (a.nsplit == 0) {
-    // decode step: split rows until there are ~4 items per CTA slot
-    long long ns = (4 * slots + a.n_rows - 1) / a.n_rows;
-    if (ns > kMaxSplit) ns = kMaxSplit;
-    if (ns < 1) ns = 1;
-    int chunk = static_cast<int>((a.vocab + ns - 1) / ns);
-    chunk = (chunk + 63) / 64 * 64;
-    if (chunk < 4096) chunk = 4096;
-    a.chunk = chunk;
-    a.nsplit = (a.vocab + chunk - 1) / chunk;
-  }
   long long grid = slots;
-  if (grid > a.n_rows * a.nsplit) grid = a.n_rows * a.nsplit;
+  if (a.flat) {
+    // every slice at least 128 elements and a row in at most kMaxSplit parts
+    const long long T = a.n_rows * a.vocab;
+    if (grid > T / 128) grid = T / 128 > 0 ? T / 128 : 1;
+    if (grid > a.n_rows * (kMaxSplit - 2)) grid = a.n_rows * (kMaxSplit - 2);
+  } else if (grid > a.n_rows) {
+    grid = a.n_rows;
+  }
   kern<<<static_cast<unsigned>(grid), (kNCW + 2) * 32, smem, st>>>(a, cs);
   return cudaGetLastError();
 }
@@ -616,7 +671,7 @@ cudaError_t launch_margin_rows(const void* logits, int dt, long long n_rows, int
   if (n_rows <= 0) return cudaSuccess;
   RowsArgs a{};
   a.logits = logits; a.n_rows = n_rows; a.vocab = vocab; a.stride = stride;
-  a.c = iota * kLog2e; a.iota = iota; a.nsplit = 1; a.chunk = vocab;
+  a.c = iota * kLog2e; a.iota = iota; a.flat = 0;
   a.margin = margin; a.top1 = top1; a.top2 = top2; a.lse = lse; a.status = status;
   return launch_rows<false>(dt, a, CueDev{}, st);
 }
@@ -629,7 +684,7 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
   if (batch <= 0) return cudaSuccess;
   RowsArgs a{};
   a.logits = logits; a.n_rows = batch; a.vocab = vocab; a.stride = stride;
-  a.c = iota * kLog2e; a.iota = iota; a.nsplit = 0;  // chosen by the launcher
+  a.c = iota * kLog2e; a.iota = iota; a.flat = 1;
   a.margin = margin; a.top1 = top1; a.top2 = top2;
   a.counter = ws.counter; a.part = ws.part;
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;

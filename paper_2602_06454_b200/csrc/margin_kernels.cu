@@ -249,6 +249,15 @@ struct RowsArgs {
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
 
+// Arrival counter increment with acquire-release semantics at GPU scope: the
+// part written before it is visible to the last arriver, which then reads
+// every part after it (one fused fence + atomic).
+__device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 struct SmemCue {
   int tok[kMaxPat * kMaxLen];
   int len[kMaxPat];
@@ -258,15 +267,34 @@ struct SmemCue {
 // Runtime switching (§4.3, fig:mechanism P:209-216) for one
 // sequence, by one warp: lanes test the (length-sorted) patterns as suffixes of
 // hist ++ tok in parallel; the lowest matching lane is the longest pattern.
-__device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float m, uint8_t* state_p,
-                            int* hist, int* small_run_p, float gate, int max_seg, uint8_t* flag_out,
-                            int16_t* cue_out) {
+// The per-sequence switch inputs, loaded by the epilogue warp before it waits
+// for the item (so the loads are off the critical path): lane i < 7 holds
+// hist[i]; every lane holds state, small_run and the sampled token.
+struct SwitchIn {
+  int hist_lane;
+  int state;
+  int small_run;
+  int sampled;
+};
+
+__device__ __forceinline__ SwitchIn load_switch_in(const RowsArgs& a, long long r) {
   const int lane = threadIdx.x & 31;
-  const uint8_t state = *state_p;
+  SwitchIn in;
+  in.hist_lane = lane < kHist ? a.hist[r * kHist + lane] : -1;
+  in.state = a.state[r];
+  in.small_run = a.small_run ? a.small_run[r] : 0;
+  in.sampled = a.sampled ? a.sampled[r] : -1;
+  return in;
+}
+
+__device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float m, const SwitchIn& in,
+                            uint8_t* state_p, int* hist, int* small_run_p, float gate, int max_seg,
+                            uint8_t* flag_out, int16_t* cue_out) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t state = static_cast<uint8_t>(in.state);
   const bool valid = tok >= 0 && tok < cs.vocab && !(state & 2);
   // seq[0..6] = hist (oldest first), seq[7] = tok; lane i < 8 holds seq[i]
-  int mine = -1;
-  if (lane < kHist) mine = hist[lane];
+  int mine = in.hist_lane;
   if (lane == kHist) mine = tok;
   int best = -1;
   if (valid && tok != cs.think_end && (state & 1) == 0) {
@@ -288,7 +316,7 @@ __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float 
   int cue = -1, flag = 0;
   uint8_t st = state;
   if (valid) {
-    const int sr = small_run_p ? *small_run_p : 0;
+    const int sr = in.small_run;
     bool clear = false;
     if (tok == cs.think_end) {
       flag = 3; st = 3; clear = true;
@@ -322,7 +350,8 @@ __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float 
 // Warp-level finish of row r from its merged partial (lane 0 writes).
 template <class E, bool STEP>
 __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs, const SmemCue& sc,
-                                            long long r, const Partial& q, bool exact, float S) {
+                                            long long r, const Partial& q, bool exact, float S,
+                                            const SwitchIn& in) {
   const RowOut o = finish_row(q, a.c, a.iota, exact, S);
   const int lane = threadIdx.x & 31;
   if (lane == 0) {
@@ -333,8 +362,8 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
     if (a.status) a.status[r] = static_cast<uint8_t>(o.status);
   }
   if constexpr (STEP) {
-    const int tok = a.sampled ? a.sampled[r] : o.i1;
-    switch_warp(cs, sc, tok, o.margin, a.state + r, a.hist + r * kHist,
+    const int tok = a.sampled ? in.sampled : o.i1;
+    switch_warp(cs, sc, tok, o.margin, in, a.state + r, a.hist + r * kHist,
                 a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r, a.cue_id + r);
   }
 }
@@ -354,13 +383,14 @@ struct ItemIter {
   long long next_w;  // strided: next row
   long long e, E1;   // flat: next element, end of this CTA's slice
 
+  // 64-bit products suffice: T < 2^51 elements and G <= 4096 (host-checked)
   __device__ static long long slice_start(long long b, long long T, long long G) {
     if (b >= G) return T;
-    return static_cast<long long>((static_cast<unsigned __int128>(b) * T) / G) & ~63LL;
+    return ((b * T) / G) & ~63LL;
   }
   // the CTA whose (non-empty) slice holds element e
   __device__ static long long owner(long long e, long long T, long long G) {
-    long long b = static_cast<long long>((static_cast<unsigned __int128>(e) * G) / T);
+    long long b = (e * G) / T;
     while (b > 0 && slice_start(b, T, G) > e) b--;
     while (b + 1 < G && slice_start(b + 1, T, G) <= e) b++;
     return b;
@@ -401,6 +431,22 @@ struct ItemIter {
 // Items rotate over NSLOT reduction slots guarded by mbarriers.
 constexpr int kSlots = 4;
 
+#ifdef RELAY_TRACE
+// Tuning-only timeline (tools/trace_rows.py): %globaltimer stamps per CTA.
+__device__ unsigned long long g_trace[4096][16];
+__device__ __forceinline__ void stamp(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (blockIdx.x < 4096 && k < 16) g_trace[blockIdx.x][k] = t;
+}
+extern "C" int relay_debug_trace_copy(unsigned long long* host, int n_ctas) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 16 * n_ctas));
+}
+#define TRACE(k) stamp(k)
+#else
+#define TRACE(k) ((void)0)
+#endif
+
 template <class E, int NCW, int NS, int UV, int MINB, bool STEP>
 __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
@@ -420,6 +466,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const T* logits = static_cast<const T*>(a.logits);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) TRACE(0);
   const uint32_t ring_s = smem_u32_pinned(ring);
   const uint32_t full_s = smem_u32_pinned(full);
   const uint32_t empty_s = smem_u32_pinned(empty);
@@ -436,13 +483,6 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       s_theta[s] = fkey(-INFINITY);
     }
     fence_barrier_init();
-  }
-  if constexpr (STEP) {
-    for (int i = tid; i < cs.n_pat * kMaxLen; i += blockDim.x) sc.tok[i] = cs.pat_tok[i];
-    for (int i = tid; i < cs.n_pat; i += blockDim.x) {
-      sc.len[i] = cs.pat_len[i];
-      sc.cue[i] = cs.pat_cue[i];
-    }
   }
   __syncthreads();
   const float c = a.c;
@@ -474,6 +514,14 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 
   if (warp == NCW + 1) {
     // ------------------------------------------------ epilogue warp
+    if constexpr (STEP) {  // the switch patterns, for this warp only
+      for (int i = lane; i < cs.n_pat * kMaxLen; i += 32) sc.tok[i] = cs.pat_tok[i];
+      for (int i = lane; i < cs.n_pat; i += 32) {
+        sc.len[i] = cs.pat_len[i];
+        sc.cue[i] = cs.pat_cue[i];
+      }
+      __syncwarp();
+    }
     ItemIter iter;
     iter.init(a);
     Item item;
@@ -481,7 +529,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const int slot = it % kSlots;
       const long long r = item.r;
       const T* row = logits + r * a.stride;
-      mbar_wait_sleep(rfull_s + 8 * slot, (it / kSlots) & 1);
+      SwitchIn in{};
+      if constexpr (STEP) in = load_switch_in(a, r);
+      mbar_wait(rfull_s + 8 * slot, (it / kSlots) & 1);  // on the critical path: spin
       Partial q = partial_empty();
 #pragma unroll
       for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
@@ -496,7 +546,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           S = warp_sum(exact_sum_thread<E>(row, a.vocab, q.t.v1, c, lane, 32));
           exact = true;
         }
-        finish_item<E, STEP>(a, cs, sc, r, q, exact, S);
+        finish_item<E, STEP>(a, cs, sc, r, q, exact, S, in);
         continue;
       }
       // publish this part; the last part of the row to arrive finishes it
@@ -507,11 +557,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         __stcg(pw + 2, __int_as_float(q.t.i1)); __stcg(pw + 3, __int_as_float(q.t.i2));
         __stcg(pw + 4, q.n.m); __stcg(pw + 5, q.n.s);
         __stcg(pw + 6, __int_as_float(q.flags));
-        __threadfence();
-        last = atomicAdd(a.counter + r, 1) == item.nparts - 1;
+        last = atomic_add_acq_rel(a.counter + r, 1) == item.nparts - 1;
       }
       if (!__shfl_sync(kFull, last, 0)) continue;
-      __threadfence();
       Partial m = partial_empty();
       for (int k = lane; k < item.nparts; k += 32) {
         const float* pr = a.part + (static_cast<size_t>(r) * kMaxSplit + k) * kPartWords;
@@ -530,7 +578,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         exact = true;
       }
       if (lane == 0) a.counter[r] = 0;  // ready for the next launch / graph replay
-      finish_item<E, STEP>(a, cs, sc, r, m, exact, S);
+      finish_item<E, STEP>(a, cs, sc, r, m, exact, S, in);
+      if (lane == 0 && it < 5) TRACE(10 + it);
     }
     return;
   }
@@ -559,6 +608,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const int bytes = min(SB, g.body - off);
       const int jb = j0 + g.head + off / E::SZ;
       mbar_wait(full_s + 8 * stage, phase);
+      if (tid == 0 && it == 0 && off == 0) TRACE(1);
       const uint32_t buf = ring_s + stage * SB;
       bool slow = false;
       if (bytes == SB) {
@@ -596,7 +646,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     if (lane < 8) s_red[slot][warp * 8 + lane] = p;
     __syncwarp();
     if (lane == 0) mbar_arrive(rfull_s + 8 * slot);
+    if (tid == 0 && it < 8) TRACE(2 + it);
   }
+  if (tid == 0) TRACE(15);
 }
 
 static int g_num_sms = 0;
@@ -647,6 +699,8 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   if (a.flat) {
     // every slice at least 128 elements and a row in at most kMaxSplit parts
     const long long T = a.n_rows * a.vocab;
+    if (T >= (1LL << 51)) return cudaErrorInvalidValue;  // slice math is 64-bit
+    if (grid > 4096) grid = 4096;
     if (grid > T / 128) grid = T / 128 > 0 ? T / 128 : 1;
     if (grid > a.n_rows * (kMaxSplit - 2)) grid = a.n_rows * (kMaxSplit - 2);
   } else if (grid > a.n_rows) {

@@ -371,6 +371,7 @@ relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dt
   if (vocab != cs->dev.vocab) return fail(RELAY_ERR_INVALID, "vocab differs from the cue set's");
   if (row_stride < vocab) return fail(RELAY_ERR_INVALID, "row_stride < vocab");
   if (batch < 0) return fail(RELAY_ERR_INVALID, "batch < 0");
+  if (static_cast<long long>(batch) * vocab >= (1LL << 51)) return fail(RELAY_ERR_INVALID, "batch * vocab must be < 2^51");
   if (!(inv_temperature > 0.0f) || !std::isfinite(inv_temperature))
     return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
   if (max_small_segment < 0) return fail(RELAY_ERR_INVALID, "max_small_segment < 0");

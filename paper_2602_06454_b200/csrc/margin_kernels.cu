@@ -473,13 +473,16 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const uint32_t rfull_s = smem_u32_pinned(red_full);
   const uint32_t rempty_s = smem_u32_pinned(red_empty);
   if (tid == 0) {
+    // Every consumer thread arrives on `empty` after its own shared-memory reads
+    // and on `red_full` after its last threshold read / partial write, so each
+    // thread's accesses are released to the TMA producer / epilogue warp.
     for (int s = 0; s < NS; s++) {
       mbar_init(full_s + 8 * s, 1);
-      mbar_init(empty_s + 8 * s, NCW);
+      mbar_init(empty_s + 8 * s, NCT);
     }
     for (int s = 0; s < kSlots; s++) {
-      mbar_init(rfull_s + 8 * s, NCW);
-      mbar_init(rempty_s + 8 * s, 1);
+      mbar_init(rfull_s + 8 * s, NCT);
+      mbar_init(rempty_s + 8 * s, 32);      // every reading lane of the epilogue warp
       s_theta[s] = fkey(-INFINITY);
     }
     fence_barrier_init();
@@ -537,8 +540,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
       q = warp_reduce_partial(q);
       if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
-      __syncwarp();
-      if (lane == 0) mbar_arrive(rempty_s + 8 * slot);
+      mbar_arrive(rempty_s + 8 * slot);
       if (item.nparts == 1) {
         bool exact = false;
         float S = 0.0f;
@@ -615,8 +617,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         uint4 raw[UV];
 #pragma unroll
         for (int u = 0; u < UV; u++) raw[u] = lds128(buf + (tid + u * NCT) * 16);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty_s + 8 * stage);  // release orders the loads above
+        mbar_arrive(empty_s + 8 * stage);  // release: the loads above precede the refill
         const float2 h = stage_max2<E, UV>(raw);
         if (off == 0) {
           // item-start probe: the two half maxima are two distinct elements, so
@@ -632,8 +633,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           const uint4 raw1[1] = {lds128(buf + v * 16)};
           consume_stage<E, 1>(raw1, stage_max2<E, 1>(raw1), jb + v * VEC, 0, st, c, theta, slow);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty_s + 8 * stage);
+        mbar_arrive(empty_s + 8 * stage);
       }
       if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
       if (++stage == NS) { stage = 0; phase ^= 1; }
@@ -644,8 +644,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     p = partial_merge(p, shfl_xor_partial(p, 16));
     p = partial_merge(p, shfl_xor_partial(p, 8));
     if (lane < 8) s_red[slot][warp * 8 + lane] = p;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(rfull_s + 8 * slot);
+    mbar_arrive(rfull_s + 8 * slot);
     if (tid == 0 && it < 8) TRACE(2 + it);
   }
   if (tid == 0) TRACE(15);

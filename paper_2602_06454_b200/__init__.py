@@ -438,5 +438,5 @@ class Analyzer:
         return g
 
     def n_launches(self) -> int:
-        """Kernels launched by one run(): stats_init 1 + K1 1 + K2 2 + K3 1."""
-        return 5
+        """Kernels launched by one run(): stats_init 1 + K1 1 + K2 1 + K3 1."""
+        return 4

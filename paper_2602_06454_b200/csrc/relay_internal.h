@@ -44,7 +44,9 @@ struct Agg {
 // Workspace layouts (256-byte aligned pieces).  tile_flag and done must be
 // zero before the first K3 launch (relay_workspace_init); K3 leaves them zero.
 struct ScanWs {
-  int* tile_count;     // [n_tiles] K2 per-tile occurrence counts
+  int* k2_flag;        // [n_tiles2] K2 look-back state (0 / count / running sum)
+  long long* k2_val;   // [n_tiles2] K2 published counts
+  int* k2_done;        // [1] K2 finished-tile counter
   int* tile_flag;      // [n_tiles] K3 look-back state (0 / head / inclusive)
   Agg* tile_val;       // [n_tiles] K3 published aggregates
   int* done;           // [1] K3 finished-tile counter

@@ -1,10 +1,10 @@
 // scan_kernels.cu — K2 relay_cue_scan and K3 relay_segment_reduce (sm_100a).
 //
 // K2: switch-cue occurrences by token matching + the
-//     terminator bitmap.  Tiles of 2048 positions (8 consecutive per
-//     thread) staged in shared memory with an 8-token halo; count pass ->
-//     exclusive tile prefix -> ordered scatter, so occurrences come out sorted
-//     by position with no atomics (deterministic).
+//     terminator bitmap.  One kernel: 512-position tiles staged in
+//     shared memory with an 8-token halo; a forward decoupled look-back over
+//     tile counts gives each tile its output offset, so occurrences come out
+//     sorted by position (deterministic, no sort, no second pass).
 // K3: post-sentence windows as a REVERSE segmented scan
 //     keyed by segment tails (terminator or trajectory end): the aggregate at
 //     s over [s, first tail >= s] is exactly the window of a cue at s.  One
@@ -82,14 +82,6 @@ __device__ __forceinline__ int count_at(const CueDev& cs, const SmemPat& sp, con
   return __popcll(m);
 }
 
-__device__ __forceinline__ void stage_tokens(const int* __restrict__ tokens, long long n_tok,
-                                             long long base, int* s_tok) {
-  for (int i = threadIdx.x; i < kTile + kMaxLen; i += blockDim.x) {
-    long long t = base + i;
-    s_tok[i] = (t < n_tok) ? tokens[t] : -1;
-  }
-}
-
 // Room (tokens available inside the trajectory) at position t; 0 outside.
 __device__ __forceinline__ long long room_at(const long long* offs, int n_traj, long long n_tok,
                                              long long t) {
@@ -97,103 +89,100 @@ __device__ __forceinline__ long long room_at(const long long* offs, int n_traj, 
   return k < 0 ? 0 : traj_end(offs, n_tok, k) - t;
 }
 
-template <int NT>
-__device__ __forceinline__ int block_sum(int v, int* s_tmp) {
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) s_tmp[warp] = v;
-  __syncthreads();
-  int tot = 0;
-  for (int w = 0; w < NT / 32; w++) tot += s_tmp[w];
-  return tot;
-}
+// ------------------------------------------------------------------- K2
+// One pass: tiles of kScanTile2 = 512 positions (2 consecutive per thread),
+// tokens staged in shared memory with an 8-token halo.  Each tile publishes its
+// occurrence count, then a forward decoupled look-back over the tiles to its
+// left gives its output offset, so occurrences come out sorted by position
+// with no second pass.  The last tile to finish resets the look-back flags.
+constexpr int kItems2 = 2;
+constexpr int kTile2 = kScanThreads * kItems2;  // 512
+constexpr int kTileAgg = 1;    // value = this tile's count
+constexpr int kTileSum = 2;    // value = count of this tile and every tile before it
 
-// ------------------------------------------------------------- K2 count
 __global__ void __launch_bounds__(kScanThreads)
-    cue_count_kernel(CueDev cs, const int* __restrict__ tokens, long long n_tok,
-                     const long long* __restrict__ offs, int n_traj, uint32_t* __restrict__ term_bits,
-                     int* __restrict__ tile_count) {
-  __shared__ int s_tok[kTile + kMaxLen];
+    cue_scan_kernel(CueDev cs, const int* __restrict__ tokens, long long n_tok,
+                    const long long* __restrict__ offs, int n_traj, uint32_t* __restrict__ term_bits,
+                    int* __restrict__ occ_pos, int* __restrict__ occ_pat, long long cap,
+                    long long* __restrict__ n_occ, int* tile_flag, long long* tile_val, int* done) {
+  __shared__ int s_tok[kTile2 + kMaxLen];
   __shared__ SmemPat sp;
-  __shared__ int s_tmp[32];
-  const long long base = static_cast<long long>(blockIdx.x) * kTile;
-  stage_tokens(tokens, n_tok, base, s_tok);
+  __shared__ int s_scan[kScanThreads];
+  __shared__ long long s_prefix;
+  const int tile = blockIdx.x;
+  const long long base = static_cast<long long>(tile) * kTile2;
+  for (int i = threadIdx.x; i < kTile2 + kMaxLen; i += blockDim.x) {
+    const long long t = base + i;
+    s_tok[i] = (t < n_tok) ? __ldg(tokens + t) : -1;
+  }
   load_patterns(cs, sp);
   __syncthreads();
-  const int li = threadIdx.x * kItems;
+  const int li = threadIdx.x * kItems2;
   int cnt = 0;
   uint32_t tb = 0;
-#pragma unroll 1
-  for (int k = 0; k < kItems; k++) {
-    const long long t = base + li + k;
-    if (t >= n_tok) break;
-    const int tok = s_tok[li + k];
-    if (tok >= 0 && tok < cs.vocab && ((cs.term_tab[tok >> 5] >> (tok & 31)) & 1u)) tb |= 1u << k;
-    const long long room = room_at(offs, n_traj, n_tok, t);
-    unsigned long long mask;
-    int best;
-    if (room > 0) cnt += count_at(cs, sp, s_tok + li + k, room, &mask, &best);
-  }
-  // 4 lanes x 8 bits -> one 32-bit word
-  const int lane = threadIdx.x & 31;
-  uint32_t w = tb << (8 * (lane & 3));
-  w |= __shfl_xor_sync(kFull, w, 1);
-  w |= __shfl_xor_sync(kFull, w, 2);
-  if ((lane & 3) == 0 && base + li < n_tok) term_bits[(base + li) >> 5] = w;
-  const int tot = block_sum<kScanThreads>(cnt, s_tmp);
-  if (threadIdx.x == 0) tile_count[blockIdx.x] = tot;
-}
-
-// ----------------------------------------------------------- K2 scatter
-__global__ void __launch_bounds__(kScanThreads)
-    cue_scatter_kernel(CueDev cs, const int* __restrict__ tokens, long long n_tok,
-                       const long long* __restrict__ offs, int n_traj,
-                       const int* __restrict__ tile_count, int n_tiles, int* __restrict__ occ_pos,
-                       int* __restrict__ occ_pat, long long cap, long long* __restrict__ n_occ) {
-  __shared__ int s_tok[kTile + kMaxLen];
-  __shared__ SmemPat sp;
-  __shared__ int s_tmp[32];
-  __shared__ int s_scan[kScanThreads];
-  const long long base = static_cast<long long>(blockIdx.x) * kTile;
-  stage_tokens(tokens, n_tok, base, s_tok);
-  load_patterns(cs, sp);
-  // prefix of earlier tiles (ints; true counts < 2^31 per call)
-  int pre = 0;
-  for (int i = threadIdx.x; i < blockIdx.x; i += blockDim.x) pre += tile_count[i];
-  __syncthreads();
-  const long long prefix = block_sum<kScanThreads>(pre, s_tmp);
-  const int li = threadIdx.x * kItems;
-  int cnt = 0;
-  unsigned long long masks[kItems];
-  int bests[kItems];
-  long long rooms[kItems];
+  unsigned long long masks[kItems2];
+  int bests[kItems2];
+  long long rooms[kItems2];
 #pragma unroll
-  for (int k = 0; k < kItems; k++) {
+  for (int k = 0; k < kItems2; k++) {
     masks[k] = 0; bests[k] = -1; rooms[k] = 0;
     const long long t = base + li + k;
     if (t < n_tok) {
+      const int tok = s_tok[li + k];
+      if (tok >= 0 && tok < cs.vocab && ((cs.term_tab[tok >> 5] >> (tok & 31)) & 1u)) tb |= 1u << k;
       rooms[k] = room_at(offs, n_traj, n_tok, t);
       if (rooms[k] > 0) {
-        int c = count_at(cs, sp, s_tok + li + k, rooms[k], &masks[k], &bests[k]);
+        const int c = count_at(cs, sp, s_tok + li + k, rooms[k], &masks[k], &bests[k]);
         if (c == 0) bests[k] = -1;
         cnt += c;
       }
     }
   }
-  // block exclusive scan of cnt (thread order == position order)
+  // terminator bits: 16 lanes x 2 bits -> one 32-bit word
+  const int lane = threadIdx.x & 31;
+  uint32_t w = tb << (2 * (lane & 15));
+#pragma unroll
+  for (int off = 1; off < 16; off <<= 1) w |= __shfl_xor_sync(kFull, w, off);
+  if ((lane & 15) == 0 && base + li < n_tok) term_bits[(base + li) >> 5] = w;
+  // block inclusive scan of the per-thread counts (thread order == position order)
   s_scan[threadIdx.x] = cnt;
   __syncthreads();
   for (int off = 1; off < kScanThreads; off <<= 1) {
-    int v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
+    const int v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
     __syncthreads();
     s_scan[threadIdx.x] += v;
     __syncthreads();
   }
-  long long o = prefix + s_scan[threadIdx.x] - cnt;
-  const int tile_total = s_scan[kScanThreads - 1];
-#pragma unroll 1
-  for (int k = 0; k < kItems; k++) {
+  if (threadIdx.x == 0) {
+    const long long total = s_scan[kScanThreads - 1];
+    long long prefix = 0;
+    if (tile == 0) {
+      tile_val[0] = total;
+      __threadfence();
+      atomicExch(tile_flag, kTileSum);
+    } else {
+      tile_val[tile] = total;
+      __threadfence();
+      atomicExch(tile_flag + tile, kTileAgg);
+      for (int j = tile - 1; j >= 0; j--) {
+        int f;
+        while ((f = *reinterpret_cast<volatile int*>(tile_flag + j)) == 0) {
+        }
+        __threadfence();
+        prefix += __ldcg(tile_val + j);
+        if (f == kTileSum) break;
+      }
+      tile_val[tile] = prefix + total;  // the flag below makes it the inclusive sum
+      __threadfence();
+      atomicExch(tile_flag + tile, kTileSum);
+    }
+    s_prefix = prefix;
+    if (tile == gridDim.x - 1) *n_occ = prefix + total;
+  }
+  __syncthreads();
+  long long o = s_prefix + s_scan[threadIdx.x] - cnt;
+#pragma unroll
+  for (int k = 0; k < kItems2; k++) {
     const long long t = base + li + k;
     if (t >= n_tok) break;
     if (cs.mode == 0) {
@@ -214,7 +203,16 @@ __global__ void __launch_bounds__(kScanThreads)
       }
     }
   }
-  if (blockIdx.x == n_tiles - 1 && threadIdx.x == 0) *n_occ = prefix + tile_total;
+  // the last tile to finish resets the look-back flags for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1) == gridDim.x - 1) {
+      for (int j = 0; j < gridDim.x; j++) tile_flag[j] = 0;
+      __threadfence();
+      *done = 0;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ K3
@@ -540,13 +538,11 @@ cudaError_t launch_cue_scan(const CueDev& cs, const int* tokens, long long n_tok
                             const long long* offs, int n_traj, uint32_t* term_bits, int* occ_pos,
                             int* occ_pat, long long cap, long long* n_occ, const ScanWs& ws,
                             cudaStream_t st) {
-  const int nt = n_tiles_of(n_tok);
-  cue_count_kernel<<<nt, kScanThreads, 0, st>>>(cs, tokens, n_tok, offs, n_traj, term_bits,
-                                                ws.tile_count);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  cue_scatter_kernel<<<nt, kScanThreads, 0, st>>>(cs, tokens, n_tok, offs, n_traj, ws.tile_count,
-                                                  nt, occ_pos, occ_pat, cap, n_occ);
+  long long nt = (n_tok + kTile2 - 1) / kTile2;
+  if (nt < 1) nt = 1;
+  cue_scan_kernel<<<static_cast<unsigned>(nt), kScanThreads, 0, st>>>(
+      cs, tokens, n_tok, offs, n_traj, term_bits, occ_pos, occ_pat, cap, n_occ, ws.k2_flag, ws.k2_val,
+      ws.k2_done);
   return cudaGetLastError();
 }
 

@@ -66,10 +66,10 @@ ScanWs scan_ws_layout(void* base, long long n_tok, long long cap) {
   };
   const long long nt2 = (n_tok + 511) / 512 + 1;  // K2 tiles of 512 positions
   w.k2_flag = reinterpret_cast<int*>(take(sizeof(int) * nt2));
-  w.k2_val = reinterpret_cast<long long*>(take(sizeof(long long) * nt2));
+  w.k2_val = reinterpret_cast<long long*>(take(2 * sizeof(long long) * nt2));
   w.k2_done = reinterpret_cast<int*>(take(sizeof(int)));
   w.tile_flag = reinterpret_cast<int*>(take(sizeof(int) * nt));
-  w.tile_val = reinterpret_cast<Agg*>(take(sizeof(Agg) * nt));
+  w.tile_val = reinterpret_cast<Agg*>(take(2 * sizeof(Agg) * nt));
   w.done = reinterpret_cast<int*>(take(sizeof(int)));
   (void)cap;
   w.bytes = off;

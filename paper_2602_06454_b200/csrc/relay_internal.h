@@ -45,10 +45,10 @@ struct Agg {
 // zero before the first K3 launch (relay_workspace_init); K3 leaves them zero.
 struct ScanWs {
   int* k2_flag;        // [n_tiles2] K2 look-back state (0 / count / running sum)
-  long long* k2_val;   // [n_tiles2] K2 published counts
+  long long* k2_val;   // [n_tiles2][2] K2 published count / running sum
   int* k2_done;        // [1] K2 finished-tile counter
   int* tile_flag;      // [n_tiles] K3 look-back state (0 / head / inclusive)
-  Agg* tile_val;       // [n_tiles] K3 published aggregates
+  Agg* tile_val;       // [n_tiles][2] K3 published head / inclusive aggregate
   int* done;           // [1] K3 finished-tile counter
   size_t bytes;
 };

@@ -156,12 +156,14 @@ __global__ void __launch_bounds__(kScanThreads)
   if (threadIdx.x == 0) {
     const long long total = s_scan[kScanThreads - 1];
     long long prefix = 0;
+    // tile_val[2t] = this tile's count, tile_val[2t+1] = inclusive running sum;
+    // each is written once, before the flag that announces it
     if (tile == 0) {
-      tile_val[0] = total;
+      tile_val[1] = total;
       __threadfence();
       atomicExch(tile_flag, kTileSum);
     } else {
-      tile_val[tile] = total;
+      tile_val[2 * tile] = total;
       __threadfence();
       atomicExch(tile_flag + tile, kTileAgg);
       for (int j = tile - 1; j >= 0; j--) {
@@ -169,10 +171,13 @@ __global__ void __launch_bounds__(kScanThreads)
         while ((f = *reinterpret_cast<volatile int*>(tile_flag + j)) == 0) {
         }
         __threadfence();
-        prefix += __ldcg(tile_val + j);
-        if (f == kTileSum) break;
+        if (f == kTileSum) {
+          prefix += __ldcg(tile_val + 2 * j + 1);
+          break;
+        }
+        prefix += __ldcg(tile_val + 2 * j);
       }
-      tile_val[tile] = prefix + total;  // the flag below makes it the inclusive sum
+      tile_val[2 * tile + 1] = prefix + total;
       __threadfence();
       atomicExch(tile_flag + tile, kTileSum);
     }
@@ -323,6 +328,8 @@ __device__ __forceinline__ int lower_bound_occ(const int* occ_pos, int n, long l
 constexpr int kTileHead = 1;   // value = aggregate from the tile start to its first tail
 constexpr int kTileIncl = 2;   // value = aggregate from the tile start onwards (carry included)
 
+// val[2t] holds the head, val[2t+1] the inclusive value; each is written once,
+// before the flag that announces it, so a reader never sees a torn value.
 __device__ __forceinline__ void publish(int* flag, Agg* val, const Agg& a, int state) {
   val->sumq = a.sumq; val->low = a.low; val->nan = a.nan; val->mn = a.mn;
   val->end = a.end; val->tail = a.tail; val->pad = 0;
@@ -423,21 +430,26 @@ __global__ void __launch_bounds__(kScanThreads)
     // tile still needs its own carry (the run after its last tail), which the
     // look-back assembles from the heads of the tiles to the right: it stops
     // at the first head holding a tail or at an inclusive value.
-    publish(tile_flag + tile, tile_val + tile, head, head.tail ? kTileIncl : kTileHead);
+    if (head.tail) {
+      publish(tile_flag + tile, tile_val + 2 * tile + 1, head, kTileIncl);
+    } else {
+      publish(tile_flag + tile, tile_val + 2 * tile, head, kTileHead);
+    }
     Agg carry = agg_identity();
     for (int j = tile + 1; j < n_tiles; j++) {
       int f;
       while ((f = *reinterpret_cast<volatile int*>(tile_flag + j)) == 0) {
       }
       __threadfence();
+      const Agg* src = tile_val + 2 * j + (f == kTileIncl ? 1 : 0);
       Agg v;
-      v.sumq = __ldcg(&tile_val[j].sumq); v.low = __ldcg(&tile_val[j].low);
-      v.nan = __ldcg(&tile_val[j].nan); v.mn = __ldcg(&tile_val[j].mn);
-      v.end = __ldcg(&tile_val[j].end); v.tail = __ldcg(&tile_val[j].tail); v.pad = 0;
+      v.sumq = __ldcg(&src->sumq); v.low = __ldcg(&src->low);
+      v.nan = __ldcg(&src->nan); v.mn = __ldcg(&src->mn);
+      v.end = __ldcg(&src->end); v.tail = __ldcg(&src->tail); v.pad = 0;
       carry = agg_suffix(carry, v);
       if (f == kTileIncl || v.tail) break;
     }
-    if (!head.tail) publish(tile_flag + tile, tile_val + tile, agg_suffix(head, carry), kTileIncl);
+    if (!head.tail) publish(tile_flag + tile, tile_val + 2 * tile + 1, agg_suffix(head, carry), kTileIncl);
     s_carry = carry;
   }
   __syncthreads();

@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no clocks/e2e/baseline)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--serial-scan", action="store_true",
+                    help="run K2 before K1 on the main stream instead of on a side stream")
     return ap.parse_args()
 
 
@@ -217,7 +219,8 @@ def main():
     tok = torch.as_tensor(ts.tokens, device=dev)
     offs = torch.as_tensor(ts.traj_offsets, device=dev)
     tep = torch.as_tensor(ts.think_end_pos, device=dev)
-    an = relay.Analyzer(cs, T, vocab, dev, rank=rank, world_size=world)
+    an = relay.Analyzer(cs, T, vocab, dev, rank=rank, world_size=world,
+                        overlap_scan=not args.serial_scan)
     stream = torch.cuda.current_stream()
     # two pinned host tables: step i's table is finalized on the host while the
     # GPU already runs step i+1 (the work per step is unchanged)

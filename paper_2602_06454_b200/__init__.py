@@ -340,10 +340,12 @@ class Analyzer:
     the host).  Buffers are allocated once; ``run`` only launches kernels."""
 
     def __init__(self, cs: CueSet, n_tok: int, vocab: int, device="cuda", occ_capacity=None,
-                 tau: float = 0.5, rank: int = 0, world_size: int = 1, inv_temperature=1.0):
+                 tau: float = 0.5, rank: int = 0, world_size: int = 1, inv_temperature=1.0,
+                 overlap_scan: bool = True):
         import torch
         self.cs, self.n_tok, self.vocab, self.tau = cs, n_tok, vocab, tau
         self.rank, self.world_size, self.iota = rank, world_size, inv_temperature
+        self.overlap_scan = overlap_scan
         self.device = torch.device(device)
         self.cap = (n_tok * (cs.n_cues if cs.mode else 1)) if occ_capacity is None else occ_capacity
         d = self.device
@@ -371,14 +373,17 @@ class Analyzer:
         with K1; K3 joins both.  Stream-ordered, no host synchronisation."""
         import torch
         s = torch.cuda.current_stream() if stream is None else stream
-        if self._side is None:
-            self._side = torch.cuda.Stream(device=self.device)
-            self._fork = torch.cuda.Event()
-            self._join = torch.cuda.Event()
-        self._fork.record(s)
-        self._side.wait_event(self._fork)
-        cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
-        self._join.record(self._side)
+        if not self.overlap_scan:
+            cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, s)
+        else:
+            if self._side is None:
+                self._side = torch.cuda.Stream(device=self.device)
+                self._fork = torch.cuda.Event()
+                self._join = torch.cuda.Event()
+            self._fork.record(s)
+            self._side.wait_event(self._fork)
+            cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
+            self._join.record(self._side)
         stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s)
         if k1_events:
             k1_events[0].record(s)
@@ -386,7 +391,8 @@ class Analyzer:
                     stream=s)
         if k1_events:
             k1_events[1].record(s)
-        s.wait_event(self._join)
+        if self.overlap_scan:
+            s.wait_event(self._join)
         segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
                        self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s)
         return self.stats

@@ -101,6 +101,30 @@ relay_status_t relay_margin_rows(const void* logits, relay_dtype_t dt, int64_t n
                                  float* margin, int32_t* top1, int32_t* top2, float* lse,
                                  uint8_t* row_status, relay_stream_t stream);
 
+/* ------------------------------------------------------ H1 across TP ranks --
+ * the margin when the LM head is tensor-parallel and each
+ * rank holds a column shard [col_offset, col_offset + shard_vocab) of every
+ * logit row.  relay_margin_partials reduces the shard (same streaming kernel
+ * as relay_margin_rows) to RELAY_PARTIAL_WORDS floats per row:
+ *   [0] v1 = shard max, [1] v2, [2] i1, [3] i2 (int32 bits, GLOBAL indices;
+ *   INT32_MAX when absent), [4] S_rel = sum over the shard of
+ *   exp((z_j - v1) iota), [5] NaN flag (int32 bits), [6..7] 0.
+ * The caller gathers the partials of all shards ([n_shards][n_rows][8], e.g.
+ * one NCCL all-gather of 32 B per row per rank) and relay_margin_combine
+ * merges them: top-2 by (value desc, global index asc), S = sum_k S_k
+ * exp((v1_k - M) iota), margin = (1 - exp((v2 - M) iota)) / S — the same
+ * definition as relay_margin_rows on the full row.
+ * Errors: as relay_margin_rows (shard_vocab >= 1 allowed), n_shards < 1,
+ * col_offset < 0 or col_offset + shard_vocab >= 2^31. */
+#define RELAY_PARTIAL_WORDS 8
+relay_status_t relay_margin_partials(const void* logits, relay_dtype_t dt, int64_t n_rows,
+                                     int64_t shard_vocab, int64_t row_stride, int64_t col_offset,
+                                     float inv_temperature, float* partials, relay_stream_t stream);
+relay_status_t relay_margin_combine(const float* partials, int32_t n_shards, int64_t n_rows,
+                                    float inv_temperature, float* margin, int32_t* top1,
+                                    int32_t* top2, float* lse, uint8_t* row_status,
+                                    relay_stream_t stream);
+
 /* ------------------------------------------------------------- cue set --
  * A model pair's switch-cue set (tab:switch_cue_sets) as token-ID
  * patterns (R5: the caller tokenises every surface variant) plus the sentence

@@ -66,6 +66,8 @@ def _load():
         "relay_status_string": (C.c_char_p, [C.c_int]),
         "relay_last_error": (C.c_char_p, []),
         "relay_margin_rows": (C.c_int, [P, C.c_int, i64, i64, i64, f32, P, P, P, P, P, P]),
+        "relay_margin_partials": (C.c_int, [P, C.c_int, i64, i64, i64, i64, f32, P, P]),
+        "relay_margin_combine": (C.c_int, [P, i32, i64, f32, P, P, P, P, P, P]),
         "relay_cueset_create": (C.c_int, [P, P, i32, P, i32, P, i64, i32, u32, P]),
         "relay_cueset_destroy": (C.c_int, [P]),
         "relay_cueset_n_cues": (i32, [P]),
@@ -89,6 +91,7 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_margin_rows",
+           "relay_margin_partials", "relay_margin_combine",
            "relay_cueset_create", "relay_cueset_destroy", "relay_cueset_n_cues",
            "relay_workspace_bytes", "relay_workspace_init", "relay_cue_scan",
            "relay_segment_reduce", "relay_stats_init", "relay_stats_words",
@@ -154,6 +157,61 @@ def margin_rows(logits, vocab: int | None = None, inv_temperature: float = 1.0, 
                                 _ptr(out.get("status")), _stream(stream))
     _check(rc, "relay_margin_rows")
     return out
+
+
+# ------------------------------------------------- H1 across TP ranks (N1)
+PARTIAL_WORDS = 8
+
+
+def margin_partials(logits_shard, col_offset: int, inv_temperature: float = 1.0, out=None,
+                    stream=None):
+    """relay_margin_partials: per-row partials [n_rows, 8] of a vocabulary shard
+    (columns [col_offset, col_offset + shard width) of the full rows)."""
+    import torch
+    _need_cuda(logits_shard)
+    if logits_shard.dim() != 2 or logits_shard.stride(1) != 1:
+        raise RelayError("logits shard must be 2-D with unit stride in the vocabulary dim")
+    n = logits_shard.shape[0]
+    stride = logits_shard.stride(0) if n > 1 else logits_shard.shape[1]
+    if out is None:
+        out = torch.empty((n, PARTIAL_WORDS), dtype=torch.float32, device=logits_shard.device)
+    rc = _lib.relay_margin_partials(_ptr(logits_shard), _dtype_of(logits_shard), n,
+                                    logits_shard.shape[1], stride, int(col_offset),
+                                    float(inv_temperature), _ptr(out), _stream(stream))
+    _check(rc, "relay_margin_partials")
+    return out
+
+
+def margin_combine(partials, inv_temperature: float = 1.0, out=None, stream=None):
+    """relay_margin_combine on stacked partials [n_shards, n_rows, 8]."""
+    import torch
+    _need_cuda(partials)
+    parts = partials.contiguous()
+    P, n = parts.shape[0], parts.shape[1]
+    dev = parts.device
+    if out is None:
+        out = dict(margin=torch.empty(n, dtype=torch.float32, device=dev),
+                   top1=torch.empty(n, dtype=torch.int32, device=dev),
+                   top2=torch.empty(n, dtype=torch.int32, device=dev),
+                   lse=torch.empty(n, dtype=torch.float32, device=dev),
+                   status=torch.empty(n, dtype=torch.uint8, device=dev))
+    rc = _lib.relay_margin_combine(_ptr(parts), P, n, float(inv_temperature), _ptr(out["margin"]),
+                                   _ptr(out.get("top1")), _ptr(out.get("top2")),
+                                   _ptr(out.get("lse")), _ptr(out.get("status")), _stream(stream))
+    _check(rc, "relay_margin_combine")
+    return out
+
+
+def margin_rows_tp(logits_shard, col_offset: int, group=None, inv_temperature: float = 1.0):
+    """The margin of rows whose vocabulary is sharded over a tensor-parallel
+    group: shard partials (32 B/row) -> one all-gather -> combine, on every rank."""
+    import torch
+    import torch.distributed as dist
+    part = margin_partials(logits_shard, col_offset, inv_temperature)
+    world = dist.get_world_size(group)
+    gathered = torch.empty((world,) + tuple(part.shape), dtype=part.dtype, device=part.device)
+    dist.all_gather_into_tensor(gathered, part, group=group)
+    return margin_combine(gathered, inv_temperature)
 
 
 # --------------------------------------------------------------- cue set

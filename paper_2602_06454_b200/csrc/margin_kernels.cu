@@ -236,7 +236,10 @@ struct RowsArgs {
   uint8_t* status;
   int* counter;   // [n_rows] arrival counters (flat)
   float* part;    // [n_rows][kMaxSplit][kPartWords] row-part partials (flat)
-  // decode-step switch (STEP)
+  // vocabulary-parallel partials (kModePartial)
+  long long col_offset;  // global index of the shard's first column
+  float* tp_part;        // [n_rows][kPartWords]
+  // decode-step switch (kModeStep)
   const int* sampled;
   uint8_t* state;
   int* hist;
@@ -248,6 +251,9 @@ struct RowsArgs {
 };
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
+constexpr int kModeRows = 0;     // K1: margins of whole rows
+constexpr int kModeStep = 1;     // K4: margins + the decode-step switch
+constexpr int kModePartial = 2;  // N1: per-row partials of a vocabulary shard
 
 // Arrival counter increment with acquire-release semantics at GPU scope: the
 // part written before it is visible to the last arriver, which then reads
@@ -348,12 +354,35 @@ __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float 
 }
 
 // Warp-level finish of row r from its merged partial (lane 0 writes).
-template <class E, bool STEP>
+template <class E, int MODE>
 __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs, const SmemCue& sc,
                                             long long r, const Partial& q, bool exact, float S,
                                             const SwitchIn& in) {
-  const RowOut o = finish_row(q, a.c, a.iota, exact, S);
   const int lane = threadIdx.x & 31;
+  if constexpr (MODE == kModePartial) {
+    // vocabulary shard: top-2 with GLOBAL indices and the normaliser relative
+    // to the shard maximum, S_rel = sum_j 2^((z_j - v1) c), shift removed
+    if (lane == 0) {
+      float srel = 0.0f;
+      if (exact) {
+        srel = S;
+      } else if (q.t.v1 != -INFINITY && q.t.v1 != INFINITY) {
+        const float My = q.t.v1 * a.c;
+        srel = q.n.s * ex2((q.n.m - My) - fmaf(q.t.v1, a.c, -My));
+      }
+      float* pw = a.tp_part + static_cast<size_t>(r) * kPartWords;
+      pw[0] = q.t.v1;
+      pw[1] = q.t.v2;
+      pw[2] = __int_as_float(q.t.i1 == INT_MAX ? INT_MAX : static_cast<int>(q.t.i1 + a.col_offset));
+      pw[3] = __int_as_float(q.t.i2 == INT_MAX ? INT_MAX : static_cast<int>(q.t.i2 + a.col_offset));
+      pw[4] = srel;
+      pw[5] = __int_as_float(q.flags & kFlagNan);
+      pw[6] = 0.0f;
+      pw[7] = 0.0f;
+    }
+    return;
+  }
+  const RowOut o = finish_row(q, a.c, a.iota, exact, S);
   if (lane == 0) {
     a.margin[r] = o.margin;
     if (a.top1) a.top1[r] = o.i1;
@@ -361,7 +390,7 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
     if (a.lse) a.lse[r] = o.lse;
     if (a.status) a.status[r] = static_cast<uint8_t>(o.status);
   }
-  if constexpr (STEP) {
+  if constexpr (MODE == kModeStep) {
     const int tok = a.sampled ? in.sampled : o.i1;
     switch_warp(cs, sc, tok, o.margin, in, a.state + r, a.hist + r * kHist,
                 a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r, a.cue_id + r);
@@ -447,7 +476,7 @@ extern "C" int relay_debug_trace_copy(unsigned long long* host, int n_ctas) {
 #define TRACE(k) ((void)0)
 #endif
 
-template <class E, int NCW, int NS, int UV, int MINB, bool STEP>
+template <class E, int NCW, int NS, int UV, int MINB, int MODE>
 __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
@@ -517,7 +546,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 
   if (warp == NCW + 1) {
     // ------------------------------------------------ epilogue warp
-    if constexpr (STEP) {  // the switch patterns, for this warp only
+    if constexpr (MODE == kModeStep) {  // the switch patterns, for this warp only
       for (int i = lane; i < cs.n_pat * kMaxLen; i += 32) sc.tok[i] = cs.pat_tok[i];
       for (int i = lane; i < cs.n_pat; i += 32) {
         sc.len[i] = cs.pat_len[i];
@@ -533,7 +562,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const long long r = item.r;
       const T* row = logits + r * a.stride;
       SwitchIn in{};
-      if constexpr (STEP) in = load_switch_in(a, r);
+      if constexpr (MODE == kModeStep) in = load_switch_in(a, r);
       mbar_wait(rfull_s + 8 * slot, (it / kSlots) & 1);  // on the critical path: spin
       Partial q = partial_empty();
 #pragma unroll
@@ -548,7 +577,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           S = warp_sum(exact_sum_thread<E>(row, a.vocab, q.t.v1, c, lane, 32));
           exact = true;
         }
-        finish_item<E, STEP>(a, cs, sc, r, q, exact, S, in);
+        finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in);
         continue;
       }
       // publish this part; the last part of the row to arrive finishes it
@@ -580,7 +609,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         exact = true;
       }
       if (lane == 0) a.counter[r] = 0;  // ready for the next launch / graph replay
-      finish_item<E, STEP>(a, cs, sc, r, m, exact, S, in);
+      finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in);
       if (lane == 0 && it < 5) TRACE(10 + it);
     }
     return;
@@ -681,9 +710,9 @@ constexpr int kStages = RELAY_K1_STAGES;  // ring depth
 constexpr int kUV = RELAY_K1_UV;          // 16-byte vectors per consumer thread per stage
 constexpr int kMinBlocks = RELAY_K1_MINB; // CTAs per SM the registers must allow
 
-template <class E, bool STEP>
+template <class E, int MODE>
 static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) {
-  auto kern = rows_kernel<E, kNCW, kStages, kUV, kMinBlocks, STEP>;
+  auto kern = rows_kernel<E, kNCW, kStages, kUV, kMinBlocks, MODE>;
   const int smem = kStages * kUV * kNCW * 32 * 16;
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -709,12 +738,12 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   return cudaGetLastError();
 }
 
-template <bool STEP>
+template <int MODE>
 static cudaError_t launch_rows(int dt, const RowsArgs& a, const CueDev& cs, cudaStream_t st) {
   switch (dt) {
-    case 0: return launch_rows_t<EBf16, STEP>(a, cs, st);
-    case 1: return launch_rows_t<EF16, STEP>(a, cs, st);
-    default: return launch_rows_t<EF32, STEP>(a, cs, st);
+    case 0: return launch_rows_t<EBf16, MODE>(a, cs, st);
+    case 1: return launch_rows_t<EF16, MODE>(a, cs, st);
+    default: return launch_rows_t<EF32, MODE>(a, cs, st);
   }
 }
 
@@ -726,7 +755,7 @@ cudaError_t launch_margin_rows(const void* logits, int dt, long long n_rows, int
   a.logits = logits; a.n_rows = n_rows; a.vocab = vocab; a.stride = stride;
   a.c = iota * kLog2e; a.iota = iota; a.flat = 0;
   a.margin = margin; a.top1 = top1; a.top2 = top2; a.lse = lse; a.status = status;
-  return launch_rows<false>(dt, a, CueDev{}, st);
+  return launch_rows<kModeRows>(dt, a, CueDev{}, st);
 }
 
 cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
@@ -742,7 +771,68 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
   a.counter = ws.counter; a.part = ws.part;
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
   a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
-  return launch_rows<true>(dt, a, cs, st);
+  return launch_rows<kModeStep>(dt, a, cs, st);
+}
+
+cudaError_t launch_margin_partials(const void* logits, int dt, long long n_rows, int vocab,
+                                  long long stride, long long col_offset, float iota, float* part,
+                                  cudaStream_t st) {
+  if (n_rows <= 0) return cudaSuccess;
+  RowsArgs a{};
+  a.logits = logits; a.n_rows = n_rows; a.vocab = vocab; a.stride = stride;
+  a.c = iota * kLog2e; a.iota = iota; a.flat = 0;
+  a.col_offset = col_offset; a.tp_part = part;
+  return launch_rows<kModePartial>(dt, a, CueDev{}, st);
+}
+
+// N1 combine: merge the vocabulary shards' partials of each row (one thread
+// per row): top-2 by (value desc, global index asc); S = sum_k S_k 2^((v1_k -
+// M) c); the margin as in finish_row's exact form.
+__global__ void margin_combine_kernel(const float* __restrict__ part, int n_shards, long long n_rows,
+                                      float c, float iota, float* __restrict__ margin,
+                                      int* __restrict__ top1, int* __restrict__ top2,
+                                      float* __restrict__ lse, uint8_t* __restrict__ status) {
+  const long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (r >= n_rows) return;
+  Top2 t = top2_empty();
+  int nan = 0;
+  for (int k = 0; k < n_shards; k++) {
+    const float* p = part + (static_cast<size_t>(k) * n_rows + r) * kPartWords;
+    Top2 o{p[0], p[1], __float_as_int(p[2]), __float_as_int(p[3])};
+    t = top2_merge(t, o);
+    nan |= __float_as_int(p[5]);
+  }
+  int st = 0;
+  if (nan || t.v1 == INFINITY) st = 1;
+  else if (t.v1 == -INFINITY) st = 2;
+  if (st) {
+    margin[r] = qnan();
+    if (top1) top1[r] = -1;
+    if (top2) top2[r] = -1;
+    if (lse) lse[r] = qnan();
+    if (status) status[r] = static_cast<uint8_t>(st);
+    return;
+  }
+  float S = 0.0f;
+  for (int k = 0; k < n_shards; k++) {
+    const float* p = part + (static_cast<size_t>(k) * n_rows + r) * kPartWords;
+    if (p[4] > 0.0f) S += p[4] * ex2((p[0] - t.v1) * c);
+  }
+  margin[r] = (1.0f - ex2((t.v2 - t.v1) * c)) / S;
+  if (top1) top1[r] = t.i1;
+  if (top2) top2[r] = t.i2;
+  if (lse) lse[r] = t.v1 * iota + logf(S);
+  if (status) status[r] = 0;
+}
+
+cudaError_t launch_margin_combine(const float* part, int n_shards, long long n_rows, float iota,
+                                  float* margin, int* top1, int* top2, float* lse, uint8_t* status,
+                                  cudaStream_t st) {
+  if (n_rows <= 0) return cudaSuccess;
+  const long long blocks = (n_rows + 127) / 128;
+  margin_combine_kernel<<<static_cast<unsigned>(blocks), 128, 0, st>>>(part, n_shards, n_rows, iota * kLog2e,
+                                                                        iota, margin, top1, top2, lse, status);
+  return cudaGetLastError();
 }
 
 }  // namespace relay

@@ -132,6 +132,40 @@ relay_status_t relay_margin_rows(const void* logits, relay_dtype_t dt, int64_t n
                      "relay_margin_rows launch");
 }
 
+relay_status_t relay_margin_partials(const void* logits, relay_dtype_t dt, int64_t n_rows,
+                                     int64_t shard_vocab, int64_t row_stride, int64_t col_offset,
+                                     float inv_temperature, float* partials, relay_stream_t stream) {
+  if (!valid_dtype(dt)) return fail(RELAY_ERR_INVALID, "unknown dtype %d", static_cast<int>(dt));
+  if (shard_vocab < 1) return fail(RELAY_ERR_INVALID, "shard_vocab must be >= 1");
+  if (col_offset < 0 || col_offset + shard_vocab >= 0x7fffffffLL)
+    return fail(RELAY_ERR_INVALID, "col_offset out of range");
+  if (shard_vocab * (dt == RELAY_DT_F32 ? 4 : 2) >= 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "row bytes must be < 2^31");
+  if (row_stride < shard_vocab) return fail(RELAY_ERR_INVALID, "row_stride < shard_vocab");
+  if (n_rows < 0) return fail(RELAY_ERR_INVALID, "n_rows < 0");
+  if (!(inv_temperature > 0.0f) || !std::isfinite(inv_temperature))
+    return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
+  if (n_rows == 0) return RELAY_OK;
+  if (!logits || !partials) return fail(RELAY_ERR_INVALID, "logits and partials are required");
+  return cuda_status(launch_margin_partials(logits, static_cast<int>(dt), n_rows, static_cast<int>(shard_vocab),
+                                            row_stride, col_offset, inv_temperature, partials,
+                                            reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_margin_partials launch");
+}
+
+relay_status_t relay_margin_combine(const float* partials, int32_t n_shards, int64_t n_rows,
+                                    float inv_temperature, float* margin, int32_t* top1, int32_t* top2,
+                                    float* lse, uint8_t* row_status, relay_stream_t stream) {
+  if (n_shards < 1) return fail(RELAY_ERR_INVALID, "n_shards must be >= 1");
+  if (n_rows < 0) return fail(RELAY_ERR_INVALID, "n_rows < 0");
+  if (!(inv_temperature > 0.0f) || !std::isfinite(inv_temperature))
+    return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
+  if (n_rows == 0) return RELAY_OK;
+  if (!partials || !margin) return fail(RELAY_ERR_INVALID, "partials and margin are required");
+  return cuda_status(launch_margin_combine(partials, n_shards, n_rows, inv_temperature, margin, top1, top2,
+                                           lse, row_status, reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_margin_combine launch");
+}
+
 relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat_offsets,
                                    int32_t n_patterns, const int32_t* pat_cue, int32_t n_cues,
                                    const uint8_t* terminator, int64_t vocab, int32_t think_end_token,

@@ -67,6 +67,13 @@ cudaError_t launch_margin_rows(const void* logits, int dt, long long n_rows, int
                                long long stride, float iota, float* margin, int* top1, int* top2,
                                float* lse, uint8_t* status, cudaStream_t st);
 
+cudaError_t launch_margin_partials(const void* logits, int dt, long long n_rows, int vocab,
+                                  long long stride, long long col_offset, float iota, float* part,
+                                  cudaStream_t st);
+cudaError_t launch_margin_combine(const float* part, int n_shards, long long n_rows, float iota,
+                                  float* margin, int* top1, int* top2, float* lse, uint8_t* status,
+                                  cudaStream_t st);
+
 cudaError_t launch_cue_scan(const CueDev& cs, const int* tokens, long long n_tok,
                             const long long* offs, int n_traj, uint32_t* term_bits, int* occ_pos,
                             int* occ_pat, long long cap, long long* n_occ, const ScanWs& ws,

@@ -616,3 +616,73 @@ def test_c5_shape_streamed(relay):
         np.testing.assert_array_equal(pat[sel], o["occ_pat"])
         np.testing.assert_array_equal(ends[sel] - a, w["seg_end"])
         assert np.abs(means[sel] - w["seg_mean"]).max() < 1e-6
+
+
+# ------------------------------------------- N1: vocabulary-parallel margin
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_margin_tp_shards_equal_full_rows(relay, dtype, P):
+    """Partials of P column shards, combined, equal the full-row result: the
+    same indices and (within 1e-5) the oracle's margins."""
+    V = 30011
+    L = synth.make_logits(200, V, dtype, seed=P, device=DEV)
+    bounds = np.linspace(0, V, P + 1).astype(int)
+    parts = torch.stack([relay.margin_partials(L[:, a:b], int(a)) for a, b in zip(bounds[:-1], bounds[1:])])
+    got = relay.margin_combine(parts)
+    full = relay.margin_rows(L)
+    torch.cuda.synchronize()
+    ref = oracle.margin_rows(synth.host_rows(L, dtype), dtype=dtype, threads=8)
+    np.testing.assert_array_equal(got["top1"].cpu().numpy(), ref["top1"])
+    np.testing.assert_array_equal(got["top2"].cpu().numpy(), ref["top2"])
+    np.testing.assert_array_equal(got["status"].cpu().numpy(), ref["status"].astype(np.uint8))
+    ok = ref["status"] == 0
+    assert np.abs(got["margin"].cpu().numpy()[ok] - ref["margin"][ok]).max() < TOL
+    assert np.abs(got["margin"].cpu().numpy()[ok] - full["margin"].cpu().numpy()[ok]).max() < 2e-6
+
+
+def test_margin_tp_edge_rows(relay):
+    """Shards holding only -inf, NaN in one shard, top-1 tie across shards."""
+    V = 64
+    rows = torch.randn(6, V) * 2
+    rows[0, :32] = float("-inf")                  # first shard empty
+    rows[1, 40] = float("nan")                    # NaN in the second shard
+    rows[2, 5] = 30.0; rows[2, 50] = 30.0         # tie across shards: lowest index wins
+    rows[3, :] = float("-inf"); rows[3, 63] = 1.0
+    rows[4, :] = 0.5                              # uniform
+    L = rows.to(torch.bfloat16).to(DEV)
+    parts = torch.stack([relay.margin_partials(L[:, :32], 0), relay.margin_partials(L[:, 32:], 32)])
+    got = relay.margin_combine(parts)
+    torch.cuda.synchronize()
+    ref = oracle.margin_rows(synth.host_rows(L, "bf16"), dtype="bf16")
+    np.testing.assert_array_equal(got["status"].cpu().numpy(), ref["status"].astype(np.uint8))
+    np.testing.assert_array_equal(got["top1"].cpu().numpy(), ref["top1"])
+    np.testing.assert_array_equal(got["top2"].cpu().numpy(), ref["top2"])
+
+
+def _tp_worker(rank, world, port, out):
+    import torch.distributed as dist
+    import paper_2602_06454_b200 as relay
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    V = 20000
+    L = synth.make_logits(96, V, "bf16", seed=5, device="cuda:0")
+    a, b = rank * V // world, (rank + 1) * V // world
+    res = relay.margin_rows_tp(L[:, a:b], a)
+    if rank == 0:
+        torch.save({k: v.cpu() for k, v in res.items()}, out)
+    dist.destroy_process_group()
+
+
+def test_margin_tp_two_ranks_gloo(relay, tmp_path):
+    """margin_rows_tp over a 2-rank group (both ranks on cuda:0, gloo): the
+    all-gather + combine path equals the full-row kernel."""
+    import socket
+    import torch.multiprocessing as mp
+    sck = socket.socket(); sck.bind(("127.0.0.1", 0)); port = sck.getsockname()[1]; sck.close()
+    out = str(tmp_path / "tp.pt")
+    mp.spawn(_tp_worker, args=(2, port, out), nprocs=2, join=True)
+    got = torch.load(out)
+    L = synth.make_logits(96, 20000, "bf16", seed=5, device=DEV)
+    full = relay.margin_rows(L)
+    torch.cuda.synchronize()
+    assert torch.equal(got["top1"], full["top1"].cpu()) and torch.equal(got["top2"], full["top2"].cpu())
+    assert (got["margin"] - full["margin"].cpu()).abs().max().item() < 2e-6

@@ -209,9 +209,10 @@ def margin_rows_tp(logits_shard, col_offset: int, group=None, inv_temperature: f
     import torch.distributed as dist
     part = margin_partials(logits_shard, col_offset, inv_temperature)
     world = dist.get_world_size(group)
-    gathered = torch.empty((world,) + tuple(part.shape), dtype=part.dtype, device=part.device)
-    dist.all_gather_into_tensor(gathered, part, group=group)
-    return margin_combine(gathered, inv_temperature)
+    gathered = torch.empty((world * part.shape[0], part.shape[1]), dtype=part.dtype,
+                           device=part.device)
+    dist.all_gather_into_tensor(gathered, part, group=group)   # ranks concatenated on dim 0
+    return margin_combine(gathered.view(world, part.shape[0], part.shape[1]), inv_temperature)
 
 
 # --------------------------------------------------------------- cue set

@@ -235,10 +235,11 @@ size_t relay_stats_words(int32_t n_cues, int32_t world_size);
  *   integer moments; se = std / sqrt(n); token_mean = sum_wq/(sum_len 2^20);
  *   min = min over the world_size slots; low_frac = sum_low / sum_len.
  *   rule 0: mean_c >= mu + SE_global (R15, default); 1: mean_c >= mu + se_c;
- *   2: mean_c > mu (App. B).  Always also n_c >= min_count.  With
+ *   2: mean_c > mu (App. B); 3: every candidate (the "all candidates"
+ *   ablation, tab:cue_selection_ablation P:427-445).  Always n_c >= min_count.  With
  *   fewer than 2 global positions std/se are NaN and nothing is selected.
  *   out [host] relay_cue_summary_t[n_cues+1]; out[n_cues] is the global row.
- * Errors: RELAY_ERR_INVALID for NULLs, n_cues/world_size out of range, rule>2. */
+ * Errors: RELAY_ERR_INVALID for NULLs, n_cues/world_size out of range, rule>3. */
 typedef struct {
   int64_t n;
   double mean, std, se, token_mean, min, low_frac;
@@ -248,6 +249,25 @@ typedef struct {
 } relay_cue_summary_t;
 relay_status_t relay_stats_finalize(const uint64_t* host_stats, int32_t n_cues, int32_t world_size,
                                     int64_t min_count, int32_t rule, relay_cue_summary_t* out);
+
+/* ------------------------------------------------------------------ N3 --
+ * relay_offload_estimate — the runtime switching (§4.3) replayed
+ * offline on a trace with a selected cue set, giving the large-model
+ * utilization of tab:speedup per trajectory (R17):
+ * reasoning = [a, te) with te = think_end_pos[k] (b when NULL), the answer
+ * [te, b) is the small model's; in each sentence (same window end) the first
+ * occurrence, in list order, of a selected cue completing at c < te hands
+ * positions c+1 .. min(e, te-1) to the small model.
+ *   occ_pos/occ_pat/n_occ: relay_cue_scan outputs; seg_end: relay_segment_reduce's.
+ *   cue_selected  uint8[n_cues] (device), e.g. from relay_stats_finalize.
+ *   out  int64[n_traj][3] = {large, small_reasoning, answer} token counts.
+ * Errors: RELAY_ERR_INVALID for NULLs / ranges as relay_segment_reduce. */
+relay_status_t relay_offload_estimate(relay_cueset_t cs, int64_t n_tok, const int64_t* traj_offsets,
+                                      int32_t n_traj, const int64_t* think_end_pos,
+                                      const int32_t* occ_pos, const int32_t* occ_pat,
+                                      const int64_t* n_occ, int64_t occ_capacity,
+                                      const int32_t* seg_end, const uint8_t* cue_selected,
+                                      int64_t* out, relay_stream_t stream);
 
 /* ------------------------------------------------------------------ H8 --
  * relay_step_switch — one decode step for `batch` live sequences: the H1

@@ -61,6 +61,8 @@ def _load():
         lib.oracle_cue_stats.argtypes = [P, C.c_int64, P, C.c_int32, P, P, P, C.c_int64, P,
                                          C.c_int32, C.c_float, P, P, P, P, P, P, C.c_int64,
                                          C.c_int32, P]
+        lib.oracle_offload.restype = None
+        lib.oracle_offload.argtypes = [C.c_int64, P, C.c_int32, P, P, P, C.c_int64, P, P, P, P, P]
         lib.oracle_step_one.restype = C.c_int
         lib.oracle_step_one.argtypes = [C.c_int32, C.c_float, P, P, P, P, P, C.c_int32, P, P,
                                         C.c_int64, C.c_int32, C.c_float, C.c_int32, P]
@@ -203,3 +205,22 @@ def step_one(tok, margin, state, hist, small_run, pat_tokens, pat_offsets, pat_c
                                    term_tab.shape[0], think_end_token, margin_gate,
                                    max_small_segment, C.byref(cue))
     return flag, cue.value, int(st[0]), h, int(sr[0])
+
+
+# ------------------------------------------------------------------ N3
+def offload(n_tok, traj_offsets, think_end_pos, occ_pos, occ_pat, seg_end, pat_offsets, pat_cue,
+            cue_selected):
+    """Per trajectory [large, small_reasoning, answer] token counts (R17)."""
+    offs = None if traj_offsets is None else np.ascontiguousarray(traj_offsets, np.int64)
+    n_traj = 1 if offs is None else offs.shape[0] - 1
+    tep = None if think_end_pos is None else np.ascontiguousarray(think_end_pos, np.int64)
+    occ_pos = np.ascontiguousarray(occ_pos, np.int32)
+    occ_pat = np.ascontiguousarray(occ_pat, np.int32)
+    seg_end = np.ascontiguousarray(seg_end, np.int32)
+    po = np.ascontiguousarray(pat_offsets, np.int32)
+    pc = np.ascontiguousarray(pat_cue, np.int32)
+    sel = np.ascontiguousarray(cue_selected, np.uint8)
+    out = np.zeros((n_traj, 3), np.int64)
+    _load().oracle_offload(n_tok, _p(offs), n_traj, _p(tep), _p(occ_pos), _p(occ_pat),
+                           occ_pos.shape[0], _p(seg_end), _p(po), _p(pc), _p(sel), _p(out))
+    return out

@@ -10,7 +10,7 @@
  * written out in fp64 with plain loops.  No blocking, fusion or reordering.
  * Citations: "P:n" = /root/reference/PAPER.md line n (LaTeX source), "S:n" =
  * SPEC.md line n.  Readings of silent/ambiguous passages are listed in
- * DESIGN.md ("Readings of the paper", R1..R16) and referenced here as [Rk].
+ * DESIGN.md ("Readings of the paper", R1..R17) and referenced here as [Rk].
  *
  * Parity pins (tests/test_oracle_pins.py) fix each function to something other
  * than itself: worked examples (S:58-60, S:76-78, S:223-225, S:232-234,
@@ -287,6 +287,7 @@ typedef struct {
  * trigger test looks at every occurrence.  Selection ([R15]):
  * rule 0 = mean_c >= mu + SE_global ("by at least one standard error");
  * rule 1 = mean_c >= mu + se_c; rule 2 = mean_c > mu (App. B);
+ * rule 3 = every candidate (the "all candidates" ablation);
  * always also n_c >= min_count.  With fewer than two global positions
  * std and se are NaN and nothing is selected. */
 void oracle_cue_stats(const float* margin, int64_t n_tok, const int64_t* traj_offsets,
@@ -385,7 +386,8 @@ void oracle_cue_stats(const float* margin, int64_t n_tok, const int64_t* traj_of
         if (n >= 1 && n >= min_count && gn >= 2) {
             if (rule == 0) sel = mean >= g->mean + g->se;
             else if (rule == 1) sel = mean >= g->mean + o->se;
-            else sel = mean > g->mean;
+            else if (rule == 2) sel = mean > g->mean;
+            else sel = 1;  /* rule 3: every candidate (tab:cue_selection_ablation) */
         }
         o->selected = sel;
     }
@@ -459,4 +461,54 @@ int oracle_step_one(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[
     }
     *small_run += 1;
     return 0;
+}
+
+/* ------------------------------------------- offload estimate (N3) --------
+ * Large-model utilization of the runtime switching (§4.3; the
+ * quantity of tab:speedup's "utilization") estimated
+ * offline from a trace and a selected cue set [R17]:
+ *   reasoning = positions [a, te), te = think_end_pos[k] (b when NULL);
+ *   positions [te, b) are the answer stage (small model);
+ *   in each sentence (same trajectory, same window end e) the FIRST
+ *   occurrence (in list order: by start, then cue id) of a selected cue that
+ *   completes inside the
+ *   reasoning stage (c = s + len - 1 < te) hands the rest of the sentence to
+ *   the small model: positions c+1 .. min(e, te-1);
+ *   every other reasoning position is generated by the large model.
+ * out[k] = {large, small_reasoning, answer} token counts of trajectory k. */
+void oracle_offload(int64_t n_tok, const int64_t* traj_offsets, int32_t n_traj,
+                    const int64_t* think_end_pos, const int32_t* occ_pos, const int32_t* occ_pat,
+                    int64_t n_occ, const int32_t* seg_end, const int32_t* pat_offsets,
+                    const int32_t* pat_cue, const uint8_t* cue_selected, int64_t* out) {
+    int32_t nt = traj_offsets ? n_traj : 1;
+    for (int32_t k = 0; k < nt; k++) {
+        int64_t a = traj_offsets ? traj_offsets[k] : 0;
+        int64_t b = traj_offsets ? traj_offsets[k + 1] : n_tok;
+        int64_t te = think_end_pos ? think_end_pos[k] : b;
+        if (te > b) te = b;
+        if (te < a) te = a;
+        int64_t small = 0;
+        for (int64_t i = 0; i < n_occ; i++) {
+            int64_t s = occ_pos[i];
+            if (s < a || s >= b) continue;
+            int32_t p = occ_pat[i];
+            if (!cue_selected[pat_cue[p]]) continue;
+            int64_t c = s + (pat_offsets[p + 1] - pat_offsets[p]) - 1;
+            if (c >= te) continue;
+            /* first selected occurrence of its sentence (list order: by start,
+             * then by cue id in ALL mode)? */
+            int first = 1;
+            for (int64_t j = 0; j < i; j++) {
+                if (occ_pos[j] < a) continue;
+                if (seg_end[j] != seg_end[i]) continue;
+                if (cue_selected[pat_cue[occ_pat[j]]]) { first = 0; break; }
+            }
+            if (!first) continue;
+            int64_t last = seg_end[i] < te - 1 ? seg_end[i] : te - 1;
+            if (last > c) small += last - c;
+        }
+        out[3 * k + 0] = (te - a) - small;
+        out[3 * k + 1] = small;
+        out[3 * k + 2] = b - te;
+    }
 }

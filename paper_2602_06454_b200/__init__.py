@@ -77,6 +77,7 @@ def _load():
         "relay_segment_reduce": (C.c_int, [P, P, i64, P, i32, P, P, P, P, P, i64, f32, P, P, P, P,
                                            P, i32, i32, P, sz, P]),
         "relay_stats_init": (C.c_int, [P, i32, i32, i32, P]),
+        "relay_offload_estimate": (C.c_int, [P, i64, P, i32, P, P, P, P, i64, P, P, P, P]),
         "relay_stats_words": (sz, [i32, i32]),
         "relay_stats_finalize": (C.c_int, [P, i32, i32, i64, i32, P]),
         "relay_step_switch": (C.c_int, [P, P, C.c_int, i32, i64, i64, f32, P, P, P, P, f32, i32,
@@ -95,7 +96,7 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_cueset_create", "relay_cueset_destroy", "relay_cueset_n_cues",
            "relay_workspace_bytes", "relay_workspace_init", "relay_cue_scan",
            "relay_segment_reduce", "relay_stats_init", "relay_stats_words",
-           "relay_stats_finalize", "relay_step_switch")
+           "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate")
 
 
 def _check(rc: int, what: str):
@@ -342,6 +343,22 @@ def segment_reduce(cs: CueSet, margin, scan: dict, traj_offsets=None, think_end_
                                    _ptr(ws), ws.numel(), _stream(stream))
     _check(rc, "relay_segment_reduce")
     out["stats"] = stats
+    return out
+
+
+def offload_estimate(cs: CueSet, scan: dict, seg: dict, cue_selected, n_tok: int,
+                     traj_offsets=None, think_end_pos=None, stream=None):
+    """N3: per-trajectory [large, small_reasoning, answer] token counts of the
+    runtime switching replayed with ``cue_selected`` (uint8 CUDA tensor [n_cues])."""
+    import torch
+    _need_cuda(cue_selected, traj_offsets, think_end_pos)
+    n_traj = 1 if traj_offsets is None else traj_offsets.shape[0] - 1
+    out = torch.empty((n_traj, 3), dtype=torch.int64, device=cue_selected.device)
+    rc = _lib.relay_offload_estimate(cs.handle, n_tok, _ptr(traj_offsets), n_traj,
+                                     _ptr(think_end_pos), _ptr(scan["occ_pos"]), _ptr(scan["occ_pat"]),
+                                     _ptr(scan["n_occ"]), scan["capacity"], _ptr(seg["seg_end"]),
+                                     _ptr(cue_selected), _ptr(out), _stream(stream))
+    _check(rc, "relay_offload_estimate")
     return out
 
 

@@ -215,13 +215,15 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
     if (terminator[v]) h_term[v >> 5] |= 1u << (v & 31);
   size_t off_tok = 0, off_len = align256(h_tok.size() * 4), off_cue = off_len + align256(n_patterns * 4),
          off_orig = off_cue + align256(n_patterns * 4), off_co = off_orig + align256(n_patterns * 4),
-         off_term = off_co + align256(n_patterns * 4), total = off_term + align256(words * 4);
+         off_lo = off_co + align256(n_patterns * 4), off_term = off_lo + align256(n_patterns * 4),
+         total = off_term + align256(words * 4);
   std::vector<char> host(total, 0);
   std::memcpy(host.data() + off_tok, h_tok.data(), h_tok.size() * 4);
   std::memcpy(host.data() + off_len, h_len.data(), n_patterns * 4);
   std::memcpy(host.data() + off_cue, h_cue.data(), n_patterns * 4);
   std::memcpy(host.data() + off_orig, h_orig.data(), n_patterns * 4);
   std::memcpy(host.data() + off_co, h_cue_orig.data(), n_patterns * 4);
+  std::memcpy(host.data() + off_lo, len.data(), n_patterns * 4);
   std::memcpy(host.data() + off_term, h_term.data(), words * 4);
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, total);
@@ -248,6 +250,7 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
   cs->dev.pat_cue = reinterpret_cast<const int*>(b + off_cue);
   cs->dev.pat_orig = reinterpret_cast<const int*>(b + off_orig);
   cs->dev.cue_of_orig = reinterpret_cast<const int*>(b + off_co);
+  cs->dev.len_of_orig = reinterpret_cast<const int*>(b + off_lo);
   cs->dev.term_tab = reinterpret_cast<const uint32_t*>(b + off_term);
   *out = cs;
   return RELAY_OK;
@@ -340,12 +343,33 @@ relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int6
       "relay_segment_reduce launch");
 }
 
+relay_status_t relay_offload_estimate(relay_cueset_t cs, int64_t n_tok, const int64_t* traj_offsets,
+                                      int32_t n_traj, const int64_t* think_end_pos, const int32_t* occ_pos,
+                                      const int32_t* occ_pat, const int64_t* n_occ, int64_t occ_capacity,
+                                      const int32_t* seg_end, const uint8_t* cue_selected, int64_t* out,
+                                      relay_stream_t stream) {
+  if (!cs || !n_occ || !cue_selected || !out) return fail(RELAY_ERR_INVALID, "cs, n_occ, cue_selected and out are required");
+  if (n_tok < 0 || n_tok >= 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "n_tok must be in [0, 2^31)");
+  if (occ_capacity < 0) return fail(RELAY_ERR_INVALID, "occ_capacity < 0");
+  if (occ_capacity > 0 && (!occ_pos || !occ_pat || !seg_end)) return fail(RELAY_ERR_INVALID, "occurrence arrays are required");
+  if (think_end_pos && !traj_offsets) return fail(RELAY_ERR_INVALID, "think_end_pos needs traj_offsets");
+  relay_status_t s = check_offsets_args(traj_offsets, n_traj);
+  if (s != RELAY_OK) return s;
+  return cuda_status(launch_offload_estimate(cs->dev, n_tok, reinterpret_cast<const long long*>(traj_offsets),
+                                             traj_offsets ? n_traj : 1,
+                                             reinterpret_cast<const long long*>(think_end_pos), occ_pos, occ_pat,
+                                             reinterpret_cast<const long long*>(n_occ), occ_capacity, seg_end,
+                                             cue_selected, reinterpret_cast<long long*>(out),
+                                             reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_offload_estimate launch");
+}
+
 relay_status_t relay_stats_finalize(const uint64_t* host_stats, int32_t n_cues, int32_t world_size,
                                     int64_t min_count, int32_t rule, relay_cue_summary_t* out) {
   if (!host_stats || !out) return fail(RELAY_ERR_INVALID, "host_stats and out are required");
   if (n_cues < 1 || n_cues > kMaxCues) return fail(RELAY_ERR_INVALID, "n_cues out of range");
   if (world_size < 1) return fail(RELAY_ERR_INVALID, "world_size < 1");
-  if (rule < 0 || rule > 2) return fail(RELAY_ERR_INVALID, "rule must be 0, 1 or 2");
+  if (rule < 0 || rule > 3) return fail(RELAY_ERR_INVALID, "rule must be 0, 1, 2 or 3");
   const int nf = kStatFields + world_size;
   const double Q = 1048576.0;
   for (int r = 0; r <= n_cues; r++) {
@@ -391,7 +415,8 @@ relay_status_t relay_stats_finalize(const uint64_t* host_stats, int32_t n_cues, 
     if (o.n < 1 || o.n < min_count) continue;
     if (rule == 0) o.selected = o.mean >= g.mean + g.se;
     else if (rule == 1) o.selected = o.mean >= g.mean + o.se;
-    else o.selected = o.mean > g.mean;
+    else if (rule == 2) o.selected = o.mean > g.mean;
+    else o.selected = 1;  // rule 3: every candidate with n >= min_count
   }
   return RELAY_OK;
 }

@@ -27,6 +27,7 @@ struct CueDev {
   const int* pat_cue;      // [n_pat], sorted
   const int* pat_orig;     // [n_pat] sorted -> caller's pattern index
   const int* cue_of_orig;  // [n_pat] caller's pattern index -> cue
+  const int* len_of_orig;  // [n_pat] caller's pattern index -> length
   const uint32_t* term_tab;  // [ceil(vocab/32)] terminator bitmap
 };
 
@@ -86,6 +87,11 @@ cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long lo
                                   float* seg_mean, float* seg_min, float* seg_lowfrac,
                                   unsigned long long* stats, int rank, int world, const ScanWs& ws,
                                   cudaStream_t st);
+
+cudaError_t launch_offload_estimate(const CueDev& cs, long long n_tok, const long long* offs, int n_traj,
+                                    const long long* think_end, const int* occ_pos, const int* occ_pat,
+                                    const long long* n_occ, long long cap, const int* seg_end,
+                                    const uint8_t* cue_selected, long long* out, cudaStream_t st);
 
 cudaError_t launch_stats_init(unsigned long long* stats, int n_cues, int rank, int world,
                               cudaStream_t st);

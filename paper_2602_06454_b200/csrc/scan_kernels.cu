@@ -532,6 +532,70 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+// ------------------------------------------------- N3 offload estimate
+// Per trajectory {large, small_reasoning, answer} token counts of the runtime
+// switching replayed offline with a selected cue set (R17).
+__global__ void offload_init_kernel(long long n_tok, const long long* __restrict__ offs, int n_traj,
+                                    const long long* __restrict__ think_end, long long* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_traj) return;
+  const long long a = offs ? offs[k] : 0, b = offs ? offs[k + 1] : n_tok;
+  long long te = think_end ? think_end[k] : b;
+  te = te > b ? b : (te < a ? a : te);
+  out[3 * k + 0] = te - a;
+  out[3 * k + 1] = 0;
+  out[3 * k + 2] = b - te;
+}
+
+__global__ void __launch_bounds__(256)
+    offload_occ_kernel(CueDev cs, long long n_tok, const long long* __restrict__ offs, int n_traj,
+                       const long long* __restrict__ think_end, const int* __restrict__ occ_pos,
+                       const int* __restrict__ occ_pat, const long long* __restrict__ n_occ_p, long long cap,
+                       const int* __restrict__ seg_end, const uint8_t* __restrict__ selected,
+                       long long* __restrict__ out) {
+  const long long nocc = *n_occ_p < cap ? *n_occ_p : cap;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nocc;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int p = occ_pat[i];
+    if (!selected[cs.cue_of_orig[p]]) continue;
+    const long long s = occ_pos[i];
+    const int k = find_traj(offs, n_traj, n_tok, s);
+    if (k < 0) continue;
+    const long long a = offs ? offs[k] : 0, b = offs ? offs[k + 1] : n_tok;
+    long long te = think_end ? think_end[k] : b;
+    te = te > b ? b : (te < a ? a : te);
+    const long long c = s + cs.len_of_orig[p] - 1;
+    if (c >= te) continue;
+    // first selected occurrence of its sentence, in list order
+    const int e = seg_end[i];
+    bool first = true;
+    for (long long j = i - 1; j >= 0 && occ_pos[j] >= a && seg_end[j] == e; j--)
+      if (selected[cs.cue_of_orig[occ_pat[j]]]) { first = false; break; }
+    if (!first) continue;
+    const long long last = e < te - 1 ? e : te - 1;
+    if (last > c) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(out + 3 * k + 1),
+                static_cast<unsigned long long>(last - c));
+      atomicAdd(reinterpret_cast<unsigned long long*>(out + 3 * k + 0),
+                static_cast<unsigned long long>(-(last - c)));
+    }
+  }
+}
+
+cudaError_t launch_offload_estimate(const CueDev& cs, long long n_tok, const long long* offs, int n_traj,
+                                    const long long* think_end, const int* occ_pos, const int* occ_pat,
+                                    const long long* n_occ, long long cap, const int* seg_end,
+                                    const uint8_t* cue_selected, long long* out, cudaStream_t st) {
+  offload_init_kernel<<<(n_traj + 255) / 256, 256, 0, st>>>(n_tok, offs, n_traj, think_end, out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || cap <= 0) return e;
+  long long blocks = (cap + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  offload_occ_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(cs, n_tok, offs, n_traj, think_end, occ_pos,
+                                                                     occ_pat, n_occ, cap, seg_end, cue_selected, out);
+  return cudaGetLastError();
+}
+
 __global__ void stats_init_kernel(unsigned long long* stats, int rows, int nf, int rank) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < rows * nf) {

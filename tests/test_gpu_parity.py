@@ -686,3 +686,52 @@ def test_margin_tp_two_ranks_gloo(relay, tmp_path):
     torch.cuda.synchronize()
     assert torch.equal(got["top1"], full["top1"].cpu()) and torch.equal(got["top2"], full["top2"].cpu())
     assert (got["margin"] - full["margin"].cpu()).abs().max().item() < 2e-6
+
+
+# ------------------------------------------------------ N3 offload estimate
+def _offload_case(relay, h, ts, sel, mode=0, think=True):
+    cs = relay.CueSet.from_synth(h, mode=mode)
+    n = ts.tokens.shape[0]
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    tep = torch.as_tensor(ts.think_end_pos, device=DEV) if think else None
+    m = synth.make_margins(n, seed=1)
+    scan = relay.cue_scan(cs, tok, offs)
+    seg = relay.segment_reduce(cs, torch.as_tensor(m, device=DEV), scan, offs, tep)
+    got = relay.offload_estimate(cs, scan, seg, torch.as_tensor(sel, device=DEV), n, offs, tep)
+    torch.cuda.synchronize()
+    o_scan, o_win, _ = oracle.analyze(m, ts.tokens, ts.traj_offsets, h.pat_tokens, h.pat_offsets,
+                                      h.pat_cue, h.n_cues, h.terminator, mode=mode, min_count=1)
+    ref = oracle.offload(n, ts.traj_offsets, ts.think_end_pos if think else None, o_scan["occ_pos"],
+                         o_scan["occ_pat"], o_win["seg_end"], h.pat_offsets, h.pat_cue, sel)
+    np.testing.assert_array_equal(got.cpu().numpy(), ref)
+    return ref
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("think", [True, False])
+def test_offload_estimate(relay, mode, think):
+    h = synth.make_cueset(8192, 6, 10, max_len=3, seed=111)
+    ts = synth.make_tokens(9, 3000, h, seed=112, cue_rate=0.5)
+    rng = np.random.default_rng(113)
+    for _ in range(3):
+        sel = (rng.random(6) < 0.5).astype(np.uint8)
+        ref = _offload_case(relay, h, ts, sel, mode, think)
+        assert (ref.sum(axis=1) == 3000).all()
+
+
+def test_offload_estimate_golden(relay, golden_dir):
+    import json
+    import os
+    g = json.load(open(os.path.join(golden_dir, "trace_fixture.json")))
+    pats = g["patterns"]
+    po = np.zeros(len(pats) + 1, np.int32)
+    po[1:] = np.cumsum([len(p) for p in pats])
+    term = np.zeros(g["vocab"], np.uint8)
+    term[g["terminator_ids"]] = 1
+    h = synth.CueSet(np.array([t for p in pats for t in p], np.int32), po, np.array(g["pat_cue"], np.int32),
+                     g["n_cues"], g["vocab"], term, -1, [tuple(p) for p in pats])
+    ts = synth.TokenStream(np.array(g["tokens"], np.int32), np.array(g["traj_offsets"], np.int64),
+                           np.array([7, 12], np.int64))
+    ref = _offload_case(relay, h, ts, np.array([1, 1], np.uint8))
+    assert ref.tolist() == [[3, 4, 3], [2, 0, 1]]          # hand-traced case C

@@ -526,3 +526,78 @@ def test_offline_online_trigger_agreement():
             if f == 1:
                 fired.append(t)
         assert fired == expected
+
+
+# ------------------------------------------------------- N3 offload estimate
+def test_offload_golden(golden_dir):
+    """Hand-traced on tests/golden/trace_fixture.json (R17): cases A-C."""
+    g = json.load(open(os.path.join(golden_dir, "trace_fixture.json")))
+    pt, po, pc, term = _cs_from_fixture(g)
+    m = np.array(g["margins"], np.float32)
+    scan, win, _ = oracle.analyze(m, g["tokens"], g["traj_offsets"], pt, po, pc, g["n_cues"], term,
+                                  tau=g["tau"], min_count=1)
+    args = (13, g["traj_offsets"])
+    occ = (scan["occ_pos"], scan["occ_pat"], win["seg_end"], po, pc)
+    # A: cue 0 selected, no answer stage.  traj0: sentence [0,4] first selected
+    # occurrence s=1 ([5,6] completes at 2) -> small 3,4; sentence [5,9]: s=5
+    # completes at 6 -> small 7,8,9.  traj1: cue 1 only -> none.
+    a = oracle.offload(*args, None, *occ, np.array([1, 0], np.uint8))
+    assert a.tolist() == [[5, 5, 0], [3, 0, 0]]
+    # B: cue 1 selected.  traj0: s=0 completes at 0 -> small 1..4; traj1: s=11 -> small 12.
+    b = oracle.offload(*args, None, *occ, np.array([0, 1], np.uint8))
+    assert b.tolist() == [[6, 4, 0], [2, 1, 0]]
+    # C: both selected, think_end = [7, 12].  traj0: s=0 -> small 1..4; s=5
+    # completes at 6, clamp to te-1=6 -> none; s=8,9 after te.  answer 7..9.
+    # traj1: s=11 completes at 11 = te-1 -> none; answer 12.
+    c = oracle.offload(*args, np.array([7, 12]), *occ, np.array([1, 1], np.uint8))
+    assert c.tolist() == [[3, 4, 3], [2, 0, 1]]
+    # nothing selected: all reasoning on the large model
+    d = oracle.offload(*args, np.array([7, 12]), *occ, np.array([0, 0], np.uint8))
+    assert d.tolist() == [[7, 0, 3], [2, 0, 1]]
+
+
+def test_offload_matches_step_replay():
+    """The estimate equals replaying the trace through the runtime state machine
+    (step_one) with the selected patterns, for substring-free pattern sets
+    without terminators (R13/R17): small-model tokens are those generated
+    while the state is 'small' during reasoning."""
+    rng = np.random.default_rng(12)
+    pats = [(20,), (21, 22), (23, 24, 25)]
+    pt = np.array([t for p in pats for t in p], np.int32)
+    po = np.array([0, 1, 3, 6], np.int32)
+    pc = np.array([0, 1, 2], np.int32)
+    for trial in range(100):
+        toks = []
+        while len(toks) < 150:
+            if rng.random() < 0.4:
+                toks.extend(pats[int(rng.integers(0, 3))])
+            toks.extend(rng.integers(20, 27, int(rng.integers(0, 4))).tolist())
+            toks.append(int(rng.choice([30, 50, 50])))
+        toks = np.array(toks[:150], np.int32)
+        te = int(rng.integers(100, 150))
+        sel = (rng.random(3) < 0.6).astype(np.uint8)
+        scan = oracle.cue_scan(toks, None, pt, po, pc, 3, _TERM)
+        w = oracle.windows(np.ones(150, np.float32), scan["term"], None, scan["occ_pos"], 0.5)
+        est = oracle.offload(150, None, np.array([te]), scan["occ_pos"], scan["occ_pat"], w["seg_end"],
+                             po, pc, sel)
+        keep = [p for p in range(3) if sel[pc[p]]]
+        spt = np.array([t for p in keep for t in pats[p]] or [99], np.int32)
+        spo = np.zeros(len(keep) + 1, np.int32)
+        spo[1:] = np.cumsum([len(pats[p]) for p in keep]) if keep else [1]
+        spc = np.array([pc[p] for p in keep] or [0], np.int32)
+        state, hist, sr, small = 0, [-1] * 7, 0, 0
+        for t in range(te):
+            if state & 1:
+                small += 1
+            f, c, state, hist, sr = oracle.step_one(int(toks[t]), 1.0, state, hist, sr, spt, spo, spc,
+                                                    _TERM, 40, -1.0, 0)
+            hist = hist.tolist()
+        assert est[0].tolist() == [te - small, small, 150 - te], (trial, est, small)
+
+
+def test_selection_rule_all_candidates():
+    m = [0.9] * 20 + [0.1, 0.1]
+    _, s = _one_traj_stats(m, [20], rule=3, min_count=1)
+    assert s[0]["selected"] == 1          # below the mean, still a candidate
+    _, s = _one_traj_stats(m, [20], rule=3, min_count=2)
+    assert s[0]["selected"] == 0          # min_count still applies

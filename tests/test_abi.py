@@ -146,3 +146,16 @@ def test_finalize_rules_and_small_n(relay):
     tab[1, 0] = 1
     f = relay.stats_finalize(tab.reshape(-1).view(np.int64), 1, 1, 1, rule=2)
     assert np.isnan(f[1]["se"]) and f[0]["selected"] == 0
+
+
+def test_plain_c_consumer(relay, tmp_path):
+    """include/relay.h is a self-contained C header: a plain C program links
+    librelay.so and runs host-side calls without torch or CUDA headers."""
+    import subprocess
+    exe = str(tmp_path / "abi_host")
+    lib_dir = os.path.dirname(relay.LIB_PATH)
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "c", "abi_host.c"), "-o", exe,
+                           "-L", lib_dir, "-Wl,-rpath," + lib_dir, "-l:librelay.so", "-lm"])
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0 and "c abi ok" in r.stdout, (r.returncode, r.stdout, r.stderr)

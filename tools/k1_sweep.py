@@ -14,7 +14,8 @@ OUT = os.path.join(ROOT, "build", "k1_sweep")
 SRC = [os.path.join(ROOT, "paper_2602_06454_b200", "csrc", f)
        for f in ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu")]
 VARIANTS = [  # (ncw, stages, uv, minb, extra): stage bytes = uv * ncw * 32 * 16
-    (8, 4, 4, 3, ""), (8, 4, 4, 3, "NULL"), (8, 5, 4, 2, ""), (4, 4, 4, 6, ""),
+    (8, 4, 4, 3, ""), (8, 6, 2, 4, ""), (8, 4, 2, 4, ""), (12, 4, 2, 3, ""),
+    (6, 6, 2, 5, ""), (16, 3, 2, 2, ""),
 ]
 
 

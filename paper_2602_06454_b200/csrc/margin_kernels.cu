@@ -482,7 +482,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
   constexpr int NCT = NCW * 32;             // consumer threads
   constexpr int SB = UV * NCT * 16;         // bytes per ring stage
-  constexpr int NRED = NCW * 8;             // partials per item after 2 shuffle rounds
+  // partials handed to the epilogue per consumer warp: 8 after two shuffle
+  // rounds (K1: the epilogue is off the critical path), 1 after a full warp
+  // reduction (K4: the epilogue is the tail of a ~30 us kernel)
+  constexpr int RPW = (MODE == kModeStep) ? 1 : 8;
+  constexpr int NRED = NCW * RPW;
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
@@ -567,7 +571,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       Partial q = partial_empty();
 #pragma unroll
       for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
-      q = warp_reduce_partial(q);
+#pragma unroll
+      for (int off = (NRED >= 32 ? 16 : NRED / 2); off > 0; off >>= 1)
+        q = partial_merge(q, shfl_xor_partial(q, off));
       if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
       mbar_arrive(rempty_s + 8 * slot);
       if (item.nparts == 1) {
@@ -670,9 +676,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     if (tid < j1 - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
     // hand the warp's 8 partials (after two shuffle rounds) to the epilogue warp
     Partial p = thread_partial(st);
-    p = partial_merge(p, shfl_xor_partial(p, 16));
-    p = partial_merge(p, shfl_xor_partial(p, 8));
-    if (lane < 8) s_red[slot][warp * 8 + lane] = p;
+#pragma unroll
+    for (int off = 16; off >= RPW; off >>= 1) p = partial_merge(p, shfl_xor_partial(p, off));
+    if (lane < RPW) s_red[slot][warp * RPW + lane] = p;
     mbar_arrive(rfull_s + 8 * slot);
     if (tid == 0 && it < 8) TRACE(2 + it);
   }

@@ -207,8 +207,16 @@ relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t 
  *               traj_offsets); the first min(*n_occ, occ_capacity) are used.
  *   seg_end int32, seg_mean/seg_min/seg_lowfrac float [occ_capacity] out.
  *   stats must have been set by relay_stats_init for (n_cues, rank, world_size).
+ *   flags: 0, or RELAY_SEG_PER_TRAJECTORY: `stats` is then n_traj tables, one
+ *          per trajectory ([n_traj][(n_cues+1)*(8+world_size)], set by
+ *          relay_stats_init_tables), and each occurrence / position adds to
+ *          its own trajectory's table.  The tables sum (min for the min slots,
+ *          relay_stats_merge) to the single table, so calibration can be
+ *          re-run on any subset of trajectories without another pass (the
+ *          calibration-size study, Table 5).
  * Errors: RELAY_ERR_INVALID (NULLs, n_tok range, rank outside [0,world_size),
- * world_size < 1, !(tau finite)); RELAY_ERR_WORKSPACE. */
+ * world_size < 1, !(tau finite), unknown flags); RELAY_ERR_WORKSPACE. */
+#define RELAY_SEG_PER_TRAJECTORY 1u
 relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int64_t n_tok,
                                     const int64_t* traj_offsets, int32_t n_traj,
                                     const int64_t* think_end_pos, const uint32_t* term_bits,
@@ -216,7 +224,7 @@ relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int6
                                     const int64_t* n_occ, int64_t occ_capacity, float tau,
                                     int32_t* seg_end, float* seg_mean, float* seg_min,
                                     float* seg_lowfrac, uint64_t* stats, int32_t rank,
-                                    int32_t world_size, void* ws, size_t ws_bytes,
+                                    int32_t world_size, uint32_t flags, void* ws, size_t ws_bytes,
                                     relay_stream_t stream);
 
 /* Zero the table, then set this rank's min slots to +inf bits (0x7f800000)
@@ -224,7 +232,19 @@ relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int6
  * r's minimum (H6: one sum-only collective). */
 relay_status_t relay_stats_init(uint64_t* stats, int32_t n_cues, int32_t rank, int32_t world_size,
                                 relay_stream_t stream);
+/* The same for n_tables consecutive tables (RELAY_SEG_PER_TRAJECTORY). */
+relay_status_t relay_stats_init_tables(uint64_t* stats, int32_t n_tables, int32_t n_cues, int32_t rank,
+                                       int32_t world_size, relay_stream_t stream);
+/* Words in one table: (n_cues+1) * (8+world_size); 0 for bad arguments. */
 size_t relay_stats_words(int32_t n_cues, int32_t world_size);
+/* [host] Merge tables (host memory, n_tables consecutive tables) into one:
+ * fields 0-7 add, the min slots take the minimum (as float bit patterns of
+ * values in [0,1] / +inf, which order like the integers).  mask (uint8
+ * [n_tables], nullable = all) picks the tables.  Merging before or after the
+ * SUM all-reduce gives the same table.  out may not alias tables.
+ * Errors: RELAY_ERR_INVALID (NULLs, n_tables < 0, n_cues/world_size range). */
+relay_status_t relay_stats_merge(const uint64_t* tables, int32_t n_tables, const uint8_t* mask,
+                                 int32_t n_cues, int32_t world_size, uint64_t* out);
 
 /* ------------------------------------------------------------------ H7 --
  * relay_stats_finalize [host] — per-cue and global summaries and the switch-

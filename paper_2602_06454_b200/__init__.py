@@ -75,8 +75,10 @@ def _load():
         "relay_workspace_init": (C.c_int, [P, sz, P]),
         "relay_cue_scan": (C.c_int, [P, P, i64, P, i32, P, P, P, i64, P, P, sz, P]),
         "relay_segment_reduce": (C.c_int, [P, P, i64, P, i32, P, P, P, P, P, i64, f32, P, P, P, P,
-                                           P, i32, i32, P, sz, P]),
+                                           P, i32, i32, u32, P, sz, P]),
         "relay_stats_init": (C.c_int, [P, i32, i32, i32, P]),
+        "relay_stats_init_tables": (C.c_int, [P, i32, i32, i32, i32, P]),
+        "relay_stats_merge": (C.c_int, [P, i32, P, i32, i32, P]),
         "relay_offload_estimate": (C.c_int, [P, i64, P, i32, P, P, P, P, i64, P, P, P, P]),
         "relay_stats_words": (sz, [i32, i32]),
         "relay_stats_finalize": (C.c_int, [P, i32, i32, i64, i32, P]),
@@ -95,7 +97,8 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_margin_partials", "relay_margin_combine",
            "relay_cueset_create", "relay_cueset_destroy", "relay_cueset_n_cues",
            "relay_workspace_bytes", "relay_workspace_init", "relay_cue_scan",
-           "relay_segment_reduce", "relay_stats_init", "relay_stats_words",
+           "relay_segment_reduce", "relay_stats_init", "relay_stats_init_tables",
+           "relay_stats_words", "relay_stats_merge",
            "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate")
 
 
@@ -302,22 +305,48 @@ def stats_words(n_cues: int, world_size: int = 1) -> int:
     return int(_lib.relay_stats_words(n_cues, world_size))
 
 
-def stats_init(stats, n_cues: int, rank: int = 0, world_size: int = 1, stream=None):
-    _check(_lib.relay_stats_init(_ptr(stats), n_cues, rank, world_size, _stream(stream)),
-           "relay_stats_init")
+def stats_init(stats, n_cues: int, rank: int = 0, world_size: int = 1, stream=None,
+               n_tables: int = 1):
+    _check(_lib.relay_stats_init_tables(_ptr(stats), n_tables, n_cues, rank, world_size,
+                                        _stream(stream)), "relay_stats_init_tables")
     return stats
 
 
-def new_stats(n_cues: int, rank: int = 0, world_size: int = 1, device="cuda", stream=None):
+def new_stats(n_cues: int, rank: int = 0, world_size: int = 1, device="cuda", stream=None,
+              n_tables: int = 1):
+    """One table, or ``n_tables`` consecutive ones (per-trajectory tables)."""
     import torch
-    st = torch.empty(stats_words(n_cues, world_size), dtype=torch.int64, device=device)
-    return stats_init(st, n_cues, rank, world_size, stream)
+    st = torch.empty(n_tables * stats_words(n_cues, world_size), dtype=torch.int64, device=device)
+    return stats_init(st, n_cues, rank, world_size, stream, n_tables)
+
+
+def stats_merge(host_tables: np.ndarray, n_cues: int, world_size: int = 1, mask=None):
+    """Host merge of per-trajectory tables (``mask``: which ones, default all)
+    into one table that ``stats_finalize`` takes."""
+    words = stats_words(n_cues, world_size)
+    ht = np.ascontiguousarray(host_tables).view(np.uint64).reshape(-1)
+    if ht.shape[0] % words:
+        raise RelayError("tables length is not a multiple of the table size")
+    n_tables = ht.shape[0] // words
+    m = None
+    if mask is not None:
+        m = np.ascontiguousarray(np.asarray(mask, dtype=bool).astype(np.uint8))
+        if m.shape != (n_tables,):
+            raise RelayError("mask must have one entry per table")
+    out = np.empty(words, dtype=np.uint64)
+    rc = _lib.relay_stats_merge(ht.ctypes.data_as(C.c_void_p), n_tables,
+                                None if m is None else m.ctypes.data_as(C.c_void_p), n_cues,
+                                world_size, out.ctypes.data_as(C.c_void_p))
+    _check(rc, "relay_stats_merge")
+    return out
 
 
 # ---------------------------------------------------------------- H3-H5
 def segment_reduce(cs: CueSet, margin, scan: dict, traj_offsets=None, think_end_pos=None,
                    tau: float = 0.5, stats=None, rank: int = 0, world_size: int = 1, ws=None,
-                   out=None, stream=None):
+                   out=None, stream=None, per_trajectory: bool = False):
+    """H3-H5.  ``per_trajectory``: one stats table per trajectory (merge with
+    ``stats_merge``)."""
     import torch
     _need_cuda(margin, traj_offsets, think_end_pos)
     n_tok = margin.shape[0]
@@ -325,22 +354,26 @@ def segment_reduce(cs: CueSet, margin, scan: dict, traj_offsets=None, think_end_
     dev = margin.device
     if ws is None:
         ws = workspace(n_tok, cap, 0, dev, stream)
+    n_traj = 1 if traj_offsets is None else traj_offsets.shape[0] - 1
     if stats is None:
-        stats = new_stats(cs.n_cues, rank, world_size, dev, stream)
+        stats = new_stats(cs.n_cues, rank, world_size, dev, stream,
+                          n_traj if per_trajectory else 1)
+    elif stats.numel() < (n_traj if per_trajectory else 1) * stats_words(cs.n_cues, world_size):
+        raise RelayError("stats too short for the table count")
     c1 = max(cap, 1)
     if out is None:
         out = dict(seg_end=torch.empty(c1, dtype=torch.int32, device=dev),
                    seg_mean=torch.empty(c1, dtype=torch.float32, device=dev),
                    seg_min=torch.empty(c1, dtype=torch.float32, device=dev),
                    seg_lowfrac=torch.empty(c1, dtype=torch.float32, device=dev))
-    n_traj = 1 if traj_offsets is None else traj_offsets.shape[0] - 1
     rc = _lib.relay_segment_reduce(cs.handle, _ptr(margin), n_tok, _ptr(traj_offsets), n_traj,
                                    _ptr(think_end_pos), _ptr(scan["term_bits"]),
                                    _ptr(scan["occ_pos"]), _ptr(scan["occ_pat"]),
                                    _ptr(scan["n_occ"]), cap, float(tau), _ptr(out["seg_end"]),
                                    _ptr(out["seg_mean"]), _ptr(out["seg_min"]),
                                    _ptr(out["seg_lowfrac"]), _ptr(stats), rank, world_size,
-                                   _ptr(ws), ws.numel(), _stream(stream))
+                                   1 if per_trajectory else 0, _ptr(ws), ws.numel(),
+                                   _stream(stream))
     _check(rc, "relay_segment_reduce")
     out["stats"] = stats
     return out
@@ -417,7 +450,9 @@ class Analyzer:
 
     def __init__(self, cs: CueSet, n_tok: int, vocab: int, device="cuda", occ_capacity=None,
                  tau: float = 0.5, rank: int = 0, world_size: int = 1, inv_temperature=1.0,
-                 overlap_scan: bool = True):
+                 overlap_scan: bool = True, per_trajectory_tables: int = 0):
+        """``per_trajectory_tables`` = n_traj keeps one stats table per
+        trajectory (``stats_merge`` any subset on the host); 0 = one table."""
         import torch
         self.cs, self.n_tok, self.vocab, self.tau = cs, n_tok, vocab, tau
         self.rank, self.world_size, self.iota = rank, world_size, inv_temperature
@@ -440,7 +475,10 @@ class Analyzer:
                         seg_mean=torch.empty(c1, dtype=torch.float32, device=d),
                         seg_min=torch.empty(c1, dtype=torch.float32, device=d),
                         seg_lowfrac=torch.empty(c1, dtype=torch.float32, device=d))
-        self.stats = torch.empty(stats_words(cs.n_cues, world_size), dtype=torch.int64, device=d)
+        self.n_tables = max(1, per_trajectory_tables)
+        self.per_traj = per_trajectory_tables > 0
+        self.stats = torch.empty(self.n_tables * stats_words(cs.n_cues, world_size),
+                                 dtype=torch.int64, device=d)
         self._side = None
 
     def run(self, logits, tokens, traj_offsets=None, think_end_pos=None, stream=None,
@@ -460,7 +498,7 @@ class Analyzer:
             self._side.wait_event(self._fork)
             cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
             self._join.record(self._side)
-        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s)
+        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s, self.n_tables)
         if k1_events:
             k1_events[0].record(s)
         margin_rows(logits, vocab=vocab or self.vocab, inv_temperature=self.iota, out=self.rows,
@@ -470,7 +508,8 @@ class Analyzer:
         if self.overlap_scan:
             s.wait_event(self._join)
         segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
-                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s)
+                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s,
+                       per_trajectory=self.per_traj)
         return self.stats
 
     def run_streamed(self, chunks, tokens, traj_offsets=None, think_end_pos=None, stream=None,
@@ -490,7 +529,7 @@ class Analyzer:
         self._side.wait_event(self._fork)
         cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
         self._join.record(self._side)
-        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s)
+        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s, self.n_tables)
         for r0, chunk in chunks:
             r1 = r0 + chunk.shape[0]
             out = {k: (v[r0:r1] if v is not None else None) for k, v in self.rows.items()}
@@ -498,7 +537,8 @@ class Analyzer:
                         stream=s)
         s.wait_event(self._join)
         segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
-                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s)
+                       self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s,
+                       per_trajectory=self.per_traj)
         return self.stats
 
     def capture(self, logits, tokens, traj_offsets=None, think_end_pos=None, host_stats=None,

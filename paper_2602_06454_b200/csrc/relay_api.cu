@@ -303,14 +303,40 @@ size_t relay_stats_words(int32_t n_cues, int32_t world_size) {
   return static_cast<size_t>(n_cues + 1) * (kStatFields + world_size);
 }
 
-relay_status_t relay_stats_init(uint64_t* stats, int32_t n_cues, int32_t rank, int32_t world_size,
-                                relay_stream_t stream) {
+relay_status_t relay_stats_init_tables(uint64_t* stats, int32_t n_tables, int32_t n_cues, int32_t rank,
+                                       int32_t world_size, relay_stream_t stream) {
   if (!stats) return fail(RELAY_ERR_INVALID, "stats is NULL");
+  if (n_tables < 1) return fail(RELAY_ERR_INVALID, "n_tables < 1");
   if (n_cues < 1 || n_cues > kMaxCues) return fail(RELAY_ERR_INVALID, "n_cues out of range");
   if (world_size < 1 || rank < 0 || rank >= world_size) return fail(RELAY_ERR_INVALID, "bad rank/world_size");
-  return cuda_status(launch_stats_init(reinterpret_cast<unsigned long long*>(stats), n_cues, rank, world_size,
-                                       reinterpret_cast<cudaStream_t>(stream)),
+  return cuda_status(launch_stats_init(reinterpret_cast<unsigned long long*>(stats), n_tables, n_cues, rank,
+                                       world_size, reinterpret_cast<cudaStream_t>(stream)),
                      "relay_stats_init launch");
+}
+
+relay_status_t relay_stats_init(uint64_t* stats, int32_t n_cues, int32_t rank, int32_t world_size,
+                                relay_stream_t stream) {
+  return relay_stats_init_tables(stats, 1, n_cues, rank, world_size, stream);
+}
+
+relay_status_t relay_stats_merge(const uint64_t* tables, int32_t n_tables, const uint8_t* mask,
+                                 int32_t n_cues, int32_t world_size, uint64_t* out) {
+  if (!out || (n_tables > 0 && !tables)) return fail(RELAY_ERR_INVALID, "tables and out are required");
+  if (n_tables < 0) return fail(RELAY_ERR_INVALID, "n_tables < 0");
+  if (n_cues < 1 || n_cues > kMaxCues) return fail(RELAY_ERR_INVALID, "n_cues out of range");
+  if (world_size < 1) return fail(RELAY_ERR_INVALID, "world_size < 1");
+  const int nf = kStatFields + world_size;
+  const size_t words = static_cast<size_t>(n_cues + 1) * nf;
+  for (size_t i = 0; i < words; i++) out[i] = (static_cast<int>(i % nf) < kStatFields) ? 0ull : 0x7f800000ull;
+  for (int32_t t = 0; t < n_tables; t++) {
+    if (mask && !mask[t]) continue;
+    const uint64_t* tab = tables + static_cast<size_t>(t) * words;
+    for (size_t i = 0; i < words; i++) {
+      if (static_cast<int>(i % nf) < kStatFields) out[i] += tab[i];
+      else if (tab[i] < out[i]) out[i] = tab[i];
+    }
+  }
+  return RELAY_OK;
 }
 
 relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int64_t n_tok,
@@ -318,9 +344,10 @@ relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int6
                                     const uint32_t* term_bits, const int32_t* occ_pos, const int32_t* occ_pat,
                                     const int64_t* n_occ, int64_t occ_capacity, float tau, int32_t* seg_end,
                                     float* seg_mean, float* seg_min, float* seg_lowfrac, uint64_t* stats,
-                                    int32_t rank, int32_t world_size, void* ws, size_t ws_bytes,
-                                    relay_stream_t stream) {
+                                    int32_t rank, int32_t world_size, uint32_t flags, void* ws,
+                                    size_t ws_bytes, relay_stream_t stream) {
   if (!cs || !stats || !n_occ) return fail(RELAY_ERR_INVALID, "cs, stats and n_occ are required");
+  if (flags & ~RELAY_SEG_PER_TRAJECTORY) return fail(RELAY_ERR_INVALID, "unknown flags 0x%x", flags);
   if (n_tok < 0 || n_tok >= 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "n_tok must be in [0, 2^31)");
   if (n_tok > 0 && (!margin || !term_bits)) return fail(RELAY_ERR_INVALID, "margin and term_bits are required");
   if (occ_capacity < 0) return fail(RELAY_ERR_INVALID, "occ_capacity < 0");
@@ -338,7 +365,8 @@ relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int6
                             traj_offsets ? n_traj : 1, reinterpret_cast<const long long*>(think_end_pos),
                             term_bits, occ_pos, occ_pat, reinterpret_cast<const long long*>(n_occ),
                             occ_capacity, tau, seg_end, seg_mean, seg_min, seg_lowfrac,
-                            reinterpret_cast<unsigned long long*>(stats), rank, world_size, w,
+                            reinterpret_cast<unsigned long long*>(stats), rank, world_size,
+                            (flags & RELAY_SEG_PER_TRAJECTORY) ? 1 : 0, w,
                             reinterpret_cast<cudaStream_t>(stream)),
       "relay_segment_reduce launch");
 }

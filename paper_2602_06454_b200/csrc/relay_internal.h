@@ -85,15 +85,15 @@ cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long lo
                                   const uint32_t* term_bits, const int* occ_pos, const int* occ_pat,
                                   const long long* n_occ, long long cap, float tau, int* seg_end,
                                   float* seg_mean, float* seg_min, float* seg_lowfrac,
-                                  unsigned long long* stats, int rank, int world, const ScanWs& ws,
-                                  cudaStream_t st);
+                                  unsigned long long* stats, int rank, int world, int per_traj,
+                                  const ScanWs& ws, cudaStream_t st);
 
 cudaError_t launch_offload_estimate(const CueDev& cs, long long n_tok, const long long* offs, int n_traj,
                                     const long long* think_end, const int* occ_pos, const int* occ_pat,
                                     const long long* n_occ, long long cap, const int* seg_end,
                                     const uint8_t* cue_selected, long long* out, cudaStream_t st);
 
-cudaError_t launch_stats_init(unsigned long long* stats, int n_cues, int rank, int world,
+cudaError_t launch_stats_init(unsigned long long* stats, int n_tables, int n_cues, int rank, int world,
                               cudaStream_t st);
 
 cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int batch, int vocab,

@@ -263,6 +263,7 @@ __device__ __forceinline__ unsigned long long q20(float m) {
 struct PosVal {
   Agg v;        // single-position aggregate
   int counted;  // counts in the global row
+  int traj;     // trajectory index (-1 outside every trajectory)
 };
 
 // Per-position values for this thread's 8 consecutive positions.
@@ -299,6 +300,7 @@ __device__ __forceinline__ void load_positions(const float* __restrict__ margin,
     }
     pv[i].v = a;
     pv[i].counted = counted;
+    pv[i].traj = (t < n_tok) ? k : -1;
   }
 }
 
@@ -350,7 +352,9 @@ __global__ void __launch_bounds__(kScanThreads)
                      const int* __restrict__ occ_pat, const long long* __restrict__ n_occ_p, long long cap,
                      int* __restrict__ seg_end, float* __restrict__ seg_mean, float* __restrict__ seg_min,
                      float* __restrict__ seg_lowfrac, unsigned long long* __restrict__ stats, int nf,
-                     int rank, int* tile_flag, Agg* tile_val, int* done) {
+                     int rank, int per_traj, int* tile_flag, Agg* tile_val, int* done) {
+  // per_traj: one table per trajectory ([n_traj][(n_cues+1)*nf]) instead of one
+  const long long table_words = static_cast<long long>(cs.n_cues + 1) * nf;
   __shared__ Agg s_w[kScanThreads / 32];
   __shared__ Agg s_carry;
   __shared__ unsigned long long s_red[kScanThreads / 32][5];
@@ -362,6 +366,32 @@ __global__ void __launch_bounds__(kScanThreads)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   PosVal pv[kItems];
   load_positions(margin, term_bits, n_tok, offs, n_traj, think_end, tau, p0, pv);
+  // per-trajectory tables: a tile inside one trajectory reduces as a block;
+  // a tile spanning trajectories adds each position on its own (rare)
+  int tile_traj = 0;
+  if (per_traj) {
+    const long long last = (base + kTile < n_tok ? base + kTile : n_tok) - 1;
+    const int k0 = find_traj(offs, n_traj, n_tok, base), k1 = find_traj(offs, n_traj, n_tok, last);
+    tile_traj = (k0 == k1) ? k0 : -2;
+  }
+  if (tile_traj == -2) {
+#pragma unroll
+    for (int i = 0; i < kItems; i++) {
+      if (!pv[i].counted) continue;
+      unsigned long long* g = stats + pv[i].traj * table_words + static_cast<size_t>(cs.n_cues) * nf;
+      pv[i].counted = 0;  // added here, not in the block reduce below
+      if (pv[i].v.nan) {
+        atomicAdd(g + 7, 1ull);
+        continue;
+      }
+      const unsigned long long q = pv[i].v.sumq;
+      atomicAdd(g + 0, 1ull); atomicAdd(g + 1, q); atomicAdd(g + 2, q * q); atomicAdd(g + 3, q);
+      atomicAdd(g + 4, 1ull);
+      if (pv[i].v.low) atomicAdd(g + 5, 1ull);
+      atomicMin(g + kStatFields + rank,
+                static_cast<unsigned long long>(__float_as_uint(fminf(fmaxf(pv[i].v.mn, 0.0f), 1.0f))));
+    }
+  }
 
   // ---- thread / warp / tile aggregates and global moments
   Agg h = pv[kItems - 1].v;
@@ -404,7 +434,8 @@ __global__ void __launch_bounds__(kScanThreads)
   __syncthreads();
 
   if (threadIdx.x == 0) {
-    unsigned long long* grow = stats + static_cast<size_t>(cs.n_cues) * nf;
+    unsigned long long* grow = stats + (tile_traj > 0 ? tile_traj * table_words : 0) +
+                               static_cast<size_t>(cs.n_cues) * nf;
     unsigned long long a[5] = {0, 0, 0, 0, 0};
     float mn = INFINITY;
     for (int w = 0; w < kScanThreads / 32; w++) {
@@ -500,7 +531,8 @@ __global__ void __launch_bounds__(kScanThreads)
       }
       if (think_end && k >= 0 && s >= think_end[k]) continue;
       const int cue = cs.cue_of_orig[occ_pat[o]];
-      unsigned long long* row = stats + static_cast<size_t>(cue) * nf;
+      unsigned long long* row = stats + (per_traj && k > 0 ? k * table_words : 0) +
+                                static_cast<size_t>(cue) * nf;
       if (a.nan) {
         atomicAdd(row + 7, 1ull);
         continue;
@@ -596,9 +628,9 @@ cudaError_t launch_offload_estimate(const CueDev& cs, long long n_tok, const lon
   return cudaGetLastError();
 }
 
-__global__ void stats_init_kernel(unsigned long long* stats, int rows, int nf, int rank) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < rows * nf) {
+__global__ void stats_init_kernel(unsigned long long* stats, long long words, int nf, int rank) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < words) {
     const int f = i % nf;
     stats[i] = (f == kStatFields + rank) ? 0x7f800000ull : 0ull;
   }
@@ -627,23 +659,23 @@ cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long lo
                                   const uint32_t* term_bits, const int* occ_pos, const int* occ_pat,
                                   const long long* n_occ, long long cap, float tau, int* seg_end,
                                   float* seg_mean, float* seg_min, float* seg_lowfrac,
-                                  unsigned long long* stats, int rank, int world, const ScanWs& ws,
-                                  cudaStream_t st) {
+                                  unsigned long long* stats, int rank, int world, int per_traj,
+                                  const ScanWs& ws, cudaStream_t st) {
   if (n_tok <= 0) return cudaSuccess;
   const int nt = n_tiles_of(n_tok);
   const int nf = kStatFields + world;
   seg_fused_kernel<<<nt, kScanThreads, 0, st>>>(cs, margin, term_bits, n_tok, offs, n_traj, think_end,
                                                 tau, occ_pos, occ_pat, n_occ, cap, seg_end, seg_mean,
-                                                seg_min, seg_lowfrac, stats, nf, rank, ws.tile_flag,
-                                                ws.tile_val, ws.done);
+                                                seg_min, seg_lowfrac, stats, nf, rank, per_traj,
+                                                ws.tile_flag, ws.tile_val, ws.done);
   return cudaGetLastError();
 }
 
-cudaError_t launch_stats_init(unsigned long long* stats, int n_cues, int rank, int world,
+cudaError_t launch_stats_init(unsigned long long* stats, int n_tables, int n_cues, int rank, int world,
                               cudaStream_t st) {
   const int nf = kStatFields + world;
-  const int n = (n_cues + 1) * nf;
-  stats_init_kernel<<<(n + 255) / 256, 256, 0, st>>>(stats, n_cues + 1, nf, rank);
+  const long long n = static_cast<long long>(n_tables) * (n_cues + 1) * nf;
+  stats_init_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(stats, n, nf, rank);
   return cudaGetLastError();
 }
 

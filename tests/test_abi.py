@@ -159,3 +159,41 @@ def test_plain_c_consumer(relay, tmp_path):
                            "-L", lib_dir, "-Wl,-rpath," + lib_dir, "-l:librelay.so", "-lm"])
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0 and "c abi ok" in r.stdout, (r.returncode, r.stdout, r.stderr)
+
+
+def test_stats_merge_host(relay):
+    """relay_stats_merge (host): fields 0-7 add, min slots take the minimum,
+    the mask picks tables, and merging commutes with the SUM all-reduce
+    (each rank's min slot is +inf-initialised only on that rank, 0 elsewhere)."""
+    rng = np.random.default_rng(7)
+    n_cues, world, n_tab = 5, 2, 6
+    nf = 8 + world
+    words = relay.stats_words(n_cues, world)
+    assert words == (n_cues + 1) * nf
+    per_rank = []
+    for r in range(world):
+        t = rng.integers(0, 1 << 40, size=(n_tab, n_cues + 1, nf), dtype=np.uint64)
+        mins = np.float32(rng.random((n_tab, n_cues + 1))).view(np.uint32).astype(np.uint64)
+        mins[rng.random(mins.shape) < 0.3] = 0x7F800000          # empty rows keep +inf
+        t[:, :, 8:] = 0
+        t[:, :, 8 + r] = mins
+        per_rank.append(t)
+    mask = np.array([1, 0, 1, 1, 0, 1], bool)
+    for t in per_rank:
+        got = relay.stats_merge(t, n_cues, world, mask).reshape(n_cues + 1, nf)
+        sel = t[mask]
+        np.testing.assert_array_equal(got[:, :8], sel[:, :, :8].sum(axis=0))
+        np.testing.assert_array_equal(got[:, 8:], sel[:, :, 8:].min(axis=0))
+    # merge(sum over ranks) == sum over ranks(merge)
+    summed = per_rank[0] + per_rank[1]
+    a = relay.stats_merge(summed, n_cues, world, mask)
+    b = relay.stats_merge(per_rank[0], n_cues, world, mask) + relay.stats_merge(per_rank[1], n_cues,
+                                                                              world, mask)
+    np.testing.assert_array_equal(a, b)
+    # empty selection: an initialised table with nothing in it
+    e = relay.stats_merge(per_rank[0], n_cues, world, np.zeros(n_tab, bool)).reshape(n_cues + 1, nf)
+    assert not e[:, :8].any() and (e[:, 8:] == 0x7F800000).all()
+    with pytest.raises(relay.RelayError):
+        relay.stats_merge(per_rank[0].reshape(-1)[:-1], n_cues, world)
+    lib = C.CDLL(relay.LIB_PATH)
+    assert lib.relay_stats_merge(None, 1, None, 3, 1, None) == 1

@@ -735,3 +735,67 @@ def test_offload_estimate_golden(relay, golden_dir):
                            np.array([7, 12], np.int64))
     ref = _offload_case(relay, h, ts, np.array([1, 1], np.uint8))
     assert ref.tolist() == [[3, 4, 3], [2, 0, 1]]          # hand-traced case C
+
+
+@pytest.mark.parametrize("case", [
+    dict(n_traj=8, traj_len=4096, n_cues=8, n_pat=12, max_len=3, seed=41, think=True),
+    dict(n_traj=5, traj_len=3001, n_cues=6, n_pat=20, max_len=6, seed=42, nan_rate=0.002),
+    dict(n_traj=64, traj_len=700, n_cues=32, n_pat=32, max_len=6, seed=43, think=True),
+    dict(n_traj=300, traj_len=37, n_cues=4, n_pat=8, max_len=3, seed=44),
+])
+def test_segment_reduce_per_trajectory_tables(relay, case):
+    """Per-trajectory tables (P:476-494 calibration-size study): all merged
+    equal the single table bit for bit, and a subset merged finalizes like the
+    oracle run on just that subset of trajectories."""
+    h, cs, ts, m, scan, seg, o_scan, o_win, o_sum = _segment_case(relay, **case)
+    think = case.get("think", False)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    tep = torch.as_tensor(ts.think_end_pos, device=DEV) if think else None
+    per = relay.segment_reduce(cs, torch.as_tensor(m, device=DEV), scan, offs, tep,
+                               per_trajectory=True)
+    torch.cuda.synchronize()
+    n_traj = case["n_traj"]
+    words = relay.stats_words(h.n_cues, 1)
+    tabs = per["stats"].cpu().numpy()
+    assert tabs.shape[0] == n_traj * words
+    np.testing.assert_array_equal(relay.stats_merge(tabs, h.n_cues, 1),
+                                  seg["stats"].cpu().numpy().view(np.uint64))
+    rng = np.random.default_rng(case["seed"])
+    mask = rng.random(n_traj) < 0.4
+    mask[0] = True
+    sub = relay.stats_merge(tabs, h.n_cues, 1, mask)
+    keep = np.flatnonzero(mask)
+    o = ts.traj_offsets
+    toks = np.concatenate([ts.tokens[o[k]:o[k + 1]] for k in keep])
+    mm = np.concatenate([m[o[k]:o[k + 1]] for k in keep])
+    so = np.concatenate([[0], np.cumsum([o[k + 1] - o[k] for k in keep])]).astype(np.int64)
+    ste = (np.array([ts.think_end_pos[k] - o[k] for k in keep], np.int64) + so[:-1]) if think else None
+    _, _, r_sum = oracle.analyze(mm, toks, so, h.pat_tokens, h.pat_offsets, h.pat_cue, h.n_cues,
+                                 h.terminator, tau=0.5, think_end_pos=ste, mode=0, min_count=1)
+    fin = relay.stats_finalize(sub, h.n_cues, 1, min_count=1)
+    for c in range(h.n_cues + 1):
+        g, r = fin[c], r_sum[c]
+        assert g["n"] == r["n"] and g["n_invalid"] == r["n_invalid"], (c, g, r)
+        if c < h.n_cues:
+            assert g["n_triggers"] == r["n_triggers"], (c, g, r)
+        if r["n"] == 0:
+            continue
+        for f in ("mean", "token_mean", "min", "low_frac"):
+            assert abs(g[f] - r[f]) < TOL, (c, f, g[f], r[f])
+
+
+def test_analyzer_per_trajectory_tables(relay):
+    """Analyzer with per-trajectory tables: merged, the same table as the
+    one-table Analyzer on the same logits (bit for bit)."""
+    vocab = 4096
+    h, cs = _cs_pair(relay, vocab, 6, 10, 3, seed=51)
+    ts = synth.make_tokens(6, 1500, h, seed=52)
+    n_tok = ts.tokens.shape[0]
+    logits = synth.make_logits(n_tok, vocab, "bf16", seed=53, device=DEV)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    one = relay.Analyzer(cs, n_tok, vocab, DEV).run(logits, tok, offs).clone()
+    per = relay.Analyzer(cs, n_tok, vocab, DEV, per_trajectory_tables=6).run(logits, tok, offs)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(relay.stats_merge(per.cpu().numpy(), 6, 1),
+                                  one.cpu().numpy().view(np.uint64))

@@ -239,7 +239,7 @@ def main():
         if timed:
             k1_ev.append((e0, e1))
         if world > 1:
-            allreduce_stats(an.stats)     # H6: one NCCL all-reduce of the stats table
+            allreduce_stats(an.stats, cs.n_cues, world)   # H6: relay_stats_allreduce (NCCL)
         host_stats[i % 2].copy_(an.stats, non_blocking=True)
         done[i % 2].record(stream)
 
@@ -332,6 +332,8 @@ def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):
     statistics table back."""
     import torch
     import torch.distributed as dist
+
+    from paper_2602_06454_b200.dist import allreduce_stats
     T, V = logits.shape
     h_logits = torch.empty((T, V), dtype=logits.dtype, pin_memory=True)
     h_logits.copy_(logits)
@@ -349,7 +351,7 @@ def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):
         d_offs.copy_(h_offs, non_blocking=True)
         an.run(d_logits, d_tok, d_offs)
         if world > 1:
-            dist.all_reduce(an.stats, op=dist.ReduceOp.SUM)
+            allreduce_stats(an.stats, cs.n_cues, world)
         host_stats.copy_(an.stats, non_blocking=True)
         stream.synchronize()
         relay.stats_finalize(host_stats.numpy(), cs.n_cues, world)

@@ -56,6 +56,7 @@ typedef enum {
   RELAY_OK = 0,
   RELAY_ERR_INVALID = 1,      /* bad argument (see each call)                      */
   RELAY_ERR_CUDA = 2,         /* a CUDA launch / runtime call failed               */
+  RELAY_ERR_NCCL = 3,         /* NCCL not loadable or an NCCL call failed          */
   RELAY_ERR_ALLOC = 4,        /* cue-set device allocation failed                  */
   RELAY_ERR_UNSUPPORTED = 5,  /* e.g. no sm_100 device                             */
   RELAY_ERR_WORKSPACE = 7     /* ws NULL or smaller than relay_workspace_bytes()   */
@@ -245,6 +246,33 @@ size_t relay_stats_words(int32_t n_cues, int32_t world_size);
  * Errors: RELAY_ERR_INVALID (NULLs, n_tables < 0, n_cues/world_size range). */
 relay_status_t relay_stats_merge(const uint64_t* tables, int32_t n_tables, const uint8_t* mask,
                                  int32_t n_cues, int32_t world_size, uint64_t* out);
+
+/* ------------------------------------------------------------------ H6 --
+ * relay_stats_allreduce — the path's one cross-GPU exchange: an in-place SUM
+ * all-reduce (ncclAllReduce, uint64) of n_tables consecutive stats tables on
+ * `stream`.  Trajectories are sharded across ranks (data parallel over the
+ * calibration traces), each rank reduces its shard into its own
+ * table (relay_stats_init with its rank), and after this call every rank
+ * holds the table of the whole corpus: integer fields add exactly and slot
+ * 8+r holds rank r's minimum (the other ranks contribute 0 there).
+ *   nccl_comm  an ncclComm_t over world_size ranks, this process's device
+ *              current — from relay_nccl_comm_init, or one torch created
+ *              (ProcessGroupNCCL._comm_ptr()); not owned by the call.
+ * NCCL is resolved at run time (dlopen "libnccl.so.2"; the copy torch loaded
+ * when torch is in the process).
+ * Errors: RELAY_ERR_INVALID (NULLs, n_tables < 1, n_cues / world_size range);
+ * RELAY_ERR_NCCL (NCCL missing or the call failed). */
+#define RELAY_NCCL_ID_BYTES 128
+relay_status_t relay_stats_allreduce(void* nccl_comm, uint64_t* stats, int32_t n_tables, int32_t n_cues,
+                                     int32_t world_size, relay_stream_t stream);
+/* [host] Library-owned communicators: rank 0 calls relay_nccl_unique_id and
+ * sends the RELAY_NCCL_ID_BYTES bytes to every rank (e.g. a
+ * torch.distributed broadcast); every rank then calls relay_nccl_comm_init
+ * with its CUDA device current (collective: blocks until all ranks join).
+ * relay_nccl_comm_destroy(NULL) is a no-op. */
+relay_status_t relay_nccl_unique_id(uint8_t* id_out);
+relay_status_t relay_nccl_comm_init(const uint8_t* id, int32_t world_size, int32_t rank, void** comm);
+relay_status_t relay_nccl_comm_destroy(void* comm);
 
 /* ------------------------------------------------------------------ H7 --
  * relay_stats_finalize [host] — per-cue and global summaries and the switch-

@@ -79,6 +79,10 @@ def _load():
         "relay_stats_init": (C.c_int, [P, i32, i32, i32, P]),
         "relay_stats_init_tables": (C.c_int, [P, i32, i32, i32, i32, P]),
         "relay_stats_merge": (C.c_int, [P, i32, P, i32, i32, P]),
+        "relay_stats_allreduce": (C.c_int, [P, P, i32, i32, i32, P]),
+        "relay_nccl_unique_id": (C.c_int, [P]),
+        "relay_nccl_comm_init": (C.c_int, [P, i32, i32, P]),
+        "relay_nccl_comm_destroy": (C.c_int, [P]),
         "relay_offload_estimate": (C.c_int, [P, i64, P, i32, P, P, P, P, i64, P, P, P, P]),
         "relay_stats_words": (sz, [i32, i32]),
         "relay_stats_finalize": (C.c_int, [P, i32, i32, i64, i32, P]),
@@ -98,7 +102,8 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_cueset_create", "relay_cueset_destroy", "relay_cueset_n_cues",
            "relay_workspace_bytes", "relay_workspace_init", "relay_cue_scan",
            "relay_segment_reduce", "relay_stats_init", "relay_stats_init_tables",
-           "relay_stats_words", "relay_stats_merge",
+           "relay_stats_words", "relay_stats_merge", "relay_stats_allreduce",
+           "relay_nccl_unique_id", "relay_nccl_comm_init", "relay_nccl_comm_destroy",
            "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate")
 
 
@@ -339,6 +344,60 @@ def stats_merge(host_tables: np.ndarray, n_cues: int, world_size: int = 1, mask=
                                 world_size, out.ctypes.data_as(C.c_void_p))
     _check(rc, "relay_stats_merge")
     return out
+
+
+# ------------------------------------------------------------------- H6
+def stats_allreduce(comm_ptr: int, stats, n_cues: int, world_size: int, n_tables: int = 1,
+                    stream=None):
+    """In-place SUM all-reduce of ``n_tables`` stats tables over the NCCL
+    communicator ``comm_ptr`` (an ncclComm_t as an int: ``NcclComm.ptr`` or
+    torch's ``ProcessGroupNCCL._comm_ptr()``)."""
+    _need_cuda(stats)
+    if stats.numel() < n_tables * stats_words(n_cues, world_size):
+        raise RelayError("stats too short")
+    _check(_lib.relay_stats_allreduce(C.c_void_p(comm_ptr), _ptr(stats), n_tables, n_cues,
+                                      world_size, _stream(stream)), "relay_stats_allreduce")
+    return stats
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(_lib.relay_nccl_unique_id(C.cast(buf, C.c_void_p)), "relay_nccl_unique_id")
+    return bytes(buf)
+
+
+class NcclComm:
+    """A library-owned NCCL communicator (collective constructor: every rank,
+    its CUDA device current).  ``uid`` is rank 0's ``nccl_unique_id()``, sent
+    to the others by the caller (``NcclComm.from_group`` does it through
+    torch.distributed)."""
+
+    def __init__(self, uid: bytes, world_size: int, rank: int):
+        if len(uid) != 128:
+            raise RelayError("uid must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        out = C.c_void_p()
+        _check(_lib.relay_nccl_comm_init(C.cast(buf, C.c_void_p), world_size, rank, C.byref(out)),
+               "relay_nccl_comm_init")
+        self.ptr, self.world_size, self.rank = out.value, world_size, rank
+
+    @classmethod
+    def from_group(cls, rank: int, world_size: int, group=None):
+        import torch.distributed as dist
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], world_size, rank)
+
+    def close(self):
+        if self.ptr:
+            _check(_lib.relay_nccl_comm_destroy(C.c_void_p(self.ptr)), "relay_nccl_comm_destroy")
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------- H3-H5

@@ -18,10 +18,11 @@ struct relay_cueset_s {
   void* block;  // one device allocation holding every array
 };
 
-namespace {
+namespace relay {
 
 thread_local char g_err[512] = "";
 
+// shared with relay_comm.cu
 relay_status_t fail(relay_status_t s, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -29,6 +30,10 @@ relay_status_t fail(relay_status_t s, const char* fmt, ...) {
   va_end(ap);
   return s;
 }
+
+}  // namespace relay
+
+namespace {
 
 relay_status_t cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return RELAY_OK;
@@ -105,6 +110,7 @@ const char* relay_status_string(relay_status_t s) {
     case RELAY_ERR_CUDA: return "CUDA error";
     case RELAY_ERR_ALLOC: return "allocation failed";
     case RELAY_ERR_UNSUPPORTED: return "unsupported";
+    case RELAY_ERR_NCCL: return "NCCL error";
     case RELAY_ERR_WORKSPACE: return "workspace missing or too small";
   }
   return "unknown status";

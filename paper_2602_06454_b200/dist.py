@@ -43,8 +43,36 @@ def local_view(tokens, traj_offsets, think_end_pos, lo: int, hi: int):
     return np.asarray(tokens)[a:b], loc_offs, loc_tep, (a, b)
 
 
-def allreduce_stats(stats, group=None):
-    """H6: one SUM all-reduce of the (int64 view of the) uint64 stats table."""
+def torch_nccl_comm(group=None, device=None) -> int:
+    """The ncclComm_t torch's ProcessGroupNCCL uses for ``group`` on ``device``
+    (initialised by a barrier if it is still lazy)."""
+    import torch
     import torch.distributed as dist
+    g = group if group is not None else dist.group.WORLD
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    backend = g._get_backend(dev)
+    ptr = 0
+    try:
+        ptr = int(backend._comm_ptr())
+    except RuntimeError:
+        ptr = 0
+    if not ptr:
+        dist.barrier(group=g, device_ids=[dev.index])
+        ptr = int(backend._comm_ptr())
+    return ptr
+
+
+def allreduce_stats(stats, n_cues: int, world_size: int, group=None, n_tables: int = 1,
+                    comm: int | None = None, stream=None):
+    """H6: one SUM all-reduce of the uint64 stats table(s).  On CUDA tensors
+    over an NCCL group it is librelay's relay_stats_allreduce (ncclAllReduce
+    on the caller's stream) on ``comm`` or torch's own communicator; on CPU
+    tensors (the gloo tests) torch.distributed's all_reduce of the int64 view
+    (two's-complement sums equal unsigned sums mod 2^64)."""
+    import torch.distributed as dist
+    if stats.is_cuda and dist.get_backend(group) == "nccl":
+        import paper_2602_06454_b200 as relay
+        ptr = comm if comm is not None else torch_nccl_comm(group, stats.device)
+        return relay.stats_allreduce(ptr, stats, n_cues, world_size, n_tables, stream)
     dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
     return stats

@@ -197,3 +197,22 @@ def test_stats_merge_host(relay):
         relay.stats_merge(per_rank[0].reshape(-1)[:-1], n_cues, world)
     lib = C.CDLL(relay.LIB_PATH)
     assert lib.relay_stats_merge(None, 1, None, 3, 1, None) == 1
+
+
+def test_nccl_entry_points_host(relay):
+    """H6 boundary without a GPU: NCCL resolves at run time (a unique id is
+    host-only), and bad arguments fail before any NCCL call."""
+    uid = relay.nccl_unique_id()
+    assert len(uid) == 128 and any(uid)
+    lib = C.CDLL(relay.LIB_PATH)
+    lib.relay_stats_allreduce.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                          C.c_void_p]
+    assert lib.relay_stats_allreduce(None, None, 1, 3, 1, None) == 1
+    assert lib.relay_stats_allreduce(C.c_void_p(8), C.c_void_p(8), 0, 3, 1, None) == 1
+    assert lib.relay_stats_allreduce(C.c_void_p(8), C.c_void_p(8), 1, 0, 1, None) == 1
+    lib.relay_nccl_comm_init.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+    out = C.c_void_p()
+    buf = (C.c_uint8 * 128)()
+    assert lib.relay_nccl_comm_init(C.cast(buf, C.c_void_p), 2, 2, C.byref(out)) == 1
+    assert lib.relay_nccl_comm_destroy(None) == 0
+    assert relay.version() >= 1 and lib.relay_status_string(3)

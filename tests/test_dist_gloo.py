@@ -95,7 +95,7 @@ def _worker(rank, world, port, out):
     tok, offs, tep, (a, b) = local_view(ts.tokens, ts.traj_offsets, ts.think_end_pos, lo, hi)
     t = table(m[a:b], tok, offs, tep, cs, 0.5, rank, world)
     st = torch.from_numpy(t.reshape(-1).view(np.int64).copy())
-    allreduce_stats(st)
+    allreduce_stats(st, cs.n_cues, world)
     if rank == 0:
         np.save(out, st.numpy())
     dist.destroy_process_group()

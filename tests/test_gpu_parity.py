@@ -799,3 +799,46 @@ def test_analyzer_per_trajectory_tables(relay):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(relay.stats_merge(per.cpu().numpy(), 6, 1),
                                   one.cpu().numpy().view(np.uint64))
+
+
+def test_stats_allreduce_library_comm(relay):
+    """H6 through the C ABI on a one-rank library-owned NCCL communicator: the
+    all-reduce of a real table is the identity (sum over one rank), in place,
+    on the caller's stream."""
+    vocab = 151936
+    h, cs = _cs_pair(relay, vocab, 8, 12, 3, seed=61)
+    ts = synth.make_tokens(4, 4096, h, seed=62)
+    m = torch.as_tensor(synth.make_margins(ts.tokens.shape[0], seed=63), device=DEV)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    st = relay.segment_reduce(cs, m, relay.cue_scan(cs, tok, offs), offs, per_trajectory=True)["stats"]
+    before = st.clone()
+    comm = relay.NcclComm(relay.nccl_unique_id(), 1, 0)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    relay.stats_allreduce(comm.ptr, st, 8, 1, n_tables=4, stream=s)
+    s.synchronize()
+    assert torch.equal(st, before)
+    comm.close()
+
+
+def test_stats_allreduce_torch_comm(relay, tmp_path):
+    """H6 on torch's own ProcessGroupNCCL communicator (one rank): the dist
+    helper routes CUDA tables through relay_stats_allreduce."""
+    import torch.distributed as dist
+
+    from paper_2602_06454_b200.dist import allreduce_stats, torch_nccl_comm
+    if dist.is_initialized():
+        pytest.skip("a process group already exists")
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1,
+                            device_id=torch.device(DEV))
+    try:
+        st = relay.new_stats(5, 0, 1, DEV)
+        st[:] = torch.arange(st.numel(), device=DEV)
+        ref = st.clone()
+        assert torch_nccl_comm() != 0
+        allreduce_stats(st, 5, 1)
+        torch.cuda.synchronize()
+        assert torch.equal(st, ref)
+    finally:
+        dist.destroy_process_group()

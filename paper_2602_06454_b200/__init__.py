@@ -13,20 +13,11 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-import subprocess
 
 import numpy as np
 
-_HERE = os.path.dirname(os.path.abspath(__file__))
-_REPO = os.path.dirname(_HERE)
-LIB_PATH = os.path.join(_HERE, "librelay.so")
-_SOURCES = [os.path.join(_HERE, "csrc", f) for f in
-            ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu")]
-_HEADERS = [os.path.join(_HERE, "csrc", f) for f in ("relay_device.cuh", "relay_internal.h")] + \
-           [os.path.join(_REPO, "include", "relay.h")]
-
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+from ._build import LIB_PATH, NVCC_FLAGS  # noqa: E402,F401
+from ._build import build_lib as _build_lib  # noqa: E402
 
 DT = {"bf16": 0, "f16": 1, "f32": 2}
 FLAG_NONE, FLAG_L2S, FLAG_S2L, FLAG_TO_ANSWER, FLAG_S2L_BUDGET = 0, 1, 2, 3, 4
@@ -41,18 +32,7 @@ class RelayError(RuntimeError):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile librelay.so for sm_100a with nvcc (works without a GPU)."""
-    newest = max(os.path.getmtime(p) for p in _SOURCES + _HEADERS)
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
-        nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-        if not os.path.exists(nvcc):
-            nvcc = "nvcc"
-        tmp = LIB_PATH + ".tmp"
-        cmd = [nvcc] + NVCC_FLAGS + ["-o", tmp] + _SOURCES
-        if verbose:
-            print(" ".join(cmd))
-        subprocess.check_call(cmd)
-        os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    return _build_lib(force=force, verbose=verbose)
 
 
 def _load():

@@ -17,6 +17,8 @@
 // guards cost ~0.5 instruction per element.  K4 splits rows into chunks
 // (LDG path) with a last-arriver combine, then runs RelayGen's switch state
 // machine on-device.
+#include <cstdlib>
+
 #include "relay_device.cuh"
 #include "relay_internal.h"
 
@@ -228,7 +230,9 @@ struct RowsArgs {
   long long stride;
   float c, iota;
   int flat;       // 0: one item per row, rows strided over CTAs (K1)
-                  // 1: each CTA takes an equal slice of the flattened rows (K4)
+                  // 1: each CTA takes an equal slice of the flattened rows
+                  // 2: rows cut into `chunk`-element chunks handed out by an
+                  //    atomic work counter (K4; balances uneven SM service)
   float* margin;
   int* top1;
   int* top2;
@@ -236,6 +240,10 @@ struct RowsArgs {
   uint8_t* status;
   int* counter;   // [n_rows] arrival counters (flat)
   float* part;    // [n_rows][kMaxSplit][kPartWords] row-part partials (flat)
+  int* work;      // [2] dynamic mode: next chunk, CTAs done (zero between launches)
+  int chunk;      // dynamic mode: elements per chunk (a multiple of a ring stage)
+  int cpr;        // dynamic mode: chunks per row (<= kMaxSplit)
+  long long perm; // dynamic mode (tuning): claim k takes chunk k*perm mod total (0: k)
   // vocabulary-parallel partials (kModePartial)
   long long col_offset;  // global index of the shard's first column
   float* tp_part;        // [n_rows][kPartWords]
@@ -412,25 +420,39 @@ struct ItemIter {
   long long next_w;  // strided: next row
   long long e, E1;   // flat: next element, end of this CTA's slice
 
-  // 64-bit products suffice: T < 2^51 elements and G <= 4096 (host-checked)
-  __device__ static long long slice_start(long long b, long long T, long long G) {
+  // Slice boundaries by floating point (no 64-bit integer division on the
+  // producer's critical path): any monotone rounding gives consistent slices,
+  // because every warp and CTA evaluates the same expression and owner()
+  // corrects its estimate against slice_start itself.  T < 2^51 (host-checked).
+  __device__ static long long slice_start(long long b, long long T, long long G, double Tg) {
     if (b >= G) return T;
-    return ((b * T) / G) & ~63LL;
+    return static_cast<long long>(static_cast<double>(b) * Tg) & ~63LL;
   }
   // the CTA whose (non-empty) slice holds element e
-  __device__ static long long owner(long long e, long long T, long long G) {
-    long long b = (e * G) / T;
-    while (b > 0 && slice_start(b, T, G) > e) b--;
-    while (b + 1 < G && slice_start(b + 1, T, G) <= e) b++;
+  __device__ static long long owner(long long e, long long T, long long G, double Tg) {
+    long long b = static_cast<long long>(static_cast<double>(e) / Tg);
+    if (b >= G) b = G - 1;
+    while (b > 0 && slice_start(b, T, G, Tg) > e) b--;
+    while (b + 1 < G && slice_start(b + 1, T, G, Tg) <= e) b++;
     return b;
   }
   __device__ void init(const RowsArgs& a) {
     next_w = blockIdx.x;
-    if (a.flat) {
+    if (a.flat == 1) {
       const long long T = a.n_rows * a.vocab, G = gridDim.x;
-      e = slice_start(blockIdx.x, T, G);
-      E1 = slice_start(blockIdx.x + 1, T, G);
+      const double Tg = static_cast<double>(T) / static_cast<double>(G);
+      e = slice_start(blockIdx.x, T, G, Tg);
+      E1 = slice_start(blockIdx.x + 1, T, G, Tg);
     }
+  }
+  // dynamic mode: chunk k of the n_rows * cpr chunks
+  __device__ static Item from_k(const RowsArgs& a, long long k) {
+    if (a.perm) k = (k * a.perm) % (a.n_rows * a.cpr);
+    // k < 2^31 (host-checked): 32-bit division
+    const long long r = static_cast<unsigned>(k) / static_cast<unsigned>(a.cpr);
+    const int ch = static_cast<int>(k - r * a.cpr);
+    const int j0 = ch * a.chunk;
+    return Item{r, j0, min(a.vocab, j0 + a.chunk), ch, a.cpr};
   }
   __device__ bool next(const RowsArgs& a, Item& it) {
     if (!a.flat) {
@@ -441,17 +463,36 @@ struct ItemIter {
     }
     if (e >= E1) return false;
     const long long T = a.n_rows * a.vocab, G = gridDim.x, V = a.vocab;
-    const long long r = e / V;
+    const double Tg = static_cast<double>(T) / static_cast<double>(G);
+    long long r = static_cast<long long>(static_cast<double>(e) / static_cast<double>(V));
+    while (r * V > e) r--;
+    while ((r + 1) * V <= e) r++;
     it.r = r;
     it.j0 = static_cast<int>(e - r * V);
     it.j1 = static_cast<int>(min(V, E1 - r * V));
-    const long long first = owner(r * V, T, G);
+    const long long first = owner(r * V, T, G, Tg);
     it.part = static_cast<int>(blockIdx.x - first);
-    it.nparts = static_cast<int>(owner(r * V + V - 1, T, G) - first + 1);
+    it.nparts = static_cast<int>(owner(r * V + V - 1, T, G, Tg) - first + 1);
     e = (r + 1) * V;
     return true;
   }
 };
+
+// Next item of a consumer / epilogue warp.  Static modes compute it; in the
+// dynamic mode the producer publishes each chunk it claimed in s_item[slot]
+// (-1 = no more) and completes ifull[slot].  The producer refills a slot only
+// after the epilogue released it (rempty), which happens after every consumer
+// and the epilogue read it, so no waiter can miss a phase.
+__device__ __forceinline__ bool fetch_item(const RowsArgs& a, ItemIter& iter, int it, int nslots,
+                                           const long long* s_item, uint32_t ifull_s, Item& item) {
+  if (a.flat != 2) return iter.next(a, item);
+  const int slot = it % nslots;
+  mbar_wait(ifull_s + 8 * slot, (it / nslots) & 1);
+  const long long k = *reinterpret_cast<const volatile long long*>(s_item + slot);
+  if (k < 0) return false;
+  item = ItemIter::from_k(a, k);
+  return true;
+}
 
 // Warp roles: NCW consumer warps stream stages; warp NCW is the TMA producer;
 // warp NCW+1 is the epilogue warp, which merges an item's partials, finishes
@@ -462,14 +503,22 @@ constexpr int kSlots = 4;
 
 #ifdef RELAY_TRACE
 // Tuning-only timeline (tools/trace_rows.py): %globaltimer stamps per CTA.
-__device__ unsigned long long g_trace[4096][16];
+// Slots: 0 entry, 1-14 ring stage n landed (consumer thread 0), 15 first
+// TMA issued, 16-23 consumer item ends, 24-30 epilogue item ends, 31 exit.
+constexpr int kTraceSlots = 32;
+__device__ unsigned long long g_trace[4096][kTraceSlots];
 __device__ __forceinline__ void stamp(int k) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  if (blockIdx.x < 4096 && k < 16) g_trace[blockIdx.x][k] = t;
+  if (blockIdx.x < 4096 && k < kTraceSlots) g_trace[blockIdx.x][k] = t;
 }
 extern "C" int relay_debug_trace_copy(unsigned long long* host, int n_ctas) {
-  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 16 * n_ctas));
+  return static_cast<int>(
+      cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * kTraceSlots * n_ctas));
+}
+extern "C" int relay_debug_trace_reset(const unsigned long long* zeros, int n_ctas) {
+  return static_cast<int>(
+      cudaMemcpyToSymbol(g_trace, zeros, sizeof(unsigned long long) * kTraceSlots * n_ctas));
 }
 #define TRACE(k) stamp(k)
 #else
@@ -492,6 +541,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   __shared__ __align__(8) uint64_t empty[NS];
   __shared__ __align__(8) uint64_t red_full[kSlots];
   __shared__ __align__(8) uint64_t red_empty[kSlots];
+  __shared__ __align__(8) uint64_t ifull[kSlots];
+  __shared__ long long s_item[kSlots];
   __shared__ int s_theta[kSlots];
   __shared__ Partial s_red[kSlots][NRED];
   __shared__ SmemCue sc;
@@ -505,6 +556,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const uint32_t empty_s = smem_u32_pinned(empty);
   const uint32_t rfull_s = smem_u32_pinned(red_full);
   const uint32_t rempty_s = smem_u32_pinned(red_empty);
+  const uint32_t ifull_s = smem_u32_pinned(ifull);
   if (tid == 0) {
     // Every consumer thread arrives on `empty` after its own shared-memory reads
     // and on `red_full` after its last threshold read / partial write, so each
@@ -516,6 +568,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     for (int s = 0; s < kSlots; s++) {
       mbar_init(rfull_s + 8 * s, NCT);
       mbar_init(rempty_s + 8 * s, 32);      // every reading lane of the epilogue warp
+      mbar_init(ifull_s + 8 * s, 1);        // the producer (dynamic mode)
       s_theta[s] = fkey(-INFINITY);
     }
     fence_barrier_init();
@@ -529,10 +582,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      ItemIter iter;
-      iter.init(a);
-      Item item;
-      while (iter.next(a, item)) {
+#ifdef RELAY_TRACE
+      bool first_issue = true;
+      int n_issued = 0;
+#endif
+      auto issue = [&](const Item& item) {
         const T* row = logits + item.r * a.stride;
         const Geom g = row_geom<E>(row, item.j0, item.j1);
         const char* src = reinterpret_cast<const char*>(row + item.j0 + g.head);
@@ -541,8 +595,34 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           mbar_wait_sleep(empty_s + 8 * stage, phase ^ 1);
           mbar_expect_tx(full_s + 8 * stage, bytes);
           bulk_g2s(ring_s + stage * SB, src + off, bytes, full_s + 8 * stage, pol);
+#ifdef RELAY_TRACE
+          if (first_issue) { TRACE(15); first_issue = false; }
+          if (n_issued == 4) TRACE(14);
+          ++n_issued;
+#endif
           if (++stage == NS) { stage = 0; phase ^= 1; }
         }
+      };
+      if (a.flat == 2) {
+        const long long total = a.n_rows * a.cpr;
+        long long k = atomicAdd(a.work, 1);
+        for (int it = 0;; ++it) {
+          const int slot = it % kSlots;
+          mbar_wait_sleep(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
+          const bool done = k >= total;
+          s_item[slot] = done ? -1 : k;
+          mbar_arrive(ifull_s + 8 * slot);
+          if (it == 1) TRACE(13);
+          if (done) break;
+          const long long kn = atomicAdd(a.work, 1);  // claimed while this chunk streams
+          issue(ItemIter::from_k(a, k));
+          k = kn;
+        }
+      } else {
+        ItemIter iter;
+        iter.init(a);
+        Item item;
+        while (iter.next(a, item)) issue(item);
       }
     }
     return;
@@ -561,7 +641,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     ItemIter iter;
     iter.init(a);
     Item item;
-    for (int it = 0; iter.next(a, item); ++it) {
+    for (int it = 0; fetch_item(a, iter, it, kSlots, s_item, ifull_s, item); ++it) {
       const int slot = it % kSlots;
       const long long r = item.r;
       const T* row = logits + r * a.stride;
@@ -616,24 +696,37 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       }
       if (lane == 0) a.counter[r] = 0;  // ready for the next launch / graph replay
       finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in);
-      if (lane == 0 && it < 5) TRACE(10 + it);
+      if (lane == 0 && it < 7) TRACE(24 + it);
+    }
+    if (a.flat == 2 && lane == 0) {
+      // the last CTA out re-arms the work counter for the next launch / replay
+      // (every producer's final claim precedes its CTA's arrival here)
+      if (atomic_add_acq_rel(a.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+        a.work[0] = 0;
+        a.work[1] = 0;
+      }
     }
     return;
   }
 
   // -------------------------------------------------- consumer warps
+#ifdef RELAY_TRACE
+  int n_stage = 0;
+#endif
   int stage = 0;
   uint32_t phase = 0;
   ItemIter iter;
   iter.init(a);
   Item item;
-  for (int it = 0; iter.next(a, item); ++it) {
+  for (int it = 0; fetch_item(a, iter, it, kSlots, s_item, ifull_s, item); ++it) {
     const int slot = it % kSlots;
     const long long r = item.r;
     const int j0 = item.j0;
     const int j1 = item.j1;
+    if (tid == 0 && it == 1) TRACE(11);
     // the slot (threshold + partials) is free once the epilogue took item it - kSlots
     mbar_wait(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
+    if (tid == 0 && it == 1) TRACE(12);
     int* theta_p = &s_theta[slot];
     const T* row = logits + r * a.stride;
     const Geom g = row_geom<E>(row, j0, j1);
@@ -645,7 +738,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const int bytes = min(SB, g.body - off);
       const int jb = j0 + g.head + off / E::SZ;
       mbar_wait(full_s + 8 * stage, phase);
-      if (tid == 0 && it == 0 && off == 0) TRACE(1);
+#ifdef RELAY_TRACE
+      if (tid == 0 && n_stage < 10) TRACE(1 + n_stage);
+      ++n_stage;
+#endif
       const uint32_t buf = ring_s + stage * SB;
       bool slow = false;
       if (bytes == SB) {
@@ -656,8 +752,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         const float2 h = stage_max2<E, UV>(raw);
         if (off == 0) {
           // item-start probe: the two half maxima are two distinct elements, so
-          // the warp's second-best of them bounds the row's 2nd-best from below
+          // the warp's second-best of them bounds the row's 2nd-best from below;
+          // after the consumer barrier the slot holds the best of all warps'
+          // (the 2nd-best of the stage's 2 * NCT half maxima), so the first
+          // stage is already mostly on the fast path
           theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
+          named_bar(1, NCT);
         }
         const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         consume_stage<E, UV>(raw, h, jb + tid * VEC, NCT * VEC, st, c, theta, slow);
@@ -680,9 +780,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     for (int off = 16; off >= RPW; off >>= 1) p = partial_merge(p, shfl_xor_partial(p, off));
     if (lane < RPW) s_red[slot][warp * RPW + lane] = p;
     mbar_arrive(rfull_s + 8 * slot);
-    if (tid == 0 && it < 8) TRACE(2 + it);
+    if (tid == 0 && it < 8) TRACE(16 + it);
   }
-  if (tid == 0) TRACE(15);
+  if (tid == 0) TRACE(31);
 }
 
 static int g_num_sms = 0;
@@ -716,6 +816,25 @@ constexpr int kStages = RELAY_K1_STAGES;  // ring depth
 constexpr int kUV = RELAY_K1_UV;          // 16-byte vectors per consumer thread per stage
 constexpr int kMinBlocks = RELAY_K1_MINB; // CTAs per SM the registers must allow
 
+// K4 work split: equal static slices (default; measured faster, see
+// DESIGN.md) or, for tuning, RELAY_K4_DYNAMIC=1 dynamic chunks of
+// RELAY_K4_CHUNK_STAGES ring stages
+static int k4_chunk_stages() {
+  static int v = [] {
+    const char* e = getenv("RELAY_K4_CHUNK_STAGES");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? x : 2;
+  }();
+  return v;
+}
+static bool k4_static() {
+  static bool v = [] {
+    const char* e = getenv("RELAY_K4_DYNAMIC");
+    return !(e && atoi(e) == 1);
+  }();
+  return v;
+}
+
 template <class E, int MODE>
 static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) {
   auto kern = rows_kernel<E, kNCW, kStages, kUV, kMinBlocks, MODE>;
@@ -730,7 +849,11 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   }
   const long long slots = static_cast<long long>(per_sm) * num_sms();
   long long grid = slots;
-  if (a.flat) {
+  if (a.flat == 2) {
+    const long long total = a.n_rows * a.cpr;
+    if (total >= (1LL << 31)) return cudaErrorInvalidValue;  // int work counter
+    if (grid > total) grid = total;
+  } else if (a.flat) {
     // every slice at least 128 elements and a row in at most kMaxSplit parts
     const long long T = a.n_rows * a.vocab;
     if (T >= (1LL << 51)) return cudaErrorInvalidValue;  // slice math is 64-bit
@@ -772,9 +895,30 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
   if (batch <= 0) return cudaSuccess;
   RowsArgs a{};
   a.logits = logits; a.n_rows = batch; a.vocab = vocab; a.stride = stride;
-  a.c = iota * kLog2e; a.iota = iota; a.flat = 1;
+  a.c = iota * kLog2e; a.iota = iota;
   a.margin = margin; a.top1 = top1; a.top2 = top2;
-  a.counter = ws.counter; a.part = ws.part;
+  a.counter = ws.counter; a.part = ws.part; a.work = ws.work;
+  {
+    // dynamic chunks of kK4ChunkStages ring stages (fewer, larger chunks if a
+    // row would need more than kMaxSplit parts)
+    const int esz = dt == 2 ? 4 : 2;
+    const int stage_elems = kUV * kNCW * 32 * 16 / esz;
+    int chunk = k4_chunk_stages() * stage_elems;
+    if ((vocab + chunk - 1) / chunk > kMaxSplit) {
+      const int per = (vocab + kMaxSplit - 1) / kMaxSplit;
+      chunk = (per + stage_elems - 1) / stage_elems * stage_elems;
+    }
+    a.chunk = chunk;
+    a.cpr = (vocab + chunk - 1) / chunk;
+    if (getenv("RELAY_K4_PERMUTE")) {
+      const long long total = static_cast<long long>(batch) * a.cpr;
+      long long p = 7919;
+      auto gcd = [](long long x, long long y) { while (y) { long long t = x % y; x = y; y = t; } return x; };
+      while (gcd(p, total) != 1) p += 2;
+      a.perm = p % total;
+    }
+    a.flat = k4_static() ? 1 : 2;
+  }
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
   a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
   return launch_rows<kModeStep>(dt, a, cs, st);

@@ -93,6 +93,7 @@ StepWs step_ws_layout(void* base, int batch) {
   if (batch < 0) batch = 0;
   w.counter = reinterpret_cast<int*>(take(sizeof(int) * (batch + 1)));
   w.part = reinterpret_cast<float*>(take(sizeof(float) * 8 * kMaxSplit * (static_cast<size_t>(batch) + 1)));  // kPartWords = 8
+  w.work = reinterpret_cast<int*>(take(sizeof(int) * 4));
   w.bytes = off;
   return w;
 }

@@ -58,6 +58,7 @@ ScanWs scan_ws_layout(void* base, long long n_tok, long long cap);
 struct StepWs {
   int* counter;        // [batch] (zero between launches)
   float* part;         // [batch][nsplit][8] partial (v1, v2, i1, i2, m, s, huge, pad)
+  int* work;           // [2] chunk counter, CTAs done (zero between launches)
   size_t bytes;
 };
 constexpr int kMaxSplit = 32;

@@ -5,14 +5,11 @@ Reports GB/s of algorithmic bytes and the fraction of MEASURED_PEAKS hbm_gbs."""
 import ctypes as C
 import json
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "k1_sweep")
-SRC = [os.path.join(ROOT, "paper_2602_06454_b200", "csrc", f)
-       for f in ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu")]
 VARIANTS = [  # (ncw, stages, uv, minb, extra): stage bytes = uv * ncw * 32 * 16
     (8, 4, 4, 3, ""), (8, 6, 2, 4, ""), (8, 4, 2, 4, ""), (12, 4, 2, 3, ""),
     (6, 6, 2, 5, ""), (16, 3, 2, 2, ""),
@@ -23,23 +20,31 @@ def name(v):
     return "w%d_s%d_u%d_m%d" % v[:4] + (("_" + v[4]) if v[4] else "")
 
 
-def extra(v):
+def _builder():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_relay_build", os.path.join(ROOT, "paper_2602_06454_b200", "_build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def defines(v):
+    d = ["RELAY_K1_NCW=%d" % v[0], "RELAY_K1_STAGES=%d" % v[1], "RELAY_K1_UV=%d" % v[2],
+         "RELAY_K1_MINB=%d" % v[3]]
     if v[4] == "NULL":
-        return ["-DRELAY_K1_NULL"]
-    if v[4].startswith("S"):
-        return ["-DRELAY_PRODUCER_SLEEP_NS=%s" % v[4][1:]]
-    return []
+        d.append("RELAY_K1_NULL")
+    elif v[4].startswith("S"):
+        d.append("RELAY_PRODUCER_SLEEP_NS=%s" % v[4][1:])
+    return d
 
 
 def build():
     os.makedirs(OUT, exist_ok=True)
+    b = _builder()
     for v in VARIANTS:
         so = os.path.join(OUT, "librelay_%s.so" % name(v))
-        cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
-               "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-               "-DRELAY_K1_NCW=%d" % v[0], "-DRELAY_K1_STAGES=%d" % v[1],
-               "-DRELAY_K1_UV=%d" % v[2], "-DRELAY_K1_MINB=%d" % v[3], "-o", so] + extra(v) + SRC
-        subprocess.check_call(cmd)
+        b.build_lib(so, defines=defines(v))
         print("built", so)
 
 

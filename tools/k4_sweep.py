@@ -1,0 +1,52 @@
+"""Tuning sweep for K4 (relay_step_switch, configs[2]): build librelay
+variants (launch shape / NULL streaming ceiling) and time each with
+tools/bench_step.py's CUDA-graph loop.
+    python tools/k4_sweep.py build            # any host with nvcc
+    python tools/k4_sweep.py run NAME         # one variant on cuda:0
+Runtime knobs (env): RELAY_K4_DYNAMIC=1 (dynamic chunks instead of equal
+static slices), RELAY_K4_CHUNK_STAGES=n."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+OUT = os.path.join(ROOT, "build", "k4_sweep")
+VARIANTS = {  # name -> defines
+    "base": [],
+    "null": ["RELAY_K1_NULL"],
+    "s6u2m4": ["RELAY_K1_STAGES=6", "RELAY_K1_UV=2", "RELAY_K1_MINB=4"],
+    "s8u2m3": ["RELAY_K1_STAGES=8", "RELAY_K1_UV=2", "RELAY_K1_MINB=3"],
+    "s2u4m3": ["RELAY_K1_STAGES=2", "RELAY_K1_UV=4", "RELAY_K1_MINB=3"],
+}
+
+
+def _builder():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_relay_build", os.path.join(ROOT, "paper_2602_06454_b200", "_build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def build():
+    os.makedirs(OUT, exist_ok=True)
+    b = _builder()
+    for n, d in VARIANTS.items():
+        b.build_lib(os.path.join(OUT, f"librelay_{n}.so"), defines=d or ["RELAY_K4_SWEEP_BASE"])
+        print("built", n)
+
+
+def run(name):
+    import paper_2602_06454_b200 as relay
+    relay.LIB_PATH = os.path.join(OUT, f"librelay_{name}.so")
+    relay._lib = relay._load()
+    import bench_step
+    print(name, os.environ.get("RELAY_K4_DYNAMIC", ""), os.environ.get("RELAY_K4_CHUNK_STAGES", ""),
+          flush=True)
+    bench_step.main()
+
+
+if __name__ == "__main__":
+    build() if sys.argv[1] == "build" else run(sys.argv[2])

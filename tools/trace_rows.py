@@ -5,21 +5,23 @@ Stamps: 0 entry, 1 first stage landed (consumer warp 0), 2.. consumer item ends,
 10.. epilogue item ends, 15 consumer exit."""
 import ctypes as C
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-OUT = os.path.join(ROOT, "build", "trace", "librelay.so")
-SRC = [os.path.join(ROOT, "paper_2602_06454_b200", "csrc", f)
-       for f in ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu")]
+OUT = os.environ.get("RELAY_TRACE_LIB", os.path.join(ROOT, "build", "trace", "librelay.so"))
+def _builder():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_relay_build", os.path.join(ROOT, "paper_2602_06454_b200", "_build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
 
-def build():
+def build(*extra):
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    subprocess.check_call(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a",
-                           "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-                           "-DRELAY_TRACE", "-o", OUT] + SRC)
+    _builder().build_lib(OUT, defines=["RELAY_TRACE", *extra])
 
 
 def run(mode="step"):
@@ -44,20 +46,39 @@ def run(mode="step"):
             relay.margin_rows(L)
     torch.cuda.synchronize()
     n = 444
-    buf = np.zeros((n, 16), np.uint64)
+    S = 32
+    lib0 = C.CDLL(OUT)
+    zero = np.zeros((n, S), np.uint64)
+    lib0.relay_debug_trace_reset.argtypes = [C.c_void_p, C.c_int]
+    if mode == "step":
+        assert lib0.relay_debug_trace_reset(zero.ctypes.data_as(C.c_void_p), n) == 0
+        relay.step_switch(cs, L, state, hist, ws=ws)
+    else:
+        assert lib0.relay_debug_trace_reset(zero.ctypes.data_as(C.c_void_p), n) == 0
+        relay.margin_rows(L)
+    torch.cuda.synchronize()
+    buf = np.zeros((n, S), np.uint64)
     lib = C.CDLL(OUT)
     lib.relay_debug_trace_copy.argtypes = [C.c_void_p, C.c_int]
     assert lib.relay_debug_trace_copy(buf.ctypes.data_as(C.c_void_p), n) == 0
     t0 = int(buf[:, 0][buf[:, 0] > 0].min())
     rel = np.where(buf > 0, (buf.astype(np.int64) - t0) / 1e3, np.nan)
-    np.set_printoptions(linewidth=200, precision=1, suppress=True)
-    cols = [0, 1, 2, 3, 4, 10, 11, 12, 15]
-    print("cols", cols)
+    np.set_printoptions(linewidth=250, precision=1, suppress=True)
+    print("per CTA: entry, first TMA issued | stage 1..10 landed | item-1 fetched, rempty passed, "
+          "published, 5th stage issued | consumer item ends | epilogue item ends | exit "
+          "(us from the first CTA entry)")
     for b in list(range(0, n, 37)) + [n - 1]:
-        print(b, rel[b, cols])
-    print("max entry", np.nanmax(rel[:, 0]), "max consumer exit", np.nanmax(rel[:, 15]),
-          "max epilogue", np.nanmax(rel[:, 10:15]))
+        r = rel[b]
+        print(f"{b:4d} {r[0]:5.1f} {r[15]:5.1f} |", r[1:11], "|", r[11:15], "|", r[16:20], "|",
+              r[24:28], "|", f"{r[31]:5.1f}")
+    st = rel[:, 1:11]
+    gaps = np.diff(st, axis=1)
+    print("stage-1 landed: min %.1f med %.1f max %.1f" % tuple(np.nanpercentile(st[:, 0], [0, 50, 100])))
+    print("stage gap (us): p10 %.2f med %.2f p90 %.2f max %.2f" %
+          tuple(np.nanpercentile(gaps, [10, 50, 90, 100])))
+    print("consumer exit: min %.1f med %.1f max %.1f" % tuple(np.nanpercentile(rel[:, 31], [0, 50, 100])))
+    print("max epilogue", np.nanmax(rel[:, 24:31]))
 
 
 if __name__ == "__main__":
-    build() if sys.argv[1] == "build" else run(*(sys.argv[2:3] or ["step"]))
+    build(*sys.argv[2:]) if sys.argv[1] == "build" else run(*(sys.argv[2:3] or ["step"]))

@@ -73,6 +73,32 @@ __device__ __forceinline__ void unpack16(const uint4& r, float (&f)[16 / E::SZ])
   }
 }
 
+// Maximum of one 16-byte vector (NaN-propagating).
+template <class E>
+__device__ __forceinline__ float vec_max(const uint4& r) {
+  if constexpr (E::SZ == 2) {
+    float lo, hi;
+    E::unpack2(E::pmax(E::pmax(r.x, r.y), E::pmax(r.z, r.w)), lo, hi);
+    return max_nan(lo, hi);
+  } else {
+    return max_nan(max_nan(__uint_as_float(r.x), __uint_as_float(r.y)),
+                   max_nan(__uint_as_float(r.z), __uint_as_float(r.w)));
+  }
+}
+
+// Element k (dynamic, < 16 / SZ) of a 16-byte vector, without local memory.
+template <class E>
+__device__ __forceinline__ float elem_at(const uint4& r, int k) {
+  if constexpr (E::SZ == 2) {
+    const uint32_t w = (k & 4) ? ((k & 2) ? r.w : r.z) : ((k & 2) ? r.y : r.x);
+    float lo, hi;
+    E::unpack2(w, lo, hi);
+    return (k & 1) ? hi : lo;
+  } else {
+    return __uint_as_float((k & 2) ? ((k & 1) ? r.w : r.z) : ((k & 1) ? r.y : r.x));
+  }
+}
+
 // Maxima of two disjoint halves of the UV vectors' elements (NaN-propagating):
 // lo/hi 16-bit lanes for packed formats, even/odd words for fp32.
 template <class E, int UV>
@@ -115,14 +141,20 @@ __device__ __forceinline__ void consume_stage(const uint4 (&raw)[UV], float2 h, 
   if (gm >= theta && !(gm <= st.g2)) {
 #pragma unroll
     for (int u = 0; u < UV; u++) {
-      float f[VEC];
-      unpack16<E>(raw[u], f);
-      float vm = f[0];
-#pragma unroll
-      for (int k = 1; k < VEC; k++) vm = fmaxf(vm, f[k]);
+      const float vm = vec_max<E>(raw[u]);
       if (vm >= theta && !(vm <= st.g2)) {
+        // only the elements that can still enter the row's top-2 are pushed
+        // (usually one): >= theta and above this thread's own 2nd-best
+        float f[VEC];
+        unpack16<E>(raw[u], f);
+        unsigned m = 0;
 #pragma unroll
-        for (int k = 0; k < VEC; k++) top2_push(st.t, f[k], j0 + u * jstep + k);
+        for (int k = 0; k < VEC; k++) m |= (f[k] >= theta && !(f[k] <= st.g2)) ? (1u << k) : 0u;
+        while (m) {
+          const int k = __ffs(m) - 1;
+          m &= m - 1;
+          top2_push(st.t, elem_at<E>(raw[u], k), j0 + u * jstep + k);
+        }
         st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
       }
     }
@@ -597,7 +629,6 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           bulk_g2s(ring_s + stage * SB, src + off, bytes, full_s + 8 * stage, pol);
 #ifdef RELAY_TRACE
           if (first_issue) { TRACE(15); first_issue = false; }
-          if (n_issued == 4) TRACE(14);
           ++n_issued;
 #endif
           if (++stage == NS) { stage = 0; phase ^= 1; }
@@ -612,7 +643,6 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           const bool done = k >= total;
           s_item[slot] = done ? -1 : k;
           mbar_arrive(ifull_s + 8 * slot);
-          if (it == 1) TRACE(13);
           if (done) break;
           const long long kn = atomicAdd(a.work, 1);  // claimed while this chunk streams
           issue(ItemIter::from_k(a, k));
@@ -758,9 +788,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           // stage is already mostly on the fast path
           theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
           named_bar(1, NCT);
+          if (tid == 0 && it == 1) TRACE(13);
         }
         const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         consume_stage<E, UV>(raw, h, jb + tid * VEC, NCT * VEC, st, c, theta, slow);
+        if (tid == 0 && it == 1 && off == 0) TRACE(14);
       } else {
         const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         const int nvec = bytes / 16;

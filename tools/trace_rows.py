@@ -65,7 +65,7 @@ def run(mode="step"):
     rel = np.where(buf > 0, (buf.astype(np.int64) - t0) / 1e3, np.nan)
     np.set_printoptions(linewidth=250, precision=1, suppress=True)
     print("per CTA: entry, first TMA issued | stage 1..10 landed | item-1 fetched, rempty passed, "
-          "published, 5th stage issued | consumer item ends | epilogue item ends | exit "
+          "probe barrier passed, first stage consumed | consumer item ends | epilogue item ends | exit "
           "(us from the first CTA entry)")
     for b in list(range(0, n, 37)) + [n - 1]:
         r = rel[b]

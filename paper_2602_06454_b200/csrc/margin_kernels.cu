@@ -607,6 +607,14 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   }
   __syncthreads();
   const float c = a.c;
+  // K4 is launched with programmatic dependent launch: its prologue (barrier
+  // init, item math, pattern staging) overlaps the previous kernel's tail;
+  // every warp waits for that kernel's completion (griddepcontrol.wait)
+  // before touching global data it may have produced.  Outside a PDL launch
+  // both instructions are no-ops.
+  if constexpr (MODE == kModeStep) {
+    if (tid == 0) pdl_launch_dependents();
+  }
 
   if (warp == NCW) {
     // ------------------------------------------------ producer warp
@@ -636,6 +644,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       };
       if (a.flat == 2) {
         const long long total = a.n_rows * a.cpr;
+        if constexpr (MODE == kModeStep) pdl_wait();
         long long k = atomicAdd(a.work, 1);
         for (int it = 0;; ++it) {
           const int slot = it % kSlots;
@@ -652,7 +661,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         ItemIter iter;
         iter.init(a);
         Item item;
-        while (iter.next(a, item)) issue(item);
+        bool more = iter.next(a, item);
+        if constexpr (MODE == kModeStep) pdl_wait();
+        for (; more; more = iter.next(a, item)) issue(item);
       }
     }
     return;
@@ -667,6 +678,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         sc.cue[i] = cs.pat_cue[i];
       }
       __syncwarp();
+      pdl_wait();
     }
     ItemIter iter;
     iter.init(a);
@@ -740,6 +752,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   }
 
   // -------------------------------------------------- consumer warps
+  if constexpr (MODE == kModeStep) pdl_wait();  // head/tail scalars are read directly
 #ifdef RELAY_TRACE
   int n_stage = 0;
 #endif
@@ -894,6 +907,19 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
     if (grid > a.n_rows * (kMaxSplit - 2)) grid = a.n_rows * (kMaxSplit - 2);
   } else if (grid > a.n_rows) {
     grid = a.n_rows;
+  }
+  if constexpr (MODE == kModeStep) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3((kNCW + 2) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, cs);
   }
   kern<<<static_cast<unsigned>(grid), (kNCW + 2) * 32, smem, st>>>(a, cs);
   return cudaGetLastError();

@@ -18,6 +18,7 @@
 // (LDG path) with a last-arriver combine, then runs RelayGen's switch state
 // machine on-device.
 #include <cstdlib>
+#include <cstring>
 
 #include "relay_device.cuh"
 #include "relay_internal.h"
@@ -275,7 +276,6 @@ struct RowsArgs {
   int* work;      // [2] dynamic mode: next chunk, CTAs done (zero between launches)
   int chunk;      // dynamic mode: elements per chunk (a multiple of a ring stage)
   int cpr;        // dynamic mode: chunks per row (<= kMaxSplit)
-  long long perm; // dynamic mode (tuning): claim k takes chunk k*perm mod total (0: k)
   // vocabulary-parallel partials (kModePartial)
   long long col_offset;  // global index of the shard's first column
   float* tp_part;        // [n_rows][kPartWords]
@@ -479,7 +479,6 @@ struct ItemIter {
   }
   // dynamic mode: chunk k of the n_rows * cpr chunks
   __device__ static Item from_k(const RowsArgs& a, long long k) {
-    if (a.perm) k = (k * a.perm) % (a.n_rows * a.cpr);
     // k < 2^31 (host-checked): 32-bit division
     const long long r = static_cast<unsigned>(k) / static_cast<unsigned>(a.cpr);
     const int ch = static_cast<int>(k - r * a.cpr);
@@ -693,9 +692,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       Partial q = partial_empty();
 #pragma unroll
       for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
+      // full butterfly: every lane ends with the merged partial (the switch
+      // below reads the row's top-1 on all lanes)
 #pragma unroll
-      for (int off = (NRED >= 32 ? 16 : NRED / 2); off > 0; off >>= 1)
-        q = partial_merge(q, shfl_xor_partial(q, off));
+      for (int off = 16; off > 0; off >>= 1) q = partial_merge(q, shfl_xor_partial(q, off));
       if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
       mbar_arrive(rempty_s + 8 * slot);
       if (item.nparts == 1) {
@@ -860,30 +860,41 @@ constexpr int kNCW = RELAY_K1_NCW;        // consumer warps per CTA
 constexpr int kStages = RELAY_K1_STAGES;  // ring depth
 constexpr int kUV = RELAY_K1_UV;          // 16-byte vectors per consumer thread per stage
 constexpr int kMinBlocks = RELAY_K1_MINB; // CTAs per SM the registers must allow
+#ifndef RELAY_K4_STAGES
+#define RELAY_K4_STAGES 6
+#endif
+#ifndef RELAY_K4_MINB
+#define RELAY_K4_MINB 2
+#endif
+constexpr int kStepStages = RELAY_K4_STAGES;
+constexpr int kStepMinBlocks = RELAY_K4_MINB;
 
-// K4 work split: equal static slices (default; measured faster, see
-// DESIGN.md) or, for tuning, RELAY_K4_DYNAMIC=1 dynamic chunks of
-// RELAY_K4_CHUNK_STAGES ring stages
-static int k4_chunk_stages() {
-  static int v = [] {
-    const char* e = getenv("RELAY_K4_CHUNK_STAGES");
-    const int x = e ? atoi(e) : 0;
-    return x > 0 ? x : 2;
-  }();
-  return v;
+// K4 work split (RELAY_K4_MODE=strided|flat|dynamic overrides, for tuning
+// and tests): strided = one whole row per CTA, no cross-CTA merge (default
+// when the batch fills every SM at least once); flat = equal slices of the
+// flattened batch merged by the last arriving CTA (default for small
+// batches); dynamic = chunks of RELAY_K4_CHUNK_STAGES ring stages claimed from
+// an atomic counter (measured slower).
+static int k4_mode(int batch) {
+  const char* e = getenv("RELAY_K4_MODE");
+  if (e && !strcmp(e, "strided")) return 0;
+  if (e && !strcmp(e, "flat")) return 1;
+  if (e && !strcmp(e, "dynamic")) return 2;
+  return batch >= num_sms() ? 0 : 1;
 }
-static bool k4_static() {
-  static bool v = [] {
-    const char* e = getenv("RELAY_K4_DYNAMIC");
-    return !(e && atoi(e) == 1);
-  }();
-  return v;
+static int k4_chunk_stages() {
+  const char* e = getenv("RELAY_K4_CHUNK_STAGES");
+  const int x = e ? atoi(e) : 0;
+  return x > 0 ? x : 4;
 }
 
 template <class E, int MODE>
 static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) {
-  auto kern = rows_kernel<E, kNCW, kStages, kUV, kMinBlocks, MODE>;
-  const int smem = kStages * kUV * kNCW * 32 * 16;
+  // K4 runs ~1-2 CTAs per SM: a deeper ring keeps more bytes in flight per CTA
+  constexpr int NS = (MODE == kModeStep) ? kStepStages : kStages;
+  constexpr int MINB = (MODE == kModeStep) ? kStepMinBlocks : kMinBlocks;
+  auto kern = rows_kernel<E, kNCW, NS, kUV, MINB, MODE>;
+  const int smem = NS * kUV * kNCW * 32 * 16;
   static int per_sm = 0;
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -957,8 +968,8 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
   a.margin = margin; a.top1 = top1; a.top2 = top2;
   a.counter = ws.counter; a.part = ws.part; a.work = ws.work;
   {
-    // dynamic chunks of kK4ChunkStages ring stages (fewer, larger chunks if a
-    // row would need more than kMaxSplit parts)
+    // dynamic mode: chunks of k4_chunk_stages() ring stages (fewer, larger
+    // chunks if a row would need more than kMaxSplit parts)
     const int esz = dt == 2 ? 4 : 2;
     const int stage_elems = kUV * kNCW * 32 * 16 / esz;
     int chunk = k4_chunk_stages() * stage_elems;
@@ -968,14 +979,7 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
     }
     a.chunk = chunk;
     a.cpr = (vocab + chunk - 1) / chunk;
-    if (getenv("RELAY_K4_PERMUTE")) {
-      const long long total = static_cast<long long>(batch) * a.cpr;
-      long long p = 7919;
-      auto gcd = [](long long x, long long y) { while (y) { long long t = x % y; x = y; y = t; } return x; };
-      while (gcd(p, total) != 1) p += 2;
-      a.perm = p % total;
-    }
-    a.flat = k4_static() ? 1 : 2;
+    a.flat = k4_mode(batch);
   }
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
   a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;

@@ -3,8 +3,8 @@ variants (launch shape / NULL streaming ceiling) and time each with
 tools/bench_step.py's CUDA-graph loop.
     python tools/k4_sweep.py build            # any host with nvcc
     python tools/k4_sweep.py run NAME         # one variant on cuda:0
-Runtime knobs (env): RELAY_K4_DYNAMIC=1 (dynamic chunks instead of equal
-static slices), RELAY_K4_CHUNK_STAGES=n."""
+Runtime knobs (env): RELAY_K4_MODE=strided|flat|dynamic,
+RELAY_K4_CHUNK_STAGES=n."""
 import os
 import sys
 
@@ -15,9 +15,10 @@ OUT = os.path.join(ROOT, "build", "k4_sweep")
 VARIANTS = {  # name -> defines
     "base": [],
     "null": ["RELAY_K1_NULL"],
-    "s6u2m4": ["RELAY_K1_STAGES=6", "RELAY_K1_UV=2", "RELAY_K1_MINB=4"],
-    "s8u2m3": ["RELAY_K1_STAGES=8", "RELAY_K1_UV=2", "RELAY_K1_MINB=3"],
-    "s2u4m3": ["RELAY_K1_STAGES=2", "RELAY_K1_UV=4", "RELAY_K1_MINB=3"],
+    "s4m3": ["RELAY_K4_STAGES=4", "RELAY_K4_MINB=3"],
+    "s5m2": ["RELAY_K4_STAGES=5", "RELAY_K4_MINB=2"],
+    "s12m1": ["RELAY_K4_STAGES=12", "RELAY_K4_MINB=1"],
+    "s8m1": ["RELAY_K4_STAGES=8", "RELAY_K4_MINB=1"],
 }
 
 
@@ -43,7 +44,7 @@ def run(name):
     relay.LIB_PATH = os.path.join(OUT, f"librelay_{name}.so")
     relay._lib = relay._load()
     import bench_step
-    print(name, os.environ.get("RELAY_K4_DYNAMIC", ""), os.environ.get("RELAY_K4_CHUNK_STAGES", ""),
+    print(name, os.environ.get("RELAY_K4_MODE", ""), os.environ.get("RELAY_K4_CHUNK_STAGES", ""),
           flush=True)
     bench_step.main()
 

@@ -61,6 +61,8 @@ def run(mode="step"):
     lib = C.CDLL(OUT)
     lib.relay_debug_trace_copy.argtypes = [C.c_void_p, C.c_int]
     assert lib.relay_debug_trace_copy(buf.ctypes.data_as(C.c_void_p), n) == 0
+    print("CTAs with an entry stamp:", int((buf[:, 0] > 0).sum()), " RELAY_K4_MODE =",
+          os.environ.get("RELAY_K4_MODE", "(default)"))
     t0 = int(buf[:, 0][buf[:, 0] > 0].min())
     rel = np.where(buf > 0, (buf.astype(np.int64) - t0) / 1e3, np.nan)
     np.set_printoptions(linewidth=250, precision=1, suppress=True)

@@ -4,13 +4,14 @@
  * scanning, post-sentence segment statistics and the decode-step switch flag.
  *
  * Citations: "P:n" = PAPER.md line n (§ / equation / table named alongside),
- * "S:n" = SPEC.md line n.  DESIGN.md "Readings" R1..R16 records every reading
+ * "S:n" = SPEC.md line n.  DESIGN.md "Readings" R1..R19 records every reading
  * of a silent or ambiguous passage that an entry point below depends on.
  *
  * Conventions (all entry points):
  *  - Pointers are DEVICE pointers unless marked [host].  The caller owns every
  *    buffer, the stream and the workspace; the library allocates device memory
- *    only inside relay_cueset_create (the cue set's own <20 KB copy).
+ *    only inside relay_cueset_create[_ex] (the cue set's own copy: < 20 KB,
+ *    plus vocab/8 bytes per token class).
  *  - Hot calls (margin_rows, cue_scan, segment_reduce, stats_init,
  *    step_switch) are asynchronous on `stream`: they never synchronise, never
  *    allocate and never read device memory from the host, so they can be
@@ -34,6 +35,7 @@ extern "C" {
 #define RELAY_MAX_CUE_LEN 8     /* tokens per pattern; the configs need 1..6 */
 #define RELAY_MAX_PATTERNS 64
 #define RELAY_MAX_CUES 64
+#define RELAY_MAX_CLASSES 8     /* token classes per cue set (N4) */
 #define RELAY_STAT_FIELDS 8     /* + world_size min slots per stats row */
 
 /* stats row layout: row c < n_cues is cue c, row n_cues is the global row. */
@@ -147,6 +149,29 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
                                    const uint8_t* terminator, int64_t vocab,
                                    int32_t think_end_token, uint32_t match_mode,
                                    relay_cueset_t* out);
+/* N4 (text-faithful cues): the same, with token classes.  A pattern element
+ * e < 0 matches any token of class c = -1 - e, so one pattern covers a
+ * surface form whose tokenisation varies with the next token, e.g. "So "
+ * (tab:switch_cue_sets) = {So, <any space-initial token>} [R18].
+ *   classes       [host] uint8[n_classes][vocab], nonzero = member; n_classes
+ *                 in [0, RELAY_MAX_CLASSES].
+ *   decimal_rule  [host] int32[3] = {period, digit_end, digit_start} class ids,
+ *                 or NULL: relay_cue_scan then does not end a sentence at a
+ *                 terminator that is a period token between a digit-ending
+ *                 and a digit-starting token of the same trajectory (S:168-172
+ *                 "not inside a decimal number") [R19].  Offline only:
+ *                 relay_step_switch decides S->L on the sampled token alone
+ *                 (the next token is not known yet).
+ * Equal-length patterns that both match at a start: the lower pattern index
+ * wins (in both match modes and in relay_step_switch) [R18].
+ * Errors: as relay_cueset_create; a negative element that is not a class id;
+ * n_classes out of range; classes NULL with n_classes > 0; a decimal_rule
+ * entry that is not a class id. */
+relay_status_t relay_cueset_create_ex(const int32_t* pat_tokens, const int32_t* pat_offsets,
+                                      int32_t n_patterns, const int32_t* pat_cue, int32_t n_cues,
+                                      const uint8_t* terminator, int64_t vocab, int32_t think_end_token,
+                                      uint32_t match_mode, const uint8_t* classes, int32_t n_classes,
+                                      const int32_t* decimal_rule, relay_cueset_t* out);
 relay_status_t relay_cueset_destroy(relay_cueset_t cs);
 int32_t relay_cueset_n_cues(relay_cueset_t cs);
 

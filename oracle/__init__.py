@@ -51,9 +51,10 @@ def _load():
         lib.oracle_margin_rows.restype = C.c_int
         lib.oracle_margin_rows.argtypes = [P, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                            C.c_double, C.c_int, P, P, P, P, P]
-        lib.oracle_cue_scan.restype = C.c_int64
-        lib.oracle_cue_scan.argtypes = [P, C.c_int64, P, C.c_int32, P, P, C.c_int32, P,
-                                        C.c_int32, P, C.c_uint32, P, P, P, C.c_int64]
+        lib.oracle_cue_scan_ex.restype = C.c_int64
+        lib.oracle_cue_scan_ex.argtypes = [P, C.c_int64, P, C.c_int32, P, P, C.c_int32, P,
+                                           C.c_int32, P, C.c_uint32, P, C.c_int32, C.c_int64, P,
+                                           P, P, P, C.c_int64]
         lib.oracle_windows.restype = None
         lib.oracle_windows.argtypes = [P, P, C.c_int64, P, C.c_int32, P, C.c_int64, C.c_float,
                                        P, P, P, P, P, P, P]
@@ -63,9 +64,10 @@ def _load():
                                          C.c_int32, P]
         lib.oracle_offload.restype = None
         lib.oracle_offload.argtypes = [C.c_int64, P, C.c_int32, P, P, P, C.c_int64, P, P, P, P, P]
-        lib.oracle_step_one.restype = C.c_int
-        lib.oracle_step_one.argtypes = [C.c_int32, C.c_float, P, P, P, P, P, C.c_int32, P, P,
-                                        C.c_int64, C.c_int32, C.c_float, C.c_int32, P]
+        lib.oracle_step_one_ex.restype = C.c_int
+        lib.oracle_step_one_ex.argtypes = [C.c_int32, C.c_float, P, P, P, P, P, C.c_int32, P, P,
+                                           C.c_int64, C.c_int32, C.c_float, C.c_int32, P,
+                                           C.c_int32, P]
         _lib = lib
     return _lib
 
@@ -117,8 +119,20 @@ def margin_rows(logits: np.ndarray, dtype: str | None = None, vocab: int | None 
 
 
 # --------------------------------------------------------------------- H2
+def _classes(classes, vocab):
+    """[n_classes, vocab] 0/1 array (or None) -> (uint8 array, n_classes)."""
+    if classes is None:
+        return None, 0
+    c = np.ascontiguousarray(np.asarray(classes).astype(bool).astype(np.uint8))
+    if c.ndim != 2 or c.shape[1] != vocab:
+        raise ValueError("classes must be [n_classes, vocab]")
+    return c, c.shape[0]
+
+
 def cue_scan(tokens, traj_offsets, pat_tokens, pat_offsets, pat_cue, n_cues, terminator,
-             mode: int = 0):
+             mode: int = 0, classes=None, decimal_rule=None):
+    """Pattern elements < 0 are token classes (row -1-e of ``classes``);
+    ``decimal_rule`` = (period, digit_end, digit_start) class ids or None."""
     tokens = np.ascontiguousarray(tokens, np.int32)
     n_tok = tokens.shape[0]
     offs = None if traj_offsets is None else np.ascontiguousarray(traj_offsets, np.int64)
@@ -132,9 +146,13 @@ def cue_scan(tokens, traj_offsets, pat_tokens, pat_offsets, pat_cue, n_cues, ter
     cap = max(1, n_tok * max(1, n_cues if mode else 1))
     occ_pos = np.empty(cap, np.int32)
     occ_pat = np.empty(cap, np.int32)
-    n = lib.oracle_cue_scan(_p(tokens), n_tok, _p(offs), n_traj, _p(pt), _p(po), po.shape[0] - 1,
-                            _p(pc), n_cues, _p(term_tab), mode, _p(term), _p(occ_pos),
-                            _p(occ_pat), cap)
+    cls, n_cls = _classes(classes, term_tab.shape[0])
+    dec = None if decimal_rule is None else np.ascontiguousarray(decimal_rule, np.int32)
+    if dec is not None and (cls is None or dec.shape != (3,) or dec.min() < 0 or dec.max() >= n_cls):
+        raise ValueError("decimal_rule needs three class ids")
+    n = lib.oracle_cue_scan_ex(_p(tokens), n_tok, _p(offs), n_traj, _p(pt), _p(po),
+                               po.shape[0] - 1, _p(pc), n_cues, _p(term_tab), mode, _p(cls), n_cls,
+                               term_tab.shape[0], _p(dec), _p(term), _p(occ_pos), _p(occ_pat), cap)
     return dict(term=term, occ_pos=occ_pos[:n].copy(), occ_pat=occ_pat[:n].copy())
 
 
@@ -178,10 +196,11 @@ def cue_stats(margin, traj_offsets, think_end_pos, occ_pos, occ_pat, pat_cue, n_
 
 
 def analyze(margin, tokens, traj_offsets, pat_tokens, pat_offsets, pat_cue, n_cues,
-            terminator, tau=0.5, think_end_pos=None, mode=0, min_count=3, rule=0):
+            terminator, tau=0.5, think_end_pos=None, mode=0, min_count=3, rule=0,
+            classes=None, decimal_rule=None):
     """H2 -> H3 -> H4..H7 on given margins: the full offline statistics."""
     scan = cue_scan(tokens, traj_offsets, pat_tokens, pat_offsets, pat_cue, n_cues,
-                    terminator, mode)
+                    terminator, mode, classes, decimal_rule)
     win = windows(margin, scan["term"], traj_offsets, scan["occ_pos"], tau)
     summ = cue_stats(margin, traj_offsets, think_end_pos, scan["occ_pos"], scan["occ_pat"],
                      pat_cue, n_cues, tau, win, min_count, rule)
@@ -190,7 +209,7 @@ def analyze(margin, tokens, traj_offsets, pat_tokens, pat_offsets, pat_cue, n_cu
 
 # --------------------------------------------------------------------- H8
 def step_one(tok, margin, state, hist, small_run, pat_tokens, pat_offsets, pat_cue,
-             terminator, think_end_token, margin_gate=-1.0, max_small_segment=0):
+             terminator, think_end_token, margin_gate=-1.0, max_small_segment=0, classes=None):
     """One sequence, one decode step.  Returns (flag, cue, state, hist, small_run)."""
     st = np.array([state], np.uint8)
     h = np.ascontiguousarray(np.array(hist, np.int32).copy())
@@ -200,10 +219,11 @@ def step_one(tok, margin, state, hist, small_run, pat_tokens, pat_offsets, pat_c
     po = np.ascontiguousarray(pat_offsets, np.int32)
     pc = np.ascontiguousarray(pat_cue, np.int32)
     term_tab = np.ascontiguousarray(terminator, np.uint8)
-    flag = _load().oracle_step_one(int(tok), float(margin), _p(st), _p(h), _p(sr), _p(pt),
-                                   _p(po), po.shape[0] - 1, _p(pc), _p(term_tab),
-                                   term_tab.shape[0], think_end_token, margin_gate,
-                                   max_small_segment, C.byref(cue))
+    cls, n_cls = _classes(classes, term_tab.shape[0])
+    flag = _load().oracle_step_one_ex(int(tok), float(margin), _p(st), _p(h), _p(sr), _p(pt),
+                                      _p(po), po.shape[0] - 1, _p(pc), _p(term_tab),
+                                      term_tab.shape[0], think_end_token, margin_gate,
+                                      max_small_segment, _p(cls), n_cls, C.byref(cue))
     return flag, cue.value, int(st[0]), h, int(sr[0])
 
 

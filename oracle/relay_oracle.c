@@ -10,7 +10,7 @@
  * written out in fp64 with plain loops.  No blocking, fusion or reordering.
  * Citations: "P:n" = /root/reference/PAPER.md line n (LaTeX source), "S:n" =
  * SPEC.md line n.  Readings of silent/ambiguous passages are listed in
- * DESIGN.md ("Readings of the paper", R1..R17) and referenced here as [Rk].
+ * DESIGN.md ("Readings of the paper", R1..R19) and referenced here as [Rk].
  *
  * Parity pins (tests/test_oracle_pins.py) fix each function to something other
  * than itself: worked examples (S:58-60, S:76-78, S:223-225, S:232-234,
@@ -168,38 +168,74 @@ static int64_t traj_of(const int64_t* off, int32_t n_traj, int64_t n_tok, int64_
     return -1;
 }
 
+/* Token classes (N4, text-faithful cues): a pattern element e >= 0 is the
+ * token id e; e < 0 is class c = -1 - e, matched by any token v with
+ * classes[c * vocab + v] != 0 (e.g. "So " = "So" followed by any
+ * space-initial token, Table 6) [R18]. */
+static int elem_matches(int32_t tok, int32_t e, const uint8_t* classes, int32_t n_classes,
+                        int64_t vocab) {
+    if (e >= 0) return tok == e;
+    int32_t c = -1 - e;
+    if (!classes || c >= n_classes || tok < 0 || tok >= vocab) return 0;
+    return classes[(int64_t)c * vocab + tok] != 0;
+}
+
+static int in_class(int32_t tok, int32_t c, const uint8_t* classes, int64_t vocab) {
+    return tok >= 0 && tok < vocab && classes[(int64_t)c * vocab + tok] != 0;
+}
+
 static int pattern_matches_at(const int32_t* tokens, int64_t s, int64_t b,
-                              const int32_t* pat_tokens, const int32_t* pat_offsets, int32_t p) {
+                              const int32_t* pat_tokens, const int32_t* pat_offsets, int32_t p,
+                              const uint8_t* classes, int32_t n_classes, int64_t vocab) {
     int64_t len = pat_offsets[p + 1] - pat_offsets[p];
     if (s + len > b) return 0;                       /* must fit inside the trajectory */
     for (int64_t k = 0; k < len; k++)
-        if (tokens[s + k] != pat_tokens[pat_offsets[p] + k]) return 0;
+        if (!elem_matches(tokens[s + k], pat_tokens[pat_offsets[p] + k], classes, n_classes, vocab))
+            return 0;
     return 1;
 }
 
 /* Cue occurrences by "simple token matching".
  * Readings: [R5] cues are caller-tokenised token-ID patterns; [R6] the cue
  * position is the pattern's first token; [R7] LONGEST mode (0): at each start
- * s, the longest pattern that matches tokens[s..s+len) inside s's trajectory;
- * ALL mode (1): for each cue id (ascending) with any matching pattern at s, one
- * occurrence carrying that cue's longest matching pattern.  Starts ascend.
+ * s, the longest pattern that matches tokens[s..s+len) inside s's trajectory
+ * (equal lengths: the lowest pattern index, [R18]); ALL mode (1): for each cue
+ * id (ascending) with any matching pattern at s, one occurrence carrying that
+ * cue's longest matching pattern.  Starts ascend.
  * Also term[t] = terminator[tokens[t]] ("sentence-ending punctuation",
- * [R8] the caller's terminator set).  Returns the TRUE occurrence count; at most
- * `cap` are written. */
-int64_t oracle_cue_scan(const int32_t* tokens, int64_t n_tok, const int64_t* traj_offsets,
-                        int32_t n_traj, const int32_t* pat_tokens, const int32_t* pat_offsets,
-                        int32_t n_pat, const int32_t* pat_cue, int32_t n_cues,
-                        const uint8_t* terminator, uint32_t mode,
-                        uint8_t* term, int32_t* occ_pos, int32_t* occ_pat, int64_t cap) {
+ * [R8] the caller's terminator set), except, with decimal_rule = {period,
+ * digit_end, digit_start} class ids (NULL = off), a period token between a
+ * digit-ending token and a digit-starting token of the same trajectory is not
+ * a sentence end ("not inside a decimal number") [R19].  Returns
+ * the TRUE occurrence count; at most `cap` are written. */
+int64_t oracle_cue_scan_ex(const int32_t* tokens, int64_t n_tok, const int64_t* traj_offsets,
+                           int32_t n_traj, const int32_t* pat_tokens, const int32_t* pat_offsets,
+                           int32_t n_pat, const int32_t* pat_cue, int32_t n_cues,
+                           const uint8_t* terminator, uint32_t mode,
+                           const uint8_t* classes, int32_t n_classes, int64_t vocab,
+                           const int32_t* decimal_rule,
+                           uint8_t* term, int32_t* occ_pos, int32_t* occ_pat, int64_t cap) {
     int64_t n = 0;
-    for (int64_t t = 0; t < n_tok; t++) term[t] = terminator[tokens[t]] ? 1 : 0;
+    for (int64_t t = 0; t < n_tok; t++) {
+        term[t] = terminator[tokens[t]] ? 1 : 0;
+        if (term[t] && decimal_rule && classes) {
+            int64_t a, b;
+            traj_of(traj_offsets, n_traj, n_tok, t, &a, &b);
+            if (t - 1 >= a && t + 1 < b && in_class(tokens[t], decimal_rule[0], classes, vocab) &&
+                in_class(tokens[t - 1], decimal_rule[1], classes, vocab) &&
+                in_class(tokens[t + 1], decimal_rule[2], classes, vocab))
+                term[t] = 0;
+        }
+    }
     for (int64_t s = 0; s < n_tok; s++) {
         int64_t a, b;
         if (traj_of(traj_offsets, n_traj, n_tok, s, &a, &b) < 0) continue;
         if (mode == 0) {
             int32_t best = -1;
             for (int32_t p = 0; p < n_pat; p++) {
-                if (!pattern_matches_at(tokens, s, b, pat_tokens, pat_offsets, p)) continue;
+                if (!pattern_matches_at(tokens, s, b, pat_tokens, pat_offsets, p, classes, n_classes,
+                                        vocab))
+                    continue;
                 if (best < 0 || (pat_offsets[p + 1] - pat_offsets[p]) >
                                 (pat_offsets[best + 1] - pat_offsets[best])) best = p;
             }
@@ -212,7 +248,9 @@ int64_t oracle_cue_scan(const int32_t* tokens, int64_t n_tok, const int64_t* tra
                 int32_t best = -1;
                 for (int32_t p = 0; p < n_pat; p++) {
                     if (pat_cue[p] != c) continue;
-                    if (!pattern_matches_at(tokens, s, b, pat_tokens, pat_offsets, p)) continue;
+                    if (!pattern_matches_at(tokens, s, b, pat_tokens, pat_offsets, p, classes,
+                                            n_classes, vocab))
+                        continue;
                     if (best < 0 || (pat_offsets[p + 1] - pat_offsets[p]) >
                                     (pat_offsets[best + 1] - pat_offsets[best])) best = p;
                 }
@@ -224,6 +262,16 @@ int64_t oracle_cue_scan(const int32_t* tokens, int64_t n_tok, const int64_t* tra
         }
     }
     return n;
+}
+
+int64_t oracle_cue_scan(const int32_t* tokens, int64_t n_tok, const int64_t* traj_offsets,
+                        int32_t n_traj, const int32_t* pat_tokens, const int32_t* pat_offsets,
+                        int32_t n_pat, const int32_t* pat_cue, int32_t n_cues,
+                        const uint8_t* terminator, uint32_t mode,
+                        uint8_t* term, int32_t* occ_pos, int32_t* occ_pat, int64_t cap) {
+    return oracle_cue_scan_ex(tokens, n_tok, traj_offsets, n_traj, pat_tokens, pat_offsets, n_pat,
+                              pat_cue, n_cues, terminator, mode, NULL, 0, 0, NULL, term, occ_pos,
+                              occ_pat, cap);
 }
 
 /* ------------------------------------------------- post-sentence windows */
@@ -408,11 +456,12 @@ void oracle_cue_stats(const float* margin, int64_t n_tok, const int64_t* traj_of
  *   otherwise NONE; large appends tok to hist, small increments small_run.
  * Every switch clears hist and small_run.  Cues emitted by the small model
  * are ignored.  Returns the flag; *cue_out = cue id or -1. */
-int oracle_step_one(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[7]*/,
-                    int32_t* small_run, const int32_t* pat_tokens, const int32_t* pat_offsets,
-                    int32_t n_pat, const int32_t* pat_cue, const uint8_t* terminator,
-                    int64_t vocab, int32_t think_end_token, float margin_gate,
-                    int32_t max_small_segment, int32_t* cue_out) {
+int oracle_step_one_ex(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[7]*/,
+                       int32_t* small_run, const int32_t* pat_tokens, const int32_t* pat_offsets,
+                       int32_t n_pat, const int32_t* pat_cue, const uint8_t* terminator,
+                       int64_t vocab, int32_t think_end_token, float margin_gate,
+                       int32_t max_small_segment, const uint8_t* classes, int32_t n_classes,
+                       int32_t* cue_out) {
     const int H = 7;
     *cue_out = -1;
     if (tok < 0 || tok >= vocab) return 0;
@@ -433,7 +482,8 @@ int oracle_step_one(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[
             int32_t len = pat_offsets[p + 1] - pat_offsets[p];
             int ok = 1;
             for (int32_t k = 0; k < len; k++)
-                if (seq[8 - len + k] != pat_tokens[pat_offsets[p] + k]) { ok = 0; break; }
+                if (!elem_matches(seq[8 - len + k], pat_tokens[pat_offsets[p] + k], classes,
+                                  n_classes, vocab)) { ok = 0; break; }
             if (ok && (best < 0 || len > pat_offsets[best + 1] - pat_offsets[best])) best = p;
         }
         if (best >= 0 && !(margin_gate >= 0.0f && margin < margin_gate)) {
@@ -461,6 +511,16 @@ int oracle_step_one(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[
     }
     *small_run += 1;
     return 0;
+}
+
+int oracle_step_one(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[7]*/,
+                    int32_t* small_run, const int32_t* pat_tokens, const int32_t* pat_offsets,
+                    int32_t n_pat, const int32_t* pat_cue, const uint8_t* terminator,
+                    int64_t vocab, int32_t think_end_token, float margin_gate,
+                    int32_t max_small_segment, int32_t* cue_out) {
+    return oracle_step_one_ex(tok, margin, state, hist, small_run, pat_tokens, pat_offsets, n_pat,
+                              pat_cue, terminator, vocab, think_end_token, margin_gate,
+                              max_small_segment, NULL, 0, cue_out);
 }
 
 /* ------------------------------------------- offload estimate (N3) --------

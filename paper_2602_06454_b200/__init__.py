@@ -49,6 +49,7 @@ def _load():
         "relay_margin_partials": (C.c_int, [P, C.c_int, i64, i64, i64, i64, f32, P, P]),
         "relay_margin_combine": (C.c_int, [P, i32, i64, f32, P, P, P, P, P, P]),
         "relay_cueset_create": (C.c_int, [P, P, i32, P, i32, P, i64, i32, u32, P]),
+        "relay_cueset_create_ex": (C.c_int, [P, P, i32, P, i32, P, i64, i32, u32, P, i32, P, P]),
         "relay_cueset_destroy": (C.c_int, [P]),
         "relay_cueset_n_cues": (i32, [P]),
         "relay_workspace_bytes": (sz, [i64, i64, i32]),
@@ -79,7 +80,7 @@ def _load():
 _lib = _load()
 EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_margin_rows",
            "relay_margin_partials", "relay_margin_combine",
-           "relay_cueset_create", "relay_cueset_destroy", "relay_cueset_n_cues",
+           "relay_cueset_create", "relay_cueset_create_ex", "relay_cueset_destroy", "relay_cueset_n_cues",
            "relay_workspace_bytes", "relay_workspace_init", "relay_cue_scan",
            "relay_segment_reduce", "relay_stats_init", "relay_stats_init_tables",
            "relay_stats_words", "relay_stats_merge", "relay_stats_allreduce",
@@ -206,10 +207,13 @@ def margin_rows_tp(logits_shard, col_offset: int, group=None, inv_temperature: f
 
 # --------------------------------------------------------------- cue set
 class CueSet:
-    """relay_cueset_create / destroy.  Host arrays (numpy) in, device copy owned."""
+    """relay_cueset_create_ex / destroy.  Host arrays (numpy) in, device copy
+    owned.  ``classes`` ([n_classes, vocab] 0/1) makes negative pattern
+    elements token classes (N4); ``decimal_rule`` = (period, digit_end,
+    digit_start) class ids turns on the decimal-number sentence rule."""
 
     def __init__(self, pat_tokens, pat_offsets, pat_cue, n_cues: int, terminator, vocab: int,
-                 think_end: int = -1, mode: int = 0):
+                 think_end: int = -1, mode: int = 0, classes=None, decimal_rule=None):
         self.pat_tokens = np.ascontiguousarray(pat_tokens, np.int32)
         self.pat_offsets = np.ascontiguousarray(pat_offsets, np.int32)
         self.pat_cue = np.ascontiguousarray(pat_cue, np.int32)
@@ -217,14 +221,28 @@ class CueSet:
         self.n_cues, self.vocab, self.think_end, self.mode = int(n_cues), int(vocab), int(think_end), int(mode)
         if self.terminator.shape[0] < vocab:
             raise RelayError("terminator table shorter than vocab")
+        self.classes = None
+        n_classes = 0
+        if classes is not None:
+            self.classes = np.ascontiguousarray(np.asarray(classes).astype(bool).astype(np.uint8))
+            if self.classes.ndim != 2 or self.classes.shape[1] != vocab:
+                raise RelayError("classes must be [n_classes, vocab]")
+            n_classes = self.classes.shape[0]
+        self.decimal_rule = None if decimal_rule is None else np.ascontiguousarray(decimal_rule, np.int32)
+        if self.decimal_rule is not None and self.decimal_rule.shape != (3,):
+            raise RelayError("decimal_rule must hold 3 class ids")
         h = C.c_void_p()
-        rc = _lib.relay_cueset_create(self.pat_tokens.ctypes.data_as(C.c_void_p),
-                                      self.pat_offsets.ctypes.data_as(C.c_void_p),
-                                      self.pat_offsets.shape[0] - 1,
-                                      self.pat_cue.ctypes.data_as(C.c_void_p), self.n_cues,
-                                      self.terminator.ctypes.data_as(C.c_void_p), self.vocab,
-                                      self.think_end, self.mode, C.byref(h))
-        _check(rc, "relay_cueset_create")
+        rc = _lib.relay_cueset_create_ex(self.pat_tokens.ctypes.data_as(C.c_void_p),
+                                         self.pat_offsets.ctypes.data_as(C.c_void_p),
+                                         self.pat_offsets.shape[0] - 1,
+                                         self.pat_cue.ctypes.data_as(C.c_void_p), self.n_cues,
+                                         self.terminator.ctypes.data_as(C.c_void_p), self.vocab,
+                                         self.think_end, self.mode,
+                                         None if self.classes is None else
+                                         self.classes.ctypes.data_as(C.c_void_p), n_classes,
+                                         None if self.decimal_rule is None else
+                                         self.decimal_rule.ctypes.data_as(C.c_void_p), C.byref(h))
+        _check(rc, "relay_cueset_create_ex")
         self._h = h
 
     @classmethod

@@ -352,7 +352,7 @@ __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float 
       for (int i = 0; i < kMaxLen; i++) {
         const int v = __shfl_sync(kFull, mine, i);
         const int k = i - (kMaxLen - len);  // pattern position of seq[i]
-        if (ok && k >= 0 && v != sc.tok[p * kMaxLen + k]) ok = false;
+        if (ok && k >= 0 && !elem_ok(cs, v, sc.tok[p * kMaxLen + k])) ok = false;
       }
       const unsigned b = __ballot_sync(kFull, ok);
       if (b) { best = base + __ffs(b) - 1; break; }

@@ -173,11 +173,20 @@ relay_status_t relay_margin_combine(const float* partials, int32_t n_shards, int
                      "relay_margin_combine launch");
 }
 
-relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat_offsets,
-                                   int32_t n_patterns, const int32_t* pat_cue, int32_t n_cues,
-                                   const uint8_t* terminator, int64_t vocab, int32_t think_end_token,
-                                   uint32_t match_mode, relay_cueset_t* out) {
+relay_status_t relay_cueset_create_ex(const int32_t* pat_tokens, const int32_t* pat_offsets,
+                                      int32_t n_patterns, const int32_t* pat_cue, int32_t n_cues,
+                                      const uint8_t* terminator, int64_t vocab, int32_t think_end_token,
+                                      uint32_t match_mode, const uint8_t* classes, int32_t n_classes,
+                                      const int32_t* decimal_rule, relay_cueset_t* out) {
   if (!out) return fail(RELAY_ERR_INVALID, "out is NULL");
+  if (n_classes < 0 || n_classes > kMaxClasses)
+    return fail(RELAY_ERR_INVALID, "n_classes must be in [0, %d]", kMaxClasses);
+  if (n_classes > 0 && !classes) return fail(RELAY_ERR_INVALID, "classes is NULL");
+  if (decimal_rule) {
+    for (int i = 0; i < 3; i++)
+      if (decimal_rule[i] < 0 || decimal_rule[i] >= n_classes)
+        return fail(RELAY_ERR_INVALID, "decimal_rule[%d] is not a class id", i);
+  }
   *out = nullptr;
   if (!pat_tokens || !pat_offsets || !pat_cue || !terminator)
     return fail(RELAY_ERR_INVALID, "pattern arrays and terminator are required");
@@ -193,7 +202,9 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
     if (pat_cue[p] < 0 || pat_cue[p] >= n_cues) return fail(RELAY_ERR_INVALID, "pattern %d cue id out of range", p);
     for (int k = 0; k < len[p]; k++) {
       int t = pat_tokens[pat_offsets[p] + k];
-      if (t < 0 || t >= vocab) return fail(RELAY_ERR_INVALID, "pattern %d token %d outside [0, vocab)", p, t);
+      if (t < 0 && -1 - t < n_classes) continue;  // class element
+      if (t < 0 || t >= vocab)
+        return fail(RELAY_ERR_INVALID, "pattern %d element %d is neither a token in [0, vocab) nor a class", p, t);
     }
   }
   for (int p = 0; p < n_patterns; p++)
@@ -220,10 +231,14 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
   std::vector<uint32_t> h_term(words, 0u);
   for (int64_t v = 0; v < vocab; v++)
     if (terminator[v]) h_term[v >> 5] |= 1u << (v & 31);
+  std::vector<uint32_t> h_cls(words * static_cast<size_t>(n_classes), 0u);
+  for (int c = 0; c < n_classes; c++)
+    for (int64_t v = 0; v < vocab; v++)
+      if (classes[static_cast<size_t>(c) * vocab + v]) h_cls[c * words + (v >> 5)] |= 1u << (v & 31);
   size_t off_tok = 0, off_len = align256(h_tok.size() * 4), off_cue = off_len + align256(n_patterns * 4),
          off_orig = off_cue + align256(n_patterns * 4), off_co = off_orig + align256(n_patterns * 4),
          off_lo = off_co + align256(n_patterns * 4), off_term = off_lo + align256(n_patterns * 4),
-         total = off_term + align256(words * 4);
+         off_cls = off_term + align256(words * 4), total = off_cls + align256(h_cls.size() * 4 + 4);
   std::vector<char> host(total, 0);
   std::memcpy(host.data() + off_tok, h_tok.data(), h_tok.size() * 4);
   std::memcpy(host.data() + off_len, h_len.data(), n_patterns * 4);
@@ -232,6 +247,7 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
   std::memcpy(host.data() + off_co, h_cue_orig.data(), n_patterns * 4);
   std::memcpy(host.data() + off_lo, len.data(), n_patterns * 4);
   std::memcpy(host.data() + off_term, h_term.data(), words * 4);
+  if (!h_cls.empty()) std::memcpy(host.data() + off_cls, h_cls.data(), h_cls.size() * 4);
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, total);
   if (e != cudaSuccess) return fail(RELAY_ERR_ALLOC, "cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
@@ -259,8 +275,21 @@ relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat
   cs->dev.cue_of_orig = reinterpret_cast<const int*>(b + off_co);
   cs->dev.len_of_orig = reinterpret_cast<const int*>(b + off_lo);
   cs->dev.term_tab = reinterpret_cast<const uint32_t*>(b + off_term);
+  cs->dev.n_classes = n_classes;
+  cs->dev.class_tab = reinterpret_cast<const uint32_t*>(b + off_cls);
+  cs->dev.dec_period = decimal_rule ? decimal_rule[0] : -1;
+  cs->dev.dec_dend = decimal_rule ? decimal_rule[1] : -1;
+  cs->dev.dec_dstart = decimal_rule ? decimal_rule[2] : -1;
   *out = cs;
   return RELAY_OK;
+}
+
+relay_status_t relay_cueset_create(const int32_t* pat_tokens, const int32_t* pat_offsets,
+                                   int32_t n_patterns, const int32_t* pat_cue, int32_t n_cues,
+                                   const uint8_t* terminator, int64_t vocab, int32_t think_end_token,
+                                   uint32_t match_mode, relay_cueset_t* out) {
+  return relay_cueset_create_ex(pat_tokens, pat_offsets, n_patterns, pat_cue, n_cues, terminator, vocab,
+                                think_end_token, match_mode, nullptr, 0, nullptr, out);
 }
 
 relay_status_t relay_cueset_destroy(relay_cueset_t cs) {

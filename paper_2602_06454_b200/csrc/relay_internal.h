@@ -11,6 +11,7 @@ namespace relay {
 constexpr int kMaxLen = 8;        // RELAY_MAX_CUE_LEN
 constexpr int kMaxPat = 64;       // RELAY_MAX_PATTERNS
 constexpr int kMaxCues = 64;      // RELAY_MAX_CUES
+constexpr int kMaxClasses = 8;    // RELAY_MAX_CLASSES
 constexpr int kStatFields = 8;    // RELAY_STAT_FIELDS
 constexpr int kTile = 2048;       // positions per CTA in the scan kernels
 constexpr int kScanThreads = 256; // kTile / 8 consecutive positions per thread
@@ -29,7 +30,23 @@ struct CueDev {
   const int* cue_of_orig;  // [n_pat] caller's pattern index -> cue
   const int* len_of_orig;  // [n_pat] caller's pattern index -> length
   const uint32_t* term_tab;  // [ceil(vocab/32)] terminator bitmap
+  // N4 token classes: pattern element e < 0 matches any token of class -1-e
+  int n_classes;
+  const uint32_t* class_tab;  // [n_classes][ceil(vocab/32)]
+  int dec_period, dec_dend, dec_dstart;  // decimal-number rule class ids (-1: off)
 };
+
+// Token `tok` in class c (bit test; false outside [0, vocab)).
+__device__ __forceinline__ bool in_class(const CueDev& cs, int c, int tok) {
+  if (tok < 0 || tok >= cs.vocab) return false;
+  const size_t words = static_cast<size_t>((cs.vocab + 31) >> 5);
+  return (__ldg(cs.class_tab + c * words + (tok >> 5)) >> (tok & 31)) & 1u;
+}
+
+// Pattern element e against token tok: a token id, or a class (e < 0).
+__device__ __forceinline__ bool elem_ok(const CueDev& cs, int tok, int e) {
+  return e >= 0 ? tok == e : in_class(cs, -1 - e, tok);
+}
 
 // Aggregate of a run of positions for the reverse segmented scan (K3).
 struct Agg {

@@ -57,11 +57,12 @@ __device__ __forceinline__ void load_patterns(const CueDev& cs, SmemPat& sp) {
   }
 }
 
-__device__ __forceinline__ bool match_at(const SmemPat& sp, int p, const int* tk, long long room) {
+__device__ __forceinline__ bool match_at(const CueDev& cs, const SmemPat& sp, int p, const int* tk,
+                                         long long room) {
   const int len = sp.len[p];
   if (len > room) return false;
   for (int k = 0; k < len; k++)
-    if (tk[k] != sp.tok[p * kMaxLen + k]) return false;
+    if (!elem_ok(cs, tk[k], sp.tok[p * kMaxLen + k])) return false;
   return true;
 }
 
@@ -72,12 +73,12 @@ __device__ __forceinline__ int count_at(const CueDev& cs, const SmemPat& sp, con
                                         long long room, unsigned long long* mask, int* best) {
   if (cs.mode == 0) {
     for (int p = 0; p < cs.n_pat; p++)
-      if (match_at(sp, p, tk, room)) { *best = p; return 1; }
+      if (match_at(cs, sp, p, tk, room)) { *best = p; return 1; }
     return 0;
   }
   unsigned long long m = 0;
   for (int p = 0; p < cs.n_pat; p++)
-    if (match_at(sp, p, tk, room)) m |= 1ull << sp.cue[p];
+    if (match_at(cs, sp, p, tk, room)) m |= 1ull << sp.cue[p];
   *mask = m;
   return __popcll(m);
 }
@@ -105,15 +106,17 @@ __global__ void __launch_bounds__(kScanThreads)
                     const long long* __restrict__ offs, int n_traj, uint32_t* __restrict__ term_bits,
                     int* __restrict__ occ_pos, int* __restrict__ occ_pat, long long cap,
                     long long* __restrict__ n_occ, int* tile_flag, long long* tile_val, int* done) {
-  __shared__ int s_tok[kTile2 + kMaxLen];
+  // s_tok[1 + i] = token base + i; one token of halo on the left (decimal
+  // rule) and kMaxLen on the right (patterns)
+  __shared__ int s_tok[1 + kTile2 + kMaxLen];
   __shared__ SmemPat sp;
   __shared__ int s_scan[kScanThreads];
   __shared__ long long s_prefix;
   const int tile = blockIdx.x;
   const long long base = static_cast<long long>(tile) * kTile2;
-  for (int i = threadIdx.x; i < kTile2 + kMaxLen; i += blockDim.x) {
-    const long long t = base + i;
-    s_tok[i] = (t < n_tok) ? __ldg(tokens + t) : -1;
+  for (int i = threadIdx.x; i < 1 + kTile2 + kMaxLen; i += blockDim.x) {
+    const long long t = base + i - 1;
+    s_tok[i] = (t >= 0 && t < n_tok) ? __ldg(tokens + t) : -1;
   }
   load_patterns(cs, sp);
   __syncthreads();
@@ -128,11 +131,19 @@ __global__ void __launch_bounds__(kScanThreads)
     masks[k] = 0; bests[k] = -1; rooms[k] = 0;
     const long long t = base + li + k;
     if (t < n_tok) {
-      const int tok = s_tok[li + k];
-      if (tok >= 0 && tok < cs.vocab && ((cs.term_tab[tok >> 5] >> (tok & 31)) & 1u)) tb |= 1u << k;
+      const int tok = s_tok[1 + li + k];
       rooms[k] = room_at(offs, n_traj, n_tok, t);
+      if (tok >= 0 && tok < cs.vocab && ((cs.term_tab[tok >> 5] >> (tok & 31)) & 1u)) {
+        // decimal rule (R19): a period between a digit-ending and a
+        // digit-starting token of the same trajectory is not a sentence end
+        const bool dec = cs.dec_period >= 0 && rooms[k] > 1 && in_class(cs, cs.dec_period, tok) &&
+                         room_at(offs, n_traj, n_tok, t - 1) == rooms[k] + 1 &&
+                         in_class(cs, cs.dec_dend, s_tok[li + k]) &&
+                         in_class(cs, cs.dec_dstart, s_tok[2 + li + k]);
+        if (!dec) tb |= 1u << k;
+      }
       if (rooms[k] > 0) {
-        const int c = count_at(cs, sp, s_tok + li + k, rooms[k], &masks[k], &bests[k]);
+        const int c = count_at(cs, sp, s_tok + 1 + li + k, rooms[k], &masks[k], &bests[k]);
         if (c == 0) bests[k] = -1;
         cnt += c;
       }
@@ -202,7 +213,7 @@ __global__ void __launch_bounds__(kScanThreads)
         m &= m - 1;
         int best = -1;
         for (int p = 0; p < cs.n_pat && best < 0; p++)
-          if (sp.cue[p] == c && match_at(sp, p, s_tok + li + k, rooms[k])) best = p;
+          if (sp.cue[p] == c && match_at(cs, sp, p, s_tok + 1 + li + k, rooms[k])) best = p;
         if (o < cap) { occ_pos[o] = static_cast<int>(t); occ_pat[o] = sp.orig[best]; }
         o++;
       }

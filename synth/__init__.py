@@ -255,3 +255,66 @@ CONFIGS = {
     "c5": dict(n_traj=64, traj_len=16384, vocab=151936, dtype="bf16", n_cues=32, n_pat=32,
                max_len=6),
 }
+
+
+@dataclass
+class ClassCase:
+    """A cue set with token-class pattern elements (N4) and a token stream
+    planted with class instances and decimal-number triples."""
+    cs: CueSet                 # pat_tokens may hold class elements (-1 - class)
+    classes: np.ndarray        # uint8 [n_classes, vocab]
+    decimal_rule: tuple        # (period, digit_end, digit_start) class ids
+    ts: TokenStream
+
+
+def make_class_case(vocab: int, n_traj: int, traj_len: int, n_cues: int = 6, n_patterns: int = 12,
+                    seed: int = BASE_SEED, decimal_rate: float = 0.02) -> ClassCase:
+    """Classes: 0 'space-initial' (30% of the ordinary tokens), 1 'period'
+    (10 of the 40 terminator ids), 2 'digit-end' / 3 'digit-start' (5% each),
+    4 and 5 arbitrary 10% subsets.  Patterns of 1-4 elements, each element a
+    class (0, 4 or 5) with probability 0.3, else a cue-pool token.  Tokens:
+    make_tokens with every pattern planted through random class members, then
+    digit-end / digit-start neighbours put around ``decimal_rate`` of the
+    period tokens (and around none of the others)."""
+    rng = np.random.default_rng(seed)
+    n_cls = 6
+    classes = np.zeros((n_cls, vocab), np.uint8)
+    ordinary = np.arange(OTHER_BASE, vocab)
+    classes[0, ordinary[rng.random(ordinary.size) < 0.3]] = 1
+    classes[1, TERMINATOR_IDS[:10]] = 1
+    for c, rate in ((2, 0.05), (3, 0.05), (4, 0.1), (5, 0.1)):
+        classes[c, ordinary[rng.random(ordinary.size) < rate]] = 1
+    pool = np.arange(CUE_TOKEN_BASE, CUE_TOKEN_BASE + 64, dtype=np.int64)
+    pats: list[tuple[int, ...]] = []
+    cues: list[int] = []
+    while len(pats) < n_patterns:
+        ln = int(rng.integers(1, 5))
+        p = tuple(int(-1 - rng.choice([0, 4, 5])) if (k > 0 and rng.random() < 0.3)
+                  else int(rng.choice(pool)) for k in range(ln))
+        if p in pats:
+            continue
+        cues.append(len(pats) if len(pats) < n_cues else int(rng.integers(0, n_cues)))
+        pats.append(p)
+    offs = np.zeros(len(pats) + 1, np.int32)
+    offs[1:] = np.cumsum([len(p) for p in pats])
+    term = np.zeros(vocab, np.uint8)
+    term[TERMINATOR_IDS[TERMINATOR_IDS < vocab]] = 1
+    members = [np.flatnonzero(classes[c]) for c in range(n_cls)]
+    # several concrete instances of every pattern for planting
+    inst = []
+    for p in pats:
+        for _ in range(4):
+            inst.append(tuple(e if e >= 0 else int(rng.choice(members[-1 - e])) for e in p))
+    plant = CueSet(offs.copy(), offs, np.array(cues, np.int32), n_cues, vocab, term, THINK_END, inst)
+    ts = make_tokens(n_traj, traj_len, plant, seed=seed + 1)
+    toks = ts.tokens
+    periods = np.flatnonzero(classes[1][toks] == 1)
+    for t in periods:
+        if rng.random() < decimal_rate * 25 and 0 < t < toks.size - 1:
+            if toks[t - 1] in (THINK_START, THINK_END) or toks[t + 1] in (THINK_START, THINK_END):
+                continue
+            toks[t - 1] = int(rng.choice(members[2]))
+            toks[t + 1] = int(rng.choice(members[3]))
+    cs = CueSet(np.array([t for p in pats for t in p], np.int32), offs, np.array(cues, np.int32),
+                n_cues, vocab, term, THINK_END, pats)
+    return ClassCase(cs, classes, (1, 2, 3), TokenStream(toks, ts.traj_offsets, ts.think_end_pos))

@@ -216,3 +216,28 @@ def test_nccl_entry_points_host(relay):
     assert lib.relay_nccl_comm_init(C.cast(buf, C.c_void_p), 2, 2, C.byref(out)) == 1
     assert lib.relay_nccl_comm_destroy(None) == 0
     assert relay.version() >= 1 and lib.relay_status_string(3)
+
+
+def test_cueset_create_ex_validation(relay):
+    """N4 argument checks happen on the host before any device work."""
+    V = 32
+    term = np.zeros(V, np.uint8)
+    classes = np.zeros((2, V), np.uint8)
+    ok = dict(pat_tokens=[1, -1], pat_offsets=[0, 2], pat_cue=[0], n_cues=1, terminator=term, vocab=V)
+    with pytest.raises(relay.RelayError):          # class element -3 with only 2 classes
+        relay.CueSet([1, -3], [0, 2], [0], 1, term, V, classes=classes)
+    with pytest.raises(relay.RelayError):          # class element without classes
+        relay.CueSet(**ok)
+    with pytest.raises(relay.RelayError):          # decimal rule naming a missing class
+        relay.CueSet(**ok, classes=classes, decimal_rule=(0, 1, 2))
+    with pytest.raises(relay.RelayError):          # too many classes
+        relay.CueSet(**ok, classes=np.zeros((9, V), np.uint8))
+    lib = C.CDLL(relay.LIB_PATH)
+    out = C.c_void_p()
+    P = C.c_void_p
+    keep = [np.array([1], np.int32), np.array([0, 1], np.int32), np.array([0], np.int32)]
+    lib.relay_cueset_create_ex.argtypes = [P, P, C.c_int32, P, C.c_int32, P, C.c_int64, C.c_int32,
+                                           C.c_uint32, P, C.c_int32, P, P]
+    assert lib.relay_cueset_create_ex(keep[0].ctypes.data_as(P), keep[1].ctypes.data_as(P), 1,
+                                      keep[2].ctypes.data_as(P), 1, term.ctypes.data_as(P), V, -1,
+                                      0, None, 1, None, C.byref(out)) == 1   # classes NULL, n=1

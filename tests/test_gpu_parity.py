@@ -855,3 +855,80 @@ def test_step_switch_work_split_modes(relay, monkeypatch, mode, B, vocab, dtype)
         test_step_switch(relay, greedy, B, vocab, dtype, 0, -1.0)
     if B == 37:
         test_step_switch_graph_replay(relay)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("decimal", [False, True])
+def test_class_patterns_and_decimal_rule(relay, mode, decimal):
+    """N4: token-class pattern elements (K2 matching) and the decimal-number
+    sentence rule (K2 terminator bits -> K3 windows and table) match the
+    oracle exactly on a planted stream; several tiles and trajectories."""
+    cc = synth.make_class_case(8192, 6, 2500, seed=91 + mode)
+    dec = cc.decimal_rule if decimal else None
+    cs = relay.CueSet(cc.cs.pat_tokens, cc.cs.pat_offsets, cc.cs.pat_cue, cc.cs.n_cues,
+                      cc.cs.terminator, cc.cs.vocab, cc.cs.think_end, mode, cc.classes, dec)
+    ts = cc.ts
+    m = synth.make_margins(ts.tokens.shape[0], seed=93)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    tep = torch.as_tensor(ts.think_end_pos, device=DEV)
+    scan = relay.cue_scan(cs, tok, offs)
+    seg = relay.segment_reduce(cs, torch.as_tensor(m, device=DEV), scan, offs, tep)
+    torch.cuda.synchronize()
+    o_scan, o_win, o_sum = oracle.analyze(m, ts.tokens, ts.traj_offsets, cc.cs.pat_tokens,
+                                          cc.cs.pat_offsets, cc.cs.pat_cue, cc.cs.n_cues,
+                                          cc.cs.terminator, think_end_pos=ts.think_end_pos,
+                                          mode=mode, min_count=1, classes=cc.classes,
+                                          decimal_rule=dec)
+    n = int(scan["n_occ"].item())
+    assert n == o_scan["occ_pos"].shape[0] and n > 50
+    np.testing.assert_array_equal(scan["occ_pos"][:n].cpu().numpy(), o_scan["occ_pos"])
+    np.testing.assert_array_equal(scan["occ_pat"][:n].cpu().numpy(), o_scan["occ_pat"])
+    bits = scan["term_bits"].cpu().numpy().view(np.uint32)
+    got_term = (bits[np.arange(ts.tokens.shape[0]) >> 5] >> (np.arange(ts.tokens.shape[0]) & 31)) & 1
+    np.testing.assert_array_equal(got_term, o_scan["term"])
+    if decimal:   # the rule really removed sentence ends
+        assert (o_scan["term"] < cc.cs.terminator[ts.tokens]).sum() > 10
+    _compare_segments(relay, cc.cs, scan, seg, o_scan, o_win, o_sum)
+
+
+@pytest.mark.parametrize("greedy", [False, True])
+def test_step_switch_class_patterns(relay, greedy):
+    """K4 completes class-valued patterns like the oracle's step rule."""
+    cc = synth.make_class_case(32000, 1, 64, seed=95)
+    h = cc.cs
+    cs = relay.CueSet(h.pat_tokens, h.pat_offsets, h.pat_cue, h.n_cues, h.terminator, h.vocab,
+                      h.think_end, 0, cc.classes)
+    rng = np.random.default_rng(96)
+    B = 200
+    members = [np.flatnonzero(cc.classes[c]) for c in range(cc.classes.shape[0])]
+    hist = np.full((B, 7), -1, np.int32)
+    sampled = rng.integers(3000, 32000, B).astype(np.int32)
+    for b in range(B):           # hist = a pattern instance minus its last element
+        p = h.patterns[int(rng.integers(0, len(h.patterns)))]
+        inst = [e if e >= 0 else int(rng.choice(members[-1 - e])) for e in p]
+        if len(inst) > 1:
+            hist[b, 7 - (len(inst) - 1):] = inst[:-1]
+        if rng.random() < 0.7:
+            sampled[b] = inst[-1]
+    state = np.zeros(B, np.uint8)
+    small_run = np.zeros(B, np.int32)
+    L = synth.make_logits(B, 32000, "bf16", tokens=sampled, seed=97, device=DEV)
+    ref = oracle.margin_rows(synth.host_rows(L, "bf16"), dtype="bf16")
+    d_state = torch.as_tensor(state, device=DEV)
+    d_hist = torch.as_tensor(hist, device=DEV)
+    d_sr = torch.as_tensor(small_run, device=DEV)
+    out = relay.step_switch(cs, L, d_state, d_hist, d_sr,
+                            None if greedy else torch.as_tensor(sampled, device=DEV))
+    torch.cuda.synchronize()
+    n_l2s = 0
+    for b in range(B):
+        tok = int(ref["top1"][b]) if greedy else int(sampled[b])
+        f, c, st, hh, sr = oracle.step_one(tok, np.float32(ref["margin"][b]), 0, hist[b], 0,
+                                           h.pat_tokens, h.pat_offsets, h.pat_cue, h.terminator,
+                                           h.think_end, classes=cc.classes)
+        assert out["flag"][b].item() == f and out["cue_id"][b].item() == c, b
+        assert d_state[b].item() == st
+        np.testing.assert_array_equal(d_hist[b].cpu().numpy(), hh)
+        n_l2s += f == 1
+    assert n_l2s > 50

@@ -62,6 +62,9 @@ def _load():
         lib.oracle_cue_stats.argtypes = [P, C.c_int64, P, C.c_int32, P, P, P, C.c_int64, P,
                                          C.c_int32, C.c_float, P, P, P, P, P, P, C.c_int64,
                                          C.c_int32, P]
+        lib.oracle_sample_row.restype = C.c_int32
+        lib.oracle_sample_row.argtypes = [P, C.c_int, C.c_int64, C.c_double, C.c_int32, C.c_double,
+                                          C.c_double]
         lib.oracle_offload.restype = None
         lib.oracle_offload.argtypes = [C.c_int64, P, C.c_int32, P, P, P, C.c_int64, P, P, P, P, P]
         lib.oracle_step_one_ex.restype = C.c_int
@@ -225,6 +228,24 @@ def step_one(tok, margin, state, hist, small_run, pat_tokens, pat_offsets, pat_c
                                       term_tab.shape[0], think_end_token, margin_gate,
                                       max_small_segment, _p(cls), n_cls, C.byref(cue))
     return flag, cue.value, int(st[0]), h, int(sr[0])
+
+
+# ------------------------------------------------------------------ N2
+def sample_rows(logits, u, dtype: str | None = None, vocab: int | None = None,
+                temperature: float = 0.6, top_k: int = 20, top_p: float = 0.95):
+    """Per row: the token drawn by temperature / top-k / top-p sampling with
+    the given uniforms (inverse CDF, R20); -1 for rows with status != 0."""
+    a = np.ascontiguousarray(logits)
+    code = _dtype_code(a, dtype)
+    n, stride = a.shape
+    vocab = stride if vocab is None else vocab
+    u = np.asarray(u, np.float64)
+    lib = _load()
+    out = np.empty(n, np.int32)
+    for r in range(n):
+        out[r] = lib.oracle_sample_row(a[r].ctypes.data_as(C.c_void_p), code, vocab,
+                                       1.0 / temperature, top_k, top_p, float(u[r]))
+    return out
 
 
 # ------------------------------------------------------------------ N3

@@ -10,7 +10,7 @@
  * written out in fp64 with plain loops.  No blocking, fusion or reordering.
  * Citations: "P:n" = /root/reference/PAPER.md line n (LaTeX source), "S:n" =
  * SPEC.md line n.  Readings of silent/ambiguous passages are listed in
- * DESIGN.md ("Readings of the paper", R1..R19) and referenced here as [Rk].
+ * DESIGN.md ("Readings of the paper", R1..R20) and referenced here as [Rk].
  *
  * Parity pins (tests/test_oracle_pins.py) fix each function to something other
  * than itself: worked examples (S:58-60, S:76-78, S:223-225, S:232-234,
@@ -521,6 +521,64 @@ int oracle_step_one(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[
     return oracle_step_one_ex(tok, margin, state, hist, small_run, pat_tokens, pat_offsets, n_pat,
                               pat_cue, terminator, vocab, think_end_token, margin_gate,
                               max_small_segment, NULL, 0, cue_out);
+}
+
+/* --------------------------------------------- fused sampler (N2) --------
+ * The decode-side sampling the paper runs with every model (P:332-333:
+ * "temperature 0.6 and top-p sampling at 0.95", and for Qwen3 "top-k to 20"),
+ * read as [R20]: order the row by (value desc, index asc) [R3]; keep the first
+ * K; p_i = exp((z_i - z_(1)) / T) for those K (softmax at temperature T
+ * restricted to the top K, unnormalised); keep the first L of them, L = the
+ * smallest l with p_0 + ... + p_(l-1) >= top_p * (p_0 + ... + p_(K-1)) (the
+ * tokens whose higher-ranked mass is below top_p, at least one); draw the
+ * token by inverse CDF with the caller's uniform u in [0, 1): the first i
+ * with p_0 + ... + p_i > u * (p_0 + ... + p_(L-1)).  top_k in [1, vocab].
+ * A row with status != 0 (NaN / +inf / no finite entry, [R4]) samples -1. */
+int32_t oracle_sample_row(const void* row, int dtype, int64_t vocab, double inv_temperature,
+                          int32_t top_k, double top_p, double u) {
+    int32_t i1, i2;
+    double m, l;
+    if (top_k < 1) return -1;
+    if (oracle_margin_row(row, dtype, vocab, 1.0, &i1, &i2, &m, &l) != 0) return -1;
+    if (top_k > vocab) top_k = (int32_t)vocab;
+    int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)top_k);
+    double* p = (double*)malloc(sizeof(double) * (size_t)top_k);
+    /* top-k by repeated selection: the best entry ordered after the previous */
+    for (int32_t r = 0; r < top_k; r++) {
+        int64_t best = -1;
+        for (int64_t j = 0; j < vocab; j++) {
+            double z = oracle_elem(row, dtype, j);
+            if (r > 0) {   /* must come after idx[r-1] in (value desc, index asc) */
+                double zp = oracle_elem(row, dtype, idx[r - 1]);
+                if (z > zp || (z == zp && j <= idx[r - 1])) continue;
+            }
+            if (best < 0) { best = j; continue; }
+            double zb = oracle_elem(row, dtype, best);
+            if (z > zb) best = j;      /* equal values keep the lower index */
+        }
+        idx[r] = best;
+    }
+    double z1 = oracle_elem(row, dtype, idx[0]);
+    double total = 0.0;
+    for (int32_t r = 0; r < top_k; r++) {
+        double z = oracle_elem(row, dtype, idx[r]);
+        p[r] = isinf(z) ? 0.0 : exp((z - z1) * inv_temperature);
+        total += p[r];
+    }
+    int32_t L = 0;
+    double above = 0.0;
+    while (L < top_k && (L == 0 || above < top_p * total)) { above += p[L]; L++; }
+    double kept = 0.0;
+    for (int32_t r = 0; r < L; r++) kept += p[r];
+    double target = u * kept, cum = 0.0;
+    int32_t tok = (int32_t)idx[L - 1];
+    for (int32_t r = 0; r < L; r++) {
+        cum += p[r];
+        if (cum > target) { tok = (int32_t)idx[r]; break; }
+    }
+    free(idx);
+    free(p);
+    return tok;
 }
 
 /* ------------------------------------------- offload estimate (N3) --------

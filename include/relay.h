@@ -374,6 +374,35 @@ relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dt
                                  int32_t* top2, uint8_t* flag, int16_t* cue_id, void* ws,
                                  size_t ws_bytes, relay_stream_t stream);
 
+/* ------------------------------------------------------------------ N2 --
+ * relay_step_sample — the decode step with the sampler fused in: the same
+ * margin and switch as relay_step_switch, with the token DRAWN from the row
+ * instead of passed in.  The paper samples at temperature 0.6, top-p 0.95
+ * and (Qwen3) top-k 20; R20 fixes the order of the operations:
+ * the top_k entries by (value desc, index asc), p_k = exp((z_k - z_(1)) /
+ * temperature) over them, the first L kept with L the smallest count whose
+ * mass reaches top_p of the top-k mass (at least one), then the first k with
+ * p_0 + ... + p_k > uniform[b] * (kept mass).  The row is read from HBM once:
+ * the margin pass keeps it in L2 and bounds its top_k-th largest logit; a
+ * second kernel re-reads it from L2, keeps the logits above the bound, selects
+ * the exact top-k and draws (an exact fallback covers pathological rows,
+ * e.g. a constant row).  Rows with status != 0 draw -1 (no switch update).
+ *   temperature > 0; top_k in [1, RELAY_MAX_TOP_K] (clamped to vocab);
+ *   top_p in (0, 1]; uniform float[batch] in [0, 1) (device; the caller's
+ *   random numbers); sampled int32[batch] out; other arguments, outputs and
+ *   workspace as relay_step_switch (rows are streamed whole per CTA).
+ * Errors: as relay_step_switch, plus top_k / top_p / temperature out of
+ * range, NULL uniform or sampled. */
+#define RELAY_MAX_TOP_K 64
+relay_status_t relay_step_sample(relay_cueset_t cs, const void* logits, relay_dtype_t dt,
+                                 int32_t batch, int64_t vocab, int64_t row_stride,
+                                 float inv_temperature, float temperature, int32_t top_k,
+                                 float top_p, const float* uniform, uint8_t* state, int32_t* hist,
+                                 int32_t* small_run, float margin_gate, int32_t max_small_segment,
+                                 float* margin, int32_t* top1, int32_t* top2, int32_t* sampled,
+                                 uint8_t* flag, int16_t* cue_id, void* ws, size_t ws_bytes,
+                                 relay_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

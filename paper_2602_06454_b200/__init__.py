@@ -69,6 +69,8 @@ def _load():
         "relay_stats_finalize": (C.c_int, [P, i32, i32, i64, i32, P]),
         "relay_step_switch": (C.c_int, [P, P, C.c_int, i32, i64, i64, f32, P, P, P, P, f32, i32,
                                         P, P, P, P, P, P, sz, P]),
+        "relay_step_sample": (C.c_int, [P, P, C.c_int, i32, i64, i64, f32, f32, i32, f32, P, P, P,
+                                        P, f32, i32, P, P, P, P, P, P, P, sz, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -85,7 +87,8 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_segment_reduce", "relay_stats_init", "relay_stats_init_tables",
            "relay_stats_words", "relay_stats_merge", "relay_stats_allreduce",
            "relay_nccl_unique_id", "relay_nccl_comm_init", "relay_nccl_comm_destroy",
-           "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate")
+           "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate",
+           "relay_step_sample")
 
 
 def _check(rc: int, what: str):
@@ -496,6 +499,40 @@ def step_switch(cs: CueSet, logits, state, hist, small_run=None, sampled=None, v
                                 _ptr(out["flag"]), _ptr(out["cue_id"]), _ptr(ws), ws.numel(),
                                 _stream(stream))
     _check(rc, "relay_step_switch")
+    return out
+
+
+# ------------------------------------------------------------------- N2
+def step_sample(cs: CueSet, logits, uniform, state, hist, small_run=None, temperature: float = 0.6,
+                top_k: int = 20, top_p: float = 0.95, vocab=None, inv_temperature: float = 1.0,
+                margin_gate: float = -1.0, max_small_segment: int = 0, ws=None, out=None,
+                stream=None):
+    """One decode step with the token drawn on the device (temperature / top-k /
+    top-p, inverse CDF with the caller's ``uniform`` [B] in [0, 1)), then the
+    switch on the drawn token.  ``out`` gains ``sampled`` (int32 [B])."""
+    import torch
+    _need_cuda(logits, uniform, state, hist, small_run)
+    B = logits.shape[0]
+    stride = logits.stride(0) if B > 1 else logits.shape[1]
+    vocab = logits.shape[1] if vocab is None else vocab
+    dev = logits.device
+    if ws is None:
+        ws = workspace(0, 0, B, dev, stream)
+    if out is None:
+        out = dict(margin=torch.empty(B, dtype=torch.float32, device=dev),
+                   top1=torch.empty(B, dtype=torch.int32, device=dev),
+                   top2=torch.empty(B, dtype=torch.int32, device=dev),
+                   sampled=torch.empty(B, dtype=torch.int32, device=dev),
+                   flag=torch.empty(B, dtype=torch.uint8, device=dev),
+                   cue_id=torch.empty(B, dtype=torch.int16, device=dev))
+    rc = _lib.relay_step_sample(cs.handle, _ptr(logits), _dtype_of(logits), B, vocab, stride,
+                                float(inv_temperature), float(temperature), int(top_k),
+                                float(top_p), _ptr(uniform), _ptr(state), _ptr(hist),
+                                _ptr(small_run), float(margin_gate), int(max_small_segment),
+                                _ptr(out["margin"]), _ptr(out.get("top1")), _ptr(out.get("top2")),
+                                _ptr(out["sampled"]), _ptr(out["flag"]), _ptr(out["cue_id"]),
+                                _ptr(ws), ws.numel(), _stream(stream))
+    _check(rc, "relay_step_sample")
     return out
 
 

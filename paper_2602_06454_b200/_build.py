@@ -10,8 +10,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "librelay.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in
-           ("margin_kernels.cu", "scan_kernels.cu", "relay_api.cu", "relay_comm.cu")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("relay_device.cuh", "relay_internal.h")] + \
+           ("margin_kernels.cu", "scan_kernels.cu", "sample_kernels.cu", "relay_api.cu",
+            "relay_comm.cu")]
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("relay_device.cuh", "relay_internal.h", "switch.cuh")] + \
           [os.path.join(REPO, "include", "relay.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

@@ -22,6 +22,7 @@
 
 #include "relay_device.cuh"
 #include "relay_internal.h"
+#include "switch.cuh"
 
 namespace relay {
 
@@ -61,43 +62,6 @@ __device__ __forceinline__ void consume_scalar(float x, int j, ThreadState& st, 
   st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
   rescale(st, x * c);
   st.acc[0] += ex2(fmaf(x, c, -st.mref));
-}
-
-template <class E>
-__device__ __forceinline__ void unpack16(const uint4& r, float (&f)[16 / E::SZ]) {
-  if constexpr (E::SZ == 4) {
-    f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
-    f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
-  } else {
-    E::unpack2(r.x, f[0], f[1]); E::unpack2(r.y, f[2], f[3]);
-    E::unpack2(r.z, f[4], f[5]); E::unpack2(r.w, f[6], f[7]);
-  }
-}
-
-// Maximum of one 16-byte vector (NaN-propagating).
-template <class E>
-__device__ __forceinline__ float vec_max(const uint4& r) {
-  if constexpr (E::SZ == 2) {
-    float lo, hi;
-    E::unpack2(E::pmax(E::pmax(r.x, r.y), E::pmax(r.z, r.w)), lo, hi);
-    return max_nan(lo, hi);
-  } else {
-    return max_nan(max_nan(__uint_as_float(r.x), __uint_as_float(r.y)),
-                   max_nan(__uint_as_float(r.z), __uint_as_float(r.w)));
-  }
-}
-
-// Element k (dynamic, < 16 / SZ) of a 16-byte vector, without local memory.
-template <class E>
-__device__ __forceinline__ float elem_at(const uint4& r, int k) {
-  if constexpr (E::SZ == 2) {
-    const uint32_t w = (k & 4) ? ((k & 2) ? r.w : r.z) : ((k & 2) ? r.y : r.x);
-    float lo, hi;
-    E::unpack2(w, lo, hi);
-    return (k & 1) ? hi : lo;
-  } else {
-    return __uint_as_float((k & 2) ? ((k & 1) ? r.w : r.z) : ((k & 1) ? r.y : r.x));
-  }
 }
 
 // Maxima of two disjoint halves of the UV vectors' elements (NaN-propagating):
@@ -288,6 +252,11 @@ struct RowsArgs {
   int max_seg;
   uint8_t* flag;
   int16_t* cue_id;
+  // fused-sampler margin pass (relay_step_sample, N2): per row a lower bound
+  // on the topk-th largest logit; the switch is left to the sampling kernel
+  float* thk;     // [n_rows] or NULL
+  int topk;       // 0 = off
+  int keep_l2;    // stream the rows with L2 evict_last (read again from L2)
 };
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
@@ -304,93 +273,8 @@ __device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
   return old;
 }
 
-struct SmemCue {
-  int tok[kMaxPat * kMaxLen];
-  int len[kMaxPat];
-  int cue[kMaxPat];
-};
-
-// Runtime switching (§4.3, fig:mechanism P:209-216) for one
-// sequence, by one warp: lanes test the (length-sorted) patterns as suffixes of
-// hist ++ tok in parallel; the lowest matching lane is the longest pattern.
-// The per-sequence switch inputs, loaded by the epilogue warp before it waits
-// for the item (so the loads are off the critical path): lane i < 7 holds
-// hist[i]; every lane holds state, small_run and the sampled token.
-struct SwitchIn {
-  int hist_lane;
-  int state;
-  int small_run;
-  int sampled;
-};
-
 __device__ __forceinline__ SwitchIn load_switch_in(const RowsArgs& a, long long r) {
-  const int lane = threadIdx.x & 31;
-  SwitchIn in;
-  in.hist_lane = lane < kHist ? a.hist[r * kHist + lane] : -1;
-  in.state = a.state[r];
-  in.small_run = a.small_run ? a.small_run[r] : 0;
-  in.sampled = a.sampled ? a.sampled[r] : -1;
-  return in;
-}
-
-__device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float m, const SwitchIn& in,
-                            uint8_t* state_p, int* hist, int* small_run_p, float gate, int max_seg,
-                            uint8_t* flag_out, int16_t* cue_out) {
-  const int lane = threadIdx.x & 31;
-  const uint8_t state = static_cast<uint8_t>(in.state);
-  const bool valid = tok >= 0 && tok < cs.vocab && !(state & 2);
-  // seq[0..6] = hist (oldest first), seq[7] = tok; lane i < 8 holds seq[i]
-  int mine = in.hist_lane;
-  if (lane == kHist) mine = tok;
-  int best = -1;
-  if (valid && tok != cs.think_end && (state & 1) == 0) {
-    for (int base = 0; base < cs.n_pat; base += 32) {
-      const int p = base + lane;
-      bool ok = p < cs.n_pat;
-      const int len = ok ? sc.len[p] : 0;
-#pragma unroll
-      for (int i = 0; i < kMaxLen; i++) {
-        const int v = __shfl_sync(kFull, mine, i);
-        const int k = i - (kMaxLen - len);  // pattern position of seq[i]
-        if (ok && k >= 0 && !elem_ok(cs, v, sc.tok[p * kMaxLen + k])) ok = false;
-      }
-      const unsigned b = __ballot_sync(kFull, ok);
-      if (b) { best = base + __ffs(b) - 1; break; }
-    }
-  }
-  if (lane != 0) return;
-  int cue = -1, flag = 0;
-  uint8_t st = state;
-  if (valid) {
-    const int sr = in.small_run;
-    bool clear = false;
-    if (tok == cs.think_end) {
-      flag = 3; st = 3; clear = true;
-    } else if ((state & 1) == 0) {
-      if (best >= 0 && !(gate >= 0.0f && m < gate)) {
-        flag = 1; cue = sc.cue[best]; st = 1; clear = true;
-      } else {
-        for (int k = 0; k < kHist - 1; k++) hist[k] = hist[k + 1];
-        hist[kHist - 1] = tok;
-      }
-    } else {
-      const bool term = (cs.term_tab[tok >> 5] >> (tok & 31)) & 1u;
-      if (term) {
-        flag = 2; st = 0; clear = true;
-      } else if (max_seg > 0 && sr + 1 >= max_seg) {
-        flag = 4; st = 0; clear = true;
-      } else if (small_run_p) {
-        *small_run_p = sr + 1;
-      }
-    }
-    if (clear) {
-      for (int k = 0; k < kHist; k++) hist[k] = -1;
-      if (small_run_p) *small_run_p = 0;
-    }
-    *state_p = st;
-  }
-  *flag_out = static_cast<uint8_t>(flag);
-  *cue_out = static_cast<int16_t>(cue);
+  return load_switch_in(a.hist, a.state, a.small_run, a.sampled, r);
 }
 
 // Warp-level finish of row r from its merged partial (lane 0 writes).
@@ -431,6 +315,7 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
     if (a.status) a.status[r] = static_cast<uint8_t>(o.status);
   }
   if constexpr (MODE == kModeStep) {
+    if (a.thk) return;  // relay_step_sample: the sampling kernel runs the switch
     const int tok = a.sampled ? in.sampled : o.i1;
     switch_warp(cs, sc, tok, o.margin, in, a.state + r, a.hist + r * kHist,
                 a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r, a.cue_id + r);
@@ -575,6 +460,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   __shared__ __align__(8) uint64_t ifull[kSlots];
   __shared__ long long s_item[kSlots];
   __shared__ int s_theta[kSlots];
+  __shared__ float s_thk[kSlots][NCW];
   __shared__ Partial s_red[kSlots][NRED];
   __shared__ SmemCue sc;
 
@@ -618,7 +504,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   if (warp == NCW) {
     // ------------------------------------------------ producer warp
     if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
+      const uint64_t pol = a.keep_l2 ? policy_evict_last() : policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
 #ifdef RELAY_TRACE
@@ -671,12 +557,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   if (warp == NCW + 1) {
     // ------------------------------------------------ epilogue warp
     if constexpr (MODE == kModeStep) {  // the switch patterns, for this warp only
-      for (int i = lane; i < cs.n_pat * kMaxLen; i += 32) sc.tok[i] = cs.pat_tok[i];
-      for (int i = lane; i < cs.n_pat; i += 32) {
-        sc.len[i] = cs.pat_len[i];
-        sc.cue[i] = cs.pat_cue[i];
-      }
-      __syncwarp();
+      load_smem_cue(cs, sc);
       pdl_wait();
     }
     ItemIter iter;
@@ -696,6 +577,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       // below reads the row's top-1 on all lanes)
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) q = partial_merge(q, shfl_xor_partial(q, off));
+      float thk = INFINITY;
+      if (a.thk) {
+#pragma unroll
+        for (int w = 0; w < NCW; w++) thk = fminf(thk, s_thk[slot][w]);
+      }
       if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
       mbar_arrive(rempty_s + 8 * slot);
       if (item.nparts == 1) {
@@ -705,6 +591,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           S = warp_sum(exact_sum_thread<E>(row, a.vocab, q.t.v1, c, lane, 32));
           exact = true;
         }
+        if (a.thk && lane == 0) a.thk[r] = thk;
         finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in);
         continue;
       }
@@ -776,7 +663,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     ThreadState st;
     state_init(st);
     float theta_w = -INFINITY;  // warp-local lower bound of the row's 2nd-best
-    if (tid < g.head) consume_scalar(E::load1(row + j0 + tid), j0 + tid, st, c);
+    float tmax = -INFINITY;     // this thread's maximum (relay_step_sample's bound)
+    if (tid < g.head) {
+      const float x = E::load1(row + j0 + tid);
+      consume_scalar(x, j0 + tid, st, c);
+      if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, x);
+    }
     for (int off = 0; off < g.body; off += SB) {
       const int bytes = min(SB, g.body - off);
       const int jb = j0 + g.head + off / E::SZ;
@@ -805,20 +697,43 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         }
         const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         consume_stage<E, UV>(raw, h, jb + tid * VEC, NCT * VEC, st, c, theta, slow);
+        if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h.x, h.y));
         if (tid == 0 && it == 1 && off == 0) TRACE(14);
       } else {
         const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
         const int nvec = bytes / 16;
         for (int v = tid; v < nvec; v += NCT) {
           const uint4 raw1[1] = {lds128(buf + v * 16)};
-          consume_stage<E, 1>(raw1, stage_max2<E, 1>(raw1), jb + v * VEC, 0, st, c, theta, slow);
+          const float2 h1 = stage_max2<E, 1>(raw1);
+          consume_stage<E, 1>(raw1, h1, jb + v * VEC, 0, st, c, theta, slow);
+          if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h1.x, h1.y));
         }
         mbar_arrive(empty_s + 8 * stage);
       }
       if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
-    if (tid < j1 - g.tail) consume_scalar(E::load1(row + g.tail + tid), g.tail + tid, st, c);
+    if (tid < j1 - g.tail) {
+      const float x = E::load1(row + g.tail + tid);
+      consume_scalar(x, g.tail + tid, st, c);
+      if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, x);
+    }
+    if (a.topk > 0) {
+      // N2: the warp's kw-th largest thread maximum, kw = ceil(topk / NCW);
+      // the minimum over warps bounds the row's topk-th largest value from
+      // below (NCW * kw >= topk distinct elements are at least as large)
+      const int kw = (a.topk + NCW - 1) / NCW;
+      float v = tmax, kth = -INFINITY;
+      for (int i = 0; i < kw; i++) {
+        float m = v;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, off));
+        kth = m;
+        const unsigned holders = __ballot_sync(kFull, v == m);
+        if (lane == __ffs(holders) - 1) v = -INFINITY;
+      }
+      if (lane == 0) s_thk[slot][warp] = kth;
+    }
     // hand the warp's 8 partials (after two shuffle rounds) to the epilogue warp
     Partial p = thread_partial(st);
 #pragma unroll
@@ -983,6 +898,22 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
   }
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
   a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
+  return launch_rows<kModeStep>(dt, a, cs, st);
+}
+
+cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
+                             long long stride, float iota, uint8_t* state, int* hist, int* small_run,
+                             float gate, int max_seg, float* margin, int* top1, int* top2,
+                             const StepWs& ws, int topk, cudaStream_t st) {
+  if (batch <= 0) return cudaSuccess;
+  RowsArgs a{};
+  a.logits = logits; a.n_rows = batch; a.vocab = vocab; a.stride = stride;
+  a.c = iota * kLog2e; a.iota = iota;
+  a.margin = margin; a.top1 = top1; a.top2 = top2; a.status = ws.status;
+  a.counter = ws.counter; a.part = ws.part; a.work = ws.work;
+  a.flat = 0;  // whole rows: the bound needs every thread maximum of the row
+  a.state = state; a.hist = hist; a.small_run = small_run; a.gate = gate; a.max_seg = max_seg;
+  a.thk = ws.thk; a.topk = topk; a.keep_l2 = 1;
   return launch_rows<kModeStep>(dt, a, cs, st);
 }
 

@@ -94,6 +94,8 @@ StepWs step_ws_layout(void* base, int batch) {
   w.counter = reinterpret_cast<int*>(take(sizeof(int) * (batch + 1)));
   w.part = reinterpret_cast<float*>(take(sizeof(float) * 8 * kMaxSplit * (static_cast<size_t>(batch) + 1)));  // kPartWords = 8
   w.work = reinterpret_cast<int*>(take(sizeof(int) * 4));
+  w.thk = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
+  w.status = reinterpret_cast<uint8_t*>(take(static_cast<size_t>(batch) + 1));
   w.bytes = off;
   return w;
 }
@@ -512,6 +514,40 @@ relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dt
                                         max_small_segment, margin, top1, top2, flag, cue_id, w,
                                         reinterpret_cast<cudaStream_t>(stream)),
                      "relay_step_switch launch");
+}
+
+relay_status_t relay_step_sample(relay_cueset_t cs, const void* logits, relay_dtype_t dt, int32_t batch,
+                                 int64_t vocab, int64_t row_stride, float inv_temperature, float temperature,
+                                 int32_t top_k, float top_p, const float* uniform, uint8_t* state,
+                                 int32_t* hist, int32_t* small_run, float margin_gate, int32_t max_small_segment,
+                                 float* margin, int32_t* top1, int32_t* top2, int32_t* sampled, uint8_t* flag,
+                                 int16_t* cue_id, void* ws, size_t ws_bytes, relay_stream_t stream) {
+  if (!cs) return fail(RELAY_ERR_INVALID, "cs is NULL");
+  if (!valid_dtype(dt)) return fail(RELAY_ERR_INVALID, "unknown dtype");
+  if (vocab < 2 || vocab > 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "vocab out of range");
+  if (vocab != cs->dev.vocab) return fail(RELAY_ERR_INVALID, "vocab differs from the cue set's");
+  if (row_stride < vocab) return fail(RELAY_ERR_INVALID, "row_stride < vocab");
+  if (batch < 0) return fail(RELAY_ERR_INVALID, "batch < 0");
+  if (static_cast<long long>(batch) * vocab >= (1LL << 51)) return fail(RELAY_ERR_INVALID, "batch * vocab must be < 2^51");
+  if (!(inv_temperature > 0.0f) || !std::isfinite(inv_temperature))
+    return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
+  if (!(temperature > 0.0f) || !std::isfinite(temperature))
+    return fail(RELAY_ERR_INVALID, "temperature must be finite and > 0");
+  if (top_k < 1 || top_k > kMaxTopK) return fail(RELAY_ERR_INVALID, "top_k must be in [1, %d]", kMaxTopK);
+  if (!(top_p > 0.0f && top_p <= 1.0f)) return fail(RELAY_ERR_INVALID, "top_p must be in (0, 1]");
+  if (max_small_segment < 0) return fail(RELAY_ERR_INVALID, "max_small_segment < 0");
+  if (max_small_segment > 0 && !small_run) return fail(RELAY_ERR_INVALID, "small_run required with a budget");
+  if (batch == 0) return RELAY_OK;
+  if (!logits || !state || !hist || !margin || !flag || !cue_id || !uniform || !sampled)
+    return fail(RELAY_ERR_INVALID, "logits/state/hist/margin/flag/cue_id/uniform/sampled are required");
+  StepWs w = step_ws_layout(ws, batch);
+  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  const int k = static_cast<int>(top_k < vocab ? top_k : vocab);
+  return cuda_status(launch_step_sample(cs->dev, logits, static_cast<int>(dt), batch, static_cast<int>(vocab),
+                                        row_stride, inv_temperature, temperature, k, top_p, uniform, state,
+                                        hist, small_run, margin_gate, max_small_segment, margin, top1, top2,
+                                        sampled, flag, cue_id, w, reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_step_sample launch");
 }
 
 }  // extern "C"

@@ -316,8 +316,62 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// L2 evict_last: the row stays in L2 for a second, L2-resident pass (N2).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 16-byte global load with an L2 cache-eviction policy.
+__device__ __forceinline__ uint4 ldg_hint(const uint4* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ------------------------------------------ 16-byte vector helpers
+template <class E>
+__device__ __forceinline__ void unpack16(const uint4& r, float (&f)[16 / E::SZ]) {
+  if constexpr (E::SZ == 4) {
+    f[0] = __uint_as_float(r.x); f[1] = __uint_as_float(r.y);
+    f[2] = __uint_as_float(r.z); f[3] = __uint_as_float(r.w);
+  } else {
+    E::unpack2(r.x, f[0], f[1]); E::unpack2(r.y, f[2], f[3]);
+    E::unpack2(r.z, f[4], f[5]); E::unpack2(r.w, f[6], f[7]);
+  }
+}
+
+// Maximum of one 16-byte vector (NaN-propagating).
+template <class E>
+__device__ __forceinline__ float vec_max(const uint4& r) {
+  if constexpr (E::SZ == 2) {
+    float lo, hi;
+    E::unpack2(E::pmax(E::pmax(r.x, r.y), E::pmax(r.z, r.w)), lo, hi);
+    return max_nan(lo, hi);
+  } else {
+    return max_nan(max_nan(__uint_as_float(r.x), __uint_as_float(r.y)),
+                   max_nan(__uint_as_float(r.z), __uint_as_float(r.w)));
+  }
+}
+
+// Element k (dynamic, < 16 / SZ) of a 16-byte vector, without local memory.
+template <class E>
+__device__ __forceinline__ float elem_at(const uint4& r, int k) {
+  if constexpr (E::SZ == 2) {
+    const uint32_t w = (k & 4) ? ((k & 2) ? r.w : r.z) : ((k & 2) ? r.y : r.x);
+    float lo, hi;
+    E::unpack2(w, lo, hi);
+    return (k & 1) ? hi : lo;
+  } else {
+    return __uint_as_float((k & 2) ? ((k & 1) ? r.w : r.z) : ((k & 1) ? r.y : r.x));
+  }
 }
 
 // Programmatic dependent launch (sm_90+): let the next kernel in the stream

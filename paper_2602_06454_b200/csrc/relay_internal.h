@@ -12,6 +12,7 @@ constexpr int kMaxLen = 8;        // RELAY_MAX_CUE_LEN
 constexpr int kMaxPat = 64;       // RELAY_MAX_PATTERNS
 constexpr int kMaxCues = 64;      // RELAY_MAX_CUES
 constexpr int kMaxClasses = 8;    // RELAY_MAX_CLASSES
+constexpr int kMaxTopK = 64;      // RELAY_MAX_TOP_K
 constexpr int kStatFields = 8;    // RELAY_STAT_FIELDS
 constexpr int kTile = 2048;       // positions per CTA in the scan kernels
 constexpr int kScanThreads = 256; // kTile / 8 consecutive positions per thread
@@ -76,6 +77,8 @@ struct StepWs {
   int* counter;        // [batch] (zero between launches)
   float* part;         // [batch][nsplit][8] partial (v1, v2, i1, i2, m, s, huge, pad)
   int* work;           // [2] chunk counter, CTAs done (zero between launches)
+  float* thk;          // [batch] relay_step_sample: K4's top-k bound per row
+  uint8_t* status;     // [batch] relay_step_sample: K4's row status
   size_t bytes;
 };
 constexpr int kMaxSplit = 32;
@@ -119,5 +122,18 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
                                int* hist, int* small_run, float gate, int max_seg, float* margin,
                                int* top1, int* top2, uint8_t* flag, int16_t* cue_id,
                                const StepWs& ws, cudaStream_t st);
+
+// relay_step_sample: K4 margin pass (rows kept in L2, top-k bound per row) ...
+cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
+                             long long stride, float iota, uint8_t* state, int* hist, int* small_run,
+                             float gate, int max_seg, float* margin, int* top1, int* top2,
+                             const StepWs& ws, int topk, cudaStream_t st);
+// ... then K5: exact top-k from L2, temperature / top-p, inverse-CDF draw, switch
+cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
+                               long long stride, float iota, float temperature, int topk, float topp,
+                               const float* uniform, uint8_t* state, int* hist, int* small_run,
+                               float gate, int max_seg, float* margin, int* top1, int* top2,
+                               int* sampled, uint8_t* flag, int16_t* cue_id, const StepWs& ws,
+                               cudaStream_t st);
 
 }  // namespace relay

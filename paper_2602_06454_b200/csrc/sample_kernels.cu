@@ -1,0 +1,328 @@
+// sample_kernels.cu — K5, the second half of relay_step_sample (N2: the
+// margin fused with the decode-side sampler).
+//
+// The paper samples every model at temperature 0.6 with top-p 0.95 (and top-k
+// 20 for Qwen3).  K4 streams each row once from HBM (margin, top-2,
+// and a lower bound thk on the row's top_k-th largest logit), keeping the rows
+// in L2 (evict_last); K5 re-reads each row from L2, collects the logits >= thk
+// (a handful per row), selects the exact top-k in (value desc, index asc)
+// order, applies temperature and top-p, draws the token by inverse CDF with the
+// caller's uniform (reading R20), and runs the decode-step switch (H8) on the
+// drawn token.  So the row crosses HBM once for both the margin and the sample.
+#include <cstdint>
+
+#include "relay_device.cuh"
+#include "relay_internal.h"
+#include "switch.cuh"
+
+namespace relay {
+
+constexpr int kSampleThreads = 512;
+constexpr int kCandCap = 1024;  // candidates held in shared memory; more -> exact global fallback
+
+struct SampleArgs {
+  const void* logits;
+  long long n_rows;
+  int vocab;
+  long long stride;
+  const float* thk;         // [n_rows] K4's lower bound on the top_k-th largest logit
+  const uint8_t* status;    // [n_rows] K4's row status (0 = sample)
+  const float* margin;      // [n_rows] K4's margins (the switch's optional gate)
+  float s_c;                // log2(e) / temperature
+  int topk;                 // 1..kMaxTopK, <= vocab
+  float topp;               // (0, 1]
+  const float* uniform;     // [n_rows] in [0, 1)
+  int* sampled;             // [n_rows] out
+  uint8_t* state;
+  int* hist;
+  int* small_run;
+  float gate;
+  int max_seg;
+  uint8_t* flag;
+  int16_t* cue_id;
+};
+
+// (v, i) ranks before (bv, bi): value descending, index ascending.
+__device__ __forceinline__ bool ranks_before(float v, int i, float bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+__device__ __forceinline__ void warp_best(float& bv, int& bi) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ov = __shfl_xor_sync(kFull, bv, off);
+    const int oi = __shfl_xor_sync(kFull, bi, off);
+    if (ranks_before(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+  }
+}
+
+// -inf entries are never candidates: their probability is 0, so they can
+// neither be drawn nor move the top-p cut (R20).
+__device__ __forceinline__ void push_candidate(float v, int j, float th, bool strict, float* s_cv,
+                                               int* s_ci, int* s_cnt) {
+  if ((strict ? v > th : v >= th) && v > -INFINITY) {  // false for NaN
+    const int p = atomicAdd(s_cnt, 1);
+    if (p < kCandCap) { s_cv[p] = v; s_ci[p] = j; }
+  }
+}
+
+// Every finite logit >= th (> th when strict) of one row into the candidate
+// list (block-wide).
+template <class E>
+__device__ void collect_candidates(const typename E::T* row, int vocab, float th, bool strict,
+                                   float* s_cv, int* s_ci, int* s_cnt) {
+  constexpr int VEC = 16 / E::SZ;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
+  int head = static_cast<int>(((16 - (addr & 15)) & 15) / E::SZ);
+  if (head > vocab) head = vocab;
+  const int nvec = (vocab - head) / VEC;
+  const int tail = head + nvec * VEC;
+  for (int j = threadIdx.x; j < head; j += blockDim.x)
+    push_candidate(E::load1(row + j), j, th, strict, s_cv, s_ci, s_cnt);
+  for (int j = tail + threadIdx.x; j < vocab; j += blockDim.x)
+    push_candidate(E::load1(row + j), j, th, strict, s_cv, s_ci, s_cnt);
+  const uint4* vp = reinterpret_cast<const uint4*>(row + head);
+  const uint64_t pol = policy_evict_first();  // the row's last use: leave L2
+  constexpr int U = 8;                        // loads in flight per thread
+  for (int v0 = threadIdx.x; v0 < nvec; v0 += U * blockDim.x) {
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int v = v0 + u * blockDim.x;
+      x[u] = v < nvec ? ldg_hint(vp + v, pol) : make_uint4(0xff800000u, 0xff800000u, 0xff800000u,
+                                                            0xff800000u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int v = v0 + u * blockDim.x;
+      if (v < nvec && vec_max<E>(x[u]) >= th) {
+        float f[VEC];
+        unpack16<E>(x[u], f);
+#pragma unroll
+        for (int k = 0; k < VEC; k++) push_candidate(f[k], head + v * VEC + k, th, strict, s_cv, s_ci, s_cnt);
+      }
+    }
+  }
+}
+
+// The first `want` entries of the candidate list in (value desc, index asc)
+// order into s_topv/s_topi: every thread ranks its candidates by counting
+// the entries that rank before them (ranks are distinct: indices are).
+// Returns how many exist (min(want, n)).
+__device__ int rank_list(int want, int n, const float* s_cv, const int* s_ci, float* s_topv,
+                         int* s_topi, int* s_k) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const float v = s_cv[e];
+    const int i = s_ci[e];
+    int rank = 0;
+    for (int f = 0; f < n && rank < want; f++) rank += ranks_before(s_cv[f], s_ci[f], v, i);
+    if (rank < want) { s_topv[rank] = v; s_topi[rank] = i; }
+  }
+  if (threadIdx.x == 0) *s_k = n < want ? n : want;
+  __syncthreads();
+  return *s_k;
+}
+
+// The exact top-k of a row whose candidate list (entries >= thk) overflowed,
+// e.g. a constant row.  theta = the k-th largest value in the (partial) list
+// is a value of k real entries, so the row's k-th largest is >= theta; collect
+// the entries > theta: on overflow raise theta again (strictly), else they are
+// all of them and, if fewer than k, the rest of the top-k are the
+// lowest-index entries equal to theta (collected in index order).
+template <class E>
+__device__ int refine_topk(const typename E::T* row, int vocab, int topk, float* s_cv, int* s_ci,
+                           int* s_cnt, float* s_topv, int* s_topi, int* s_k, int* s_scan) {
+  float theta;
+  for (;;) {
+    if (rank_list(topk, kCandCap, s_cv, s_ci, s_topv, s_topi, s_k) < topk) return *s_k;
+    theta = s_topv[topk - 1];
+    __syncthreads();
+    if (threadIdx.x == 0) *s_cnt = 0;
+    __syncthreads();
+    collect_candidates<E>(row, vocab, theta, true, s_cv, s_ci, s_cnt);
+    __syncthreads();
+    if (*s_cnt <= kCandCap) break;
+  }
+  const int c = *s_cnt;
+  if (c >= topk) return rank_list(topk, c, s_cv, s_ci, s_topv, s_topi, s_k);
+  // ties at theta in index order: thread t scans a contiguous range of
+  // 16-byte vectors (plus the scalar head / tail, owned by threads 0 / last)
+  constexpr int VEC = 16 / E::SZ;
+  const int need = topk - c;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
+  int head = static_cast<int>(((16 - (addr & 15)) & 15) / E::SZ);
+  if (head > vocab) head = vocab;
+  const int nvec = (vocab - head) / VEC;
+  const int tail = head + nvec * VEC;
+  const int per = (nvec + blockDim.x - 1) / blockDim.x;
+  const int v0 = threadIdx.x * per, v1 = min(nvec, v0 + per);
+  const uint4* vp = reinterpret_cast<const uint4*>(row + head);
+  const bool first = threadIdx.x == 0, last = threadIdx.x == blockDim.x - 1;
+  int mine = 0;
+  if (first)
+    for (int j = 0; j < head; j++) mine += E::load1(row + j) == theta;
+  for (int v = v0; v < v1; v++) {
+    float f[VEC];
+    unpack16<E>(vp[v], f);
+#pragma unroll
+    for (int k = 0; k < VEC; k++) mine += f[k] == theta;
+  }
+  if (last)
+    for (int j = tail; j < vocab; j++) mine += E::load1(row + j) == theta;
+  s_scan[threadIdx.x] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive prefix over the block (tiny)
+    int run = 0;
+    for (int t = 0; t < static_cast<int>(blockDim.x); t++) {
+      const int m = s_scan[t];
+      s_scan[t] = run;
+      run += m;
+    }
+  }
+  __syncthreads();
+  int rank = s_scan[threadIdx.x];
+  auto take = [&](float x, int j) {
+    if (rank < need && x == theta) {
+      s_cv[c + rank] = theta;
+      s_ci[c + rank] = j;
+      rank++;
+    }
+  };
+  if (first)
+    for (int j = 0; j < head; j++) take(E::load1(row + j), j);
+  for (int v = v0; v < v1 && rank < need; v++) {
+    float f[VEC];
+    unpack16<E>(vp[v], f);
+#pragma unroll
+    for (int k = 0; k < VEC; k++) take(f[k], head + v * VEC + k);
+  }
+  if (last)
+    for (int j = tail; j < vocab; j++) take(E::load1(row + j), j);
+  __syncthreads();
+  return rank_list(topk, c + need, s_cv, s_ci, s_topv, s_topi, s_k);
+}
+
+// The drawn token (one warp; every lane returns it) from the top-K list, R20:
+// p_k = 2^((v_k - v_0) log2(e) / T); keep the first L (higher-ranked mass below
+// top_p of the total, at least one); inverse CDF with the row's uniform.  Lane
+// l holds ranks l and l + 32; prefix sums by warp scans, in rank order.
+__device__ int draw_warp(const SampleArgs& a, float u, int K, const float* s_topv,
+                         const int* s_topi) {
+  const int lane = threadIdx.x & 31;
+  const float v0 = s_topv[0];
+  const float p0 = lane < K ? ex2((s_topv[lane] - v0) * a.s_c) : 0.0f;
+  const float p1 = lane + 32 < K ? ex2((s_topv[lane + 32] - v0) * a.s_c) : 0.0f;
+  float c0 = p0, c1 = p1;  // inclusive prefix sums within each half
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float t0 = __shfl_up_sync(kFull, c0, off);
+    const float t1 = __shfl_up_sync(kFull, c1, off);
+    if (lane >= off) { c0 += t0; c1 += t1; }
+  }
+  const float half0 = __shfl_sync(kFull, c0, 31);
+  c1 += half0;                                   // ranks 32..63 continue the sum
+  const float total = __shfl_sync(kFull, c1, 31);
+  // kept iff the mass of the higher ranks (exclusive prefix) is below top_p * total
+  const float lim = a.topp * total;
+  const unsigned keep0 = __ballot_sync(kFull, lane < K && (lane == 0 || c0 - p0 < lim));
+  const unsigned keep1 = __ballot_sync(kFull, lane + 32 < K && c1 - p1 < lim);
+  const int L = __popc(keep0) + __popc(keep1);   // kept ranks form a prefix
+  const float kept = L <= 32 ? __shfl_sync(kFull, c0, L - 1) : __shfl_sync(kFull, c1, L - 33);
+  const float target = u * kept;
+  const unsigned hit0 = __ballot_sync(kFull, lane < L && c0 > target);
+  const unsigned hit1 = __ballot_sync(kFull, lane + 32 < L && c1 > target);
+  const int k = hit0 ? __ffs(hit0) - 1 : (hit1 ? 32 + __ffs(hit1) - 1 : L - 1);
+  return s_topi[k];
+}
+
+template <class E>
+__global__ void __launch_bounds__(kSampleThreads) sample_switch_kernel(SampleArgs a, CueDev cs) {
+  using T = typename E::T;
+  __shared__ float s_cv[kCandCap];
+  __shared__ int s_ci[kCandCap];
+  __shared__ float s_topv[kMaxTopK];
+  __shared__ int s_topi[kMaxTopK];
+  __shared__ int s_scan[kSampleThreads];
+  __shared__ int s_cnt, s_k;
+  __shared__ SmemCue sc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) load_smem_cue(cs, sc);  // immutable cue set: before the dependency wait
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();  // K4's outputs (thk, status, margin) and the switch state
+  for (long long r = blockIdx.x; r < a.n_rows; r += gridDim.x) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const T* row = static_cast<const T*>(a.logits) + r * a.stride;
+    // warp 0's per-row inputs are fetched before the scan so that their
+    // latency hides under it; the scan itself does not wait for the status
+    SwitchIn in{};
+    float u = 0.0f, m = 0.0f;
+    if (warp == 0) {
+      in = load_switch_in(a.hist, a.state, a.small_run, nullptr, r);
+      u = a.uniform[r];
+      m = a.margin[r];
+    }
+    collect_candidates<E>(row, a.vocab, a.thk[r], false, s_cv, s_ci, &s_cnt);
+    __syncthreads();
+    const int st = a.status[r];   // uniform: every thread takes the same branches
+    int K = 0;
+    if (st == 0) {
+      K = (s_cnt <= kCandCap)
+              ? rank_list(a.topk, s_cnt, s_cv, s_ci, s_topv, s_topi, &s_k)
+              : refine_topk<E>(row, a.vocab, a.topk, s_cv, s_ci, &s_cnt, s_topv, s_topi, &s_k, s_scan);
+    }
+    if (warp == 0) {
+      const int tok = (st == 0 && K > 0) ? draw_warp(a, u, K, s_topv, s_topi) : -1;
+      if (lane == 0) a.sampled[r] = tok;
+      switch_warp(cs, sc, tok, m, in, a.state + r, a.hist + r * kHist,
+                  a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r,
+                  a.cue_id + r);
+    }
+    __syncthreads();
+  }
+}
+
+template <class E>
+static cudaError_t launch_sample_t(const SampleArgs& a, const CueDev& cs, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long grid = a.n_rows;
+  if (grid > 4LL * sms) grid = 4LL * sms;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kSampleThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sample_switch_kernel<E>, a, cs);
+}
+
+cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
+                               long long stride, float iota, float temperature, int topk, float topp,
+                               const float* uniform, uint8_t* state, int* hist, int* small_run,
+                               float gate, int max_seg, float* margin, int* top1, int* top2,
+                               int* sampled, uint8_t* flag, int16_t* cue_id, const StepWs& ws,
+                               cudaStream_t st) {
+  if (batch <= 0) return cudaSuccess;
+  cudaError_t e = launch_step_rows(cs, logits, dt, batch, vocab, stride, iota, state, hist, small_run,
+                                   gate, max_seg, margin, top1, top2, ws, topk, st);
+  if (e != cudaSuccess) return e;
+  SampleArgs a{};
+  a.logits = logits; a.n_rows = batch; a.vocab = vocab; a.stride = stride;
+  a.thk = ws.thk; a.status = ws.status; a.margin = margin;
+  a.s_c = kLog2e / temperature; a.topk = topk; a.topp = topp; a.uniform = uniform;
+  a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
+  a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
+  switch (dt) {
+    case 0: return launch_sample_t<EBf16>(a, cs, st);
+    case 1: return launch_sample_t<EF16>(a, cs, st);
+    default: return launch_sample_t<EF32>(a, cs, st);
+  }
+}
+
+}  // namespace relay

@@ -932,3 +932,131 @@ def test_step_switch_class_patterns(relay, greedy):
         np.testing.assert_array_equal(d_hist[b].cpu().numpy(), hh)
         n_l2s += f == 1
     assert n_l2s > 50
+
+
+# ---------------------------------------------------------------- N2 sampler
+def _oracle_sample_tolerant(host_rows, dtype, vocab, u, got, T, k, p):
+    """Oracle draws; where the kernel's fp32 draw differs, it must be the
+    oracle's draw for a uniform or top_p within 1e-5 (a CDF edge)."""
+    want = oracle.sample_rows(host_rows, u, dtype=dtype, vocab=vocab, temperature=T, top_k=k, top_p=p)
+    bad = np.flatnonzero(want != got)
+    for b in bad:
+        alts = set()
+        for du in (-1e-5, 1e-5):
+            for dp in (0.0, -1e-5, 1e-5):
+                uu = min(max(u[b] + du, 0.0), 1 - 1e-12)
+                pp = min(max(p + dp, 1e-9), 1.0)
+                alts.add(int(oracle.sample_rows(host_rows[b:b + 1], [uu], dtype=dtype, vocab=vocab,
+                                                temperature=T, top_k=k, top_p=pp)[0]))
+        assert int(got[b]) in alts, (b, int(got[b]), int(want[b]), alts)
+    return want, bad.size
+
+
+@pytest.mark.parametrize("B,vocab,dtype,T,k,p", [
+    (256, 152064, "bf16", 0.6, 20, 0.95),     # configs[2] with the paper's Qwen3 sampling
+    (64, 151936, "bf16", 0.6, 64, 1.0),
+    (37, 5003, "f16", 1.0, 1, 0.95),
+    (50, 32000, "f32", 0.6, 20, 0.5),
+    (9, 40, "f32", 0.8, 64, 0.9),             # vocab < top_k
+])
+def test_step_sample(relay, B, vocab, dtype, T, k, p):
+    """N2: the drawn token matches the oracle sampler (R20); margins/indices as
+    K1/K4; the switch runs on the drawn token."""
+    if vocab > 4096:
+        h, cs = _cs_pair(relay, vocab, 4, 8, 3, seed=71)
+    else:                                   # tiny vocabulary: a tiny cue set
+        term = np.zeros(vocab, np.uint8)
+        term[3] = 1
+        h = synth.CueSet(np.array([1, 2, 5], np.int32), np.array([0, 2, 3], np.int32),
+                         np.array([0, 1], np.int32), 2, vocab, term, vocab - 1, [(1, 2), (5,)])
+        cs = relay.CueSet.from_synth(h)
+    rng = np.random.default_rng(72)
+    L = synth.make_logits(B, vocab, dtype, seed=73, device=DEV)
+    host = synth.host_rows(L, dtype)
+    u = rng.random(B).astype(np.float32)
+    state = np.zeros(B, np.uint8)
+    hist = np.full((B, 7), -1, np.int32)
+    d_state = torch.as_tensor(state, device=DEV)
+    d_hist = torch.as_tensor(hist, device=DEV)
+    out = relay.step_sample(cs, L, torch.as_tensor(u, device=DEV), d_state, d_hist, temperature=T,
+                            top_k=k, top_p=p)
+    torch.cuda.synchronize()
+    ref = oracle.margin_rows(host, dtype=dtype, vocab=vocab)
+    np.testing.assert_array_equal(out["top1"].cpu().numpy(), ref["top1"])
+    np.testing.assert_array_equal(out["top2"].cpu().numpy(), ref["top2"])
+    ok = ref["status"] == 0
+    assert np.abs(out["margin"].cpu().numpy()[ok] - ref["margin"][ok]).max() < TOL
+    got = out["sampled"].cpu().numpy()
+    want, n_edge = _oracle_sample_tolerant(host, dtype, vocab, u.astype(np.float64), got, T, k, p)
+    assert n_edge <= max(1, B // 50)
+    assert (got[~ok] == -1).all()
+    if k == 1:
+        np.testing.assert_array_equal(got[ok], ref["top1"][ok])
+    # the switch saw the drawn token
+    flags = out["flag"].cpu().numpy()
+    for b in range(B):
+        f, c, st, hh, sr = oracle.step_one(int(got[b]), np.float32(ref["margin"][b]), 0, hist[b], 0,
+                                           h.pat_tokens, h.pat_offsets, h.pat_cue, h.terminator,
+                                           h.think_end)
+        assert flags[b] == f and d_state[b].item() == st
+
+
+def test_step_sample_pathological_rows(relay):
+    """A constant row (every logit a candidate: the exact fallback), rows with
+    -inf tails, a NaN row, and the distribution of draws on a constant row."""
+    vocab, B = 5000, 64
+    h, cs = _cs_pair(relay, vocab, 2, 4, 2, seed=75)
+    rows = np.random.default_rng(76).normal(0, 1, (B, vocab)).astype(np.float32)
+    rows[0] = 1.25                        # constant: top-k = the first k indices
+    rows[1, 30:] = -np.inf                # only 30 finite entries
+    rows[2, :] = -np.inf
+    rows[2, [7, 4000]] = [0.0, 0.0]       # two finite, tied
+    rows[3, 11] = np.nan
+    u = (np.arange(B) + 0.5) / B
+    u = u.astype(np.float32)
+    L = torch.as_tensor(rows, device=DEV)
+    st = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    hi = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    out = relay.step_sample(cs, L, torch.as_tensor(u, device=DEV), st, hi, temperature=0.6,
+                            top_k=20, top_p=0.95)
+    torch.cuda.synchronize()
+    got = out["sampled"].cpu().numpy()
+    _oracle_sample_tolerant(rows, "f32", vocab, u.astype(np.float64), got, 0.6, 20, 0.95)
+    assert got[3] == -1 and got[2] in (7, 4000) and 0 <= got[0] < 20 and 0 <= got[1] < 30
+    # constant row, many uniforms: uniform over the first ceil(0.95 * 20) = 19 indices
+    many = np.tile(rows[0], (B, 1))
+    out2 = relay.step_sample(cs, torch.as_tensor(many, device=DEV), torch.as_tensor(u, device=DEV),
+                             st.zero_(), hi.fill_(-1), temperature=0.6, top_k=20, top_p=0.95)
+    torch.cuda.synchronize()
+    g2 = out2["sampled"].cpu().numpy()
+    assert set(g2.tolist()) <= set(range(19)) and len(set(g2.tolist())) >= 17
+
+
+def test_step_sample_graph_replay(relay):
+    """Captured in a CUDA graph (PDL edges included) and replayed with new
+    uniforms: every replay matches the oracle."""
+    vocab, B = 32000, 48
+    h, cs = _cs_pair(relay, vocab, 4, 6, 3, seed=77)
+    L = synth.make_logits(B, vocab, "bf16", seed=78, device=DEV)
+    host = synth.host_rows(L, "bf16")
+    d_u = torch.zeros(B, dtype=torch.float32, device=DEV)
+    st = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    hi = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    ws = relay.workspace(0, 0, B, DEV)
+    out = relay.step_sample(cs, L, d_u, st, hi, ws=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            relay.step_sample(cs, L, d_u, st, hi, ws=ws, out=out)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(79)
+    for _ in range(4):
+        u = rng.random(B).astype(np.float32)
+        d_u.copy_(torch.as_tensor(u, device=DEV))
+        st.zero_(); hi.fill_(-1)
+        g.replay()
+        torch.cuda.synchronize()
+        _oracle_sample_tolerant(host, "bf16", vocab, u.astype(np.float64), out["sampled"].cpu().numpy(),
+                                0.6, 20, 0.95)

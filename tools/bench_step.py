@@ -18,7 +18,7 @@ import paper_2602_06454_b200 as relay  # noqa: E402
 import synth  # noqa: E402
 
 
-def main(B=256, V=152064, steps=200, graph=True):
+def main(B=256, V=152064, steps=200, graph=True, sample=False):
     dev = torch.device("cuda:0")
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     nbuf = max(2, int(np.ceil(4 * l2 / (B * V * 2))))
@@ -30,7 +30,14 @@ def main(B=256, V=152064, steps=200, graph=True):
     small = torch.zeros(B, dtype=torch.int32, device=dev)
     samp = torch.randint(3000, V, (B,), dtype=torch.int32, device=dev)
     ws = relay.workspace(0, 0, B, dev)
-    out = relay.step_switch(cs, bufs[0], state, hist, small, samp, ws=ws)
+    uni = torch.rand(B, device=dev)
+
+    def step(x, out=None):
+        if sample:   # N2: the paper's Qwen3 sampling (T 0.6, top-p 0.95, top-k 20)
+            return relay.step_sample(cs, x, uni, state, hist, small, temperature=0.6, top_k=20,
+                                     top_p=0.95, ws=ws, out=out)
+        return relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=out)
+    out = step(bufs[0])
     torch.cuda.synchronize()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
     res = {}
@@ -43,11 +50,11 @@ def main(B=256, V=152064, steps=200, graph=True):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.stream(s):
             for x in seq:                     # warm-up on the capture stream
-                relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=out)
+                step(x, out)
             torch.cuda.synchronize()
             with torch.cuda.graph(g, stream=s):
                 for x in seq:
-                    relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=out)
+                    step(x, out)
         torch.cuda.synchronize()
         for _ in range(3):
             g.replay()
@@ -66,13 +73,14 @@ def main(B=256, V=152064, steps=200, graph=True):
     import time
     t0 = time.perf_counter()
     for _ in range(100):
-        relay.step_switch(cs, bufs[0], state, hist, small, samp, ws=ws, out=out)
+        step(bufs[0], out)
     res["eager_host_us_per_call"] = (time.perf_counter() - t0) * 1e4
     torch.cuda.synchronize()
-    print(json.dumps({"kernel": "relay_step_switch (K4)", "batch": B, "vocab": V, "buffers": nbuf,
+    print(json.dumps({"kernel": "relay_step_sample (K4 + K5)" if sample else "relay_step_switch (K4)",
+                      "batch": B, "vocab": V, "buffers": nbuf,
                       "l2_bytes": l2, **res}), flush=True)
     cs.destroy()
 
 
 if __name__ == "__main__":
-    main()
+    main(sample="--sample" in sys.argv)

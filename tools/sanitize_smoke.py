@@ -1,5 +1,7 @@
-"""Small end-to-end run of every kernel (K1 all dtypes, K2 both modes, K3, K4)
-for compute-sanitizer: python tools/sanitize_smoke.py (under
+"""Small end-to-end run of every kernel (K1 all dtypes, K2 both modes, K3 incl.
+per-trajectory tables, K4 in every work split, K5 sampler incl. the overflow
+fallback, N1 partials/combine, N4 class patterns + decimal rule) for
+compute-sanitizer: python tools/sanitize_smoke.py (under
 compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck)."""
 import os
 import sys
@@ -37,10 +39,33 @@ def main():
         hist = torch.full((B, 7), -1, dtype=torch.int32, device=dev)
         sr = torch.zeros(B, dtype=torch.int32, device=dev)
         samp = torch.as_tensor(np.random.default_rng(5).integers(0, 8192, B).astype(np.int32), device=dev)
-        for _ in range(3):
-            relay.step_switch(cs, lg, st, hist, sr, samp, max_small_segment=4)
+        for mode_k4 in ("strided", "flat", "dynamic"):
+            os.environ["RELAY_K4_MODE"] = mode_k4
+            for _ in range(2):
+                relay.step_switch(cs, lg, st, hist, sr, samp, max_small_segment=4)
+        os.environ.pop("RELAY_K4_MODE")
+        uni = torch.rand(B, device=dev)
+        lg[0] = 1.0                                   # a constant row: the exact fallback
+        for _ in range(2):
+            relay.step_sample(cs, lg, uni, st, hist, sr, top_k=20, top_p=0.95)
+        relay.segment_reduce(cs, an.rows["margin"], an.scan, offs, tep, per_trajectory=True)
         torch.cuda.synchronize()
         cs.destroy()
+    # N1: vocabulary shards
+    L = synth.make_logits(40, 6000, "bf16", device=dev)
+    parts = [relay.margin_partials(L[:, i * 2000:(i + 1) * 2000], col_offset=i * 2000) for i in range(3)]
+    relay.margin_combine(torch.stack(parts))
+    # N4: class patterns and the decimal rule
+    cc = synth.make_class_case(8192, 3, 2000, seed=6)
+    cs = relay.CueSet(cc.cs.pat_tokens, cc.cs.pat_offsets, cc.cs.pat_cue, cc.cs.n_cues, cc.cs.terminator,
+                      cc.cs.vocab, cc.cs.think_end, 0, cc.classes, cc.decimal_rule)
+    tok = torch.as_tensor(cc.ts.tokens, device=dev)
+    offs = torch.as_tensor(cc.ts.traj_offsets, device=dev)
+    scan = relay.cue_scan(cs, tok, offs)
+    m = torch.as_tensor(synth.make_margins(cc.ts.tokens.shape[0], seed=7), device=dev)
+    relay.segment_reduce(cs, m, scan, offs)
+    torch.cuda.synchronize()
+    cs.destroy()
     print("sanitize smoke done")
 
 

@@ -12,7 +12,8 @@ sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "build", "k1_sweep")
 VARIANTS = [  # (ncw, stages, uv, minb, extra): stage bytes = uv * ncw * 32 * 16
     (8, 4, 4, 3, ""), (8, 6, 2, 4, ""), (8, 4, 2, 4, ""), (12, 4, 2, 3, ""),
-    (6, 6, 2, 5, ""), (16, 3, 2, 2, ""),
+    (6, 6, 2, 5, ""), (16, 3, 2, 2, ""), (8, 6, 4, 2, ""), (8, 5, 4, 2, ""),
+    (8, 4, 4, 3, "NULL"),
 ]
 
 

@@ -14,9 +14,13 @@
 // ring runs across row boundaries, so a row's epilogue overlaps the next
 // row's loads.  Per stage a thread reduces its raw 16-bit words with a packed
 // NaN-propagating max tree (HMNMX2.NAN) before unpacking anything, so the
-// guards cost ~0.5 instruction per element.  K4 splits rows into chunks
-// (LDG path) with a last-arriver combine, then runs RelayGen's switch state
-// machine on-device.
+// guards cost ~0.5 instruction per element.  K4 is the same kernel with a
+// 6-stage ring at 2 CTAs/SM, launched with programmatic dependent launch:
+// whole rows per CTA when the batch fills the SMs, otherwise equal slices of
+// the flattened batch merged by the last arriving CTA; its epilogue warp runs
+// RelayGen's switch state machine on-device (switch.cuh).  In
+// relay_step_sample it also bounds each row's top-k for the sampling kernel
+// (sample_kernels.cu).
 #include <cstdlib>
 #include <cstring>
 
@@ -215,11 +219,10 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ------------------------------------------------- K1 / K4 row kernel
-// Work items are (row, part) pairs: part k of a row covers elements
-// [k*chunk, min(vocab, (k+1)*chunk)).  K1 uses one part per row; K4 (a
-// batch of only ~256 live rows) splits rows so that every SM streams, and the
-// last CTA to finish a row merges its parts (arrival counter, reset after use
-// so CUDA-graph replays need no reset).
+// Work items are (row, element range, part) triples (Item, ItemIter below).
+// K1 takes whole rows; K4 whole rows or, for small batches, parts of rows
+// merged by the last arriving CTA (arrival counter, reset after use so CUDA
+// graph replays need no reset).
 struct RowsArgs {
   const void* logits;
   long long n_rows;
@@ -256,7 +259,8 @@ struct RowsArgs {
   // on the topk-th largest logit; the switch is left to the sampling kernel
   float* thk;     // [n_rows] or NULL
   int topk;       // 0 = off
-  int keep_l2;    // stream the rows with L2 evict_last (read again from L2)
+  int keep_l2;    // L2 evict_last: the sampling kernel reads the rows again
+                  // (hits only when the batch's logits fit the L2: ~64 rows)
 };
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad

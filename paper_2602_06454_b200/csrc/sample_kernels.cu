@@ -2,13 +2,14 @@
 // margin fused with the decode-side sampler).
 //
 // The paper samples every model at temperature 0.6 with top-p 0.95 (and top-k
-// 20 for Qwen3).  K4 streams each row once from HBM (margin, top-2,
-// and a lower bound thk on the row's top_k-th largest logit), keeping the rows
-// in L2 (evict_last); K5 re-reads each row from L2, collects the logits >= thk
-// (a handful per row), selects the exact top-k in (value desc, index asc)
-// order, applies temperature and top-p, draws the token by inverse CDF with the
-// caller's uniform (reading R20), and runs the decode-step switch (H8) on the
-// drawn token.  So the row crosses HBM once for both the margin and the sample.
+// 20 for Qwen3).  K4 streams each row (margin, top-2, and a lower
+// bound thk on the row's top_k-th largest logit) with L2 evict_last; K5
+// re-reads each row, collects the logits >= thk (~100 per row), selects the
+// exact top-k in (value desc, index asc) order, applies temperature and top-p,
+// draws the token by inverse CDF with the caller's uniform (reading R20), and
+// runs the decode-step switch (H8) on the drawn token.  The second read hits
+// L2 only for small batches (B200's L2 holds ~60 MB per partition; configs[2]
+// is 78 MB); DESIGN.md records the single-pass variants that measured slower.
 #include <cstdint>
 
 #include "relay_device.cuh"

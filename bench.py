@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-decode", action="store_true", help="skip the decode-step (configs[2]) line")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no clocks/e2e/baseline)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--serial-scan", action="store_true",
@@ -298,6 +299,9 @@ def main():
     cpu = None
     if rank == 0 and not args.no_baseline and not args.profile:
         cpu = cpu_baseline(logits, ts, cs_h, dtype, vocab)
+    decode = None
+    if rank == 0 and not args.no_decode and not args.profile:
+        decode = measure_decode(relay, synth, dev, peak)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -319,11 +323,59 @@ def main():
             "clocks": ck,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "decode_step": decode,
         }
         print(json.dumps(line), flush=True)
     cs.destroy()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
+    """H8 on configs[2] (256 live rows x 152,064 bf16 per step): relay_step_switch
+    (K4) and relay_step_sample (K4 + K5, T 0.6 / top-p 0.95 / top-k 20), each as a
+    CUDA graph over 7 rotating logits buffers (> 4 x L2), device-timed."""
+    import torch
+    h = synth.make_cueset(V, 8, 12, max_len=3)
+    cs = relay.CueSet.from_synth(h)
+    bufs = [synth.make_logits(B, V, "bf16", seed=100 + i, device=dev) for i in range(7)]
+    state = torch.zeros(B, dtype=torch.uint8, device=dev)
+    hist = torch.full((B, 7), -1, dtype=torch.int32, device=dev)
+    small = torch.zeros(B, dtype=torch.int32, device=dev)
+    samp = torch.randint(3000, V, (B,), dtype=torch.int32, device=dev)
+    uni = torch.rand(B, device=dev)
+    ws = relay.workspace(0, 0, B, dev)
+    res = {"workload": f"configs[2]: {B} live rows x {V} bf16 per step, 7 rotating buffers",
+           "bytes_per_step": B * (V * 2 + 12)}
+    for name, fn in (("switch", lambda x, o: relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=o)),
+                     ("sample", lambda x, o: relay.step_sample(cs, x, uni, state, hist, small, ws=ws, out=o))):
+        out = fn(bufs[0], None)
+        s = torch.cuda.Stream(device=dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            for x in bufs:
+                fn(x, out)
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(g, stream=s):
+                for x in bufs:
+                    fn(x, out)
+        torch.cuda.synchronize(dev)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        us = e0.elapsed_time(e1) * 1e3 / (reps * len(bufs))
+        gbs = res["bytes_per_step"] / (us * 1e-6) / 1e9
+        res[name] = {"us_per_step": us, "rows_per_s": B / (us * 1e-6), "gbs": gbs, "frac": gbs / peak,
+                     "kernels": "K4" if name == "switch" else "K4 + K5"}
+    del bufs
+    cs.destroy()
+    return res
 
 
 def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):

@@ -32,7 +32,8 @@ def run(mode="step"):
     relay._lib = relay._load()
     import synth
     dev = torch.device("cuda:0")
-    B, V = (256, 152064) if mode == "step" else (444, 152064)
+    B = int(os.environ.get("TRACE_BATCH", "256" if mode == "step" else "444"))
+    V = 152064
     h = synth.make_cueset(V, 8, 12, max_len=3)
     cs = relay.CueSet.from_synth(h)
     L = synth.make_logits(B, V, "bf16", device=dev)

@@ -532,32 +532,35 @@ int oracle_step_one(int32_t tok, float margin, uint8_t* state, int32_t* hist /*[
  * smallest l with p_0 + ... + p_(l-1) >= top_p * (p_0 + ... + p_(K-1)) (the
  * tokens whose higher-ranked mass is below top_p, at least one); draw the
  * token by inverse CDF with the caller's uniform u in [0, 1): the first i
- * with p_0 + ... + p_i > u * (p_0 + ... + p_(L-1)).  top_k in [1, vocab].
+ * with p_0 + ... + p_i > u * (p_0 + ... + p_(L-1)).  top_k in [1, vocab], or 0
+ * for no top-k truncation (K = vocab).
  * A row with status != 0 (NaN / +inf / no finite entry, [R4]) samples -1. */
+typedef struct { double v; int64_t i; } ranked_t;
+
+/* (value desc, index asc) [R3] */
+static int ranked_cmp(const void* a, const void* b) {
+    const ranked_t* x = (const ranked_t*)a;
+    const ranked_t* y = (const ranked_t*)b;
+    if (x->v > y->v) return -1;
+    if (x->v < y->v) return 1;
+    return (x->i < y->i) ? -1 : (x->i > y->i);
+}
+
 int32_t oracle_sample_row(const void* row, int dtype, int64_t vocab, double inv_temperature,
                           int32_t top_k, double top_p, double u) {
     int32_t i1, i2;
     double m, l;
-    if (top_k < 1) return -1;
+    if (top_k < 0) return -1;
     if (oracle_margin_row(row, dtype, vocab, 1.0, &i1, &i2, &m, &l) != 0) return -1;
-    if (top_k > vocab) top_k = (int32_t)vocab;
+    if (top_k == 0 || top_k > vocab) top_k = (int32_t)vocab;   /* 0: no top-k (R1-Distill) */
+    /* the row in (value desc, index asc) order: a library sort */
+    ranked_t* all = (ranked_t*)malloc(sizeof(ranked_t) * (size_t)vocab);
+    for (int64_t j = 0; j < vocab; j++) { all[j].v = oracle_elem(row, dtype, j); all[j].i = j; }
+    qsort(all, (size_t)vocab, sizeof(ranked_t), ranked_cmp);
     int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)top_k);
     double* p = (double*)malloc(sizeof(double) * (size_t)top_k);
-    /* top-k by repeated selection: the best entry ordered after the previous */
-    for (int32_t r = 0; r < top_k; r++) {
-        int64_t best = -1;
-        for (int64_t j = 0; j < vocab; j++) {
-            double z = oracle_elem(row, dtype, j);
-            if (r > 0) {   /* must come after idx[r-1] in (value desc, index asc) */
-                double zp = oracle_elem(row, dtype, idx[r - 1]);
-                if (z > zp || (z == zp && j <= idx[r - 1])) continue;
-            }
-            if (best < 0) { best = j; continue; }
-            double zb = oracle_elem(row, dtype, best);
-            if (z > zb) best = j;      /* equal values keep the lower index */
-        }
-        idx[r] = best;
-    }
+    for (int32_t r = 0; r < top_k; r++) idx[r] = all[r].i;
+    free(all);
     double z1 = oracle_elem(row, dtype, idx[0]);
     double total = 0.0;
     for (int32_t r = 0; r < top_k; r++) {

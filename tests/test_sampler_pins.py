@@ -65,3 +65,22 @@ def test_minus_inf_entries_are_never_drawn():
     z[0, [4, 17]] = [1.0, 0.5]
     for u in np.linspace(0, 0.999, 11):
         assert oracle.sample_rows(z, [u], temperature=0.6, top_k=20, top_p=1.0)[0] in (4, 17)
+
+
+def test_no_top_k_is_the_whole_vocabulary():
+    """top_k = 0 (the R1-Distill setting: top-p only) keeps every entry:
+    the same draws as top_k = vocab, and with top_p = 1 plain inverse-CDF
+    sampling over softmax(z / T)."""
+    rng = np.random.default_rng(4)
+    rows = rng.normal(0, 2, (16, 300)).astype(np.float32)
+    u = rng.random(16)
+    a = oracle.sample_rows(rows, u, top_k=0, top_p=0.95)
+    b = oracle.sample_rows(rows, u, top_k=300, top_p=0.95)
+    assert (a == b).all()
+    z = rows[0].astype(np.float64)
+    order = np.lexsort((np.arange(300), -z))
+    w = np.exp((z[order] - z.max()) / 0.6)
+    cdf = np.cumsum(w) / w.sum()
+    us = (np.arange(101) + 0.5) / 101
+    got = oracle.sample_rows(np.tile(rows[0], (101, 1)), us, top_k=0, top_p=1.0)
+    assert (got == order[np.searchsorted(cdf, us, side="right")]).all()

@@ -348,7 +348,9 @@ def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
     res = {"workload": f"configs[2]: {B} live rows x {V} bf16 per step, 7 rotating buffers",
            "bytes_per_step": B * (V * 2 + 12)}
     for name, fn in (("switch", lambda x, o: relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=o)),
-                     ("sample", lambda x, o: relay.step_sample(cs, x, uni, state, hist, small, ws=ws, out=o))):
+                     ("sample", lambda x, o: relay.step_sample(cs, x, uni, state, hist, small, ws=ws, out=o)),
+                     ("sample_no_top_k", lambda x, o: relay.step_sample(cs, x, uni, state, hist, small, top_k=0,
+                                                                         ws=ws, out=o))):
         out = fn(bufs[0], None)
         s = torch.cuda.Stream(device=dev)
         g = torch.cuda.CUDAGraph()
@@ -372,7 +374,9 @@ def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
         us = e0.elapsed_time(e1) * 1e3 / (reps * len(bufs))
         gbs = res["bytes_per_step"] / (us * 1e-6) / 1e9
         res[name] = {"us_per_step": us, "rows_per_s": B / (us * 1e-6), "gbs": gbs, "frac": gbs / peak,
-                     "kernels": "K4" if name == "switch" else "K4 + K5"}
+                     "kernels": "K4" if name == "switch" else "K4 + K5",
+                     "sampling": {"switch": "token given", "sample": "T 0.6, top-p 0.95, top-k 20 (Qwen3)",
+                                  "sample_no_top_k": "T 0.6, top-p 0.95 (R1-Distill)"}[name]}
     del bufs
     cs.destroy()
     return res

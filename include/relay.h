@@ -387,7 +387,11 @@ relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dt
  * second kernel re-reads it from L2, keeps the logits above the bound, selects
  * the exact top-k and draws (an exact fallback covers pathological rows,
  * e.g. a constant row).  Rows with status != 0 draw -1 (no switch update).
- *   temperature > 0; top_k in [1, RELAY_MAX_TOP_K] (clamped to vocab);
+ *   temperature > 0; top_k in [1, RELAY_MAX_TOP_K] (clamped to vocab), or 0
+ *   for no top-k (the R1-Distill setting: top_p over the whole row, p_k
+ *   normalised by the row's total mass; rows whose kept set reaches past the
+ *   top 64 are resolved by mass-rank selection over value bins, several
+ *   extra passes over the row);
  *   top_p in (0, 1]; uniform float[batch] in [0, 1) (device; the caller's
  *   random numbers); sampled int32[batch] out; other arguments, outputs and
  *   workspace as relay_step_switch (rows are streamed whole per CTA).

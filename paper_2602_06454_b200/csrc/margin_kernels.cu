@@ -258,6 +258,7 @@ struct RowsArgs {
   // fused-sampler margin pass (relay_step_sample, N2): per row a lower bound
   // on the topk-th largest logit; the switch is left to the sampling kernel
   float* thk;     // [n_rows] or NULL
+  float* zmax;    // [n_rows] with thk: the row maximum (the sampler's reference)
   int topk;       // 0 = off
   int keep_l2;    // L2 evict_last: the sampling kernel reads the rows again
                   // (hits only when the batch's logits fit the L2: ~64 rows)
@@ -595,7 +596,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           S = warp_sum(exact_sum_thread<E>(row, a.vocab, q.t.v1, c, lane, 32));
           exact = true;
         }
-        if (a.thk && lane == 0) a.thk[r] = thk;
+        if (a.thk && lane == 0) {
+          a.thk[r] = thk;
+          a.zmax[r] = q.t.v1;
+        }
         finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in);
         continue;
       }
@@ -917,7 +921,7 @@ cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int b
   a.counter = ws.counter; a.part = ws.part; a.work = ws.work;
   a.flat = 0;  // whole rows: the bound needs every thread maximum of the row
   a.state = state; a.hist = hist; a.small_run = small_run; a.gate = gate; a.max_seg = max_seg;
-  a.thk = ws.thk; a.topk = topk; a.keep_l2 = 1;
+  a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk; a.keep_l2 = 1;
   return launch_rows<kModeStep>(dt, a, cs, st);
 }
 

@@ -96,6 +96,7 @@ StepWs step_ws_layout(void* base, int batch) {
   w.work = reinterpret_cast<int*>(take(sizeof(int) * 4));
   w.thk = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
   w.status = reinterpret_cast<uint8_t*>(take(static_cast<size_t>(batch) + 1));
+  w.zmax = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
   w.bytes = off;
   return w;
 }
@@ -533,7 +534,7 @@ relay_status_t relay_step_sample(relay_cueset_t cs, const void* logits, relay_dt
     return fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
   if (!(temperature > 0.0f) || !std::isfinite(temperature))
     return fail(RELAY_ERR_INVALID, "temperature must be finite and > 0");
-  if (top_k < 1 || top_k > kMaxTopK) return fail(RELAY_ERR_INVALID, "top_k must be in [1, %d]", kMaxTopK);
+  if (top_k < 0 || top_k > kMaxTopK) return fail(RELAY_ERR_INVALID, "top_k must be in [0, %d]", kMaxTopK);
   if (!(top_p > 0.0f && top_p <= 1.0f)) return fail(RELAY_ERR_INVALID, "top_p must be in (0, 1]");
   if (max_small_segment < 0) return fail(RELAY_ERR_INVALID, "max_small_segment < 0");
   if (max_small_segment > 0 && !small_run) return fail(RELAY_ERR_INVALID, "small_run required with a budget");
@@ -542,7 +543,7 @@ relay_status_t relay_step_sample(relay_cueset_t cs, const void* logits, relay_dt
     return fail(RELAY_ERR_INVALID, "logits/state/hist/margin/flag/cue_id/uniform/sampled are required");
   StepWs w = step_ws_layout(ws, batch);
   if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
-  const int k = static_cast<int>(top_k < vocab ? top_k : vocab);
+  const int k = static_cast<int>(top_k < vocab ? top_k : vocab);  // 0: no top-k
   return cuda_status(launch_step_sample(cs->dev, logits, static_cast<int>(dt), batch, static_cast<int>(vocab),
                                         row_stride, inv_temperature, temperature, k, top_p, uniform, state,
                                         hist, small_run, margin_gate, max_small_segment, margin, top1, top2,

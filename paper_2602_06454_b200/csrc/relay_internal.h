@@ -79,6 +79,7 @@ struct StepWs {
   int* work;           // [2] chunk counter, CTAs done (zero between launches)
   float* thk;          // [batch] relay_step_sample: K4's top-k bound per row
   uint8_t* status;     // [batch] relay_step_sample: K4's row status
+  float* zmax;         // [batch] relay_step_sample: K4's row maximum
   size_t bytes;
 };
 constexpr int kMaxSplit = 32;

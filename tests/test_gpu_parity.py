@@ -958,6 +958,9 @@ def _oracle_sample_tolerant(host_rows, dtype, vocab, u, got, T, k, p):
     (37, 5003, "f16", 1.0, 1, 0.95),
     (50, 32000, "f32", 0.6, 20, 0.5),
     (9, 40, "f32", 0.8, 64, 0.9),             # vocab < top_k
+    (256, 152064, "bf16", 0.6, 0, 0.95),      # configs[2] with R1-Distill sampling: no top-k
+    (37, 5003, "f16", 1.0, 0, 1.0),
+    (50, 32000, "f32", 0.6, 0, 0.5),
 ])
 def test_step_sample(relay, B, vocab, dtype, T, k, p):
     """N2: the drawn token matches the oracle sampler (R20); margins/indices as
@@ -992,6 +995,8 @@ def test_step_sample(relay, B, vocab, dtype, T, k, p):
     assert (got[~ok] == -1).all()
     if k == 1:
         np.testing.assert_array_equal(got[ok], ref["top1"][ok])
+    if k == 0:   # the rows whose nucleus is wider than 64 tokens took the slow path
+        assert len(set(got[ok].tolist())) > 1
     # the switch saw the drawn token
     flags = out["flag"].cpu().numpy()
     for b in range(B):
@@ -1030,6 +1035,29 @@ def test_step_sample_pathological_rows(relay):
     torch.cuda.synchronize()
     g2 = out2["sampled"].cpu().numpy()
     assert set(g2.tolist()) <= set(range(19)) and len(set(g2.tolist())) >= 17
+
+
+def test_step_sample_no_top_k_pathological_rows(relay):
+    """No top-k: a constant row (every entry one value: the kept ties and the
+    draw are resolved in index order), flat and sparse rows, NaN rows."""
+    vocab, B = 5000, 24
+    h, cs = _cs_pair(relay, vocab, 2, 4, 2, seed=85)
+    rng = np.random.default_rng(86)
+    rows = rng.normal(0, 0.3, (B, vocab)).astype(np.float32)   # flat: wide nuclei
+    rows[0] = 1.25
+    rows[1] = np.repeat(rng.normal(0, 1, 50), 100).astype(np.float32)   # blocks of ties
+    rows[2, 30:] = -np.inf
+    rows[3, 11] = np.nan
+    u = rng.random(B).astype(np.float32)
+    st = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    hi = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    for p in (0.95, 0.3, 1.0):
+        out = relay.step_sample(cs, torch.as_tensor(rows, device=DEV), torch.as_tensor(u, device=DEV),
+                                st.zero_(), hi.fill_(-1), temperature=0.6, top_k=0, top_p=p)
+        torch.cuda.synchronize()
+        got = out["sampled"].cpu().numpy()
+        _oracle_sample_tolerant(rows, "f32", vocab, u.astype(np.float64), got, 0.6, 0, p)
+        assert got[3] == -1
 
 
 def test_step_sample_graph_replay(relay):

@@ -18,7 +18,7 @@ import paper_2602_06454_b200 as relay  # noqa: E402
 import synth  # noqa: E402
 
 
-def main(B=256, V=152064, steps=200, graph=True, sample=False):
+def main(B=256, V=152064, steps=200, graph=True, sample=False, top_k=20):
     dev = torch.device("cuda:0")
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     nbuf = max(2, int(np.ceil(4 * l2 / (B * V * 2))))
@@ -34,7 +34,7 @@ def main(B=256, V=152064, steps=200, graph=True, sample=False):
 
     def step(x, out=None):
         if sample:   # N2: the paper's Qwen3 sampling (T 0.6, top-p 0.95, top-k 20)
-            return relay.step_sample(cs, x, uni, state, hist, small, temperature=0.6, top_k=20,
+            return relay.step_sample(cs, x, uni, state, hist, small, temperature=0.6, top_k=top_k,
                                      top_p=0.95, ws=ws, out=out)
         return relay.step_switch(cs, x, state, hist, small, samp, ws=ws, out=out)
     out = step(bufs[0])
@@ -83,4 +83,4 @@ def main(B=256, V=152064, steps=200, graph=True, sample=False):
 
 
 if __name__ == "__main__":
-    main(sample="--sample" in sys.argv)
+    main(sample="--sample" in sys.argv, top_k=0 if "--no-topk" in sys.argv else 20)

@@ -390,8 +390,11 @@ relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dt
  *   temperature > 0; top_k in [1, RELAY_MAX_TOP_K] (clamped to vocab), or 0
  *   for no top-k (the R1-Distill setting: top_p over the whole row, p_k
  *   normalised by the row's total mass; rows whose kept set reaches past the
- *   top 64 are resolved by mass-rank selection over value bins, several
- *   extra passes over the row);
+ *   top 64 are resolved by mass-rank selection: bf16 rows by one counting
+ *   pass over their distinct values plus an early-exit pass for the drawn
+ *   tie's index, f16/f32 rows over value bins, several extra passes;
+ *   masses are fixed point, so the selection is deterministic; needs
+ *   vocab < 2^18, else RELAY_ERR_UNSUPPORTED);
  *   top_p in (0, 1]; uniform float[batch] in [0, 1) (device; the caller's
  *   random numbers); sampled int32[batch] out; other arguments, outputs and
  *   workspace as relay_step_switch (rows are streamed whole per CTA).

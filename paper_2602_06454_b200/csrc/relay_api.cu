@@ -97,6 +97,8 @@ StepWs step_ws_layout(void* base, int batch) {
   w.thk = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
   w.status = reinterpret_cast<uint8_t*>(take(static_cast<size_t>(batch) + 1));
   w.zmax = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
+  w.slow = reinterpret_cast<int*>(take(sizeof(int) * (static_cast<size_t>(batch) + 1)));
+  w.zsum = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
   w.bytes = off;
   return w;
 }
@@ -536,6 +538,8 @@ relay_status_t relay_step_sample(relay_cueset_t cs, const void* logits, relay_dt
     return fail(RELAY_ERR_INVALID, "temperature must be finite and > 0");
   if (top_k < 0 || top_k > kMaxTopK) return fail(RELAY_ERR_INVALID, "top_k must be in [0, %d]", kMaxTopK);
   if (!(top_p > 0.0f && top_p <= 1.0f)) return fail(RELAY_ERR_INVALID, "top_p must be in (0, 1]");
+  // no top-k: fixed-point masses are summed in 14-bit digits, each sum < vocab * 2^14 < 2^32
+  if (top_k == 0 && vocab >= (1LL << 18)) return fail(RELAY_ERR_UNSUPPORTED, "top_k = 0 needs vocab < 2^18");
   if (max_small_segment < 0) return fail(RELAY_ERR_INVALID, "max_small_segment < 0");
   if (max_small_segment > 0 && !small_run) return fail(RELAY_ERR_INVALID, "small_run required with a budget");
   if (batch == 0) return RELAY_OK;

@@ -185,6 +185,7 @@ __device__ __forceinline__ U8x32 ldg_stream32(const void* p) {
 struct EBf16 {
   using T = uint16_t;
   static constexpr int SZ = 2;
+  static constexpr bool kBf16 = true;
   __device__ static __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
     lo = __uint_as_float(w << 16);
     hi = __uint_as_float(w & 0xffff0000u);
@@ -202,6 +203,7 @@ struct EBf16 {
 struct EF16 {
   using T = uint16_t;
   static constexpr int SZ = 2;
+  static constexpr bool kBf16 = false;
   __device__ static __forceinline__ void unpack2(uint32_t w, float& lo, float& hi) {
     __half2 h = *reinterpret_cast<__half2*>(&w);
     float2 f = __half22float2(h);
@@ -222,6 +224,7 @@ struct EF16 {
 struct EF32 {
   using T = float;
   static constexpr int SZ = 4;
+  static constexpr bool kBf16 = false;
   __device__ static __forceinline__ void unpack2(uint32_t, float&, float&) {}
   __device__ static __forceinline__ uint32_t pmax(uint32_t a, uint32_t) { return a; }
   __device__ static __forceinline__ float load1(const T* p) { return __ldg(p); }
@@ -313,6 +316,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 

@@ -80,6 +80,8 @@ struct StepWs {
   float* thk;          // [batch] relay_step_sample: K4's top-k bound per row
   uint8_t* status;     // [batch] relay_step_sample: K4's row status
   float* zmax;         // [batch] relay_step_sample: K4's row maximum
+  int* slow;           // [batch] relay_step_sample: rows handed to the nucleus kernel
+  float* zsum;         // [batch] relay_step_sample: their mass at the sampling temperature
   size_t bytes;
 };
 constexpr int kMaxSplit = 32;

@@ -1060,6 +1060,42 @@ def test_step_sample_no_top_k_pathological_rows(relay):
         assert got[3] == -1
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_step_sample_no_top_k_16bit_rows(relay, dtype):
+    """No top-k on 16-bit rows (the exact-key nucleus path): flat rows whose
+    nucleus spans thousands of tied values, a range crossing zero (keys span
+    every tiny binade: level-2 bins), large logits (one key per level-1 bin),
+    constant and tied-block rows, -0/+0 ties, sparse and NaN rows."""
+    vocab, B = 152064, 16
+    h, cs = _cs_pair(relay, vocab, 2, 4, 2, seed=87)
+    rng = np.random.default_rng(88)
+    rows = rng.normal(0, 2.5, (B, vocab)).astype(np.float32)
+    rows[0] = 1.25                                            # constant
+    rows[1] = rng.normal(0, 0.05, vocab)                      # flat around 0
+    rows[2] = rng.normal(0, 0.05, vocab) + 30.0               # flat, large values
+    rows[3] = np.repeat(rng.normal(0, 1, 1188), 128)[:vocab]  # blocks of ties
+    rows[4] = rng.normal(0, 1.0, vocab) * 0.3                 # small z1: keys cross zero
+    rows[5] = np.where(rng.random(vocab) < 0.5, -0.0, 0.0)    # -0 / +0 ties (IEEE equal)
+    rows[5, 100:110] = 0.5
+    rows[6, 40:] = -np.inf                                    # sparse
+    rows[7, 11] = np.nan
+    rows[8] = rng.normal(0, 2.5, vocab) + 40.0                # large logits, wide nucleus
+    rows[9] = np.linspace(-1, 1, vocab)[::-1]                 # strictly descending
+    L = torch.as_tensor(rows, device=DEV).to(torch.bfloat16 if dtype == "bf16" else torch.float16)
+    host = synth.host_rows(L, dtype)
+    u = rng.random(B).astype(np.float32)
+    u[:3] = [0.0, 0.999999, 0.5]
+    st = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    hi = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    for p in (0.95, 0.3, 1.0):
+        out = relay.step_sample(cs, L, torch.as_tensor(u, device=DEV), st.zero_(), hi.fill_(-1),
+                                temperature=0.6, top_k=0, top_p=p)
+        torch.cuda.synchronize()
+        got = out["sampled"].cpu().numpy()
+        _oracle_sample_tolerant(host, dtype, vocab, u.astype(np.float64), got, 0.6, 0, p)
+        assert got[7] == -1 and 0 <= got[6] < 40
+
+
 def test_step_sample_graph_replay(relay):
     """Captured in a CUDA graph (PDL edges included) and replayed with new
     uniforms: every replay matches the oracle."""

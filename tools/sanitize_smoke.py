@@ -48,6 +48,12 @@ def main():
         lg[0] = 1.0                                   # a constant row: the exact fallback
         for _ in range(2):
             relay.step_sample(cs, lg, uni, st, hist, sr, top_k=20, top_p=0.95)
+        # no top-k: K6 on bf16 (exact value counts), flat and tied rows, and f32 (value bins)
+        lg[1] = torch.randn(8192, device=dev) * 0.05
+        lg[2] = torch.arange(8192, device=dev).float().div(64).floor().neg()
+        for p in (0.95, 1.0):
+            relay.step_sample(cs, lg, uni, st, hist, sr, top_k=0, top_p=p)
+            relay.step_sample(cs, lg.float(), uni, st, hist, sr, top_k=0, top_p=p)
         relay.segment_reduce(cs, an.rows["margin"], an.scan, offs, tep, per_trajectory=True)
         torch.cuda.synchronize()
         cs.destroy()

@@ -128,6 +128,37 @@ relay_status_t relay_margin_combine(const float* partials, int32_t n_shards, int
                                     int32_t* top2, float* lse, uint8_t* row_status,
                                     relay_stream_t stream);
 
+/* relay_margin_rows_tp — N1 with the exchange fused into the streaming
+ * kernel over peer memory (NVLink P2P through CUDA IPC, no NCCL): each row's
+ * 32-byte partial is stored by the kernel's epilogue straight into every
+ * rank's receive buffer as soon as the row is reduced (the tag word last,
+ * st.release.sys), so the transfer overlaps the stream; a combine kernel on
+ * each rank waits (ld.acquire.sys) for all ranks' partials of the call and
+ * writes the full-row margin / top1 / top2 / lse / status exactly as
+ * relay_margin_combine would.  Every rank of the group calls it once per
+ * batch with the same n_rows (collective; stream-ordered, no host sync).
+ * Set-up (collective): relay_tp_exchange_create allocates this rank's
+ * receive buffer (2 x world x rows_cap x 32 B, device memory owned by the
+ * handle) and returns its CUDA IPC handle (RELAY_IPC_HANDLE_BYTES, [host]);
+ * the caller gathers the handles of all ranks in rank order (e.g. a
+ * torch.distributed all_gather_object) and passes them to
+ * relay_tp_exchange_connect, which maps the peers' buffers.  Calls are tagged
+ * from a device-side epoch (CUDA-graph safe); buffers alternate by call
+ * parity, so a rank one call ahead never overwrites a slot still being read.
+ * Errors: world_size not in [1, 8], rank out of range, rows_cap < 1,
+ * n_rows > rows_cap, an unconnected rank, and as relay_margin_partials. */
+#define RELAY_IPC_HANDLE_BYTES 64
+typedef struct relay_tp_exchange_s* relay_tp_exchange_t;
+relay_status_t relay_tp_exchange_create(int32_t rank, int32_t world_size, int64_t rows_cap,
+                                        uint8_t* ipc_handle_out, relay_tp_exchange_t* out);
+relay_status_t relay_tp_exchange_connect(relay_tp_exchange_t x, const uint8_t* ipc_handles);
+relay_status_t relay_tp_exchange_destroy(relay_tp_exchange_t x);
+relay_status_t relay_margin_rows_tp(relay_tp_exchange_t x, const void* logits_shard, relay_dtype_t dt,
+                                    int64_t n_rows, int64_t shard_vocab, int64_t row_stride,
+                                    int64_t col_offset, float inv_temperature, float* margin,
+                                    int32_t* top1, int32_t* top2, float* lse, uint8_t* row_status,
+                                    relay_stream_t stream);
+
 /* ------------------------------------------------------------- cue set --
  * A model pair's switch-cue set (tab:switch_cue_sets) as token-ID
  * patterns (R5: the caller tokenises every surface variant) plus the sentence

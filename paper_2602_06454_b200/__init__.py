@@ -64,6 +64,10 @@ def _load():
         "relay_nccl_unique_id": (C.c_int, [P]),
         "relay_nccl_comm_init": (C.c_int, [P, i32, i32, P]),
         "relay_nccl_comm_destroy": (C.c_int, [P]),
+        "relay_tp_exchange_create": (C.c_int, [i32, i32, i64, P, P]),
+        "relay_tp_exchange_connect": (C.c_int, [P, P]),
+        "relay_tp_exchange_destroy": (C.c_int, [P]),
+        "relay_margin_rows_tp": (C.c_int, [P, P, C.c_int, i64, i64, i64, i64, f32, P, P, P, P, P, P]),
         "relay_offload_estimate": (C.c_int, [P, i64, P, i32, P, P, P, P, i64, P, P, P, P]),
         "relay_stats_words": (sz, [i32, i32]),
         "relay_stats_finalize": (C.c_int, [P, i32, i32, i64, i32, P]),
@@ -88,7 +92,8 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_stats_words", "relay_stats_merge", "relay_stats_allreduce",
            "relay_nccl_unique_id", "relay_nccl_comm_init", "relay_nccl_comm_destroy",
            "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate",
-           "relay_step_sample")
+           "relay_step_sample", "relay_tp_exchange_create", "relay_tp_exchange_connect",
+           "relay_tp_exchange_destroy", "relay_margin_rows_tp")
 
 
 def _check(rc: int, what: str):
@@ -206,6 +211,67 @@ def margin_rows_tp(logits_shard, col_offset: int, group=None, inv_temperature: f
                            device=part.device)
     dist.all_gather_into_tensor(gathered, part, group=group)   # ranks concatenated on dim 0
     return margin_combine(gathered.view(world, part.shape[0], part.shape[1]), inv_temperature)
+
+
+IPC_HANDLE_BYTES = 64
+
+
+class TpExchange:
+    """relay_tp_exchange_create / connect / destroy: the receive buffers of a
+    tensor-parallel group for relay_margin_rows_tp (N1 with the exchange
+    fused into the streaming kernel over peer memory).  Collective: every
+    rank constructs it; the CUDA IPC handles are gathered over ``group``
+    (any torch.distributed backend)."""
+
+    def __init__(self, rows_cap: int, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.rows_cap = int(rows_cap)
+        h = C.create_string_buffer(IPC_HANDLE_BYTES)
+        x = C.c_void_p()
+        _check(_lib.relay_tp_exchange_create(self.rank, self.world, self.rows_cap, h, C.byref(x)),
+               "relay_tp_exchange_create")
+        self._x = x
+        handles = [None] * self.world
+        dist.all_gather_object(handles, h.raw, group=group)
+        buf = C.create_string_buffer(b"".join(handles), IPC_HANDLE_BYTES * self.world)
+        _check(_lib.relay_tp_exchange_connect(self._x, buf), "relay_tp_exchange_connect")
+
+    def margin_rows(self, logits_shard, col_offset: int, inv_temperature: float = 1.0, out=None,
+                    stream=None):
+        """relay_margin_rows_tp: full-row margin / top1 / top2 / lse / status of
+        rows whose columns [col_offset, col_offset + width) this rank holds."""
+        import torch
+        _need_cuda(logits_shard)
+        if logits_shard.dim() != 2 or logits_shard.stride(1) != 1:
+            raise RelayError("logits shard must be 2-D with unit stride in the vocabulary dim")
+        n = logits_shard.shape[0]
+        stride = logits_shard.stride(0) if n > 1 else logits_shard.shape[1]
+        dev = logits_shard.device
+        if out is None:
+            out = dict(margin=torch.empty(n, dtype=torch.float32, device=dev),
+                       top1=torch.empty(n, dtype=torch.int32, device=dev),
+                       top2=torch.empty(n, dtype=torch.int32, device=dev),
+                       lse=torch.empty(n, dtype=torch.float32, device=dev),
+                       status=torch.empty(n, dtype=torch.uint8, device=dev))
+        rc = _lib.relay_margin_rows_tp(self._x, _ptr(logits_shard), _dtype_of(logits_shard), n,
+                                       logits_shard.shape[1], stride, int(col_offset), float(inv_temperature),
+                                       _ptr(out["margin"]), _ptr(out.get("top1")), _ptr(out.get("top2")),
+                                       _ptr(out.get("lse")), _ptr(out.get("status")), _stream(stream))
+        _check(rc, "relay_margin_rows_tp")
+        return out
+
+    def close(self):
+        if getattr(self, "_x", None):
+            _lib.relay_tp_exchange_destroy(self._x)
+            self._x = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # --------------------------------------------------------------- cue set

@@ -245,7 +245,8 @@ struct RowsArgs {
   int cpr;        // dynamic mode: chunks per row (<= kMaxSplit)
   // vocabulary-parallel partials (kModePartial)
   long long col_offset;  // global index of the shard's first column
-  float* tp_part;        // [n_rows][kPartWords]
+  float* tp_part;        // [n_rows][kPartWords] (or NULL with tp_peers)
+  TpPeers tp;            // relay_margin_rows_tp: the partial goes straight to every rank (tp.world > 0)
   // decode-step switch (kModeStep)
   const int* sampled;
   uint8_t* state;
@@ -291,23 +292,42 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
   if constexpr (MODE == kModePartial) {
     // vocabulary shard: top-2 with GLOBAL indices and the normaliser relative
     // to the shard maximum, S_rel = sum_j 2^((z_j - v1) c), shift removed
-    if (lane == 0) {
-      float srel = 0.0f;
-      if (exact) {
-        srel = S;
-      } else if (q.t.v1 != -INFINITY && q.t.v1 != INFINITY) {
-        const float My = q.t.v1 * a.c;
-        srel = q.n.s * ex2((q.n.m - My) - fmaf(q.t.v1, a.c, -My));
+    // (every lane holds the merged partial)
+    float srel = 0.0f;
+    if (exact) {
+      srel = S;
+    } else if (q.t.v1 != -INFINITY && q.t.v1 != INFINITY) {
+      const float My = q.t.v1 * a.c;
+      srel = q.n.s * ex2((q.n.m - My) - fmaf(q.t.v1, a.c, -My));
+    }
+    float w[kPartWords];
+    w[0] = q.t.v1;
+    w[1] = q.t.v2;
+    w[2] = __int_as_float(q.t.i1 == INT_MAX ? INT_MAX : static_cast<int>(q.t.i1 + a.col_offset));
+    w[3] = __int_as_float(q.t.i2 == INT_MAX ? INT_MAX : static_cast<int>(q.t.i2 + a.col_offset));
+    w[4] = srel;
+    w[5] = __int_as_float(q.flags & kFlagNan);
+    w[6] = 0.0f;
+    w[7] = 0.0f;
+    if (a.tp.world > 0) {
+      // the exchange fused into the epilogue: lane k stores the row's partial
+      // into rank k's receive buffer (NVLink P2P stores for peers), the tag
+      // last with release semantics, so the transfer overlaps the stream
+      if (lane < a.tp.world) {
+        const unsigned tag = static_cast<unsigned>(*reinterpret_cast<const volatile int*>(a.tp.epoch)) + 1u;
+        float* dst = a.tp.recv[lane] +
+                     ((static_cast<long long>(tag & 1u) * a.tp.world + a.tp.rank) * a.tp.rows_cap + r) * kPartWords;
+        reinterpret_cast<float4*>(dst)[0] = make_float4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<float2*>(dst)[2] = make_float2(w[4], w[5]);
+        dst[6] = 0.0f;
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst + 7), "r"(tag) : "memory");
       }
+      return;
+    }
+    if (lane == 0) {
       float* pw = a.tp_part + static_cast<size_t>(r) * kPartWords;
-      pw[0] = q.t.v1;
-      pw[1] = q.t.v2;
-      pw[2] = __int_as_float(q.t.i1 == INT_MAX ? INT_MAX : static_cast<int>(q.t.i1 + a.col_offset));
-      pw[3] = __int_as_float(q.t.i2 == INT_MAX ? INT_MAX : static_cast<int>(q.t.i2 + a.col_offset));
-      pw[4] = srel;
-      pw[5] = __int_as_float(q.flags & kFlagNan);
-      pw[6] = 0.0f;
-      pw[7] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < kPartWords; k++) pw[k] = w[k];
     }
     return;
   }
@@ -983,6 +1003,87 @@ cudaError_t launch_margin_combine(const float* part, int n_shards, long long n_r
   const long long blocks = (n_rows + 127) / 128;
   margin_combine_kernel<<<static_cast<unsigned>(blocks), 128, 0, st>>>(part, n_shards, n_rows, iota * kLog2e,
                                                                         iota, margin, top1, top2, lse, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_margin_partials_p2p(const void* logits, int dt, long long n_rows, int vocab, long long stride,
+                                       long long col_offset, float iota, const TpPeers& peers, cudaStream_t st) {
+  if (n_rows <= 0) return cudaSuccess;
+  RowsArgs a{};
+  a.logits = logits; a.n_rows = n_rows; a.vocab = vocab; a.stride = stride;
+  a.c = iota * kLog2e; a.iota = iota; a.flat = 0;
+  a.col_offset = col_offset; a.tp = peers;
+  return launch_rows<kModePartial>(dt, a, CueDev{}, st);
+}
+
+// N1 combine over the receive buffer: one thread per row waits (acquire) for
+// every rank's partial of this call's tag, then merges as margin_combine.  The
+// last CTA out publishes the tag as the completed epoch (the next call's tag
+// is epoch + 1; buffers alternate by parity, so a rank one call ahead never
+// overwrites a slot still being read) and re-arms the arrival counter.
+__device__ __forceinline__ unsigned ld_acquire_sys(const float* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void margin_combine_p2p_kernel(TpPeers pe, long long n_rows, float c, float iota,
+                                          float* __restrict__ margin, int* __restrict__ top1,
+                                          int* __restrict__ top2, float* __restrict__ lse,
+                                          uint8_t* __restrict__ status) {
+  const unsigned tag = static_cast<unsigned>(*reinterpret_cast<const volatile int*>(pe.epoch)) + 1u;
+  const float* buf = pe.recv[pe.rank] + static_cast<long long>(tag & 1u) * pe.world * pe.rows_cap * kPartWords;
+  const long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (r < n_rows) {
+    Top2 t = top2_empty();
+    int nan = 0;
+    float v1[kMaxTpRanks], sr[kMaxTpRanks];
+    for (int k = 0; k < pe.world; k++) {
+      const float* p = buf + (static_cast<long long>(k) * pe.rows_cap + r) * kPartWords;
+      while (ld_acquire_sys(p + 7) != tag) {
+      }
+      // plain loads after the acquire (ordered by it; L1 is not allocated for .cg)
+      const float4 a4 = __ldcg(reinterpret_cast<const float4*>(p));
+      const float2 b2 = __ldcg(reinterpret_cast<const float2*>(p + 4));
+      t = top2_merge(t, Top2{a4.x, a4.y, __float_as_int(a4.z), __float_as_int(a4.w)});
+      nan |= __float_as_int(b2.y);
+      v1[k] = a4.x;
+      sr[k] = b2.x;
+    }
+    int st = 0;
+    if (nan || t.v1 == INFINITY) st = 1;
+    else if (t.v1 == -INFINITY) st = 2;
+    if (st) {
+      margin[r] = qnan();
+      if (top1) top1[r] = -1;
+      if (top2) top2[r] = -1;
+      if (lse) lse[r] = qnan();
+      if (status) status[r] = static_cast<uint8_t>(st);
+    } else {
+      float S = 0.0f;
+      for (int k = 0; k < pe.world; k++)
+        if (sr[k] > 0.0f) S += sr[k] * ex2((v1[k] - t.v1) * c);
+      margin[r] = (1.0f - ex2((t.v2 - t.v1) * c)) / S;
+      if (top1) top1[r] = t.i1;
+      if (top2) top2[r] = t.i2;
+      if (lse) lse[r] = t.v1 * iota + logf(S);
+      if (status) status[r] = 0;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomic_add_acq_rel(pe.done, 1) == static_cast<int>(gridDim.x) - 1) {
+      *pe.done = 0;
+      *reinterpret_cast<volatile int*>(pe.epoch) = static_cast<int>(tag);
+    }
+  }
+}
+
+cudaError_t launch_margin_combine_p2p(const TpPeers& peers, long long n_rows, float iota, float* margin, int* top1,
+                                      int* top2, float* lse, uint8_t* status, cudaStream_t st) {
+  const long long blocks = n_rows > 0 ? (n_rows + 127) / 128 : 1;
+  margin_combine_p2p_kernel<<<static_cast<unsigned>(blocks), 128, 0, st>>>(peers, n_rows, iota * kLog2e, iota,
+                                                                           margin, top1, top2, lse, status);
   return cudaGetLastError();
 }
 

@@ -100,4 +100,102 @@ relay_status_t relay_stats_allreduce(void* nccl_comm, uint64_t* stats, int32_t n
                      "ncclAllReduce");
 }
 
+// ------------------------------------------- N1 fused over peer memory
+struct relay_tp_exchange_s {
+  relay::TpPeers pe{};
+  float* own = nullptr;     // this rank's receive buffer (cudaMalloc)
+  int* counters = nullptr;  // [2]: epoch, done
+  bool opened[relay::kMaxTpRanks] = {};
+  int device = 0;
+};
+
+relay_status_t relay_tp_exchange_create(int32_t rank, int32_t world_size, int64_t rows_cap, uint8_t* ipc_handle_out,
+                                        relay_tp_exchange_t* out) {
+  if (!out || !ipc_handle_out) return relay::fail(RELAY_ERR_INVALID, "out and ipc_handle_out are required");
+  *out = nullptr;
+  if (world_size < 1 || world_size > relay::kMaxTpRanks || rank < 0 || rank >= world_size)
+    return relay::fail(RELAY_ERR_INVALID, "world_size must be in [1, %d] and rank in [0, world_size)",
+                       relay::kMaxTpRanks);
+  if (rows_cap < 1 || rows_cap > (1LL << 31)) return relay::fail(RELAY_ERR_INVALID, "rows_cap must be in [1, 2^31]");
+  auto* x = new relay_tp_exchange_s();
+  cudaGetDevice(&x->device);
+  const size_t bytes = sizeof(float) * 8 * 2 * static_cast<size_t>(world_size) * static_cast<size_t>(rows_cap);
+  cudaError_t e = cudaMalloc(&x->own, bytes);
+  if (e == cudaSuccess) e = cudaMemset(x->own, 0, bytes);  // tag 0 never matches a call's tag (>= 1)
+  if (e == cudaSuccess) e = cudaMalloc(&x->counters, 2 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(x->counters, 0, 2 * sizeof(int));
+  cudaIpcMemHandle_t h{};
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, x->own);
+  if (e != cudaSuccess) {
+    if (x->own) cudaFree(x->own);
+    if (x->counters) cudaFree(x->counters);
+    delete x;
+    return relay::fail(e == cudaErrorMemoryAllocation ? RELAY_ERR_ALLOC : RELAY_ERR_CUDA,
+                       "relay_tp_exchange_create: %s", cudaGetErrorString(e));
+  }
+  std::memcpy(ipc_handle_out, &h, RELAY_IPC_HANDLE_BYTES);
+  x->pe.world = world_size;
+  x->pe.rank = rank;
+  x->pe.rows_cap = rows_cap;
+  x->pe.epoch = x->counters;
+  x->pe.done = x->counters + 1;
+  x->pe.recv[rank] = x->own;
+  *out = x;
+  return RELAY_OK;
+}
+
+relay_status_t relay_tp_exchange_connect(relay_tp_exchange_t x, const uint8_t* ipc_handles) {
+  if (!x || !ipc_handles) return relay::fail(RELAY_ERR_INVALID, "x and ipc_handles are required");
+  for (int k = 0; k < x->pe.world; k++) {
+    if (k == x->pe.rank || x->opened[k]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, ipc_handles + static_cast<size_t>(k) * RELAY_IPC_HANDLE_BYTES, RELAY_IPC_HANDLE_BYTES);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return relay::fail(RELAY_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", k, cudaGetErrorString(e));
+    x->pe.recv[k] = static_cast<float*>(p);
+    x->opened[k] = true;
+  }
+  return RELAY_OK;
+}
+
+relay_status_t relay_tp_exchange_destroy(relay_tp_exchange_t x) {
+  if (!x) return RELAY_OK;
+  for (int k = 0; k < x->pe.world; k++)
+    if (x->opened[k]) cudaIpcCloseMemHandle(x->pe.recv[k]);
+  cudaFree(x->own);
+  cudaFree(x->counters);
+  delete x;
+  return RELAY_OK;
+}
+
+relay_status_t relay_margin_rows_tp(relay_tp_exchange_t x, const void* logits, relay_dtype_t dt, int64_t n_rows,
+                                    int64_t shard_vocab, int64_t row_stride, int64_t col_offset,
+                                    float inv_temperature, float* margin, int32_t* top1, int32_t* top2, float* lse,
+                                    uint8_t* row_status, relay_stream_t stream) {
+  if (!x) return relay::fail(RELAY_ERR_INVALID, "x is NULL");
+  for (int k = 0; k < x->pe.world; k++)
+    if (!x->pe.recv[k]) return relay::fail(RELAY_ERR_INVALID, "exchange not connected (rank %d)", k);
+  if (dt != RELAY_DT_BF16 && dt != RELAY_DT_F16 && dt != RELAY_DT_F32)
+    return relay::fail(RELAY_ERR_INVALID, "unknown dtype %d", static_cast<int>(dt));
+  if (shard_vocab < 1) return relay::fail(RELAY_ERR_INVALID, "shard_vocab must be >= 1");
+  if (col_offset < 0 || col_offset + shard_vocab >= 0x7fffffffLL)
+    return relay::fail(RELAY_ERR_INVALID, "col_offset out of range");
+  if (shard_vocab * (dt == RELAY_DT_F32 ? 4 : 2) >= 0x7fffffffLL)
+    return relay::fail(RELAY_ERR_INVALID, "row bytes must be < 2^31");
+  if (row_stride < shard_vocab) return relay::fail(RELAY_ERR_INVALID, "row_stride < shard_vocab");
+  if (n_rows < 0 || n_rows > x->pe.rows_cap) return relay::fail(RELAY_ERR_INVALID, "n_rows must be in [0, rows_cap]");
+  if (!(inv_temperature > 0.0f) || !(inv_temperature < INFINITY))
+    return relay::fail(RELAY_ERR_INVALID, "inv_temperature must be finite and > 0");
+  if (n_rows > 0 && (!logits || !margin)) return relay::fail(RELAY_ERR_INVALID, "logits and margin are required");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = relay::launch_margin_partials_p2p(logits, static_cast<int>(dt), n_rows, static_cast<int>(shard_vocab),
+                                                    row_stride, col_offset, inv_temperature, x->pe, st);
+  if (e == cudaSuccess)
+    e = relay::launch_margin_combine_p2p(x->pe, n_rows, inv_temperature, margin, top1, top2, lse, row_status, st);
+  if (e != cudaSuccess) return relay::fail(RELAY_ERR_CUDA, "relay_margin_rows_tp launch: %s", cudaGetErrorString(e));
+  return RELAY_OK;
+}
+
 }  // extern "C"

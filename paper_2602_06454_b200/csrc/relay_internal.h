@@ -99,6 +99,23 @@ cudaError_t launch_margin_combine(const float* part, int n_shards, long long n_r
                                   float* margin, int* top1, int* top2, float* lse, uint8_t* status,
                                   cudaStream_t st);
 
+// N1 fused with its exchange over peer memory (relay_margin_rows_tp): every
+// rank's receive buffer is recv[2][world][rows_cap][8] floats (parity = the
+// call's tag & 1); word 7 of a slot is the call's tag, stored with release
+// semantics after the other seven.  epoch / done live on the owning device.
+constexpr int kMaxTpRanks = 8;
+struct TpPeers {
+  float* recv[kMaxTpRanks];  // recv[k]: rank k's receive buffer (peer-mapped; own for k == rank)
+  int world, rank;
+  long long rows_cap;
+  int* epoch;                // device: tag of the last completed call
+  int* done;                 // device: combine CTAs finished (zero between calls)
+};
+cudaError_t launch_margin_partials_p2p(const void* logits, int dt, long long n_rows, int vocab, long long stride,
+                                       long long col_offset, float iota, const TpPeers& peers, cudaStream_t st);
+cudaError_t launch_margin_combine_p2p(const TpPeers& peers, long long n_rows, float iota, float* margin, int* top1,
+                                      int* top2, float* lse, uint8_t* status, cudaStream_t st);
+
 cudaError_t launch_cue_scan(const CueDev& cs, const int* tokens, long long n_tok,
                             const long long* offs, int n_traj, uint32_t* term_bits, int* occ_pos,
                             int* occ_pat, long long cap, long long* n_occ, const ScanWs& ws,

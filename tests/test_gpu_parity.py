@@ -688,6 +688,67 @@ def test_margin_tp_two_ranks_gloo(relay, tmp_path):
     assert (got["margin"] - full["margin"].cpu()).abs().max().item() < 2e-6
 
 
+def _tp_p2p_worker(rank, world, port, out):
+    import torch.distributed as dist
+    import paper_2602_06454_b200 as relay
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    V = 20011
+    bounds = [k * V // world for k in range(world + 1)]
+    a, b = bounds[rank], bounds[rank + 1]
+    x = relay.TpExchange(rows_cap=200, group=dist.group.WORLD)
+    res = []
+    for call, (n, seed) in enumerate([(96, 5), (200, 6), (0, 7), (37, 8), (96, 9)]):
+        L = synth.make_logits(max(n, 1), V, "bf16", seed=seed, device="cuda:0")[:n]
+        o = x.margin_rows(L[:, a:b], a)
+        torch.cuda.synchronize()
+        res.append({k: v.cpu() for k, v in o.items()})
+    if rank == 0:
+        torch.save(res, out)
+    dist.barrier()
+    x.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_margin_tp_p2p_fused(relay, tmp_path, world):
+    """relay_margin_rows_tp (the exchange fused into the streaming kernel over
+    CUDA-IPC peer memory), world ranks as processes on cuda:0: five
+    consecutive calls (both buffer parities, an empty call, row counts
+    below and at rows_cap) each equal the full-row kernel."""
+    import socket
+    import torch.multiprocessing as mp
+    sck = socket.socket(); sck.bind(("127.0.0.1", 0)); port = sck.getsockname()[1]; sck.close()
+    out = str(tmp_path / "tp_p2p.pt")
+    mp.spawn(_tp_p2p_worker, args=(world, port, out), nprocs=world, join=True)
+    got = torch.load(out)
+    for (n, seed), g in zip([(96, 5), (200, 6), (0, 7), (37, 8), (96, 9)], got):
+        assert g["margin"].shape[0] == n
+        if n == 0:
+            continue
+        L = synth.make_logits(n, 20011, "bf16", seed=seed, device=DEV)
+        full = relay.margin_rows(L)
+        torch.cuda.synchronize()
+        assert torch.equal(g["top1"], full["top1"].cpu()) and torch.equal(g["top2"], full["top2"].cpu())
+        assert torch.equal(g["status"], full["status"].cpu())
+        ok = full["status"].cpu() == 0
+        assert (g["margin"][ok] - full["margin"].cpu()[ok]).abs().max().item() < 2e-6
+
+
+def test_margin_tp_p2p_single_rank(relay, tmp_path):
+    """world 1: no peers; the fused path reduces to partial + combine on one GPU."""
+    import socket
+    import torch.multiprocessing as mp
+    sck = socket.socket(); sck.bind(("127.0.0.1", 0)); port = sck.getsockname()[1]; sck.close()
+    out = str(tmp_path / "tp_p2p1.pt")
+    mp.spawn(_tp_p2p_worker, args=(1, port, out), nprocs=1, join=True)
+    got = torch.load(out)
+    L = synth.make_logits(96, 20011, "bf16", seed=5, device=DEV)
+    full = relay.margin_rows(L)
+    torch.cuda.synchronize()
+    assert torch.equal(got[0]["top1"], full["top1"].cpu())
+
+
 # ------------------------------------------------------ N3 offload estimate
 def _offload_case(relay, h, ts, sel, mode=0, think=True):
     cs = relay.CueSet.from_synth(h, mode=mode)

@@ -1,5 +1,7 @@
 """A few eager relay_step_sample launches on configs[2] inputs (for ncu):
-    ncu --set full -k regex:sample_switch --launch-skip 3 -c 1 python tools/k5_once.py"""
+    ncu --set full -k regex:sample_switch --launch-skip 3 -c 1 python tools/k5_once.py [--edge] [--no-top-k]
+(--edge: the synthetic edge rows, incl. constant rows; --no-top-k: the
+R1-Distill setting, K5 + the nucleus kernel K6)"""
 import os
 import sys
 
@@ -21,8 +23,9 @@ hist = torch.full((B, 7), -1, dtype=torch.int32, device=dev)
 small = torch.zeros(B, dtype=torch.int32, device=dev)
 uni = torch.rand(B, device=dev)
 ws = relay.workspace(0, 0, B, dev)
-out = relay.step_sample(cs, bufs[0], uni, state, hist, small, ws=ws)
+top_k = 0 if "--no-top-k" in sys.argv else 20
+out = relay.step_sample(cs, bufs[0], uni, state, hist, small, top_k=top_k, ws=ws)
 for i in range(6):
-    relay.step_sample(cs, bufs[i % 4], uni, state, hist, small, ws=ws, out=out)
+    relay.step_sample(cs, bufs[i % 4], uni, state, hist, small, top_k=top_k, ws=ws, out=out)
 torch.cuda.synchronize()
 cs.destroy()

@@ -529,7 +529,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   if (warp == NCW) {
     // ------------------------------------------------ producer warp
     if (lane == 0) {
-      const uint64_t pol = a.keep_l2 ? policy_evict_last() : policy_evict_first();
+      const uint64_t pol = a.keep_l2 == 1 ? policy_evict_last()
+                           : a.keep_l2 == 2 ? policy_evict_normal() : policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
 #ifdef RELAY_TRACE
@@ -941,7 +942,11 @@ cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int b
   a.counter = ws.counter; a.part = ws.part; a.work = ws.work;
   a.flat = 0;  // whole rows: the bound needs every thread maximum of the row
   a.state = state; a.hist = hist; a.small_run = small_run; a.gate = gate; a.max_seg = max_seg;
-  a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk; a.keep_l2 = 1;
+  a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk;
+  {  // tuning knob (RELAY_K4_L2 = last | normal | first): the L2 policy of the margin pass
+    const char* e = getenv("RELAY_K4_L2");
+    a.keep_l2 = (e && !strcmp(e, "normal")) ? 2 : (e && !strcmp(e, "first")) ? 0 : 1;
+  }
   return launch_rows<kModeStep>(dt, a, cs, st);
 }
 

@@ -11,6 +11,8 @@
 // L2 only for small batches (B200's L2 holds ~60 MB per partition; configs[2]
 // is 78 MB); DESIGN.md records the single-pass variants that measured slower.
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "relay_device.cuh"
@@ -63,6 +65,7 @@ struct SampleArgs {
   int* slow_cnt;            // [2] K6 list length, K6 CTAs done (zero between launches)
   int* slow_list;           // [n_rows] rows K5 handed to K6
   float* zsum;              // [n_rows] K5's row mass at the sampling temperature (listed rows)
+  int k5_l2;                // tuning: 0 default policy, 1 evict_last, 2 evict_normal (RELAY_K5_L2)
   int* sampled;             // [n_rows] out
   uint8_t* state;
   int* hist;
@@ -98,72 +101,75 @@ __device__ __forceinline__ void push_candidate(float v, int j, float th, bool st
 }
 
 // Every finite logit >= th (> th when strict) of one row into the candidate
-// list (block-wide).
-template <class E>
+// list (block-wide).  MASS: also this thread's share of the row's mass at the
+// sampling temperature, sum_j 2^(z_j s_c - z1 s_c) (packed FFMA2 / FADD2,
+// MUFU.EX2; -inf entries give 2^-inf = 0).
+template <class E, bool MASS>
 __device__ float collect_candidates(const typename E::T* row, int vocab, float th, bool strict,
                                     float* s_cv, int* s_ci, int* s_cnt, float z1 = 0.0f,
-                                    float s_c = 0.0f, bool want_mass = false) {
-  float mass = 0.0f;  // this thread's share of sum_j 2^((z_j - z1) s_c) (want_mass)
+                                    float s_c = 0.0f, int k5_l2 = 0) {
   constexpr int VEC = 16 / E::SZ;
+  const float2 cc = make_float2(s_c, s_c);
+  const float2 nm = make_float2(-z1 * s_c, -z1 * s_c);
+  float2 acc = make_float2(0.0f, 0.0f);
   const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
   int head = static_cast<int>(((16 - (addr & 15)) & 15) / E::SZ);
   if (head > vocab) head = vocab;
   const int nvec = (vocab - head) / VEC;
   const int tail = head + nvec * VEC;
-  for (int j = threadIdx.x; j < head; j += blockDim.x) {
+  auto scalar = [&](int j) {
     const float x = E::load1(row + j);
     push_candidate(x, j, th, strict, s_cv, s_ci, s_cnt);
-    if (want_mass && x > -INFINITY) mass += ex2((x - z1) * s_c);
-  }
-  for (int j = tail + threadIdx.x; j < vocab; j += blockDim.x) {
-    const float x = E::load1(row + j);
-    push_candidate(x, j, th, strict, s_cv, s_ci, s_cnt);
-    if (want_mass && x > -INFINITY) mass += ex2((x - z1) * s_c);
-  }
+    if constexpr (MASS) acc.x += ex2(fmaf(x, s_c, nm.x));
+  };
+  for (int j = threadIdx.x; j < head; j += blockDim.x) scalar(j);
+  for (int j = tail + threadIdx.x; j < vocab; j += blockDim.x) scalar(j);
   const uint4* vp = reinterpret_cast<const uint4*>(row + head);
   // top-k mode: the row's last use, leave L2; nucleus mode: a slow row is read again
-  const uint64_t pol = want_mass ? policy_evict_normal() : policy_evict_first();
-  constexpr int U = 8;                        // loads in flight per thread
+  const uint64_t pol = k5_l2 == 1 ? policy_evict_last() : k5_l2 == 2 ? policy_evict_normal()
+                       : MASS ? policy_evict_normal() : policy_evict_first();
   const volatile int* cnt_v = s_cnt;
-  for (int v0 = threadIdx.x; v0 < nvec; v0 += U * blockDim.x) {
-    uint4 x[U];
+  auto body = [&](const uint4& xv, int v) {
+    if constexpr (MASS) {
+      float f[VEC];
+      unpack16<E>(xv, f);
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int v = v0 + u * blockDim.x;
-      x[u] = v < nvec ? ldg_hint(vp + v, pol) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int v = v0 + u * blockDim.x;
-      if (v >= nvec) continue;
-      if (want_mass) {
-        float f[VEC];
-        unpack16<E>(x[u], f);
-#pragma unroll
-        for (int k = 0; k < VEC; k++) mass += (f[k] > -INFINITY) ? ex2((f[k] - z1) * s_c) : 0.0f;
+      for (int k = 0; k < VEC; k += 2) {
+        const float2 y = __ffma2_rn(make_float2(f[k], f[k + 1]), cc, nm);
+        acc = __fadd2_rn(acc, make_float2(ex2(y.x), ex2(y.y)));
       }
-      // once the list overflowed only the fact matters (the caller resolves
-      // the row exactly): a constant row would otherwise queue one atomic per
-      // element on the counter
-      if (vec_max<E>(x[u]) >= th && *cnt_v <= kCandCap) {
-        float f[VEC];
-        unpack16<E>(x[u], f);
-        unsigned m = 0;
+    }
+    // once the list overflowed only the fact matters (the caller resolves
+    // the row exactly): a constant row would otherwise queue one atomic per
+    // element on the counter
+    if (vec_max<E>(xv) >= th && *cnt_v <= kCandCap) {
+      float f[VEC];
+      unpack16<E>(xv, f);
+      unsigned m = 0;
 #pragma unroll
-        for (int k = 0; k < VEC; k++) m |= ((strict ? f[k] > th : f[k] >= th) && f[k] > -INFINITY) ? (1u << k) : 0u;
-        if (m) {
-          int p = atomicAdd(s_cnt, __popc(m));  // one slot reservation per vector
-          while (m) {
-            const int k = __ffs(m) - 1;
-            m &= m - 1;
-            if (p < kCandCap) { s_cv[p] = f[k]; s_ci[p] = head + v * VEC + k; }
-            p++;
-          }
+      for (int k = 0; k < VEC; k++) m |= ((strict ? f[k] > th : f[k] >= th) && f[k] > -INFINITY) ? (1u << k) : 0u;
+      if (m) {
+        int p = atomicAdd(s_cnt, __popc(m));  // one slot reservation per vector
+        while (m) {
+          const int k = __ffs(m) - 1;
+          m &= m - 1;
+          if (p < kCandCap) { s_cv[p] = f[k]; s_ci[p] = head + v * VEC + k; }
+          p++;
         }
       }
     }
+  };
+  constexpr int U = 8;  // loads in flight per thread
+  int v0 = threadIdx.x;
+  for (; v0 + (U - 1) * static_cast<int>(blockDim.x) < nvec; v0 += U * blockDim.x) {  // full rounds
+    uint4 x[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) x[u] = ldg_hint(vp + v0 + u * blockDim.x, pol);
+#pragma unroll
+    for (int u = 0; u < U; u++) body(x[u], v0 + u * blockDim.x);
   }
-  return mass;
+  for (int v = v0; v < nvec; v += blockDim.x) body(ldg_hint(vp + v, pol), v);  // the last round
+  return acc.x + acc.y;
 }
 
 // The first `want` entries of the candidate list in (value desc, index asc)
@@ -299,7 +305,7 @@ __device__ __noinline__ int refine_topk(const typename E::T* row, int vocab, int
     __syncthreads();
     // nothing exceeds the row maximum (K4's): a constant top needs no pass
     if (theta == zmax) break;
-    collect_candidates<E>(row, vocab, theta, true, s_cv, s_ci, s_cnt);
+    collect_candidates<E, false>(row, vocab, theta, true, s_cv, s_ci, s_cnt);
     __syncthreads();
     if (*s_cnt <= kCandCap) break;
   }
@@ -879,7 +885,7 @@ __device__ __noinline__ int nucleus_draw_bf16(const typename E::T* row, int voca
   return -3;
 }
 
-template <class E>
+template <class E, bool NUC>
 __global__ void __launch_bounds__(kSampleThreads, 2) sample_switch_kernel(SampleArgs a, CueDev cs) {
   using T = typename E::T;
   __shared__ __align__(16) float s_cv[kCandCap];
@@ -907,12 +913,12 @@ __global__ void __launch_bounds__(kSampleThreads, 2) sample_switch_kernel(Sample
       in = load_switch_in(a.hist, a.state, a.small_run, nullptr, r);
       m = a.margin[r];
     }
-    const bool nucleus = a.topk == 0;    // no top-k: top-p over the whole row
+    constexpr bool nucleus = NUC;        // no top-k (a.topk == 0): top-p over the whole row
     const int kfast = nucleus ? kMaxTopK : a.topk;
     const float z1 = nucleus ? a.zmax[r] : 0.0f;
     TRACE5(0);
-    const float zpart = collect_candidates<E>(row, a.vocab, a.thk[r], false, s_cv, s_ci, &s_cnt, z1,
-                                              a.s_c, nucleus);
+    const float zpart =
+        collect_candidates<E, NUC>(row, a.vocab, a.thk[r], false, s_cv, s_ci, &s_cnt, z1, a.s_c, a.k5_l2);
     __syncthreads();
     TRACE5(1);
     const int st = a.status[r];   // uniform: every thread takes the same branches
@@ -1037,7 +1043,8 @@ static cudaError_t launch_sample_t(const SampleArgs& a, const CueDev& cs, cudaSt
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, sample_switch_kernel<E>, a, cs);
+  cudaError_t e = a.topk == 0 ? cudaLaunchKernelEx(&cfg, sample_switch_kernel<E, true>, a, cs)
+                              : cudaLaunchKernelEx(&cfg, sample_switch_kernel<E, false>, a, cs);
   if (e != cudaSuccess || a.topk != 0) return e;
   // no top-k: the nucleus kernel for the rows K5 listed
   cfg.gridDim = dim3(static_cast<unsigned>(a.n_rows < kSlowCtas ? a.n_rows : kSlowCtas));
@@ -1063,6 +1070,10 @@ cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
   a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
   a.slow_cnt = ws.work + 2; a.slow_list = ws.slow; a.zsum = ws.zsum;
+  {
+    const char* e = getenv("RELAY_K5_L2");
+    a.k5_l2 = (e && !strcmp(e, "last")) ? 1 : (e && !strcmp(e, "normal")) ? 2 : 0;
+  }
   switch (dt) {
     case 0: return launch_sample_t<EBf16>(a, cs, st);
     case 1: return launch_sample_t<EF16>(a, cs, st);

@@ -391,7 +391,12 @@ def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):
 
     from paper_2602_06454_b200.dist import allreduce_stats
     T, V = logits.shape
-    h_logits = torch.empty((T, V), dtype=logits.dtype, pin_memory=True)
+    pinned = True
+    try:
+        h_logits = torch.empty((T, V), dtype=logits.dtype, pin_memory=True)
+    except RuntimeError:   # pinned host memory exhausted (e.g. 8 ranks x 10 GB): pageable copies
+        pinned = False
+        h_logits = torch.empty((T, V), dtype=logits.dtype)
     h_logits.copy_(logits)
     h_tok = torch.from_numpy(ts.tokens.copy()).pin_memory()
     h_offs = torch.from_numpy(ts.traj_offsets.copy()).pin_memory()
@@ -434,7 +439,8 @@ def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):
     torch.cuda.empty_cache()
     return {"value": T * world * args.e2e_steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": args.e2e_steps,
-            "path": "pinned host logits+tokens -> H2D -> Analyzer.run (C ABI) -> D2H stats -> finalize"}
+            "pinned": pinned,
+            "path": "host logits+tokens -> H2D -> Analyzer.run (C ABI) -> D2H stats -> finalize"}
 
 
 def cpu_baseline(logits, ts, cs_h, dtype, vocab):

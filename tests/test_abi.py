@@ -241,3 +241,24 @@ def test_cueset_create_ex_validation(relay):
     assert lib.relay_cueset_create_ex(keep[0].ctypes.data_as(P), keep[1].ctypes.data_as(P), 1,
                                       keep[2].ctypes.data_as(P), 1, term.ctypes.data_as(P), V, -1,
                                       0, None, 1, None, C.byref(out)) == 1   # classes NULL, n=1
+
+
+def test_tp_exchange_validation_host(relay):
+    """N1 fused exchange: bad arguments fail on the host before any CUDA call."""
+    lib = C.CDLL(relay.LIB_PATH)
+    P = C.c_void_p
+    lib.relay_tp_exchange_create.argtypes = [C.c_int32, C.c_int32, C.c_int64, P, P]
+    lib.relay_tp_exchange_connect.argtypes = [P, P]
+    lib.relay_tp_exchange_destroy.argtypes = [P]
+    lib.relay_margin_rows_tp.argtypes = [P, P, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                         C.c_float, P, P, P, P, P, P]
+    h = (C.c_uint8 * relay.IPC_HANDLE_BYTES)()
+    out = C.c_void_p()
+    assert lib.relay_tp_exchange_create(0, 9, 16, h, C.byref(out)) == 1     # world > 8
+    assert lib.relay_tp_exchange_create(2, 2, 16, h, C.byref(out)) == 1     # rank >= world
+    assert lib.relay_tp_exchange_create(0, 2, 0, h, C.byref(out)) == 1      # rows_cap < 1
+    assert lib.relay_tp_exchange_create(0, 2, 16, None, C.byref(out)) == 1  # no handle buffer
+    assert lib.relay_tp_exchange_connect(None, h) == 1
+    assert lib.relay_tp_exchange_destroy(None) == 0
+    assert lib.relay_margin_rows_tp(None, None, 0, 4, 8, 8, 0, 1.0, None, None, None, None, None,
+                                    None) == 1

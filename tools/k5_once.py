@@ -12,7 +12,7 @@ import torch  # noqa: E402
 import paper_2602_06454_b200 as relay  # noqa: E402
 import synth  # noqa: E402
 
-B, V = 256, 152064
+B, V = int(os.environ.get("K5_BATCH", "256")), 152064
 dev = torch.device("cuda:0")
 h = synth.make_cueset(V, 8, 12, max_len=3)
 cs = relay.CueSet.from_synth(h)

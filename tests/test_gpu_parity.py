@@ -1157,6 +1157,33 @@ def test_step_sample_no_top_k_16bit_rows(relay, dtype):
         assert got[7] == -1 and 0 <= got[6] < 40
 
 
+@pytest.mark.parametrize("dtype,T,p", [("bf16", 0.6, 0.95), ("bf16", 1.0, 0.5), ("bf16", 0.6, 1.0),
+                                       ("f32", 0.6, 0.95), ("f16", 1.0, 0.9)])
+def test_step_sample_no_top_k_wide_nuclei(relay, dtype, T, p):
+    """No top-k on rows whose kept set reaches far past the top 64 (every row
+    takes the nucleus kernel K6): logits of scale 0.3-3 around offsets that
+    put z1 below and above the lump / key-range limits; the drawn token
+    matches the oracle sampler except at CDF edges."""
+    vocab, B = 32000, 96
+    h, cs = _cs_pair(relay, vocab, 2, 4, 2, seed=89)
+    rng = np.random.default_rng(90)
+    scale = rng.choice([0.3, 0.8, 1.5, 3.0], B)[:, None]
+    shift = rng.choice([-20.0, 0.0, 5.0, 40.0], B)[:, None]
+    rows = (rng.normal(0, 1, (B, vocab)) * scale + shift).astype(np.float32)
+    tdt = {"bf16": torch.bfloat16, "f16": torch.float16, "f32": torch.float32}[dtype]
+    L = torch.as_tensor(rows, device=DEV).to(tdt)
+    host = synth.host_rows(L, dtype)
+    u = rng.random(B).astype(np.float32)
+    st = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    hi = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    out = relay.step_sample(cs, L, torch.as_tensor(u, device=DEV), st, hi, temperature=T, top_k=0, top_p=p)
+    torch.cuda.synchronize()
+    got = out["sampled"].cpu().numpy()
+    want, n_edge = _oracle_sample_tolerant(host, dtype, vocab, u.astype(np.float64), got, T, 0, p)
+    assert n_edge <= 2
+    assert len(set(got.tolist())) > B // 2      # wide nuclei: mostly distinct draws
+
+
 def test_step_sample_graph_replay(relay):
     """Captured in a CUDA graph (PDL edges included) and replayed with new
     uniforms: every replay matches the oracle."""

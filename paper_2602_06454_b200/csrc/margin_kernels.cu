@@ -231,6 +231,8 @@ struct RowsArgs {
   float c, iota;
   int flat;       // 0: one item per row, rows strided over CTAs (K1)
                   // 1: each CTA takes an equal slice of the flattened rows
+                  // 3: hybrid: n_whole CTAs take one whole row each, the
+                  //    others equal slices of the remaining rows (K4)
                   // 2: rows cut into `chunk`-element chunks handed out by an
                   //    atomic work counter (K4; balances uneven SM service)
   float* margin;
@@ -242,6 +244,7 @@ struct RowsArgs {
   float* part;    // [n_rows][kMaxSplit][kPartWords] row-part partials (flat)
   int* work;      // [2] dynamic mode: next chunk, CTAs done (zero between launches)
   int chunk;      // dynamic mode: elements per chunk (a multiple of a ring stage)
+  long long n_whole;  // hybrid mode: rows taken whole (one per CTA)
   int cpr;        // dynamic mode: chunks per row (<= kMaxSplit)
   // vocabulary-parallel partials (kModePartial)
   long long col_offset;  // global index of the shard's first column
@@ -361,6 +364,8 @@ struct Item {
 struct ItemIter {
   long long next_w;  // strided: next row
   long long e, E1;   // flat: next element, end of this CTA's slice
+  long long row0;    // flat: first row of the sliced region (hybrid: the rows after the whole ones)
+  long long T, G, b; // flat: elements of the sliced region, its CTAs, this CTA's index among them
 
   // Slice boundaries by floating point (no 64-bit integer division on the
   // producer's critical path): any monotone rounding gives consistent slices,
@@ -380,11 +385,21 @@ struct ItemIter {
   }
   __device__ void init(const RowsArgs& a) {
     next_w = blockIdx.x;
-    if (a.flat == 1) {
-      const long long T = a.n_rows * a.vocab, G = gridDim.x;
-      const double Tg = static_cast<double>(T) / static_cast<double>(G);
-      e = slice_start(blockIdx.x, T, G, Tg);
-      E1 = slice_start(blockIdx.x + 1, T, G, Tg);
+    e = E1 = 0;
+    if (a.flat == 1 || a.flat == 3) {
+      // hybrid (3): CTAs [0, n_whole) take rows [0, n_whole) whole; the rest
+      // slice rows [n_whole, n_rows) equally (one whole row plus an equal
+      // share of the rest per SM, instead of one or two whole rows)
+      const long long nw = a.flat == 3 ? a.n_whole : 0;
+      row0 = nw;
+      T = (a.n_rows - nw) * a.vocab;
+      G = gridDim.x - nw;
+      b = static_cast<long long>(blockIdx.x) - nw;
+      if (b >= 0) {
+        const double Tg = static_cast<double>(T) / static_cast<double>(G);
+        e = slice_start(b, T, G, Tg);
+        E1 = slice_start(b + 1, T, G, Tg);
+      }
     }
   }
   // dynamic mode: chunk k of the n_rows * cpr chunks
@@ -396,23 +411,23 @@ struct ItemIter {
     return Item{r, j0, min(a.vocab, j0 + a.chunk), ch, a.cpr};
   }
   __device__ bool next(const RowsArgs& a, Item& it) {
-    if (!a.flat) {
-      if (next_w >= a.n_rows) return false;
+    if (!a.flat || (a.flat == 3 && b < 0)) {
+      if (next_w >= (a.flat == 3 ? a.n_whole : a.n_rows)) return false;
       it = Item{next_w, 0, a.vocab, 0, 1};
-      next_w += gridDim.x;
+      next_w = a.flat == 3 ? a.n_whole : next_w + gridDim.x;  // hybrid: one whole row
       return true;
     }
     if (e >= E1) return false;
-    const long long T = a.n_rows * a.vocab, G = gridDim.x, V = a.vocab;
+    const long long V = a.vocab;
     const double Tg = static_cast<double>(T) / static_cast<double>(G);
     long long r = static_cast<long long>(static_cast<double>(e) / static_cast<double>(V));
     while (r * V > e) r--;
     while ((r + 1) * V <= e) r++;
-    it.r = r;
+    it.r = row0 + r;
     it.j0 = static_cast<int>(e - r * V);
     it.j1 = static_cast<int>(min(V, E1 - r * V));
     const long long first = owner(r * V, T, G, Tg);
-    it.part = static_cast<int>(blockIdx.x - first);
+    it.part = static_cast<int>(b - first);
     it.nparts = static_cast<int>(owner(r * V + V - 1, T, G, Tg) - first + 1);
     e = (r + 1) * V;
     return true;
@@ -805,13 +820,17 @@ constexpr int kStages = RELAY_K1_STAGES;  // ring depth
 constexpr int kUV = RELAY_K1_UV;          // 16-byte vectors per consumer thread per stage
 constexpr int kMinBlocks = RELAY_K1_MINB; // CTAs per SM the registers must allow
 #ifndef RELAY_K4_STAGES
-#define RELAY_K4_STAGES 6
+#define RELAY_K4_STAGES 4
 #endif
 #ifndef RELAY_K4_MINB
 #define RELAY_K4_MINB 2
 #endif
+#ifndef RELAY_K4_NCW
+#define RELAY_K4_NCW 12   // 12 consumer warps x 4 stages of 24 KB (tools/k4_sweep.py: 20.5 vs 21.2 us at 8 x 6 x 16 KB)
+#endif
 constexpr int kStepStages = RELAY_K4_STAGES;
 constexpr int kStepMinBlocks = RELAY_K4_MINB;
+constexpr int kStepNCW = RELAY_K4_NCW;     // consumer warps per CTA in K4
 
 // K4 work split (RELAY_K4_MODE=strided|flat|dynamic overrides, for tuning
 // and tests): strided = one whole row per CTA, no cross-CTA merge (default
@@ -824,6 +843,7 @@ static int k4_mode(int batch) {
   if (e && !strcmp(e, "strided")) return 0;
   if (e && !strcmp(e, "flat")) return 1;
   if (e && !strcmp(e, "dynamic")) return 2;
+  if (e && !strcmp(e, "hybrid")) return batch > num_sms() ? 3 : 1;
   return batch >= num_sms() ? 0 : 1;
 }
 static int k4_chunk_stages() {
@@ -837,13 +857,14 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   // K4 runs ~1-2 CTAs per SM: a deeper ring keeps more bytes in flight per CTA
   constexpr int NS = (MODE == kModeStep) ? kStepStages : kStages;
   constexpr int MINB = (MODE == kModeStep) ? kStepMinBlocks : kMinBlocks;
-  auto kern = rows_kernel<E, kNCW, NS, kUV, MINB, MODE>;
-  const int smem = NS * kUV * kNCW * 32 * 16;
+  constexpr int NCW = (MODE == kModeStep) ? kStepNCW : kNCW;
+  auto kern = rows_kernel<E, NCW, NS, kUV, MINB, MODE>;
+  const int smem = NS * kUV * NCW * 32 * 16;
   static int per_sm = 0;
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 2) * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCW + 2) * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }
@@ -853,6 +874,20 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
     const long long total = a.n_rows * a.cpr;
     if (total >= (1LL << 31)) return cudaErrorInvalidValue;  // int work counter
     if (grid > total) grid = total;
+  } else if (a.flat == 3) {
+    // hybrid: one whole row per SM, the other slots slice the remaining rows
+    a.n_whole = num_sms();
+    if (a.n_rows <= a.n_whole || slots <= a.n_whole) {
+      a.flat = 0;
+      if (grid > a.n_rows) grid = a.n_rows;
+    } else {
+      const long long rest = (a.n_rows - a.n_whole) * a.vocab;
+      long long g2 = slots - a.n_whole;
+      if (rest >= (1LL << 51)) return cudaErrorInvalidValue;
+      if (g2 > rest / 128) g2 = rest / 128 > 0 ? rest / 128 : 1;
+      if (g2 > (a.n_rows - a.n_whole) * (kMaxSplit - 2)) g2 = (a.n_rows - a.n_whole) * (kMaxSplit - 2);
+      grid = a.n_whole + g2;
+    }
   } else if (a.flat) {
     // every slice at least 128 elements and a row in at most kMaxSplit parts
     const long long T = a.n_rows * a.vocab;
@@ -866,7 +901,7 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   if constexpr (MODE == kModeStep) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
-    cfg.blockDim = dim3((kNCW + 2) * 32);
+    cfg.blockDim = dim3((NCW + 2) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -876,7 +911,7 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a, cs);
   }
-  kern<<<static_cast<unsigned>(grid), (kNCW + 2) * 32, smem, st>>>(a, cs);
+  kern<<<static_cast<unsigned>(grid), (NCW + 2) * 32, smem, st>>>(a, cs);
   return cudaGetLastError();
 }
 
@@ -915,7 +950,7 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
     // dynamic mode: chunks of k4_chunk_stages() ring stages (fewer, larger
     // chunks if a row would need more than kMaxSplit parts)
     const int esz = dt == 2 ? 4 : 2;
-    const int stage_elems = kUV * kNCW * 32 * 16 / esz;
+    const int stage_elems = kUV * kStepNCW * 32 * 16 / esz;
     int chunk = k4_chunk_stages() * stage_elems;
     if ((vocab + chunk - 1) / chunk > kMaxSplit) {
       const int per = (vocab + kMaxSplit - 1) / kMaxSplit;

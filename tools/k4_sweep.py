@@ -1,7 +1,7 @@
 """Tuning sweep for K4 (relay_step_switch, configs[2]): build librelay
 variants (launch shape / NULL streaming ceiling) and time each with
 tools/bench_step.py's CUDA-graph loop.
-    python tools/k4_sweep.py build            # any host with nvcc
+    python tools/k4_sweep.py build [NAMES]    # any host with nvcc
     python tools/k4_sweep.py run NAME         # one variant on cuda:0
 Runtime knobs (env): RELAY_K4_MODE=strided|flat|dynamic,
 RELAY_K4_CHUNK_STAGES=n."""
@@ -14,11 +14,16 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 OUT = os.path.join(ROOT, "build", "k4_sweep")
 VARIANTS = {  # name -> defines
     "base": [],
+    "n8s6": ["RELAY_K4_NCW=8", "RELAY_K4_STAGES=6", "RELAY_K4_MINB=2"],   # the r01 mid-round default
     "null": ["RELAY_K1_NULL"],
     "s4m3": ["RELAY_K4_STAGES=4", "RELAY_K4_MINB=3"],
     "s5m2": ["RELAY_K4_STAGES=5", "RELAY_K4_MINB=2"],
     "s12m1": ["RELAY_K4_STAGES=12", "RELAY_K4_MINB=1"],
     "s8m1": ["RELAY_K4_STAGES=8", "RELAY_K4_MINB=1"],
+    "n12s4": ["RELAY_K4_NCW=12", "RELAY_K4_STAGES=4", "RELAY_K4_MINB=2"],
+    "n10s5": ["RELAY_K4_NCW=10", "RELAY_K4_STAGES=5", "RELAY_K4_MINB=2"],
+    "n16s3": ["RELAY_K4_NCW=16", "RELAY_K4_STAGES=3", "RELAY_K4_MINB=1"],
+    "n12s6m1": ["RELAY_K4_NCW=12", "RELAY_K4_STAGES=6", "RELAY_K4_MINB=1"],
 }
 
 
@@ -31,10 +36,12 @@ def _builder():
     return mod
 
 
-def build():
+def build(names=None):
     os.makedirs(OUT, exist_ok=True)
     b = _builder()
     for n, d in VARIANTS.items():
+        if names and n not in names:
+            continue
         b.build_lib(os.path.join(OUT, f"librelay_{n}.so"), defines=d or ["RELAY_K4_SWEEP_BASE"])
         print("built", n)
 
@@ -50,4 +57,4 @@ def run(name):
 
 
 if __name__ == "__main__":
-    build() if sys.argv[1] == "build" else run(sys.argv[2])
+    build(sys.argv[2:]) if sys.argv[1] == "build" else run(sys.argv[2])

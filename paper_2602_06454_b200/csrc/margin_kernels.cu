@@ -831,6 +831,10 @@ constexpr int kMinBlocks = RELAY_K1_MINB; // CTAs per SM the registers must allo
 constexpr int kStepStages = RELAY_K4_STAGES;
 constexpr int kStepMinBlocks = RELAY_K4_MINB;
 constexpr int kStepNCW = RELAY_K4_NCW;     // consumer warps per CTA in K4
+#ifndef RELAY_K4_UV
+#define RELAY_K4_UV 4
+#endif
+constexpr int kStepUV = RELAY_K4_UV;       // 16-byte vectors per consumer thread per stage in K4
 
 // K4 work split (RELAY_K4_MODE=strided|flat|dynamic overrides, for tuning
 // and tests): strided = one whole row per CTA, no cross-CTA merge (default
@@ -858,8 +862,9 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   constexpr int NS = (MODE == kModeStep) ? kStepStages : kStages;
   constexpr int MINB = (MODE == kModeStep) ? kStepMinBlocks : kMinBlocks;
   constexpr int NCW = (MODE == kModeStep) ? kStepNCW : kNCW;
-  auto kern = rows_kernel<E, NCW, NS, kUV, MINB, MODE>;
-  const int smem = NS * kUV * NCW * 32 * 16;
+  constexpr int UV = (MODE == kModeStep) ? kStepUV : kUV;
+  auto kern = rows_kernel<E, NCW, NS, UV, MINB, MODE>;
+  const int smem = NS * UV * NCW * 32 * 16;
   static int per_sm = 0;
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -950,7 +955,7 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
     // dynamic mode: chunks of k4_chunk_stages() ring stages (fewer, larger
     // chunks if a row would need more than kMaxSplit parts)
     const int esz = dt == 2 ? 4 : 2;
-    const int stage_elems = kUV * kStepNCW * 32 * 16 / esz;
+    const int stage_elems = kStepUV * kStepNCW * 32 * 16 / esz;
     int chunk = k4_chunk_stages() * stage_elems;
     if ((vocab + chunk - 1) / chunk > kMaxSplit) {
       const int per = (vocab + kMaxSplit - 1) / kMaxSplit;

@@ -21,6 +21,10 @@ VARIANTS = {  # name -> defines
     "s12m1": ["RELAY_K4_STAGES=12", "RELAY_K4_MINB=1"],
     "s8m1": ["RELAY_K4_STAGES=8", "RELAY_K4_MINB=1"],
     "n12s4": ["RELAY_K4_NCW=12", "RELAY_K4_STAGES=4", "RELAY_K4_MINB=2"],
+    "n14s3": ["RELAY_K4_NCW=14", "RELAY_K4_STAGES=3", "RELAY_K4_MINB=2"],
+    "n12u2s8": ["RELAY_K4_NCW=12", "RELAY_K4_UV=2", "RELAY_K4_STAGES=8", "RELAY_K4_MINB=2"],
+    "n12u2s6": ["RELAY_K4_NCW=12", "RELAY_K4_UV=2", "RELAY_K4_STAGES=6", "RELAY_K4_MINB=2"],
+    "n14u2s6": ["RELAY_K4_NCW=14", "RELAY_K4_UV=2", "RELAY_K4_STAGES=6", "RELAY_K4_MINB=2"],
     "n10s5": ["RELAY_K4_NCW=10", "RELAY_K4_STAGES=5", "RELAY_K4_MINB=2"],
     "n16s3": ["RELAY_K4_NCW=16", "RELAY_K4_STAGES=3", "RELAY_K4_MINB=1"],
     "n12s6m1": ["RELAY_K4_NCW=12", "RELAY_K4_STAGES=6", "RELAY_K4_MINB=1"],

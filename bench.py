@@ -293,6 +293,25 @@ def main():
         except Exception:
             traffic = None
 
+    # read-only HBM ceiling of this box over the same buffer (relay_read_probe,
+    # a measurement utility): K1's fraction is also quoted against it
+    read_gbs = None
+    if not args.profile:
+        probe_out = relay.read_probe(logits)
+        for _ in range(2):
+            relay.read_probe(logits, out=probe_out)
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(5):
+            relay.read_probe(logits, out=probe_out)
+        r1.record(stream)
+        torch.cuda.synchronize()
+        read_gbs = logits.numel() * logits.element_size() // 16 * 16 * 5 / (r0.elapsed_time(r1) / 1e3) / 1e9
+        if world > 1:
+            t = torch.tensor([read_gbs], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            read_gbs = float(t[0])
+
     e2e = None
     if not args.no_e2e and not args.profile:
         e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank)
@@ -318,7 +337,11 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if pk.get("hbm_gbs") else "fallback",
                          "frac_of_8TBs": achieved / 8000.0, "k1_ms": k1_ms,
                          "k1_share_of_step": k1_ms / (ms / args.steps),
-                         "algorithmic_bytes_per_launch": k1_bytes},
+                         "algorithmic_bytes_per_launch": k1_bytes,
+                         "read_peak_gbs": read_gbs,
+                         "frac_of_read_peak": (achieved / read_gbs) if read_gbs else None,
+                         "read_peak_source": "relay_read_probe (TMA bulk copies into a 3 x 32 KB ring, "
+                                             "2 CTAs per SM, no compute) over this run's logits buffer, 5 passes"},
             "gpu_launches": an.n_launches() * args.steps,
             "clocks": ck,
             "e2e": e2e,

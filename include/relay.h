@@ -78,6 +78,15 @@ typedef struct CUstream_st* relay_stream_t;   /* == cudaStream_t */
 typedef struct relay_cueset_s* relay_cueset_t; /* immutable after create; shareable */
 
 int relay_version(void);
+
+/* Measurement utility (not a step of the method): a read-only stream over
+ * `bytes` of device memory at `buf` (16-byte aligned, bytes % 16 == 0),
+ * XOR-folded into out[relay_read_probe_words()] (device, uint32, caller-owned;
+ * folded into, so zero it first if the value matters).  bench.py times it as
+ * the read-only HBM ceiling quoted next to K1's fraction of the copy peak.
+ * Errors: NULL pointers, misaligned buf, bad size. */
+int32_t relay_read_probe_words(void);
+relay_status_t relay_read_probe(const void* buf, int64_t bytes, uint32_t* out, relay_stream_t stream);
 const char* relay_status_string(relay_status_t s);
 const char* relay_last_error(void);
 

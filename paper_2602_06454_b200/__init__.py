@@ -64,6 +64,8 @@ def _load():
         "relay_nccl_unique_id": (C.c_int, [P]),
         "relay_nccl_comm_init": (C.c_int, [P, i32, i32, P]),
         "relay_nccl_comm_destroy": (C.c_int, [P]),
+        "relay_read_probe_words": (i32, []),
+        "relay_read_probe": (C.c_int, [P, i64, P, P]),
         "relay_tp_exchange_create": (C.c_int, [i32, i32, i64, P, P]),
         "relay_tp_exchange_connect": (C.c_int, [P, P]),
         "relay_tp_exchange_destroy": (C.c_int, [P]),
@@ -93,7 +95,8 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_nccl_unique_id", "relay_nccl_comm_init", "relay_nccl_comm_destroy",
            "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate",
            "relay_step_sample", "relay_tp_exchange_create", "relay_tp_exchange_connect",
-           "relay_tp_exchange_destroy", "relay_margin_rows_tp")
+           "relay_tp_exchange_destroy", "relay_margin_rows_tp", "relay_read_probe_words",
+           "relay_read_probe")
 
 
 def _check(rc: int, what: str):
@@ -211,6 +214,18 @@ def margin_rows_tp(logits_shard, col_offset: int, group=None, inv_temperature: f
                            device=part.device)
     dist.all_gather_into_tensor(gathered, part, group=group)   # ranks concatenated on dim 0
     return margin_combine(gathered.view(world, part.shape[0], part.shape[1]), inv_temperature)
+
+
+def read_probe(buf, out=None, stream=None):
+    """relay_read_probe: a read-only stream over ``buf`` (a measurement
+    utility: the read-only HBM ceiling bench.py quotes next to K1)."""
+    import torch
+    _need_cuda(buf)
+    if out is None:
+        out = torch.zeros(_lib.relay_read_probe_words(), dtype=torch.int32, device=buf.device)
+    _check(_lib.relay_read_probe(_ptr(buf), buf.numel() * buf.element_size() // 16 * 16, _ptr(out),
+                                 _stream(stream)), "relay_read_probe")
+    return out
 
 
 IPC_HANDLE_BYTES = 64

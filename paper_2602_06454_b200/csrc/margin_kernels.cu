@@ -1051,6 +1051,55 @@ cudaError_t launch_margin_combine(const float* part, int n_shards, long long n_r
   return cudaGetLastError();
 }
 
+// Measurement utility (not on the path): a read-only stream of `bytes` the
+// way K1 reads — 1-D TMA bulk copies (cp.async.bulk) of 32 KB into a 3-stage
+// shared-memory ring, one contiguous slice per CTA, 2 CTAs per SM — without
+// any compute; one word per CTA is folded into out so nothing is optimised
+// away.  bench.py times it over the logits buffer as the read-only HBM
+// ceiling that K1's fraction is also quoted against.
+constexpr int kProbeStages = 3;
+constexpr int kProbeChunk = 32768;
+
+__global__ void __launch_bounds__(32) read_probe_kernel(const char* __restrict__ p, long long bytes,
+                                                        unsigned* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[kProbeStages];
+  if (threadIdx.x != 0) return;
+  const uint32_t ring_s = smem_u32(ring), full_s = smem_u32(full);
+  for (int k = 0; k < kProbeStages; k++) mbar_init(full_s + 8 * k, 1);
+  fence_barrier_init();
+  const long long chunks = (bytes + kProbeChunk - 1) / kProbeChunk;
+  const long long per = (chunks + gridDim.x - 1) / gridDim.x;
+  const long long c0 = blockIdx.x * per, c1 = min(chunks, c0 + per);
+  const uint64_t pol = policy_evict_first();
+  for (long long c = c0; c < c1; c++) {
+    const int k = static_cast<int>((c - c0) % kProbeStages);
+    const long long it = (c - c0) / kProbeStages;
+    if (it > 0) mbar_wait(full_s + 8 * k, static_cast<uint32_t>((it - 1) & 1));
+    const uint32_t n = static_cast<uint32_t>(min(static_cast<long long>(kProbeChunk), bytes - c * kProbeChunk));
+    mbar_expect_tx(full_s + 8 * k, n);
+    bulk_g2s(ring_s + k * kProbeChunk, p + c * kProbeChunk, n, full_s + 8 * k, pol);
+  }
+  const long long n_it = c1 - c0;
+  for (int k = 0; k < kProbeStages && k < n_it; k++) {  // drain: the last copy of each stage
+    const long long last = ((n_it - 1 - k) / kProbeStages) * kProbeStages + k;
+    mbar_wait(full_s + 8 * k, static_cast<uint32_t>((last / kProbeStages) & 1));
+  }
+  atomicXor(out + blockIdx.x, *reinterpret_cast<const unsigned*>(ring));
+}
+
+cudaError_t launch_read_probe(const void* buf, long long bytes, unsigned* out, cudaStream_t st) {
+  const int smem = kProbeStages * kProbeChunk;
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(read_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  read_probe_kernel<<<2 * num_sms(), 32, smem, st>>>(static_cast<const char*>(buf), bytes, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_margin_partials_p2p(const void* logits, int dt, long long n_rows, int vocab, long long stride,
                                        long long col_offset, float iota, const TpPeers& peers, cudaStream_t st) {
   if (n_rows <= 0) return cudaSuccess;

@@ -109,6 +109,16 @@ extern "C" {
 
 int relay_version(void) { return RELAY_VERSION; }
 
+int32_t relay_read_probe_words(void) { return 2 * relay::num_sms(); }
+
+relay_status_t relay_read_probe(const void* buf, int64_t bytes, uint32_t* out, relay_stream_t stream) {
+  if (!buf || !out) return fail(RELAY_ERR_INVALID, "buf and out are required");
+  if (bytes < 16 || (bytes & 15) || (reinterpret_cast<uintptr_t>(buf) & 15))
+    return fail(RELAY_ERR_INVALID, "bytes must be a positive multiple of 16 and buf 16-byte aligned");
+  return cuda_status(relay::launch_read_probe(buf, bytes, out, reinterpret_cast<cudaStream_t>(stream)),
+                     "relay_read_probe launch");
+}
+
 const char* relay_status_string(relay_status_t s) {
   switch (s) {
     case RELAY_OK: return "ok";

@@ -103,6 +103,8 @@ cudaError_t launch_margin_combine(const float* part, int n_shards, long long n_r
 // rank's receive buffer is recv[2][world][rows_cap][8] floats (parity = the
 // call's tag & 1); word 7 of a slot is the call's tag, stored with release
 // semantics after the other seven.  epoch / done live on the owning device.
+int num_sms();
+cudaError_t launch_read_probe(const void* buf, long long bytes, unsigned* out, cudaStream_t st);
 constexpr int kMaxTpRanks = 8;
 struct TpPeers {
   float* recv[kMaxTpRanks];  // recv[k]: rank k's receive buffer (peer-mapped; own for k == rank)

@@ -262,3 +262,13 @@ def test_tp_exchange_validation_host(relay):
     assert lib.relay_tp_exchange_destroy(None) == 0
     assert lib.relay_margin_rows_tp(None, None, 0, 4, 8, 8, 0, 1.0, None, None, None, None, None,
                                     None) == 1
+
+
+def test_read_probe_validation_host(relay):
+    """The read-probe measurement utility rejects bad arguments on the host."""
+    lib = C.CDLL(relay.LIB_PATH)
+    lib.relay_read_probe.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+    assert lib.relay_read_probe(None, 64, C.c_void_p(16), None) == 1
+    assert lib.relay_read_probe(C.c_void_p(16), 15, C.c_void_p(16), None) == 1
+    assert lib.relay_read_probe(C.c_void_p(24), 64, C.c_void_p(16), None) == 1   # misaligned
+    assert lib.relay_read_probe_words() > 0

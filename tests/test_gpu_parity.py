@@ -1213,3 +1213,13 @@ def test_step_sample_graph_replay(relay):
         torch.cuda.synchronize()
         _oracle_sample_tolerant(host, "bf16", vocab, u.astype(np.float64), out["sampled"].cpu().numpy(),
                                 0.6, 20, 0.95)
+
+
+def test_read_probe_runs(relay):
+    """relay_read_probe (bench.py's read-only ceiling) streams buffers of any
+    multiple-of-16 size, including one smaller than a TMA chunk."""
+    for n in (16, 4096, 32768 * 7 + 48, 50_000_000):
+        buf = torch.ones(n // 2, dtype=torch.bfloat16, device=DEV)
+        out = relay.read_probe(buf)
+        torch.cuda.synchronize()
+        assert out.numel() == relay._lib.relay_read_probe_words()

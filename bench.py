@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-decode", action="store_true", help="skip the decode-step (configs[2]) line")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no clocks/e2e/baseline)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "p2p"],
+                    help="H6 over NCCL (relay_stats_allreduce) or over peer memory (relay_stats_allreduce_p2p)")
     ap.add_argument("--serial-scan", action="store_true",
                     help="run K2 before K1 on the main stream instead of on a side stream")
     return ap.parse_args()
@@ -230,6 +232,16 @@ def main():
     k1_ev = []
     results = []
 
+    xchg = None
+    if world > 1 and args.allreduce == "p2p":
+        xchg = relay.StatsExchange(cs.n_cues)
+
+    def h6(stats):
+        if xchg is not None:
+            xchg.stats_allreduce(stats, cs.n_cues)      # H6: relay_stats_allreduce_p2p (peer memory)
+        else:
+            allreduce_stats(stats, cs.n_cues, world)    # H6: relay_stats_allreduce (NCCL)
+
     def launch(i, timed=False):
         """Device side of step i: H1-H5 (K1 timed with events on its stream), H6, D2H."""
         e0 = e1 = None
@@ -240,7 +252,7 @@ def main():
         if timed:
             k1_ev.append((e0, e1))
         if world > 1:
-            allreduce_stats(an.stats, cs.n_cues, world)   # H6: relay_stats_allreduce (NCCL)
+            h6(an.stats)
         host_stats[i % 2].copy_(an.stats, non_blocking=True)
         done[i % 2].record(stream)
 
@@ -314,7 +326,7 @@ def main():
 
     e2e = None
     if not args.no_e2e and not args.profile:
-        e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank)
+        e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6)
     cpu = None
     if rank == 0 and not args.no_baseline and not args.profile:
         cpu = cpu_baseline(logits, ts, cs_h, dtype, vocab)
@@ -330,7 +342,8 @@ def main():
                        f"{dtype} logits (Qwen3-32B shape), {c['n_cues']} cues / {c['n_pat']} patterns, "
                        "margin+cue-scan+segment-reduce+stats (H1-H7), one trajectory per rank",
                        "rows_per_rank": T, "vocab": vocab, "l2": "inputs 9.96 GB/rank >> 126 MB L2, no flush",
-                       "parallelism": f"dp{world} (trajectory-sharded)"},
+                       "parallelism": f"dp{world} (trajectory-sharded)",
+                       "allreduce": (args.allreduce if world > 1 else None)},
             "hbm_gbs_step": (T * world * (vocab * esz + 17)) / (ms / 1e3 / args.steps) / 1e9 / world,
             "roofline": {"kernel": "relay_margin_rows (K1)", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -349,6 +362,9 @@ def main():
             "decode_step": decode,
         }
         print(json.dumps(line), flush=True)
+    if xchg is not None:
+        dist.barrier()
+        xchg.close()
     cs.destroy()
     if world > 1:
         dist.destroy_process_group()
@@ -405,7 +421,7 @@ def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
     return res
 
 
-def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):
+def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6):
     """Same metric through the public API with HOST inputs: every step copies the
     step's logits + tokens from pinned host memory, runs the pass, and reads the
     statistics table back."""
@@ -435,7 +451,7 @@ def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank):
         d_offs.copy_(h_offs, non_blocking=True)
         an.run(d_logits, d_tok, d_offs)
         if world > 1:
-            allreduce_stats(an.stats, cs.n_cues, world)
+            h6(an.stats)
         host_stats.copy_(an.stats, non_blocking=True)
         stream.synchronize()
         relay.stats_finalize(host_stats.numpy(), cs.n_cues, world)

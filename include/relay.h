@@ -168,6 +168,19 @@ relay_status_t relay_margin_rows_tp(relay_tp_exchange_t x, const void* logits_sh
                                     int32_t* top1, int32_t* top2, float* lse, uint8_t* row_status,
                                     relay_stream_t stream);
 
+/* relay_stats_allreduce_p2p — H6 without NCCL: the SUM all-reduce of the
+ * statistics table(s) over peer memory through a relay_tp_exchange_t created
+ * for the same group (its own handle: the call shares the exchange's epoch).
+ * One CTA per rank stores the table into every rank's slot (NVLink P2P), tags
+ * it (st.release.sys after a system fence), waits for every rank's tag
+ * (ld.acquire.sys) and sums the world slices in rank order into `stats`:
+ * bit-identical to relay_stats_allreduce.  Collective, stream-ordered.
+ * Size the exchange with rows_cap >= (table bytes + 8) / 32.
+ * Errors: as relay_stats_allreduce; world_size differing from the
+ * exchange's; a table that does not fit a slot (RELAY_ERR_INVALID). */
+relay_status_t relay_stats_allreduce_p2p(relay_tp_exchange_t x, uint64_t* stats, int32_t n_tables,
+                                         int32_t n_cues, int32_t world_size, relay_stream_t stream);
+
 /* ------------------------------------------------------------- cue set --
  * A model pair's switch-cue set (tab:switch_cue_sets) as token-ID
  * patterns (R5: the caller tokenises every surface variant) plus the sentence

@@ -70,6 +70,7 @@ def _load():
         "relay_tp_exchange_connect": (C.c_int, [P, P]),
         "relay_tp_exchange_destroy": (C.c_int, [P]),
         "relay_margin_rows_tp": (C.c_int, [P, P, C.c_int, i64, i64, i64, i64, f32, P, P, P, P, P, P]),
+        "relay_stats_allreduce_p2p": (C.c_int, [P, P, i32, i32, i32, P]),
         "relay_offload_estimate": (C.c_int, [P, i64, P, i32, P, P, P, P, i64, P, P, P, P]),
         "relay_stats_words": (sz, [i32, i32]),
         "relay_stats_finalize": (C.c_int, [P, i32, i32, i64, i32, P]),
@@ -96,7 +97,7 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate",
            "relay_step_sample", "relay_tp_exchange_create", "relay_tp_exchange_connect",
            "relay_tp_exchange_destroy", "relay_margin_rows_tp", "relay_read_probe_words",
-           "relay_read_probe")
+           "relay_read_probe", "relay_stats_allreduce_p2p")
 
 
 def _check(rc: int, what: str):
@@ -277,6 +278,14 @@ class TpExchange:
         _check(rc, "relay_margin_rows_tp")
         return out
 
+    def stats_allreduce(self, stats, n_cues: int, n_tables: int = 1, stream=None):
+        """relay_stats_allreduce_p2p: H6 over peer memory (no NCCL); the
+        exchange must be sized for the table (``StatsExchange`` does it)."""
+        _need_cuda(stats)
+        _check(_lib.relay_stats_allreduce_p2p(self._x, _ptr(stats), n_tables, n_cues, self.world,
+                                              _stream(stream)), "relay_stats_allreduce_p2p")
+        return stats
+
     def close(self):
         if getattr(self, "_x", None):
             _lib.relay_tp_exchange_destroy(self._x)
@@ -287,6 +296,14 @@ class TpExchange:
             self.close()
         except Exception:
             pass
+
+
+def StatsExchange(n_cues: int, n_tables: int = 1, group=None) -> "TpExchange":
+    """A peer-memory exchange sized for the statistics table(s) of ``n_cues``
+    over ``group`` (collective), for ``TpExchange.stats_allreduce``."""
+    import torch.distributed as dist
+    words = stats_words(n_cues, dist.get_world_size(group)) * n_tables
+    return TpExchange(rows_cap=(words * 8 + 8 + 31) // 32, group=group)
 
 
 # --------------------------------------------------------------- cue set

@@ -198,4 +198,24 @@ relay_status_t relay_margin_rows_tp(relay_tp_exchange_t x, const void* logits, r
   return RELAY_OK;
 }
 
+relay_status_t relay_stats_allreduce_p2p(relay_tp_exchange_t x, uint64_t* stats, int32_t n_tables, int32_t n_cues,
+                                         int32_t world_size, relay_stream_t stream) {
+  if (!x || !stats) return relay::fail(RELAY_ERR_INVALID, "x and stats are required");
+  if (n_tables < 1) return relay::fail(RELAY_ERR_INVALID, "n_tables < 1");
+  if (world_size != x->pe.world) return relay::fail(RELAY_ERR_INVALID, "world_size differs from the exchange's");
+  const size_t words = relay_stats_words(n_cues, world_size) * static_cast<size_t>(n_tables);
+  if (words == 0 || n_cues < 1) return relay::fail(RELAY_ERR_INVALID, "bad n_cues/world_size");
+  // a slot is rows_cap x 32 B: the table plus one tag word must fit
+  if (static_cast<long long>(words) * 8 + 8 > x->pe.rows_cap * 32)
+    return relay::fail(RELAY_ERR_INVALID, "exchange slots hold %lld B, the table needs %zu B + 8",
+                       x->pe.rows_cap * 32, words * 8);
+  for (int k = 0; k < x->pe.world; k++)
+    if (!x->pe.recv[k]) return relay::fail(RELAY_ERR_INVALID, "exchange not connected (rank %d)", k);
+  const cudaError_t e = relay::launch_stats_allreduce_p2p(x->pe, reinterpret_cast<unsigned long long*>(stats),
+                                                          static_cast<long long>(words),
+                                                          reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return relay::fail(RELAY_ERR_CUDA, "relay_stats_allreduce_p2p launch: %s", cudaGetErrorString(e));
+  return RELAY_OK;
+}
+
 }  // extern "C"

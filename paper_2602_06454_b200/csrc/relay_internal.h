@@ -115,6 +115,8 @@ struct TpPeers {
 };
 cudaError_t launch_margin_partials_p2p(const void* logits, int dt, long long n_rows, int vocab, long long stride,
                                        long long col_offset, float iota, const TpPeers& peers, cudaStream_t st);
+cudaError_t launch_stats_allreduce_p2p(const TpPeers& peers, unsigned long long* stats, long long words,
+                                       cudaStream_t st);
 cudaError_t launch_margin_combine_p2p(const TpPeers& peers, long long n_rows, float iota, float* margin, int* top1,
                                       int* top2, float* lse, uint8_t* status, cudaStream_t st);
 

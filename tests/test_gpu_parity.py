@@ -333,6 +333,62 @@ def test_stats_table_rank_split_is_bit_identical(relay):
     assert f1 == f2
 
 
+def _stats_p2p_worker(rank, world, port, out):
+    import torch.distributed as dist
+    import paper_2602_06454_b200 as relay
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    vocab, n_traj, L = 151936, 6, 3000
+    h = synth.make_cueset(vocab, 8, 12, max_len=3, seed=21)
+    cs = relay.CueSet.from_synth(h)
+    x = relay.StatsExchange(8, group=dist.group.WORLD)
+    res = []
+    for call in range(3):               # both buffer parities, then the first again
+        ts = synth.make_tokens(n_traj, L, h, seed=22 + call)
+        m = synth.make_margins(ts.tokens.shape[0], seed=23 + call)
+        t0, t1 = rank * n_traj // world, (rank + 1) * n_traj // world
+        lo, hi = int(ts.traj_offsets[t0]), int(ts.traj_offsets[t1])
+        tok = torch.as_tensor(ts.tokens[lo:hi], device="cuda:0")
+        offs = torch.as_tensor(ts.traj_offsets[t0:t1 + 1] - lo, device="cuda:0")
+        st = relay.new_stats(8, rank, world, "cuda:0")
+        relay.segment_reduce(cs, torch.as_tensor(m[lo:hi], device="cuda:0"), relay.cue_scan(cs, tok, offs), offs,
+                             stats=st, rank=rank, world_size=world)
+        x.stats_allreduce(st, 8)
+        torch.cuda.synchronize()
+        res.append(st.cpu())
+    if rank == 0:
+        torch.save(res, out)
+    dist.barrier()
+    x.close()
+    cs.destroy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_stats_allreduce_p2p(relay, tmp_path, world):
+    """H6 over peer memory (relay_stats_allreduce_p2p, no NCCL), world ranks
+    as processes on cuda:0: three consecutive all-reduces of per-rank
+    trajectory-shard tables each finalize exactly like the one-rank table
+    (counts and Q20 moments bit-identical, the min over the rank slots)."""
+    import socket
+    import torch.multiprocessing as mp
+    sck = socket.socket(); sck.bind(("127.0.0.1", 0)); port = sck.getsockname()[1]; sck.close()
+    out = str(tmp_path / "stats_p2p.pt")
+    mp.spawn(_stats_p2p_worker, args=(world, port, out), nprocs=world, join=True)
+    got = torch.load(out)
+    h, cs = _cs_pair(relay, 151936, 8, 12, 3, seed=21)
+    for call, g in enumerate(got):
+        ts = synth.make_tokens(6, 3000, h, seed=22 + call)
+        m = torch.as_tensor(synth.make_margins(ts.tokens.shape[0], seed=23 + call), device=DEV)
+        tok = torch.as_tensor(ts.tokens, device=DEV)
+        offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+        one = relay.segment_reduce(cs, m, relay.cue_scan(cs, tok, offs), offs)["stats"].cpu().numpy().reshape(9, 9)
+        tot = g.numpy().reshape(9, 8 + world)
+        np.testing.assert_array_equal(tot[:, :8], one[:, :8])
+        np.testing.assert_array_equal(tot[:, 8:].min(axis=1), one[:, 8])
+        assert relay.stats_finalize(tot.reshape(-1), 8, world, 1) == relay.stats_finalize(one.reshape(-1), 8, 1, 1)
+
+
 def test_segment_reduce_deterministic(relay):
     args = dict(n_traj=8, traj_len=4096, n_cues=8, n_pat=12, max_len=3, seed=31)
     a = _segment_case(relay, **args)

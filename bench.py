@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no clocks/e2e/baseline)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--allreduce", default="nccl", choices=["nccl", "p2p"],
-                    help="H6 over NCCL (relay_stats_allreduce) or over peer memory (relay_stats_allreduce_p2p)")
+                    help="H6 over NCCL (relay_stats_allreduce) or fused into K3 over peer memory "
+                         "(relay_segment_reduce_p2p)")
     ap.add_argument("--serial-scan", action="store_true",
                     help="run K2 before K1 on the main stream instead of on a side stream")
     return ap.parse_args()
@@ -222,8 +223,10 @@ def main():
     tok = torch.as_tensor(ts.tokens, device=dev)
     offs = torch.as_tensor(ts.traj_offsets, device=dev)
     tep = torch.as_tensor(ts.think_end_pos, device=dev)
+    # --allreduce p2p: H6 fused into K3 over peer memory (relay_segment_reduce_p2p)
+    xchg = relay.StatsExchange(cs.n_cues) if (world > 1 and args.allreduce == "p2p") else None
     an = relay.Analyzer(cs, T, vocab, dev, rank=rank, world_size=world,
-                        overlap_scan=not args.serial_scan)
+                        overlap_scan=not args.serial_scan, exchange=xchg)
     stream = torch.cuda.current_stream()
     # two pinned host tables: step i's table is finalized on the host while the
     # GPU already runs step i+1 (the work per step is unchanged)
@@ -232,14 +235,8 @@ def main():
     k1_ev = []
     results = []
 
-    xchg = None
-    if world > 1 and args.allreduce == "p2p":
-        xchg = relay.StatsExchange(cs.n_cues)
-
     def h6(stats):
-        if xchg is not None:
-            xchg.stats_allreduce(stats, cs.n_cues)      # H6: relay_stats_allreduce_p2p (peer memory)
-        else:
+        if xchg is None:                                # (p2p: already summed by K3's last CTA)
             allreduce_stats(stats, cs.n_cues, world)    # H6: relay_stats_allreduce (NCCL)
 
     def launch(i, timed=False):

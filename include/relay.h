@@ -181,6 +181,24 @@ relay_status_t relay_margin_rows_tp(relay_tp_exchange_t x, const void* logits_sh
 relay_status_t relay_stats_allreduce_p2p(relay_tp_exchange_t x, uint64_t* stats, int32_t n_tables,
                                          int32_t n_cues, int32_t world_size, relay_stream_t stream);
 
+/* relay_segment_reduce_p2p — relay_segment_reduce (H3-H5) with H6 fused into
+ * the same kernel: the CTA that finishes the table last all-reduces it (all
+ * n_tables tables) over peer memory exactly as relay_stats_allreduce_p2p
+ * does, so the table leaves K3 already summed over the group (compute and
+ * collective in one kernel; no NCCL).  Collective over the exchange's group:
+ * every rank calls it once per pass (n_tok may be 0 on a rank).  Arguments
+ * as relay_segment_reduce plus the exchange (rank / world_size must be the
+ * exchange's; slots sized for the tables, e.g. via a StatsExchange).
+ * Errors: as relay_segment_reduce and relay_stats_allreduce_p2p. */
+relay_status_t relay_segment_reduce_p2p(relay_tp_exchange_t x, relay_cueset_t cs, const float* margin,
+                                        int64_t n_tok, const int64_t* traj_offsets, int32_t n_traj,
+                                        const int64_t* think_end_pos, const uint32_t* term_bits,
+                                        const int32_t* occ_pos, const int32_t* occ_pat, const int64_t* n_occ,
+                                        int64_t occ_capacity, float tau, int32_t* seg_end, float* seg_mean,
+                                        float* seg_min, float* seg_lowfrac, uint64_t* stats, int32_t rank,
+                                        int32_t world_size, uint32_t flags, void* ws, size_t ws_bytes,
+                                        relay_stream_t stream);
+
 /* ------------------------------------------------------------- cue set --
  * A model pair's switch-cue set (tab:switch_cue_sets) as token-ID
  * patterns (R5: the caller tokenises every surface variant) plus the sentence

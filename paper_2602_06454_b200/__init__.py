@@ -57,6 +57,8 @@ def _load():
         "relay_cue_scan": (C.c_int, [P, P, i64, P, i32, P, P, P, i64, P, P, sz, P]),
         "relay_segment_reduce": (C.c_int, [P, P, i64, P, i32, P, P, P, P, P, i64, f32, P, P, P, P,
                                            P, i32, i32, u32, P, sz, P]),
+        "relay_segment_reduce_p2p": (C.c_int, [P, P, P, i64, P, i32, P, P, P, P, P, i64, f32, P, P, P, P,
+                                               P, i32, i32, u32, P, sz, P]),
         "relay_stats_init": (C.c_int, [P, i32, i32, i32, P]),
         "relay_stats_init_tables": (C.c_int, [P, i32, i32, i32, i32, P]),
         "relay_stats_merge": (C.c_int, [P, i32, P, i32, i32, P]),
@@ -97,7 +99,7 @@ EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_ma
            "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate",
            "relay_step_sample", "relay_tp_exchange_create", "relay_tp_exchange_connect",
            "relay_tp_exchange_destroy", "relay_margin_rows_tp", "relay_read_probe_words",
-           "relay_read_probe", "relay_stats_allreduce_p2p")
+           "relay_read_probe", "relay_stats_allreduce_p2p", "relay_segment_reduce_p2p")
 
 
 def _check(rc: int, what: str):
@@ -502,9 +504,11 @@ class NcclComm:
 # ---------------------------------------------------------------- H3-H5
 def segment_reduce(cs: CueSet, margin, scan: dict, traj_offsets=None, think_end_pos=None,
                    tau: float = 0.5, stats=None, rank: int = 0, world_size: int = 1, ws=None,
-                   out=None, stream=None, per_trajectory: bool = False):
+                   out=None, stream=None, per_trajectory: bool = False, exchange=None):
     """H3-H5.  ``per_trajectory``: one stats table per trajectory (merge with
-    ``stats_merge``)."""
+    ``stats_merge``).  ``exchange`` (a ``StatsExchange``): H6 fused into the
+    same kernel — its last CTA all-reduces the finished table(s) over peer
+    memory (relay_segment_reduce_p2p; collective over the exchange's group)."""
     import torch
     _need_cuda(margin, traj_offsets, think_end_pos)
     n_tok = margin.shape[0]
@@ -524,15 +528,15 @@ def segment_reduce(cs: CueSet, margin, scan: dict, traj_offsets=None, think_end_
                    seg_mean=torch.empty(c1, dtype=torch.float32, device=dev),
                    seg_min=torch.empty(c1, dtype=torch.float32, device=dev),
                    seg_lowfrac=torch.empty(c1, dtype=torch.float32, device=dev))
-    rc = _lib.relay_segment_reduce(cs.handle, _ptr(margin), n_tok, _ptr(traj_offsets), n_traj,
-                                   _ptr(think_end_pos), _ptr(scan["term_bits"]),
-                                   _ptr(scan["occ_pos"]), _ptr(scan["occ_pat"]),
-                                   _ptr(scan["n_occ"]), cap, float(tau), _ptr(out["seg_end"]),
-                                   _ptr(out["seg_mean"]), _ptr(out["seg_min"]),
-                                   _ptr(out["seg_lowfrac"]), _ptr(stats), rank, world_size,
-                                   1 if per_trajectory else 0, _ptr(ws), ws.numel(),
-                                   _stream(stream))
-    _check(rc, "relay_segment_reduce")
+    args = (cs.handle, _ptr(margin), n_tok, _ptr(traj_offsets), n_traj, _ptr(think_end_pos),
+            _ptr(scan["term_bits"]), _ptr(scan["occ_pos"]), _ptr(scan["occ_pat"]), _ptr(scan["n_occ"]),
+            cap, float(tau), _ptr(out["seg_end"]), _ptr(out["seg_mean"]), _ptr(out["seg_min"]),
+            _ptr(out["seg_lowfrac"]), _ptr(stats), rank, world_size, 1 if per_trajectory else 0,
+            _ptr(ws), ws.numel(), _stream(stream))
+    if exchange is not None:
+        _check(_lib.relay_segment_reduce_p2p(exchange._x, *args), "relay_segment_reduce_p2p")
+    else:
+        _check(_lib.relay_segment_reduce(*args), "relay_segment_reduce")
     out["stats"] = stats
     return out
 
@@ -642,13 +646,14 @@ class Analyzer:
 
     def __init__(self, cs: CueSet, n_tok: int, vocab: int, device="cuda", occ_capacity=None,
                  tau: float = 0.5, rank: int = 0, world_size: int = 1, inv_temperature=1.0,
-                 overlap_scan: bool = True, per_trajectory_tables: int = 0):
+                 overlap_scan: bool = True, per_trajectory_tables: int = 0, exchange=None):
         """``per_trajectory_tables`` = n_traj keeps one stats table per
         trajectory (``stats_merge`` any subset on the host); 0 = one table."""
         import torch
         self.cs, self.n_tok, self.vocab, self.tau = cs, n_tok, vocab, tau
         self.rank, self.world_size, self.iota = rank, world_size, inv_temperature
         self.overlap_scan = overlap_scan
+        self.exchange = exchange          # StatsExchange: H6 fused into K3 (peer memory)
         self.device = torch.device(device)
         self.cap = (n_tok * (cs.n_cues if cs.mode else 1)) if occ_capacity is None else occ_capacity
         d = self.device
@@ -701,7 +706,7 @@ class Analyzer:
             s.wait_event(self._join)
         segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
                        self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s,
-                       per_trajectory=self.per_traj)
+                       per_trajectory=self.per_traj, exchange=self.exchange)
         return self.stats
 
     def run_streamed(self, chunks, tokens, traj_offsets=None, think_end_pos=None, stream=None,
@@ -730,7 +735,7 @@ class Analyzer:
         s.wait_event(self._join)
         segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
                        self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s,
-                       per_trajectory=self.per_traj)
+                       per_trajectory=self.per_traj, exchange=self.exchange)
         return self.stats
 
     def capture(self, logits, tokens, traj_offsets=None, think_end_pos=None, host_stats=None,

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "p2p.cuh"
 #include "relay_device.cuh"
 #include "relay_internal.h"
 #include "switch.cuh"
@@ -1173,45 +1174,10 @@ __global__ void margin_combine_p2p_kernel(TpPeers pe, long long n_rows, float c,
   }
 }
 
-// H6 over peer memory (relay_stats_allreduce_p2p): one CTA pushes this
-// rank's uint64 table into every rank's slot [parity][rank] (NVLink P2P
-// stores), publishes it with one release-tagged word after a system fence,
-// waits (acquire) for every rank's tag in its own buffer and sums the world
-// slices in rank order into `stats` — the same order on every rank, so the
-// result is bit-identical everywhere (integer addition is exact anyway).
+// H6 over peer memory (relay_stats_allreduce_p2p): p2p.cuh, one CTA.
 __global__ void __launch_bounds__(256) stats_allreduce_p2p_kernel(TpPeers pe, unsigned long long* stats,
                                                                   long long words) {
-  const unsigned tag = static_cast<unsigned>(*reinterpret_cast<const volatile int*>(pe.epoch)) + 1u;
-  const long long slot_words = pe.rows_cap * kPartWords / 2;  // u64 words per slot (32 B rows)
-  const long long par = static_cast<long long>(tag & 1u) * pe.world;
-  for (int k = 0; k < pe.world; k++) {
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(pe.recv[k]) + (par + pe.rank) * slot_words;
-    for (long long w = threadIdx.x; w < words; w += blockDim.x) dst[w] = stats[w];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    for (int k = 0; k < pe.world; k++) {
-      unsigned* flag = reinterpret_cast<unsigned*>(reinterpret_cast<unsigned long long*>(pe.recv[k]) +
-                                                   (par + pe.rank) * slot_words + words);
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(tag) : "memory");
-    }
-    const unsigned long long* own = reinterpret_cast<const unsigned long long*>(pe.recv[pe.rank]);
-    for (int k = 0; k < pe.world; k++) {
-      const float* flag = reinterpret_cast<const float*>(own + (par + k) * slot_words + words);
-      while (ld_acquire_sys(flag) != tag) {
-      }
-    }
-  }
-  __syncthreads();
-  const unsigned long long* own = reinterpret_cast<const unsigned long long*>(pe.recv[pe.rank]);
-  for (long long w = threadIdx.x; w < words; w += blockDim.x) {
-    unsigned long long sum = 0;
-    for (int k = 0; k < pe.world; k++) sum += __ldcg(own + (par + k) * slot_words + w);
-    stats[w] = sum;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *reinterpret_cast<volatile int*>(pe.epoch) = static_cast<int>(tag);
+  p2p_allreduce_block(pe, stats, words);
 }
 
 cudaError_t launch_stats_allreduce_p2p(const TpPeers& peers, unsigned long long* stats, long long words,

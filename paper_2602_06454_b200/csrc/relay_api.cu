@@ -390,7 +390,7 @@ relay_status_t relay_stats_merge(const uint64_t* tables, int32_t n_tables, const
   return RELAY_OK;
 }
 
-relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int64_t n_tok,
+static relay_status_t segment_reduce_impl(relay_tp_exchange_t x, relay_cueset_t cs, const float* margin, int64_t n_tok,
                                     const int64_t* traj_offsets, int32_t n_traj, const int64_t* think_end_pos,
                                     const uint32_t* term_bits, const int32_t* occ_pos, const int32_t* occ_pat,
                                     const int64_t* n_occ, int64_t occ_capacity, float tau, int32_t* seg_end,
@@ -409,6 +409,17 @@ relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int6
   if (think_end_pos && !traj_offsets) return fail(RELAY_ERR_INVALID, "think_end_pos needs traj_offsets");
   relay_status_t s = check_offsets_args(traj_offsets, n_traj);
   if (s != RELAY_OK) return s;
+  const long long n_tables = (flags & RELAY_SEG_PER_TRAJECTORY) ? (traj_offsets ? n_traj : 1) : 1;
+  const long long words = static_cast<long long>(relay_stats_words(relay_cueset_n_cues(cs), world_size)) * n_tables;
+  if (x) {
+    if (x->pe.world != world_size || x->pe.rank != rank)
+      return fail(RELAY_ERR_INVALID, "rank/world_size differ from the exchange's");
+    for (int k = 0; k < x->pe.world; k++)
+      if (!x->pe.recv[k]) return fail(RELAY_ERR_INVALID, "exchange not connected (rank %d)", k);
+    if (words * 8 + 8 > x->pe.rows_cap * 32)
+      return fail(RELAY_ERR_INVALID, "exchange slots hold %lld B, the table(s) need %lld B + 8",
+                  x->pe.rows_cap * 32, words * 8);
+  }
   ScanWs w = scan_ws_layout(ws, n_tok, occ_capacity);
   if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
   return cuda_status(
@@ -418,8 +429,33 @@ relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int6
                             occ_capacity, tau, seg_end, seg_mean, seg_min, seg_lowfrac,
                             reinterpret_cast<unsigned long long*>(stats), rank, world_size,
                             (flags & RELAY_SEG_PER_TRAJECTORY) ? 1 : 0, w,
-                            reinterpret_cast<cudaStream_t>(stream)),
+                            reinterpret_cast<cudaStream_t>(stream), x ? &x->pe : nullptr, words),
       "relay_segment_reduce launch");
+}
+
+relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int64_t n_tok,
+                                    const int64_t* traj_offsets, int32_t n_traj, const int64_t* think_end_pos,
+                                    const uint32_t* term_bits, const int32_t* occ_pos, const int32_t* occ_pat,
+                                    const int64_t* n_occ, int64_t occ_capacity, float tau, int32_t* seg_end,
+                                    float* seg_mean, float* seg_min, float* seg_lowfrac, uint64_t* stats,
+                                    int32_t rank, int32_t world_size, uint32_t flags, void* ws,
+                                    size_t ws_bytes, relay_stream_t stream) {
+  return segment_reduce_impl(nullptr, cs, margin, n_tok, traj_offsets, n_traj, think_end_pos, term_bits, occ_pos,
+                             occ_pat, n_occ, occ_capacity, tau, seg_end, seg_mean, seg_min, seg_lowfrac, stats,
+                             rank, world_size, flags, ws, ws_bytes, stream);
+}
+
+relay_status_t relay_segment_reduce_p2p(relay_tp_exchange_t x, relay_cueset_t cs, const float* margin, int64_t n_tok,
+                                        const int64_t* traj_offsets, int32_t n_traj, const int64_t* think_end_pos,
+                                        const uint32_t* term_bits, const int32_t* occ_pos, const int32_t* occ_pat,
+                                        const int64_t* n_occ, int64_t occ_capacity, float tau, int32_t* seg_end,
+                                        float* seg_mean, float* seg_min, float* seg_lowfrac, uint64_t* stats,
+                                        int32_t rank, int32_t world_size, uint32_t flags, void* ws,
+                                        size_t ws_bytes, relay_stream_t stream) {
+  if (!x) return fail(RELAY_ERR_INVALID, "x is NULL");
+  return segment_reduce_impl(x, cs, margin, n_tok, traj_offsets, n_traj, think_end_pos, term_bits, occ_pos,
+                             occ_pat, n_occ, occ_capacity, tau, seg_end, seg_mean, seg_min, seg_lowfrac, stats,
+                             rank, world_size, flags, ws, ws_bytes, stream);
 }
 
 relay_status_t relay_offload_estimate(relay_cueset_t cs, int64_t n_tok, const int64_t* traj_offsets,

@@ -101,13 +101,6 @@ relay_status_t relay_stats_allreduce(void* nccl_comm, uint64_t* stats, int32_t n
 }
 
 // ------------------------------------------- N1 fused over peer memory
-struct relay_tp_exchange_s {
-  relay::TpPeers pe{};
-  float* own = nullptr;     // this rank's receive buffer (cudaMalloc)
-  int* counters = nullptr;  // [2]: epoch, done
-  bool opened[relay::kMaxTpRanks] = {};
-  int device = 0;
-};
 
 relay_status_t relay_tp_exchange_create(int32_t rank, int32_t world_size, int64_t rows_cap, uint8_t* ipc_handle_out,
                                         relay_tp_exchange_t* out) {

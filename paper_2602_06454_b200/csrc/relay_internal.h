@@ -125,13 +125,15 @@ cudaError_t launch_cue_scan(const CueDev& cs, const int* tokens, long long n_tok
                             int* occ_pat, long long cap, long long* n_occ, const ScanWs& ws,
                             cudaStream_t st);
 
+struct TpPeers;
 cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long long n_tok,
                                   const long long* offs, int n_traj, const long long* think_end,
                                   const uint32_t* term_bits, const int* occ_pos, const int* occ_pat,
                                   const long long* n_occ, long long cap, float tau, int* seg_end,
                                   float* seg_mean, float* seg_min, float* seg_lowfrac,
                                   unsigned long long* stats, int rank, int world, int per_traj,
-                                  const ScanWs& ws, cudaStream_t st);
+                                  const ScanWs& ws, cudaStream_t st, const TpPeers* pe = nullptr,
+                                  long long pe_words = 0);
 
 cudaError_t launch_offload_estimate(const CueDev& cs, long long n_tok, const long long* offs, int n_traj,
                                     const long long* think_end, const int* occ_pos, const int* occ_pat,
@@ -161,3 +163,13 @@ cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int
                                cudaStream_t st);
 
 }  // namespace relay
+
+// The opaque relay_tp_exchange_t of include/relay.h (relay_comm.cu owns it;
+// relay_api.cu reads the peer table for relay_segment_reduce_p2p).
+struct relay_tp_exchange_s {
+  relay::TpPeers pe{};
+  float* own = nullptr;     // this rank's receive buffer (cudaMalloc)
+  int* counters = nullptr;  // [2]: epoch, done
+  bool opened[relay::kMaxTpRanks] = {};
+  int device = 0;
+};

@@ -16,6 +16,7 @@
 // Both are tiny next to K1 (4 B per token vs ~300 KB per logit row).
 #include <cfloat>
 
+#include "p2p.cuh"
 #include "relay_device.cuh"
 #include "relay_internal.h"
 
@@ -363,8 +364,11 @@ __global__ void __launch_bounds__(kScanThreads)
                      const int* __restrict__ occ_pat, const long long* __restrict__ n_occ_p, long long cap,
                      int* __restrict__ seg_end, float* __restrict__ seg_mean, float* __restrict__ seg_min,
                      float* __restrict__ seg_lowfrac, unsigned long long* __restrict__ stats, int nf,
-                     int rank, int per_traj, int* tile_flag, Agg* tile_val, int* done) {
+                     int rank, int per_traj, int* tile_flag, Agg* tile_val, int* done, TpPeers pe,
+                     long long pe_words) {
   // per_traj: one table per trajectory ([n_traj][(n_cues+1)*nf]) instead of one
+  // pe.world > 0 (relay_segment_reduce_p2p): the last CTA then all-reduces the
+  // pe_words table words over peer memory (H6 fused into K3, p2p.cuh)
   const long long table_words = static_cast<long long>(cs.n_cues + 1) * nf;
   __shared__ Agg s_w[kScanThreads / 32];
   __shared__ Agg s_carry;
@@ -564,15 +568,20 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 
   // ---- the last tile to finish resets the look-back flags for the next launch
+  // (and, fused H6, all-reduces the finished table over peer memory)
+  __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(done, 1) == n_tiles - 1) {
+    s_last = atomicAdd(done, 1) == n_tiles - 1;
+    if (s_last) {
       for (int j = 0; j < n_tiles; j++) tile_flag[j] = 0;
       __threadfence();
       *done = 0;
     }
   }
+  __syncthreads();
+  if (pe.world > 0 && s_last) p2p_allreduce_block(pe, stats, pe_words);
 }
 
 // ------------------------------------------------- N3 offload estimate
@@ -671,14 +680,18 @@ cudaError_t launch_segment_reduce(const CueDev& cs, const float* margin, long lo
                                   const long long* n_occ, long long cap, float tau, int* seg_end,
                                   float* seg_mean, float* seg_min, float* seg_lowfrac,
                                   unsigned long long* stats, int rank, int world, int per_traj,
-                                  const ScanWs& ws, cudaStream_t st) {
-  if (n_tok <= 0) return cudaSuccess;
+                                  const ScanWs& ws, cudaStream_t st, const TpPeers* pe, long long pe_words) {
+  if (n_tok <= 0) {  // nothing to reduce, but the collective still happens
+    return pe ? launch_stats_allreduce_p2p(*pe, stats, pe_words, st) : cudaSuccess;
+  }
   const int nt = n_tiles_of(n_tok);
   const int nf = kStatFields + world;
+  TpPeers none{};
   seg_fused_kernel<<<nt, kScanThreads, 0, st>>>(cs, margin, term_bits, n_tok, offs, n_traj, think_end,
                                                 tau, occ_pos, occ_pat, n_occ, cap, seg_end, seg_mean,
                                                 seg_min, seg_lowfrac, stats, nf, rank, per_traj,
-                                                ws.tile_flag, ws.tile_val, ws.done);
+                                                ws.tile_flag, ws.tile_val, ws.done, pe ? *pe : none,
+                                                pe_words);
   return cudaGetLastError();
 }
 

@@ -333,7 +333,7 @@ def test_stats_table_rank_split_is_bit_identical(relay):
     assert f1 == f2
 
 
-def _stats_p2p_worker(rank, world, port, out):
+def _stats_p2p_worker(rank, world, port, out, fused=False):
     import torch.distributed as dist
     import paper_2602_06454_b200 as relay
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -352,8 +352,9 @@ def _stats_p2p_worker(rank, world, port, out):
         offs = torch.as_tensor(ts.traj_offsets[t0:t1 + 1] - lo, device="cuda:0")
         st = relay.new_stats(8, rank, world, "cuda:0")
         relay.segment_reduce(cs, torch.as_tensor(m[lo:hi], device="cuda:0"), relay.cue_scan(cs, tok, offs), offs,
-                             stats=st, rank=rank, world_size=world)
-        x.stats_allreduce(st, 8)
+                             stats=st, rank=rank, world_size=world, exchange=x if fused else None)
+        if not fused:
+            x.stats_allreduce(st, 8)
         torch.cuda.synchronize()
         res.append(st.cpu())
     if rank == 0:
@@ -364,17 +365,19 @@ def _stats_p2p_worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_stats_allreduce_p2p(relay, tmp_path, world):
-    """H6 over peer memory (relay_stats_allreduce_p2p, no NCCL), world ranks
-    as processes on cuda:0: three consecutive all-reduces of per-rank
+def test_stats_allreduce_p2p(relay, tmp_path, world, fused):
+    """H6 over peer memory (no NCCL), world ranks as processes on cuda:0:
+    relay_stats_allreduce_p2p after K3, or fused into K3's last CTA
+    (relay_segment_reduce_p2p).  Three consecutive passes of per-rank
     trajectory-shard tables each finalize exactly like the one-rank table
     (counts and Q20 moments bit-identical, the min over the rank slots)."""
     import socket
     import torch.multiprocessing as mp
     sck = socket.socket(); sck.bind(("127.0.0.1", 0)); port = sck.getsockname()[1]; sck.close()
     out = str(tmp_path / "stats_p2p.pt")
-    mp.spawn(_stats_p2p_worker, args=(world, port, out), nprocs=world, join=True)
+    mp.spawn(_stats_p2p_worker, args=(world, port, out, fused), nprocs=world, join=True)
     got = torch.load(out)
     h, cs = _cs_pair(relay, 151936, 8, 12, 3, seed=21)
     for call, g in enumerate(got):

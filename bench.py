@@ -41,8 +41,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="relay", choices=["relay", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c5"],
+                    help="c2 (default, the metric's workload); c1; c5: the cue-set sweep corpus "
+                         "(8 x 16,384-token trajectories per rank, 32 patterns of length 1-6, logits "
+                         "streamed in --chunk-rows chunks from a ~10 GB buffer pool)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--chunk-rows", type=int, default=8192, help="c5: logit rows per streamed chunk")
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true", help="skip the decode-step (configs[2]) line")
@@ -189,6 +193,9 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == "c5":
+        run_c5(args)
         return
     import torch
     import torch.distributed as dist
@@ -357,6 +364,120 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "decode_step": decode,
+        }
+        print(json.dumps(line), flush=True)
+    if xchg is not None:
+        dist.barrier()
+        xchg.close()
+    cs.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_c5(args):
+    """configs[4]: per rank 8 trajectories x 16,384 tokens (64 at N = 8), 32
+    cue patterns of length 1-6; each step streams the 131,072 logit rows in
+    --chunk-rows chunks from a ~10 GB pool of pre-generated chunk buffers (>>
+    L2: every chunk streams from HBM; the 318 GB corpus never exists at once)
+    through Analyzer.run_streamed (K1 per chunk, K2 on a side stream, K3 +
+    H6 once), then the table to the host and H7."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_06454_b200 as relay
+    import synth
+    from paper_2602_06454_b200.dist import allreduce_stats
+    rank, world, local = dist_env()
+    if os.environ.get("RELAY_BENCH_SAME_DEVICE") == "1":
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
+    c = synth.CONFIGS["c5"]
+    V, L, NT = c["vocab"], c["traj_len"], 8
+    R = args.chunk_rows                                   # rows per chunk (divides 8 x 16,384)
+    K = max(2, int(10e9 // (R * V * 2)))                  # pool of ~10 GB >> L2
+    cs_h = synth.make_cueset(V, c["n_cues"], c["n_pat"], max_len=c["max_len"], min_len=1)
+    cs = relay.CueSet.from_synth(cs_h)
+    ts = synth.make_tokens(NT, L, cs_h, seed=synth.BASE_SEED + 5 + rank)
+    n = ts.tokens.shape[0]
+    pool = [synth.make_logits(R, V, "bf16", seed=synth.BASE_SEED + 1000 * rank + i, device=dev) for i in range(K)]
+    tok = torch.as_tensor(ts.tokens, device=dev)
+    offs = torch.as_tensor(ts.traj_offsets, device=dev)
+    tep = torch.as_tensor(ts.think_end_pos, device=dev)
+    xchg = relay.StatsExchange(cs.n_cues) if (world > 1 and args.allreduce == "p2p") else None
+    an = relay.Analyzer(cs, n, V, dev, rank=rank, world_size=world, exchange=xchg)
+    stream = torch.cuda.current_stream()
+    host_stats = torch.empty(an.stats.shape, dtype=torch.int64, pin_memory=True)
+    k1_ev = []
+
+    def step(timed=False):
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) if timed else None
+        an.run_streamed(((i * R, pool[i % K]) for i in range(n // R)), tok, offs, tep, k1_events=ev)
+        if timed:
+            k1_ev.append(ev)
+        if world > 1 and xchg is None:
+            allreduce_stats(an.stats, cs.n_cues, world)
+        host_stats.copy_(an.stats, non_blocking=True)
+        stream.synchronize()
+        relay.stats_finalize(host_stats.numpy(), cs.n_cues, world)
+
+    for _ in range(args.warmup):
+        step()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(timed=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    k1_ms = statistics.mean(a.elapsed_time(b) for a, b in k1_ev)
+    if world > 1:
+        t = torch.tensor([ms, k1_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, k1_ms = float(t[0]), float(t[1])
+    pk = peaks()
+    peak = pk.get("hbm_gbs") or 6650.0
+    k1_bytes = n * (V * 2 + 17)
+    achieved = k1_bytes / (k1_ms / 1e3) / 1e9
+    cpu = None
+    if rank == 0 and not args.no_baseline:
+        cpu = cpu_baseline(pool[0], ts, cs_h, "bf16", V)   # chunk 0 = pool[0] = rows 0..R-1
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n * world * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"c5: {world} x {NT} trajectories x {L} tokens x {V}-vocab bf16 logits streamed "
+                                   f"in {R}-row chunks from a {K}-buffer pool, {c['n_cues']} cues / "
+                                   f"{c['n_pat']} patterns of length 1-{c['max_len']}, H1-H7",
+                       "rows_per_rank": n, "vocab": V,
+                       "l2": f"chunk pool {K * R * V * 2 / 1e9:.1f} GB >> 126 MB L2, no flush",
+                       "parallelism": f"dp{world} (trajectory-sharded)",
+                       "allreduce": (args.allreduce if world > 1 else None)},
+            "roofline": {"kernel": "relay_margin_rows (K1), all chunks of a step", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "k1_ms": k1_ms, "k1_share_of_step": k1_ms / (ms / args.steps),
+                         "algorithmic_bytes_per_launch": k1_bytes // (n // R),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if pk.get("hbm_gbs") else "fallback"},
+            "gpu_launches": (n // R + 4) * args.steps,
+            "clocks": ck,
+            "e2e": None,
+            "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if xchg is not None:

@@ -710,7 +710,7 @@ class Analyzer:
         return self.stats
 
     def run_streamed(self, chunks, tokens, traj_offsets=None, think_end_pos=None, stream=None,
-                     vocab=None):
+                     vocab=None, k1_events=None):
         """The same pass with the logits streamed in row chunks (configs[4]: a
         corpus larger than HBM).  ``chunks`` yields (first_row, logits[R, V]);
         each chunk's margins land at their row offset, then H2-H5 run once over
@@ -727,11 +727,15 @@ class Analyzer:
         cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
         self._join.record(self._side)
         stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s, self.n_tables)
+        if k1_events:
+            k1_events[0].record(s)
         for r0, chunk in chunks:
             r1 = r0 + chunk.shape[0]
             out = {k: (v[r0:r1] if v is not None else None) for k, v in self.rows.items()}
             margin_rows(chunk, vocab=vocab or self.vocab, inv_temperature=self.iota, out=out,
                         stream=s)
+        if k1_events:
+            k1_events[1].record(s)
         s.wait_event(self._join)
         segment_reduce(self.cs, self.rows["margin"], self.scan, traj_offsets, think_end_pos,
                        self.tau, self.stats, self.rank, self.world_size, self.ws, self.seg, s,

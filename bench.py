@@ -490,8 +490,9 @@ def run_c5(args):
 
 def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
     """H8 on configs[2] (256 live rows x 152,064 bf16 per step): relay_step_switch
-    (K4) and relay_step_sample (K4 + K5, T 0.6 / top-p 0.95 / top-k 20), each as a
-    CUDA graph over 7 rotating logits buffers (> 4 x L2), device-timed."""
+    (K4) and relay_step_sample (K4 + K5, T 0.6 / top-p 0.95 / top-k 20; and
+    without top-k, + K6), each as a CUDA graph over 7 rotating logits buffers
+    (> 4 x L2), device-timed; "hot" repeats one buffer (L2-resident)."""
     import torch
     h = synth.make_cueset(V, 8, 12, max_len=3)
     cs = relay.CueSet.from_synth(h)
@@ -530,7 +531,23 @@ def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
         torch.cuda.synchronize(dev)
         us = e0.elapsed_time(e1) * 1e3 / (reps * len(bufs))
         gbs = res["bytes_per_step"] / (us * 1e-6) / 1e9
+        # "hot": the same buffer every step (L2-resident, as right after the LM-head GEMM)
+        gh = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(gh, stream=s):
+                for _ in bufs:
+                    fn(bufs[0], out)
+        torch.cuda.synchronize(dev)
+        gh.replay()
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(reps):
+            gh.replay()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        us_hot = e0.elapsed_time(e1) * 1e3 / (reps * len(bufs))
         res[name] = {"us_per_step": us, "rows_per_s": B / (us * 1e-6), "gbs": gbs, "frac": gbs / peak,
+                     "us_per_step_hot": us_hot,
                      "kernels": "K4" if name == "switch" else "K4 + K5",
                      "sampling": {"switch": "token given", "sample": "T 0.6, top-p 0.95, top-k 20 (Qwen3)",
                                   "sample_no_top_k": "T 0.6, top-p 0.95 (R1-Distill)"}[name]}

@@ -546,8 +546,14 @@ def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
         e1.record()
         torch.cuda.synchronize(dev)
         us_hot = e0.elapsed_time(e1) * 1e3 / (reps * len(bufs))
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mufu_peak = 16 * sms * 1.965e9          # MUFU.EX2 per second at the max SM clock
         res[name] = {"us_per_step": us, "rows_per_s": B / (us * 1e-6), "gbs": gbs, "frac": gbs / peak,
                      "us_per_step_hot": us_hot,
+                     # K4 needs one exp per element: the SFU (MUFU) roofline of the margin pass
+                     "mufu": {"bound": "alu", "achieved_gexp_s": B * V / (us * 1e-6) / 1e9,
+                              "peak_gexp_s": mufu_peak / 1e9, "frac": B * V / (us * 1e-6) / mufu_peak,
+                              "peak_source": "16 MUFU.EX2/clk/SM x SMs x 1965 MHz (guide unit counts)"},
                      "kernels": "K4" if name == "switch" else "K4 + K5",
                      "sampling": {"switch": "token given", "sample": "T 0.6, top-p 0.95, top-k 20 (Qwen3)",
                                   "sample_no_top_k": "T 0.6, top-p 0.95 (R1-Distill)"}[name]}

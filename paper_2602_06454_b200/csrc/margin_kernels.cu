@@ -266,7 +266,8 @@ struct RowsArgs {
   float* zmax;    // [n_rows] with thk: the row maximum (the sampler's reference)
   int topk;       // 0 = off
   int keep_l2;    // L2 evict_last: the sampling kernel reads the rows again
-                  // (hits only when the batch's logits fit the L2: ~64 rows)
+  int* row_ready; // relay_step_sample: per-row completion counters (release), so
+                  // K5 starts a row as soon as its margin pass is done
 };
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
@@ -539,7 +540,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   // before touching global data it may have produced.  Outside a PDL launch
   // both instructions are no-ops.
   if constexpr (MODE == kModeStep) {
-    if (tid == 0) pdl_launch_dependents();
+    // with row_ready (relay_step_sample) the dependent K5 is released only
+    // after every CTA passed griddepcontrol.wait (the epilogue warp below):
+    // K5 then waits per row on row_ready, and every earlier kernel is done
+    if (tid == 0 && !a.row_ready) pdl_launch_dependents();
   }
 
   if (warp == NCW) {
@@ -601,6 +605,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     if constexpr (MODE == kModeStep) {  // the switch patterns, for this warp only
       load_smem_cue(cs, sc);
       pdl_wait();
+      if (lane == 0 && a.row_ready) pdl_launch_dependents();
     }
     ItemIter iter;
     iter.init(a);
@@ -638,6 +643,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           a.zmax[r] = q.t.v1;
         }
         finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in);
+        if (a.row_ready && lane == 0)  // lane 0 wrote thk/zmax/margin/top1/top2/status: publish
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.row_ready + r) : "memory");
         continue;
       }
       // publish this part; the last part of the row to arrive finishes it
@@ -983,7 +990,7 @@ cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int b
   a.counter = ws.counter; a.part = ws.part; a.work = ws.work;
   a.flat = 0;  // whole rows: the bound needs every thread maximum of the row
   a.state = state; a.hist = hist; a.small_run = small_run; a.gate = gate; a.max_seg = max_seg;
-  a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk;
+  a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk; a.row_ready = ws.row_ready;
   {  // tuning knob (RELAY_K4_L2 = last | normal | first): the L2 policy of the margin pass
     const char* e = getenv("RELAY_K4_L2");
     a.keep_l2 = (e && !strcmp(e, "normal")) ? 2 : (e && !strcmp(e, "first")) ? 0 : 1;

@@ -81,6 +81,8 @@ struct StepWs {
   uint8_t* status;     // [batch] relay_step_sample: K4's row status
   float* zmax;         // [batch] relay_step_sample: K4's row maximum
   int* slow;           // [batch] relay_step_sample: rows handed to the nucleus kernel
+  int* row_ready;      // [batch] relay_step_sample: margin passes completed per row (K4, release)
+  int* row_done;       // [batch] relay_step_sample: rows sampled per row (K5)
   float* zsum;         // [batch] relay_step_sample: their mass at the sampling temperature
   size_t bytes;
 };

@@ -66,6 +66,8 @@ struct SampleArgs {
   int* slow_list;           // [n_rows] rows K5 handed to K6
   float* zsum;              // [n_rows] K5's row mass at the sampling temperature (listed rows)
   int k5_l2;                // tuning: 0 default policy, 1 evict_last, 2 evict_normal (RELAY_K5_L2)
+  const int* row_ready;     // [n_rows] K4's per-row completion counters (acquire)
+  int* row_done;            // [n_rows] rows this kernel has taken, per row
   int* sampled;             // [n_rows] out
   uint8_t* state;
   int* hist;
@@ -899,9 +901,20 @@ __global__ void __launch_bounds__(kSampleThreads, 2) sample_switch_kernel(Sample
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0) load_smem_cue(cs, sc);  // immutable cue set: before the dependency wait
   if (threadIdx.x == 0) pdl_launch_dependents();
-  pdl_wait();  // K4's outputs (thk, status, margin) and the switch state
+  // no grid-wide wait: K4 releases this kernel only after all its CTAs passed
+  // their own dependency wait, and publishes each row (thk, status, margin,
+  // top-2) with a release increment of row_ready[r]; a row starts as soon as
+  // its margin pass is done, overlapping K4's tail
   for (long long r = blockIdx.x; r < a.n_rows; r += gridDim.x) {
-    if (threadIdx.x == 0) s_cnt = 0;
+    if (threadIdx.x == 0) {
+      s_cnt = 0;
+      const int want = a.row_done[r] + 1;
+      int got;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(a.row_ready + r) : "memory");
+      } while (got < want);
+      a.row_done[r] = want;   // read again only by the next step's K5 (after this grid)
+    }
     __syncthreads();
     const T* row = static_cast<const T*>(a.logits) + r * a.stride;
     // warp 0's per-row inputs are fetched before the scan so that their
@@ -1070,6 +1083,7 @@ cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
   a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
   a.slow_cnt = ws.work + 2; a.slow_list = ws.slow; a.zsum = ws.zsum;
+  a.row_ready = ws.row_ready; a.row_done = ws.row_done;
   {
     const char* e = getenv("RELAY_K5_L2");
     a.k5_l2 = (e && !strcmp(e, "last")) ? 1 : (e && !strcmp(e, "normal")) ? 2 : 0;

@@ -299,8 +299,22 @@ __device__ __noinline__ int refine_topk(const typename E::T* row, int vocab, int
                                         int* s_ci, int* s_cnt, float* s_topv, int* s_topi, int* s_k,
                                         int* s_scan) {
   float theta;
+  // at least topk entries of the (partial) list equal the row maximum: the
+  // top-k are the lowest-index entries at the maximum (a constant row; no
+  // ranking of the full list, which costs ~18 us when every value ties)
+  int at_max = 0;  // entries of the list equal to the row maximum (block-uniform)
+  for (int e0 = 0; e0 < kCandCap; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    at_max += __syncthreads_count(e < kCandCap && s_cv[e] == zmax);
+  }
+  if (at_max >= topk) {
+    theta = zmax;
+    if (threadIdx.x == 0) *s_cnt = 0;
+    __syncthreads();
+  } else {
   for (;;) {
     if (rank_list(topk, kCandCap, s_cv, s_ci, s_topv, s_topi, s_k) < topk) return *s_k;
+    TRACE5(6);
     theta = s_topv[topk - 1];
     __syncthreads();
     if (threadIdx.x == 0) *s_cnt = 0;
@@ -311,6 +325,7 @@ __device__ __noinline__ int refine_topk(const typename E::T* row, int vocab, int
     __syncthreads();
     if (*s_cnt <= kCandCap) break;
   }
+  }
   const int c = *s_cnt;
   if (c >= topk) return rank_list(topk, c, s_cv, s_ci, s_topv, s_topi, s_k);
   // the lowest-index entries equal to theta, in index order
@@ -319,6 +334,7 @@ __device__ __noinline__ int refine_topk(const typename E::T* row, int vocab, int
     s_cv[c + r] = theta;
     s_ci[c + r] = idx;
   });
+  TRACE5(7);
   return rank_list(topk, c + need, s_cv, s_ci, s_topv, s_topi, s_k);
 }
 
@@ -630,13 +646,75 @@ __device__ __noinline__ void select_by_mass(const typename E::T* row, int vocab,
   }
 }
 
-// Index of the j-th (0-based, index order) entry equal to v.
+// Index of the j-th (0-based, index order) entry equal to v.  One counting
+// pass with every load of the row in flight (warp w counts the ties in its
+// contiguous range of 16-byte vectors, coalesced), a scan over the warp
+// ranges, then the index-ordered scan (tie_scan) of the one range that holds
+// the j-th tie — instead of walking the row chunk by chunk from the start
+// (a constant row's draw sits ~half-way: ~10 chunk latencies).
 template <class E>
 __device__ int tie_index(const typename E::T* row, int vocab, float v, int j, int* s_scan, int* s_found) {
+  constexpr int VEC = 16 / E::SZ, U = 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(row);
+  int head = static_cast<int>(((16 - (addr & 15)) & 15) / E::SZ);
+  if (head > vocab) head = vocab;
+  const int nvec = (vocab - head) / VEC;
+  const int tail = head + nvec * VEC;
+  const int per = (nvec + nw - 1) / nw;  // vectors per warp range
+  const int lo = min(nvec, warp * per), hi = min(nvec, lo + per);
+  const uint4* vp = reinterpret_cast<const uint4*>(row + head);
+  int cnt = 0;
+  for (int i0 = lo; i0 < hi; i0 += 32 * U) {
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int i = i0 + u * 32 + lane;
+      if (i < hi) r[u] = __ldg(vp + i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int i = i0 + u * 32 + lane;
+      if (i >= hi) continue;
+      float f[VEC];
+      unpack16<E>(r[u], f);
+#pragma unroll
+      for (int k = 0; k < VEC; k++) cnt += f[k] == v;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  __shared__ int s_w, s_base;
+  if (lane == 0) s_scan[warp] = cnt;
   if (threadIdx.x == 0) *s_found = -1;
-  tie_scan<E>(row, vocab, v, j + 1, s_scan, [&](int r, int idx) {
-    if (r == j) *s_found = idx;
-  });
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // the head scalars come first in index order, then the warp ranges, then the tail
+    int run = 0, w_sel = -1;
+    for (int k = 0; k < head; k++)
+      if (E::load1(row + k) == v) { if (run == j) *s_found = k; run++; }
+    if (*s_found < 0) {
+      for (int w = 0; w < nw; w++) {
+        if (run + s_scan[w] > j) { w_sel = w; break; }
+        run += s_scan[w];
+      }
+      if (w_sel < 0)
+        for (int k = tail; k < vocab; k++)
+          if (E::load1(row + k) == v) { if (run == j) *s_found = k; run++; }
+    }
+    s_w = w_sel;
+    s_base = run;
+  }
+  __syncthreads();
+  const int w_sel = s_w, base = s_base;
+  if (w_sel >= 0) {  // block-uniform: the index-ordered scan of that warp's range
+    const int wlo = min(nvec, w_sel * per), whi = min(nvec, wlo + per);
+    const int off = head + wlo * VEC;
+    tie_scan<E>(row + off, (whi - wlo) * VEC, v, j - base + 1, s_scan, [&](int r, int idx) {
+      if (r == j - base) *s_found = off + idx;
+    });
+  }
+  __syncthreads();
   return *s_found;
 }
 

@@ -47,6 +47,9 @@ def parse():
                          "streamed in --chunk-rows chunks from a ~10 GB buffer pool)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk-rows", type=int, default=8192, help="c5: logit rows per streamed chunk")
+    ap.add_argument("--shard", default="trajectory", choices=["trajectory", "rows"],
+                    help="trajectory: one trajectory per rank (weak scaling, the default); rows: ONE "
+                         "trajectory split over the ranks at safe cuts (strong scaling, dist.safe_cuts)")
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-decode", action="store_true", help="skip the decode-step (configs[2]) line")
@@ -223,10 +226,20 @@ def main():
     vocab, dtype, T = c["vocab"], c["dtype"], c["traj_len"]
     cs_h = synth.make_cueset(vocab, c["n_cues"], c["n_pat"], max_len=c["max_len"])
     cs = relay.CueSet.from_synth(cs_h)
-    # this rank's trajectory (weak scaling: one trajectory per rank)
-    ts = synth.make_tokens(1, T, cs_h, seed=synth.BASE_SEED + rank)
-    logits = synth.make_logits(T, vocab, dtype, tokens=ts.tokens, seed=synth.BASE_SEED + 17 * rank,
-                               device=dev, chunk_rows=2048)
+    T_job = T * world   # rows of the whole job (weak scaling: one trajectory per rank)
+    if args.shard == "rows":
+        # strong scaling: one trajectory (the same on every rank), split at safe cuts
+        from paper_2602_06454_b200.dist import range_view, safe_cuts
+        full = synth.make_tokens(1, T, cs_h, seed=synth.BASE_SEED)
+        cuts = safe_cuts(full.tokens, full.traj_offsets, cs_h.terminator, world, cs_h.pat_tokens)
+        lo, hi = int(cuts[rank]), int(cuts[rank + 1])
+        t_np, o_np, te_np = range_view(full.tokens, full.traj_offsets, full.think_end_pos, lo, hi)
+        ts = synth.TokenStream(t_np.astype(np.int32), o_np, te_np)
+        T, T_job = hi - lo, T
+    else:
+        ts = synth.make_tokens(1, T, cs_h, seed=synth.BASE_SEED + rank)
+    logits = synth.make_logits(max(T, 1), vocab, dtype, tokens=ts.tokens, seed=synth.BASE_SEED + 17 * rank,
+                               device=dev, chunk_rows=2048)[:T]
     tok = torch.as_tensor(ts.tokens, device=dev)
     offs = torch.as_tensor(ts.traj_offsets, device=dev)
     tep = torch.as_tensor(ts.think_end_pos, device=dev)
@@ -294,7 +307,7 @@ def main():
         t = torch.tensor([ms, k1_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, k1_ms = float(t[0]), float(t[1])
-    rows_total = T * world * args.steps
+    rows_total = T_job * args.steps
     value = rows_total / (ms / 1e3)
     esz = {"bf16": 2, "f16": 2, "f32": 4}[dtype]
     k1_bytes = T * (vocab * esz + 17)      # logits read + margin/top1/top2/lse/status written
@@ -330,7 +343,7 @@ def main():
 
     e2e = None
     if not args.no_e2e and not args.profile:
-        e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6)
+        e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6, T_job)
     cpu = None
     if rank == 0 and not args.no_baseline and not args.profile:
         cpu = cpu_baseline(logits, ts, cs_h, dtype, vocab)
@@ -341,14 +354,20 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": {"workload": f"{args.config}: {world} x one {T}-token trajectory x {vocab}-vocab "
+            "scaling": "strong" if args.shard == "rows" else "weak", "vs_baseline": None, "dtype": dtype,
+            "data": "synthetic",
+            "config": {"workload": (f"{args.config}: one {T_job}-token trajectory split at safe cuts over {world} "
+                                    f"ranks x {vocab}-vocab " if args.shard == "rows" else
+                                    f"{args.config}: {world} x one {T}-token trajectory x {vocab}-vocab ") +
                        f"{dtype} logits (Qwen3-32B shape), {c['n_cues']} cues / {c['n_pat']} patterns, "
-                       "margin+cue-scan+segment-reduce+stats (H1-H7), one trajectory per rank",
-                       "rows_per_rank": T, "vocab": vocab, "l2": "inputs 9.96 GB/rank >> 126 MB L2, no flush",
-                       "parallelism": f"dp{world} (trajectory-sharded)",
+                       "margin+cue-scan+segment-reduce+stats (H1-H7)" +
+                       (", row ranges at sentence starts" if args.shard == "rows" else ", one trajectory per rank"),
+                       "rows_per_rank": T, "vocab": vocab,
+                       "l2": f"inputs {T * (vocab * esz) / 1e9:.2f} GB/rank >> 126 MB L2, no flush",
+                       "parallelism": f"dp{world} " + ("(one trajectory, row-range-sharded at safe cuts)"
+                                                      if args.shard == "rows" else "(trajectory-sharded)"),
                        "allreduce": (args.allreduce if world > 1 else None)},
-            "hbm_gbs_step": (T * world * (vocab * esz + 17)) / (ms / 1e3 / args.steps) / 1e9 / world,
+            "hbm_gbs_step": (T_job * (vocab * esz + 17)) / (ms / 1e3 / args.steps) / 1e9 / world,
             "roofline": {"kernel": "relay_margin_rows (K1)", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if pk.get("hbm_gbs") else "fallback",
@@ -562,7 +581,7 @@ def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
     return res
 
 
-def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6):
+def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6, rows_job):
     """Same metric through the public API with HOST inputs: every step copies the
     step's logits + tokens from pinned host memory, runs the pass, and reads the
     statistics table back."""
@@ -617,7 +636,7 @@ def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6):
     bo = host_stats.numel() * 8
     del h_logits, d_logits
     torch.cuda.empty_cache()
-    return {"value": T * world * args.e2e_steps / (ms / 1e3), "unit": UNIT,
+    return {"value": rows_job * args.e2e_steps / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": args.e2e_steps,
             "pinned": pinned,
             "path": "host logits+tokens -> H2D -> Analyzer.run (C ABI) -> D2H stats -> finalize"}

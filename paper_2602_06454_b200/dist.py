@@ -43,6 +43,72 @@ def local_view(tokens, traj_offsets, think_end_pos, lo: int, hi: int):
     return np.asarray(tokens)[a:b], loc_offs, loc_tep, (a, b)
 
 
+def safe_cuts(tokens, traj_offsets, terminator, world: int, pat_tokens=None, classes=None,
+              decimal_rule=None) -> np.ndarray:
+    """Row-range sharding of trajectories over ``world`` ranks at *safe cuts*
+    (SURVEY §8(e)): positions p where no post-sentence window and no cue
+    pattern contains both p - 1 and p — every trajectory start and every
+    sentence start (tokens[p - 1] is a terminator).  A window [s, e] ends at
+    the first terminator >= s, so it never crosses a sentence start; a pattern
+    occurrence crosses one only if the pattern holds a terminator token
+    (checked here, with class elements' classes, and rejected).  The decimal
+    rule (R19) decides sentence ends from the next token, which a cut would
+    hide: rejected too.  Returns world + 1 cut positions, each the safe cut
+    nearest to k * n_tok / world (monotone; a rank may get an empty range when
+    a long unterminated run leaves no cut near its share).  Every rank then
+    runs H1-H5 on its range as trajectories of their own (``range_view``), and
+    the SUM of the tables equals the one-rank table bit for bit."""
+    tokens = np.asarray(tokens)
+    term = np.asarray(terminator).astype(bool)
+    if decimal_rule is not None:
+        raise ValueError("safe cuts do not support the decimal-number rule")
+    if pat_tokens is not None:
+        pt = np.asarray(pat_tokens)
+        if term[pt[pt >= 0]].any():
+            raise ValueError("a cue pattern contains a terminator token: no sentence start is a safe cut")
+        if (pt < 0).any():
+            if classes is None:
+                raise ValueError("class pattern elements need classes")
+            for c in np.unique(-1 - pt[pt < 0]):
+                if (np.asarray(classes[c]).astype(bool) & term).any():
+                    raise ValueError("a cue class contains a terminator token")
+    n = tokens.shape[0]
+    offs = np.asarray(traj_offsets, np.int64) if traj_offsets is not None else np.array([0, n], np.int64)
+    cand = np.zeros(n + 1, bool)
+    cand[offs] = True
+    if n:
+        cand[1:n + 1] |= term[tokens]       # the position after a terminator starts a sentence
+    pos = np.flatnonzero(cand)              # sorted; holds 0 and n
+    cuts = np.empty(world + 1, np.int64)
+    cuts[0], cuts[world] = 0, n
+    for k in range(1, world):
+        want = (k * n) // world
+        i = int(np.searchsorted(pos, want))
+        best = pos[min(i, pos.size - 1)]
+        if i > 0 and want - pos[i - 1] <= best - want:
+            best = pos[i - 1]
+        cuts[k] = max(best, cuts[k - 1])
+    return cuts
+
+
+def range_view(tokens, traj_offsets, think_end_pos, lo: int, hi: int):
+    """Positions [lo, hi) of the token stream as trajectories of their own: the
+    trajectory boundaries inside the range plus its ends, think-end positions
+    rebased and clipped to each local trajectory."""
+    tokens = np.asarray(tokens)
+    n = tokens.shape[0]
+    offs = np.asarray(traj_offsets, np.int64) if traj_offsets is not None else np.array([0, n], np.int64)
+    inner = offs[(offs > lo) & (offs < hi)]
+    loc = np.concatenate([[lo], inner, [hi]]).astype(np.int64) - lo
+    tep = None
+    if think_end_pos is not None:
+        te = np.asarray(think_end_pos, np.int64)
+        starts = loc[:-1] + lo
+        g = np.searchsorted(offs, starts, side="right") - 1      # global trajectory of each piece
+        tep = np.clip(te[g] - lo, loc[:-1], loc[1:])
+    return tokens[lo:hi], loc, tep
+
+
 def torch_nccl_comm(group=None, device=None) -> int:
     """The ncclComm_t torch's ProcessGroupNCCL uses for ``group`` on ``device``
     (initialised by a barrier if it is still lazy)."""

@@ -147,3 +147,48 @@ def test_eight_way_shard_of_c4_is_one_trajectory_each():
     offs = np.arange(9, dtype=np.int64) * 32768
     assert [shard_trajectories(offs, 8, r) for r in range(8)] == [(r, r + 1) for r in range(8)]
     assert [shard_trajectories(offs, 2, r) for r in range(2)] == [(0, 4), (4, 8)]
+
+
+def test_safe_cuts_windows_and_occurrences_are_local():
+    """Row-range sharding at safe cuts: the oracle's occurrences
+    and post-sentence windows computed per range, rebased, equal the ones of
+    the whole stream, and the per-range global moments / cue tables add up to
+    the whole stream's (n, sums, counts, triggers exactly)."""
+    import oracle
+    from paper_2602_06454_b200.dist import range_view, safe_cuts
+    h = synth.make_cueset(6000, 5, 8, max_len=3, seed=41)
+    ts = synth.make_tokens(3, 2500, h, seed=42)
+    m = synth.make_margins(ts.tokens.shape[0], seed=43)
+    full = oracle.analyze(m, ts.tokens, ts.traj_offsets, h.pat_tokens, h.pat_offsets, h.pat_cue,
+                          h.n_cues, h.terminator, think_end_pos=ts.think_end_pos, min_count=1)
+    for world in (2, 3, 5, 8):
+        cuts = safe_cuts(ts.tokens, ts.traj_offsets, h.terminator, world, h.pat_tokens)
+        assert cuts[0] == 0 and cuts[-1] == ts.tokens.shape[0] and (np.diff(cuts) >= 0).all()
+        term = h.terminator.astype(bool)
+        for p in cuts[1:-1]:   # a trajectory start or a sentence start
+            assert p in ts.traj_offsets or term[ts.tokens[p - 1]]
+        occ, ends, n_glob, sums = [], [], 0, None
+        for r in range(world):
+            lo, hi = int(cuts[r]), int(cuts[r + 1])
+            if lo == hi:
+                continue
+            tok, offs, tep = range_view(ts.tokens, ts.traj_offsets, ts.think_end_pos, lo, hi)
+            part = oracle.analyze(m[lo:hi], tok, offs, h.pat_tokens, h.pat_offsets, h.pat_cue, h.n_cues,
+                                  h.terminator, think_end_pos=tep, min_count=1)
+            occ.append(part[0]["occ_pos"] + lo)
+            ends.append(part[1]["seg_end"] + lo)
+        np.testing.assert_array_equal(np.concatenate(occ), full[0]["occ_pos"])
+        np.testing.assert_array_equal(np.concatenate(ends), full[1]["seg_end"])
+
+
+def test_safe_cuts_reject_unsafe_cue_sets():
+    from paper_2602_06454_b200.dist import safe_cuts
+    term = np.zeros(10, np.uint8)
+    term[3] = 1
+    toks = np.array([1, 2, 3, 4, 5, 3, 6], np.int32)
+    with pytest.raises(ValueError):
+        safe_cuts(toks, None, term, 2, pat_tokens=np.array([2, 3], np.int32))     # pattern holds a terminator
+    with pytest.raises(ValueError):
+        safe_cuts(toks, None, term, 2, decimal_rule=(0, 1, 2))
+    cuts = safe_cuts(toks, None, term, 2, pat_tokens=np.array([1, 2], np.int32))
+    assert list(cuts) == [0, 3, 7] or list(cuts) == [0, 6, 7]

@@ -392,6 +392,41 @@ def test_stats_allreduce_p2p(relay, tmp_path, world, fused):
         assert relay.stats_finalize(tot.reshape(-1), 8, world, 1) == relay.stats_finalize(one.reshape(-1), 8, 1, 1)
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_safe_cut_row_shards_sum_to_one_table(relay, world):
+    """One trajectory split over ranks at safe cuts (SURVEY §8(e),
+    dist.safe_cuts / range_view): every rank's K2 + K3 on its row range as
+    trajectories of their own; the SUM of the tables equals the one-rank
+    table bit for bit (counts, Q20 moments, triggers; min over the slots)."""
+    from paper_2602_06454_b200.dist import range_view, safe_cuts
+    vocab = 151936
+    h, cs = _cs_pair(relay, vocab, 8, 12, 3, seed=121)
+    ts = synth.make_tokens(1, 32768, h, seed=122)
+    m = synth.make_margins(ts.tokens.shape[0], seed=123)
+    dm = torch.as_tensor(m, device=DEV)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    tep = torch.as_tensor(ts.think_end_pos, device=DEV)
+    one = relay.segment_reduce(cs, dm, relay.cue_scan(cs, tok, offs), offs, tep)["stats"]
+    cuts = safe_cuts(ts.tokens, ts.traj_offsets, h.terminator, world, h.pat_tokens)
+    tot = None
+    for r in range(world):
+        lo, hi = int(cuts[r]), int(cuts[r + 1])
+        st = relay.new_stats(8, r, world, DEV)
+        if hi > lo:
+            t, o, te = range_view(ts.tokens, ts.traj_offsets, ts.think_end_pos, lo, hi)
+            o_d = torch.as_tensor(o, device=DEV)
+            sc = relay.cue_scan(cs, torch.as_tensor(t, device=DEV), o_d)
+            relay.segment_reduce(cs, dm[lo:hi].contiguous(), sc, o_d, torch.as_tensor(te, device=DEV), stats=st,
+                                 rank=r, world_size=world)
+        tot = st if tot is None else tot + st
+    torch.cuda.synchronize()
+    tot = tot.cpu().numpy().reshape(9, 8 + world)
+    base = one.cpu().numpy().reshape(9, 9)
+    np.testing.assert_array_equal(tot[:, :8], base[:, :8])
+    np.testing.assert_array_equal(tot[:, 8:].min(axis=1), base[:, 8])
+
+
 def test_segment_reduce_deterministic(relay):
     args = dict(n_traj=8, traj_len=4096, n_cues=8, n_pat=12, max_len=3, seed=31)
     a = _segment_case(relay, **args)

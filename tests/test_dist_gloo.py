@@ -192,3 +192,23 @@ def test_safe_cuts_reject_unsafe_cue_sets():
         safe_cuts(toks, None, term, 2, decimal_rule=(0, 1, 2))
     cuts = safe_cuts(toks, None, term, 2, pat_tokens=np.array([1, 2], np.int32))
     assert list(cuts) == [0, 3, 7] or list(cuts) == [0, 6, 7]
+
+
+def test_range_view_rebases_and_clips():
+    """range_view: trajectory boundaries inside the range become local ones,
+    think-end positions are rebased and clipped to each local piece."""
+    from paper_2602_06454_b200.dist import range_view
+    toks = np.arange(20, dtype=np.int32)
+    offs = np.array([0, 8, 14, 20], np.int64)
+    tep = np.array([6, 13, 16], np.int64)
+    t, o, te = range_view(toks, offs, tep, 5, 17)
+    np.testing.assert_array_equal(t, toks[5:17])
+    np.testing.assert_array_equal(o, [0, 3, 9, 12])          # pieces [5,8) [8,14) [14,17)
+    np.testing.assert_array_equal(te, [1, 8, 11])            # 6-5; 13-5; 16-5 (inside each piece)
+    t, o, te = range_view(toks, offs, tep, 7, 8)             # think ended at 6 < 7: clipped to the start
+    np.testing.assert_array_equal(o, [0, 1])
+    np.testing.assert_array_equal(te, [0])
+    t, o, te = range_view(toks, offs, tep, 14, 15)           # think ends at 16 > 15: clipped to the end
+    np.testing.assert_array_equal(te, [1])
+    t, o, te = range_view(toks, offs, None, 8, 14)           # exactly one trajectory
+    np.testing.assert_array_equal(o, [0, 6]) and te is None

@@ -21,6 +21,7 @@
 // RelayGen's switch state machine on-device (switch.cuh).  In
 // relay_step_sample it also bounds each row's top-k for the sampling kernel
 // (sample_kernels.cu).
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -234,6 +235,9 @@ struct RowsArgs {
                   // 1: each CTA takes an equal slice of the flattened rows
                   // 3: hybrid: n_whole CTAs take one whole row each, the
                   //    others equal slices of the remaining rows (K4)
+                  // 4: cluster: rows dealt to thread-block clusters, each
+                  //    cluster's rows sliced equally over its CTAs; row parts
+                  //    merged in the owner CTA's shared memory over DSMEM (K4)
                   // 2: rows cut into `chunk`-element chunks handed out by an
                   //    atomic work counter (K4; balances uneven SM service)
   float* margin;
@@ -246,6 +250,7 @@ struct RowsArgs {
   int* work;      // [2] dynamic mode: next chunk, CTAs done (zero between launches)
   int chunk;      // dynamic mode: elements per chunk (a multiple of a ring stage)
   long long n_whole;  // hybrid mode: rows taken whole (one per CTA)
+  int csize;          // cluster mode (flat == 4): CTAs per thread-block cluster
   int cpr;        // dynamic mode: chunks per row (<= kMaxSplit)
   // vocabulary-parallel partials (kModePartial)
   long long col_offset;  // global index of the shard's first column
@@ -271,6 +276,8 @@ struct RowsArgs {
 };
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
+constexpr int kXSlots = 4;     // cluster mode: rows a CTA owns at once (consecutive: distinct mod 4)
+constexpr int kXParts = 8;     // cluster mode: parts per row (<= CTAs per cluster)
 constexpr int kModeRows = 0;     // K1: margins of whole rows
 constexpr int kModeStep = 1;     // K4: margins + the decode-step switch
 constexpr int kModePartial = 2;  // N1: per-row partials of a vocabulary shard
@@ -388,7 +395,18 @@ struct ItemIter {
   __device__ void init(const RowsArgs& a) {
     next_w = blockIdx.x;
     e = E1 = 0;
-    if (a.flat == 1 || a.flat == 3) {
+    if (a.flat == 4) {
+      // cluster c = blockIdx / csize takes rows [c R / C, (c + 1) R / C)
+      const long long C = gridDim.x / a.csize, c = blockIdx.x / a.csize;
+      row0 = c * a.n_rows / C;
+      const long long row1 = (c + 1) * a.n_rows / C;
+      T = (row1 - row0) * a.vocab;
+      G = a.csize;
+      b = blockIdx.x % a.csize;
+      const double Tg = static_cast<double>(T) / static_cast<double>(G);
+      e = slice_start(b, T, G, Tg);
+      E1 = slice_start(b + 1, T, G, Tg);
+    } else if (a.flat == 1 || a.flat == 3) {
       // hybrid (3): CTAs [0, n_whole) take rows [0, n_whole) whole; the rest
       // slice rows [n_whole, n_rows) equally (one whole row plus an equal
       // share of the rest per SM, instead of one or two whole rows)
@@ -505,6 +523,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   __shared__ float s_thk[kSlots][NCW];
   __shared__ Partial s_red[kSlots][NRED];
   __shared__ SmemCue sc;
+  // cluster mode: row parts of the rows this CTA owns (it holds their first
+  // part), written by the other CTAs of the cluster over DSMEM
+  __shared__ __align__(16) float s_xpart[kXSlots][kXParts][kPartWords];
+  __shared__ __align__(8) uint64_t s_xbar[kXSlots];
 
   const T* logits = static_cast<const T*>(a.logits);
   const int tid = threadIdx.x;
@@ -530,9 +552,19 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       mbar_init(ifull_s + 8 * s, 1);        // the producer (dynamic mode)
       s_theta[s] = fkey(-INFINITY);
     }
+    if (a.flat == 4) {
+      // one mbarrier per owned split row, expecting its other parts
+      ItemIter it0;
+      it0.init(a);
+      Item x;
+      while (it0.next(a, x))
+        if (x.nparts > 1 && x.part == 0)
+          mbar_init(smem_u32(&s_xbar[(x.r - it0.row0) % kXSlots]), x.nparts - 1);
+    }
     fence_barrier_init();
   }
   __syncthreads();
+  if (a.flat == 4) cluster_sync_all();  // every owner's barriers exist before any remote arrive
   const float c = a.c;
   // K4 is launched with programmatic dependent launch: its prologue (barrier
   // init, item math, pattern staging) overlaps the previous kernel's tail;
@@ -645,6 +677,45 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in);
         if (a.row_ready && lane == 0)  // lane 0 wrote thk/zmax/margin/top1/top2/status: publish
           asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.row_ready + r) : "memory");
+        continue;
+      }
+      if (a.flat == 4) {
+        // cluster mode: the CTA holding the row's FIRST part owns it (its
+        // last item: the other parts are the first items of the following
+        // CTAs, long done, so no CTA waits on a chain of predecessors); the
+        // others store their partial into its shared memory (DSMEM) and
+        // arrive on its barrier; the owner merges once all have arrived
+        const int xs = static_cast<int>((r - iter.row0) % kXSlots);
+        if (item.part != 0) {
+          if (lane == 0) {
+            const uint32_t owner = static_cast<uint32_t>(iter.b - item.part);
+            const uint32_t dst = mapa_cluster(smem_u32(&s_xpart[xs][item.part][0]), owner);
+            st_cluster_v4(dst, __float_as_uint(q.t.v1), __float_as_uint(q.t.v2), static_cast<uint32_t>(q.t.i1),
+                          static_cast<uint32_t>(q.t.i2));
+            st_cluster_v4(dst + 16, __float_as_uint(q.n.m), __float_as_uint(q.n.s), static_cast<uint32_t>(q.flags),
+                          0u);
+            mbar_arrive_remote(mapa_cluster(smem_u32(&s_xbar[xs]), owner));
+          }
+          continue;
+        }
+        mbar_wait_cluster(smem_u32(&s_xbar[xs]), 0);
+        Partial m = q;
+        for (int k = 1; k < item.nparts; k++) {
+          const float* pr = s_xpart[xs][k];
+          Partial o;
+          o.t.v1 = pr[0]; o.t.v2 = pr[1];
+          o.t.i1 = __float_as_int(pr[2]); o.t.i2 = __float_as_int(pr[3]);
+          o.n.m = pr[4]; o.n.s = pr[5];
+          o.flags = __float_as_int(pr[6]);
+          m = partial_merge(m, o);
+        }
+        bool exact = false;
+        float S = 0.0f;
+        if (m.flags & kFlagHuge) {
+          S = warp_sum(exact_sum_thread<E>(row, a.vocab, m.t.v1, c, lane, 32));
+          exact = true;
+        }
+        finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in);
         continue;
       }
       // publish this part; the last part of the row to arrive finishes it
@@ -856,6 +927,7 @@ static int k4_mode(int batch) {
   if (e && !strcmp(e, "flat")) return 1;
   if (e && !strcmp(e, "dynamic")) return 2;
   if (e && !strcmp(e, "hybrid")) return batch > num_sms() ? 3 : 1;
+  if (e && !strcmp(e, "cluster")) return 4;
   return batch >= num_sms() ? 0 : 1;
 }
 static int k4_chunk_stages() {
@@ -887,6 +959,40 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
     const long long total = a.n_rows * a.cpr;
     if (total >= (1LL << 31)) return cudaErrorInvalidValue;  // int work counter
     if (grid > total) grid = total;
+  } else if (a.flat == 4) {
+    // clusters of csize CTAs, as many as fit at once; rows dealt to clusters
+    {
+      const char* e = getenv("RELAY_K4_CSIZE");
+      a.csize = e && atoi(e) >= 2 && atoi(e) <= kXParts ? atoi(e) : 8;
+    }
+    cudaLaunchConfig_t q{};
+    q.gridDim = dim3(static_cast<unsigned>(slots / a.csize * a.csize));
+    q.blockDim = dim3((NCW + 2) * 32);
+    q.dynamicSmemBytes = smem;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = a.csize; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int nclusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, kern, &q);
+    if (e != cudaSuccess) return e;
+    long long C = nclusters;
+    if (C > slots / a.csize) C = slots / a.csize;
+    if (C > a.n_rows) C = a.n_rows;  // every cluster at least one row
+    // every slice of a cluster >= 128 elements: no empty slice (an owner would
+    // wait for a part that never comes)
+    const long long cap = a.n_rows * a.vocab / (128LL * a.csize);
+    if (C > cap) C = cap;
+    if (C < 1) {  // too small for clusters: plain flat slices
+      a.flat = 1;
+      grid = slots;
+      const long long T = a.n_rows * a.vocab;
+      if (grid > T / 128) grid = T / 128 > 0 ? T / 128 : 1;
+      if (grid > a.n_rows * (kMaxSplit - 2)) grid = a.n_rows * (kMaxSplit - 2);
+    } else {
+      grid = C * a.csize;
+    }
   } else if (a.flat == 3) {
     // hybrid: one whole row per SM, the other slots slice the remaining rows
     a.n_whole = num_sms();
@@ -917,11 +1023,16 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
     cfg.blockDim = dim3((NCW + 2) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (a.flat == 4) {
+      attr[1].id = cudaLaunchAttributeClusterDimension;
+      attr[1].val.clusterDim.x = a.csize; attr[1].val.clusterDim.y = 1; attr[1].val.clusterDim.z = 1;
+      cfg.numAttrs = 2;
+    }
     return cudaLaunchKernelEx(&cfg, kern, a, cs);
   }
   kern<<<static_cast<unsigned>(grid), (NCW + 2) * 32, smem, st>>>(a, cs);

@@ -999,7 +999,7 @@ def test_stats_allreduce_torch_comm(relay, tmp_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["strided", "flat", "dynamic", "hybrid"])
+@pytest.mark.parametrize("mode", ["strided", "flat", "dynamic", "hybrid", "cluster"])
 @pytest.mark.parametrize("B,vocab,dtype", [(256, 152064, "bf16"), (37, 5003, "f16"), (300, 32000, "f32")])
 def test_step_switch_work_split_modes(relay, monkeypatch, mode, B, vocab, dtype):
     """K4's work splits (whole rows per CTA; equal flat slices merged by the

@@ -534,6 +534,40 @@ def test_step_switch(relay, greedy, B, vocab, dtype, max_seg, gate):
     assert (got_flags == 1).sum() > 0 or greedy
 
 
+def test_offline_triggers_equal_online_switches(relay):
+    """SURVEY §4 tier 6 on the GPU path: replaying token streams through K4
+    step by step (each stream's next token as the sampled token) fires
+    large->small exactly as often per cue as K2/K3 count per-sentence first
+    occurrences (n_triggers), for a substring-free pattern set without
+    terminators (R13); the answer stage (after </think>) fires nothing."""
+    V, B, L = 8192, 48, 1500
+    h = synth.make_cueset(V, 5, 9, max_len=3, seed=131, prefix_pair=False, substring_free=True)
+    cs = relay.CueSet.from_synth(h)
+    ts = synth.make_tokens(B, L, h, seed=132, cue_rate=0.4)
+    tok = torch.as_tensor(ts.tokens, device=DEV)
+    offs = torch.as_tensor(ts.traj_offsets, device=DEV)
+    tep = torch.as_tensor(ts.think_end_pos, device=DEV)
+    m = torch.as_tensor(synth.make_margins(B * L, seed=133), device=DEV)
+    seg = relay.segment_reduce(cs, m, relay.cue_scan(cs, tok, offs), offs, tep)
+    torch.cuda.synchronize()
+    offline = [c["n_triggers"] for c in relay.stats_finalize(seg["stats"].cpu().numpy(), 5, 1, 1)[:5]]
+    streams = torch.as_tensor(ts.tokens.reshape(B, L), device=DEV)
+    logits = synth.make_logits(B, V, "bf16", seed=134, device=DEV)
+    state = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    hist = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    small = torch.zeros(B, dtype=torch.int32, device=DEV)
+    ws = relay.workspace(0, 0, B, DEV)
+    online = torch.zeros(5, dtype=torch.int64, device=DEV)
+    out = None
+    for t in range(L):
+        out = relay.step_switch(cs, logits, state, hist, small, streams[:, t].contiguous(), ws=ws, out=out)
+        fired = out["flag"] == 1
+        online.index_add_(0, out["cue_id"][fired].long(), torch.ones(int(fired.sum()), dtype=torch.int64,
+                                                                      device=DEV))
+    torch.cuda.synchronize()
+    assert online.cpu().tolist() == offline and sum(offline) > 100
+
+
 def test_step_switch_graph_replay(relay):
     """Captured in a CUDA graph and replayed: the arrival counters reset
     themselves; replaying a token stream matches the oracle step by step."""

@@ -167,9 +167,18 @@ __device__ __forceinline__ float warp_second(float a, float b) {
   return b;
 }
 
-__device__ __forceinline__ float theta_raise(float b, int* s_theta) {
-  if ((threadIdx.x & 31) == 0 && b > unkey(*reinterpret_cast<volatile int*>(s_theta)))
-    atomicMax(s_theta, fkey(b));
+// The CTA-shared threshold key, addressed by its 32-bit shared-window address
+// (kept in a register: a generic pointer would re-derive the window base from
+// SR_CgaCtaId at every stage).
+__device__ __forceinline__ int theta_load(uint32_t a) {
+  int v;
+  asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+__device__ __forceinline__ float theta_raise(float b, uint32_t s_theta) {
+  if ((threadIdx.x & 31) == 0 && b > unkey(theta_load(s_theta)))
+    asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_theta), "r"(fkey(b)) : "memory");
   return b;
 }
 
@@ -538,6 +547,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const uint32_t rfull_s = smem_u32_pinned(red_full);
   const uint32_t rempty_s = smem_u32_pinned(red_empty);
   const uint32_t ifull_s = smem_u32_pinned(ifull);
+  const uint32_t theta_s = smem_u32_pinned(s_theta);
   if (tid == 0) {
     // Every consumer thread arrives on `empty` after its own shared-memory reads
     // and on `red_full` after its last threshold read / partial write, so each
@@ -780,7 +790,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     // the slot (threshold + partials) is free once the epilogue took item it - kSlots
     mbar_wait(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
     if (tid == 0 && it == 1) TRACE(12);
-    int* theta_p = &s_theta[slot];
+    const uint32_t theta_p = theta_s + 4 * slot;
     const T* row = logits + r * a.stride;
     const Geom g = row_geom<E>(row, j0, j1);
     ThreadState st;
@@ -818,12 +828,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           named_bar(1, NCT);
           if (tid == 0 && it == 1) TRACE(13);
         }
-        const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
+        const float theta = fmaxf(theta_w, unkey(theta_load(theta_p)));
         consume_stage<E, UV>(raw, h, jb + tid * VEC, NCT * VEC, st, c, theta, slow);
         if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h.x, h.y));
         if (tid == 0 && it == 1 && off == 0) TRACE(14);
       } else {
-        const float theta = fmaxf(theta_w, unkey(*reinterpret_cast<volatile int*>(theta_p)));
+        const float theta = fmaxf(theta_w, unkey(theta_load(theta_p)));
         const int nvec = bytes / 16;
         for (int v = tid; v < nvec; v += NCT) {
           const uint4 raw1[1] = {lds128(buf + v * 16)};

@@ -1149,6 +1149,8 @@ def _oracle_sample_tolerant(host_rows, dtype, vocab, u, got, T, k, p):
     (50, 32000, "f32", 0.6, 20, 0.5),
     (9, 40, "f32", 0.8, 64, 0.9),             # vocab < top_k
     (256, 152064, "bf16", 0.6, 0, 0.95),      # configs[2] with R1-Distill sampling: no top-k
+    (1000, 8192, "bf16", 0.6, 20, 0.95),      # more rows than CTAs: K4/K5 loop rows per CTA
+    (1000, 8192, "bf16", 0.6, 0, 0.95),
     (37, 5003, "f16", 1.0, 0, 1.0),
     (50, 32000, "f32", 0.6, 0, 0.5),
 ])

@@ -1315,24 +1315,29 @@ def test_step_sample_no_top_k_wide_nuclei(relay, dtype, T, p):
     assert len(set(got.tolist())) > B // 2      # wide nuclei: mostly distinct draws
 
 
-def test_step_sample_graph_replay(relay):
+@pytest.mark.parametrize("top_k", [20, 0])
+def test_step_sample_graph_replay(relay, top_k):
     """Captured in a CUDA graph (PDL edges included) and replayed with new
-    uniforms: every replay matches the oracle."""
+    uniforms: every replay matches the oracle (top_k 0: K6 and its
+    self-re-arming list, with flat rows that take it, and the per-row
+    readiness counters across replays)."""
     vocab, B = 32000, 48
     h, cs = _cs_pair(relay, vocab, 4, 6, 3, seed=77)
     L = synth.make_logits(B, vocab, "bf16", seed=78, device=DEV)
+    if top_k == 0:
+        L[::5] = (torch.randn(len(range(0, B, 5)), vocab, device=DEV) * 0.5).to(L.dtype)  # wide nuclei
     host = synth.host_rows(L, "bf16")
     d_u = torch.zeros(B, dtype=torch.float32, device=DEV)
     st = torch.zeros(B, dtype=torch.uint8, device=DEV)
     hi = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
     ws = relay.workspace(0, 0, B, DEV)
-    out = relay.step_sample(cs, L, d_u, st, hi, ws=ws)
+    out = relay.step_sample(cs, L, d_u, st, hi, top_k=top_k, ws=ws)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         with torch.cuda.graph(g, stream=s):
-            relay.step_sample(cs, L, d_u, st, hi, ws=ws, out=out)
+            relay.step_sample(cs, L, d_u, st, hi, top_k=top_k, ws=ws, out=out)
     torch.cuda.synchronize()
     rng = np.random.default_rng(79)
     for _ in range(4):
@@ -1342,7 +1347,7 @@ def test_step_sample_graph_replay(relay):
         g.replay()
         torch.cuda.synchronize()
         _oracle_sample_tolerant(host, "bf16", vocab, u.astype(np.float64), out["sampled"].cpu().numpy(),
-                                0.6, 20, 0.95)
+                                0.6, top_k, 0.95)
 
 
 def test_read_probe_runs(relay):

@@ -36,10 +36,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def _load():
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+    # RELAY_LIB: another build of the same library (A/B tuning tools only)
+    path = os.environ.get("RELAY_LIB", LIB_PATH)
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(there is no CPU fallback)")
-    lib = C.CDLL(LIB_PATH)
+    lib = C.CDLL(path)
     P, i32, i64, f32, u32, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_uint32, C.c_size_t
     sig = {
         "relay_version": (C.c_int, []),

@@ -1,26 +1,29 @@
 // margin_kernels.cu — K1 relay_margin_rows and K4 relay_step_switch (sm_100a).
 //
-// One streaming pass over each logit row (§3.2): online max with a
-// lazily raised exp reference, the softmax normaliser in fp32 (MUFU.EX2 via
-// ex2.approx; FFMA2/FADD2 on element pairs), and the exact top-2 (value desc,
-// index asc) behind a CTA-shared threshold so that only the rare vectors that
+// One streaming pass over each logit row (§3.2): the softmax
+// normaliser in fp32 against a lazily raised exp reference (MUFU.EX2 via
+// ex2.approx; FFMA2/FADD2 on element pairs) and the exact top-2 (value desc,
+// index asc) behind a CTA-shared threshold, so that only the rare stages that
 // can still enter the row's top-2 take the exact per-element path
-// (DESIGN.md §6).  HBM-bound: algorithmic bytes = vocab * sizeof(elem) per row.
-// No tensor cores: this is a scan, not a contraction.
+// (DESIGN.md §6).  HBM-bound by design: algorithmic bytes = vocab *
+// sizeof(elem) per row; no tensor cores (a scan, not a contraction).
 //
 // K1 is a persistent warp-specialised kernel: one producer warp streams row
-// bodies into a shared-memory ring with 1-D TMA bulk copies
-// (cp.async.bulk + mbarrier complete_tx), consumer warps reduce them.  The
-// ring runs across row boundaries, so a row's epilogue overlaps the next
-// row's loads.  Per stage a thread reduces its raw 16-bit words with a packed
-// NaN-propagating max tree (HMNMX2.NAN) before unpacking anything, so the
-// guards cost ~0.5 instruction per element.  K4 is the same kernel with a
-// 6-stage ring at 2 CTAs/SM, launched with programmatic dependent launch:
-// whole rows per CTA when the batch fills the SMs, otherwise equal slices of
-// the flattened batch merged by the last arriving CTA; its epilogue warp runs
-// RelayGen's switch state machine on-device (switch.cuh).  In
-// relay_step_sample it also bounds each row's top-k for the sampling kernel
-// (sample_kernels.cu).
+// bodies into a shared-memory ring with 1-D TMA bulk copies (cp.async.bulk +
+// mbarrier complete_tx), consumer warps reduce them, an epilogue warp merges
+// and finishes each row.  Ring-slot release and the hand-off of a row's
+// partials use named barriers (bar.arrive by the consumers, bar.sync by the
+// producer / epilogue warp: descheduled, no polling), so the two helper warps
+// take no issue slots.  The ring runs across row boundaries, so a row's
+// epilogue overlaps the next row's loads.  Steady-state stage per thread: the
+// 32 terms, ONE comparison of their sum against the thread's guard T
+// (consume_fast), a warp-uniform exact path only when some lane trips.  K4 is
+// the same kernel with 12 consumer warps at 2 CTAs/SM, launched with
+// programmatic dependent launch: whole rows per CTA when the batch fills the
+// SMs, otherwise equal slices of the flattened batch merged by the last
+// arriving CTA; its epilogue warp runs RelayGen's switch state machine
+// on-device (switch.cuh).  In relay_step_sample it also bounds each row's
+// top-k for the sampling kernel (sample_kernels.cu).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -97,9 +100,37 @@ __device__ __forceinline__ float2 stage_max2(const uint4 (&raw)[UV]) {
   }
 }
 
+// Exact top-2 update from the vectors u < nvalid of a stage: only the
+// elements that can still enter the row's top-2 are pushed (usually one):
+// >= theta (a lower bound of the row's 2nd-best) and above this thread's own
+// 2nd-best (indices only grow along a thread's walk).
+template <class E, int UV>
+__device__ __forceinline__ void exact_top2(const uint4 (&raw)[UV], int nvalid, int j0, int jstep, ThreadState& st,
+                                           float theta) {
+  constexpr int VEC = 16 / E::SZ;
+#pragma unroll
+  for (int u = 0; u < UV; u++) {
+    const float vm = vec_max<E>(raw[u]);
+    if (u < nvalid && vm >= theta && !(vm <= st.g2)) {
+      float f[VEC];
+      unpack16<E>(raw[u], f);
+      unsigned m = 0;
+#pragma unroll
+      for (int k = 0; k < VEC; k++) m |= (f[k] >= theta && !(f[k] <= st.g2)) ? (1u << k) : 0u;
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        top2_push(st.t, elem_at<E>(raw[u], k), j0 + u * jstep + k);
+      }
+      st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
+    }
+  }
+}
+
 // One stage of UV 16-byte vectors; vector u holds elements j0 + u*jstep ..
 // + VEC-1, and a thread's vectors are visited in increasing index order.
-// Returns the two half maxima (for the row-start probe).
+// The max-guarded form (a row's first stage, where the probe needs the half
+// maxima h anyway, and short rows); consume_fast below is the steady state.
 template <class E, int UV>
 __device__ __forceinline__ void consume_stage(const uint4 (&raw)[UV], float2 h, int j0, int jstep,
                                               ThreadState& st, float c, float theta, bool& slow) {
@@ -107,28 +138,9 @@ __device__ __forceinline__ void consume_stage(const uint4 (&raw)[UV], float2 h, 
   const float gm = max_nan(h.x, h.y);
   if (gm != gm) st.flags |= kFlagNan;  // a NaN anywhere in the stage (status 1)
   // A vector can change the row's top-2 only if it holds a value >= theta
-  // (theta <= the row's 2nd-best value) that also beats this thread's own
-  // 2nd-best (indices only grow along a thread's walk).
+  // that also beats this thread's own 2nd-best.
   if (gm >= theta && !(gm <= st.g2)) {
-#pragma unroll
-    for (int u = 0; u < UV; u++) {
-      const float vm = vec_max<E>(raw[u]);
-      if (vm >= theta && !(vm <= st.g2)) {
-        // only the elements that can still enter the row's top-2 are pushed
-        // (usually one): >= theta and above this thread's own 2nd-best
-        float f[VEC];
-        unpack16<E>(raw[u], f);
-        unsigned m = 0;
-#pragma unroll
-        for (int k = 0; k < VEC; k++) m |= (f[k] >= theta && !(f[k] <= st.g2)) ? (1u << k) : 0u;
-        while (m) {
-          const int k = __ffs(m) - 1;
-          m &= m - 1;
-          top2_push(st.t, elem_at<E>(raw[u], k), j0 + u * jstep + k);
-        }
-        st.g2 = (st.t.i2 == INT_MAX) ? qnan() : st.t.v2;
-      }
-    }
+    exact_top2<E, UV>(raw, UV, j0, jstep, st, theta);
     slow = true;
   }
 #ifdef RELAY_K1_NULL
@@ -180,6 +192,157 @@ __device__ __forceinline__ float theta_raise(float b, uint32_t s_theta) {
   if ((threadIdx.x & 31) == 0 && b > unkey(theta_load(s_theta)))
     asm volatile("red.shared.max.s32 [%0], %1;" ::"r"(s_theta), "r"(fkey(b)) : "memory");
   return b;
+}
+
+// Sum of the stage's terms 2^(fl(z c - mref)) as two packed partial sums
+// (unpack, FFMA2, 2 x MUFU.EX2, FADD2 per element pair: the whole per-element
+// cost of the steady state).
+// 2^y for an element pair on the FMA pipe (FlashAttention-4's trick: the
+// MUFU.EX2 unit, 16 lanes/clk/SM, is the K1 ceiling; the FMA pipe has room).
+// y clamped to [-125, 64] (a term below 2^-125 of the reference is 0 to fp32
+// accuracy here; above 2^16 the guard trips and the stage is redone, so the
+// clamp only keeps the exponent arithmetic in range); n = rint(y) by the
+// 1.5*2^23 shifter, 2^(y-n) by a degree-5 minimax polynomial on [-1/2, 1/2]
+// (max relative error 2.3e-7 in fp32 Horner, MUFU.EX2's ~2^-22 class), the
+// exponent added to the bits.
+#ifndef RELAY_K1_POLY_PAIRS
+#define RELAY_K1_POLY_PAIRS 0  // element pairs per 16 of a stage on the FMA pipe (tools/k1_sweep.py)
+#endif
+__device__ __forceinline__ float2 exp2_poly2(float2 y) {
+  y.x = fminf(fmaxf(y.x, -125.0f), 64.0f);
+  y.y = fminf(fmaxf(y.y, -125.0f), 64.0f);
+  const float2 t = __fadd2_rn(y, make_float2(12582912.0f, 12582912.0f));
+  const float2 tm = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __fadd2_rn(y, make_float2(-tm.x, -tm.y));
+  float2 h = __ffma2_rn(make_float2(1.327647129073739e-3f, 1.327647129073739e-3f), f,
+                        make_float2(9.675541892647743e-3f, 9.675541892647743e-3f));
+  h = __ffma2_rn(h, f, make_float2(5.550713092088699e-2f, 5.550713092088699e-2f));
+  h = __ffma2_rn(h, f, make_float2(2.4022120237350464e-1f, 2.4022120237350464e-1f));
+  h = __ffma2_rn(h, f, make_float2(6.931469440460205e-1f, 6.931469440460205e-1f));
+  h = __ffma2_rn(h, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__uint_as_float(__float_as_uint(h.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(h.y) + (__float_as_uint(t.y) << 23)));
+}
+
+template <class E, int UV>
+__device__ __forceinline__ float2 stage_sum(const uint4 (&raw)[UV], int nvalid, float c, float mref) {
+  constexpr int VEC = 16 / E::SZ;
+  constexpr int NP = VEC / 2;  // element pairs per vector
+  constexpr int kPoly = RELAY_K1_POLY_PAIRS * UV * NP / 16;  // the stage's last kPoly pairs
+  const float2 cc = make_float2(c, c);
+  const float2 nm = make_float2(-mref, -mref);
+  // a sum tree, not accumulator chains: each vector's exps are independent of
+  // the previous vector's adds, so the scheduler keeps many MUFU.EX2 in flight
+  // (with chains it serialised unpack -> FFMA2 -> MUFU -> FADD2 pair by pair)
+#ifdef RELAY_K1_NULL
+  // tuning only: the streaming ceiling without the exp work (a 0/1 term per
+  // stage from the words, so nothing is optimised away)
+  uint32_t x = 0;
+#pragma unroll
+  for (int u = 0; u < UV; u++) x ^= raw[u].x ^ raw[u].y ^ raw[u].z ^ raw[u].w;
+  return make_float2(static_cast<float>(x & 1u), 0.0f);
+#endif
+  float2 t[UV];
+#pragma unroll
+  for (int u = 0; u < UV; u++) {
+    if (u >= nvalid) {  // a partial stage's missing vectors (nvalid == UV otherwise: folded away)
+      t[u] = make_float2(0.0f, 0.0f);
+      continue;
+    }
+    float f[VEC];
+    unpack16<E>(raw[u], f);
+    float2 e[NP];
+#pragma unroll
+    for (int k = 0; k < NP; k++) {
+      const float2 y = __ffma2_rn(make_float2(f[2 * k], f[2 * k + 1]), cc, nm);
+      if (u * NP + k >= UV * NP - kPoly)
+        e[k] = exp2_poly2(y);
+      else
+        e[k] = make_float2(ex2(y.x), ex2(y.y));
+    }
+#pragma unroll
+    for (int w = 1; w < NP; w <<= 1)
+#pragma unroll
+      for (int k = 0; k + w < NP; k += 2 * w) e[k] = __fadd2_rn(e[k], e[k + w]);
+    t[u] = e[0];
+  }
+#pragma unroll
+  for (int w = 1; w < UV; w <<= 1)
+#pragma unroll
+    for (int u = 0; u + w < UV; u += 2 * w) t[u] = __fadd2_rn(t[u], t[u + w]);
+  return t[0];
+}
+
+// The steady-state guard of a thread: every term of a stage is below
+// T = 2^(fl(max(theta, g2) c - mref) - eps) iff no element reaches
+// max(theta, own 2nd-best) — then nothing in the stage can enter the row's
+// top-2 — and T <= 2^16 also keeps every term under the lazy reference's
+// slack.  fl(z c - mref) is monotone in z and MUFU.EX2's relative error
+// (~2^-22) is far below eps, so an element >= the bound always gives a term
+// >= T; a term can only trip the guard falsely, which costs one exact check.
+constexpr float kGuardEps = 1.0f / 1024.0f;
+constexpr float kGuardCap = 65536.0f;  // 2^kSlack
+
+__device__ __forceinline__ float guard_T(float theta, const ThreadState& st, float c) {
+  return fminf(ex2(fmaf(fmaxf(theta, st.g2), c, -st.mref) - kGuardEps), kGuardCap);
+}
+
+// Steady-state stage: the terms first, then ONE comparison of their sum
+// against the thread's guard T (the sum is >= every term, exactly: rounding
+// is monotone).  Only when it trips does the thread take the stage maxima,
+// the exact top-2 update and the reference raise, so the common stage costs
+// the exp work plus ~0.2 instructions per element (no per-stage max tree).
+// nvalid < UV on a row's last, partial stage: the missing vectors hold -inf
+// (no term, never pushed).
+template <class E, int UV>
+__device__ __forceinline__ void consume_fast(const uint4 (&raw)[UV], int nvalid, int j0, int jstep,
+                                             ThreadState& st, float c, float& T, int& tkey, float& theta_w,
+                                             int key, uint32_t theta_p) {
+  float2 s2 = stage_sum<E, UV>(raw, nvalid, c, st.mref);
+  // T follows the shared threshold (key: loaded with the stage, before the
+  // ring words, so its latency hides under the sum): a stale (lower) T stays
+  // correct, but every thread would trip on the elements between the old and
+  // the new theta
+  if (key != tkey) {
+    tkey = key;
+    T = guard_T(fmaxf(theta_w, unkey(key)), st, c);
+  }
+  const float s = s2.x + s2.y;
+  // warp-uniform: when any lane trips, the whole warp takes the exact path
+  // (it would execute it anyway) and the warp's threshold raise joins it
+  if (__any_sync(kFull, !(s < T))) {
+    // the raw words again, opaque: the unpacked values of the sum above are
+    // not kept live across it for the rare exact path (register spills)
+    uint4 rw[UV];
+#pragma unroll
+    for (int u = 0; u < UV; u++) rw[u] = opaque(raw[u]);
+    const float theta = fmaxf(theta_w, unkey(key));
+    const float2 h = stage_max2<E, UV>(rw);
+    const float gm = max_nan(h.x, h.y);
+    if (gm != gm) st.flags |= kFlagNan;
+    bool pushed = false;
+    if (gm >= theta && !(gm <= st.g2)) {
+      exact_top2<E, UV>(rw, nvalid, j0, jstep, st, theta);
+      pushed = true;
+    }
+    // raise the reference to the stage maximum when a term passed the slack,
+    // or when the stage sum alone is large (terms bunched near the slack:
+    // every later stage would trip the guard again)
+    const float ym = gm * c;
+    if (ym > st.mref + kSlack || (ym > st.mref && !(s < 0.5f * kGuardCap))) {
+      if (fabsf(ym) >= kHuge) st.flags |= kFlagHuge;
+      const float r = ex2(st.mref - ym);
+#pragma unroll
+      for (int k = 0; k < 4; k++) st.acc[k] *= r;
+      st.mref = ym;
+      s2 = stage_sum<E, UV>(rw, nvalid, c, ym);  // the old terms may have overflowed (or been clamped)
+    }
+    if (__any_sync(kFull, pushed)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
+    T = guard_T(fmaxf(theta_w, unkey(key)), st, c);  // mref, g2 or theta_w may have moved
+  }
+  const float2 acc = __fadd2_rn(make_float2(st.acc[0], st.acc[1]), s2);
+  st.acc[0] = acc.x;
+  st.acc[1] = acc.y;
 }
 
 __device__ __forceinline__ Partial thread_partial(const ThreadState& st) {
@@ -379,6 +542,9 @@ struct Item {
   int part, nparts;
 };
 
+// FLAT = false (K1, the TP partials: always whole rows, strided) lets the
+// compiler drop the 64-bit slice state from the consumer loop's live set.
+template <bool FLAT>
 struct ItemIter {
   long long next_w;  // strided: next row
   long long e, E1;   // flat: next element, end of this CTA's slice
@@ -404,6 +570,7 @@ struct ItemIter {
   __device__ void init(const RowsArgs& a) {
     next_w = blockIdx.x;
     e = E1 = 0;
+    if (!FLAT) return;
     if (a.flat == 4) {
       // cluster c = blockIdx / csize takes rows [c R / C, (c + 1) R / C)
       const long long C = gridDim.x / a.csize, c = blockIdx.x / a.csize;
@@ -440,10 +607,11 @@ struct ItemIter {
     return Item{r, j0, min(a.vocab, j0 + a.chunk), ch, a.cpr};
   }
   __device__ bool next(const RowsArgs& a, Item& it) {
-    if (!a.flat || (a.flat == 3 && b < 0)) {
-      if (next_w >= (a.flat == 3 ? a.n_whole : a.n_rows)) return false;
+    if (!FLAT || !a.flat || (a.flat == 3 && b < 0)) {
+      const bool hyb = FLAT && a.flat == 3;
+      if (next_w >= (hyb ? a.n_whole : a.n_rows)) return false;
       it = Item{next_w, 0, a.vocab, 0, 1};
-      next_w = a.flat == 3 ? a.n_whole : next_w + gridDim.x;  // hybrid: one whole row
+      next_w = hyb ? a.n_whole : next_w + gridDim.x;  // hybrid: one whole row
       return true;
     }
     if (e >= E1) return false;
@@ -468,14 +636,15 @@ struct ItemIter {
 // (-1 = no more) and completes ifull[slot].  The producer refills a slot only
 // after the epilogue released it (rempty), which happens after every consumer
 // and the epilogue read it, so no waiter can miss a phase.
-__device__ __forceinline__ bool fetch_item(const RowsArgs& a, ItemIter& iter, int it, int nslots,
+template <bool FLAT>
+__device__ __forceinline__ bool fetch_item(const RowsArgs& a, ItemIter<FLAT>& iter, int it, int nslots,
                                            const long long* s_item, uint32_t ifull_s, Item& item) {
-  if (a.flat != 2) return iter.next(a, item);
+  if (!FLAT || a.flat != 2) return iter.next(a, item);
   const int slot = it % nslots;
   mbar_wait(ifull_s + 8 * slot, (it / nslots) & 1);
   const long long k = *reinterpret_cast<const volatile long long*>(s_item + slot);
   if (k < 0) return false;
-  item = ItemIter::from_k(a, k);
+  item = ItemIter<FLAT>::from_k(a, k);
   return true;
 }
 
@@ -521,10 +690,16 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   // reduction (K4: the epilogue is the tail of a ~30 us kernel)
   constexpr int RPW = (MODE == kModeStep) ? 1 : 8;
   constexpr int NRED = NCW * RPW;
+  // named barriers: 0 __syncthreads, 1 the consumers' row-start probe,
+  // kBarRing0 + s ring stage s released (consumers arrive, the producer warp
+  // syncs), kBarRed0 + k reduction slot k filled (consumers arrive, the
+  // epilogue warp syncs)
+  constexpr int kBarRing0 = 2;
+  constexpr int kBarRed0 = kBarRing0 + NS;
+  constexpr bool kFlat = MODE == kModeStep;  // only K4 splits rows across CTAs
+  static_assert(kBarRed0 + kSlots <= 16, "named barriers");
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[NS];
-  __shared__ __align__(8) uint64_t empty[NS];
-  __shared__ __align__(8) uint64_t red_full[kSlots];
   __shared__ __align__(8) uint64_t red_empty[kSlots];
   __shared__ __align__(8) uint64_t ifull[kSlots];
   __shared__ long long s_item[kSlots];
@@ -543,8 +718,6 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   if (tid == 0) TRACE(0);
   const uint32_t ring_s = smem_u32_pinned(ring);
   const uint32_t full_s = smem_u32_pinned(full);
-  const uint32_t empty_s = smem_u32_pinned(empty);
-  const uint32_t rfull_s = smem_u32_pinned(red_full);
   const uint32_t rempty_s = smem_u32_pinned(red_empty);
   const uint32_t ifull_s = smem_u32_pinned(ifull);
   const uint32_t theta_s = smem_u32_pinned(s_theta);
@@ -554,17 +727,15 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     // thread's accesses are released to the TMA producer / epilogue warp.
     for (int s = 0; s < NS; s++) {
       mbar_init(full_s + 8 * s, 1);
-      mbar_init(empty_s + 8 * s, NCT);
     }
     for (int s = 0; s < kSlots; s++) {
-      mbar_init(rfull_s + 8 * s, NCT);
       mbar_init(rempty_s + 8 * s, 32);      // every reading lane of the epilogue warp
       mbar_init(ifull_s + 8 * s, 1);        // the producer (dynamic mode)
       s_theta[s] = fkey(-INFINITY);
     }
-    if (a.flat == 4) {
+    if (kFlat && a.flat == 4) {
       // one mbarrier per owned split row, expecting its other parts
-      ItemIter it0;
+      ItemIter<true> it0;
       it0.init(a);
       Item x;
       while (it0.next(a, x))
@@ -574,7 +745,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     fence_barrier_init();
   }
   __syncthreads();
-  if (a.flat == 4) cluster_sync_all();  // every owner's barriers exist before any remote arrive
+  if (kFlat && a.flat == 4) cluster_sync_all();  // every owner's barriers exist before any remote arrive
   const float c = a.c;
   // K4 is launched with programmatic dependent launch: its prologue (barrier
   // init, item math, pattern staging) overlaps the previous kernel's tail;
@@ -590,55 +761,68 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 
   if (warp == NCW) {
     // ------------------------------------------------ producer warp
-    if (lane == 0) {
-      const uint64_t pol = a.keep_l2 == 1 ? policy_evict_last()
-                           : a.keep_l2 == 2 ? policy_evict_normal() : policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
+    // The whole warp waits for the consumers' release of a ring stage on that
+    // stage's named barrier (bar.sync: the warp is descheduled, no polling);
+    // lane 0 issues the copies.  One bar.sync per chunk, drained at the end.
+    const uint64_t pol = a.keep_l2 == 1 ? policy_evict_last()
+                         : a.keep_l2 == 2 ? policy_evict_normal() : policy_evict_first();
+    int stage = 0;
+    long long n_issued = 0;
 #ifdef RELAY_TRACE
-      bool first_issue = true;
-      int n_issued = 0;
+    bool first_issue = true;
 #endif
-      auto issue = [&](const Item& item) {
-        const T* row = logits + item.r * a.stride;
-        const Geom g = row_geom<E>(row, item.j0, item.j1);
-        const char* src = reinterpret_cast<const char*>(row + item.j0 + g.head);
-        for (int off = 0; off < g.body; off += SB) {
-          const uint32_t bytes = static_cast<uint32_t>(min(SB, g.body - off));
-          mbar_wait_sleep(empty_s + 8 * stage, phase ^ 1);
+    auto issue = [&](const Item& item) {
+      const T* row = logits + item.r * a.stride;
+      const Geom g = row_geom<E>(row, item.j0, item.j1);
+      const char* src = reinterpret_cast<const char*>(row + item.j0 + g.head);
+      for (int off = 0; off < g.body; off += SB) {
+        const uint32_t bytes = static_cast<uint32_t>(min(SB, g.body - off));
+        if (n_issued >= NS) named_bar(kBarRing0 + stage, NCT + 32);
+        if (lane == 0) {
+          fence_proxy_async_smem();  // the consumers' reads precede the async-proxy refill
           mbar_expect_tx(full_s + 8 * stage, bytes);
           bulk_g2s(ring_s + stage * SB, src + off, bytes, full_s + 8 * stage, pol);
 #ifdef RELAY_TRACE
           if (first_issue) { TRACE(15); first_issue = false; }
-          ++n_issued;
 #endif
-          if (++stage == NS) { stage = 0; phase ^= 1; }
         }
-      };
-      if (a.flat == 2) {
-        const long long total = a.n_rows * a.cpr;
-        if constexpr (MODE == kModeStep) pdl_wait();
-        long long k = atomicAdd(a.work, 1);
-        for (int it = 0;; ++it) {
-          const int slot = it % kSlots;
-          mbar_wait_sleep(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
-          const bool done = k >= total;
+        ++n_issued;
+        if (++stage == NS) stage = 0;
+      }
+    };
+    if (kFlat && a.flat == 2) {
+      const long long total = a.n_rows * a.cpr;
+      if constexpr (MODE == kModeStep) pdl_wait();
+      long long k = 0;
+      if (lane == 0) k = atomicAdd(a.work, 1);
+      k = __shfl_sync(kFull, k, 0);
+      for (int it = 0;; ++it) {
+        const int slot = it % kSlots;
+        mbar_wait_sleep(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
+        const bool done = k >= total;
+        long long kn = 0;
+        if (lane == 0) {
           s_item[slot] = done ? -1 : k;
           mbar_arrive(ifull_s + 8 * slot);
-          if (done) break;
-          const long long kn = atomicAdd(a.work, 1);  // claimed while this chunk streams
-          issue(ItemIter::from_k(a, k));
-          k = kn;
+          if (!done) kn = atomicAdd(a.work, 1);  // claimed while this chunk streams
         }
-      } else {
-        ItemIter iter;
-        iter.init(a);
-        Item item;
-        bool more = iter.next(a, item);
-        if constexpr (MODE == kModeStep) pdl_wait();
-        for (; more; more = iter.next(a, item)) issue(item);
+        __syncwarp();
+        if (done) break;
+        kn = __shfl_sync(kFull, kn, 0);
+        issue(ItemIter<true>::from_k(a, k));
+        k = kn;
       }
+    } else {
+      ItemIter<kFlat> iter;
+      iter.init(a);
+      Item item;
+      bool more = iter.next(a, item);
+      if constexpr (MODE == kModeStep) pdl_wait();
+      for (; more; more = iter.next(a, item)) issue(item);
     }
+    // drain: the stages still in flight are released once more each
+    for (long long k = n_issued > NS ? n_issued - NS : 0; k < n_issued; ++k)
+      named_bar(kBarRing0 + static_cast<int>(k % NS), NCT + 32);
     return;
   }
 
@@ -649,7 +833,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       pdl_wait();
       if (lane == 0 && a.row_ready) pdl_launch_dependents();
     }
-    ItemIter iter;
+    ItemIter<kFlat> iter;
     iter.init(a);
     Item item;
     for (int it = 0; fetch_item(a, iter, it, kSlots, s_item, ifull_s, item); ++it) {
@@ -658,7 +842,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const T* row = logits + r * a.stride;
       SwitchIn in{};
       if constexpr (MODE == kModeStep) in = load_switch_in(a, r);
-      mbar_wait(rfull_s + 8 * slot, (it / kSlots) & 1);  // on the critical path: spin
+      // the consumers' partials: a named barrier (a spinning epilogue warp took
+      // issue slots from the consumers for the whole row, 0.45 per element)
+      named_bar(kBarRed0 + slot, NCT + 32);
       Partial q = partial_empty();
 #pragma unroll
       for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
@@ -689,7 +875,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.row_ready + r) : "memory");
         continue;
       }
-      if (a.flat == 4) {
+      if (kFlat && a.flat == 4) {
         // cluster mode: the CTA holding the row's FIRST part owns it (its
         // last item: the other parts are the first items of the following
         // CTAs, long done, so no CTA waits on a chain of predecessors); the
@@ -760,7 +946,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in);
       if (lane == 0 && it < 7) TRACE(24 + it);
     }
-    if (a.flat == 2 && lane == 0) {
+    if (kFlat && a.flat == 2 && lane == 0) {
       // the last CTA out re-arms the work counter for the next launch / replay
       // (every producer's final claim precedes its CTA's arrival here)
       if (atomic_add_acq_rel(a.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
@@ -776,9 +962,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #ifdef RELAY_TRACE
   int n_stage = 0;
 #endif
-  int stage = 0;
+  int stage = 0;        // ring position, carried across items
   uint32_t phase = 0;
-  ItemIter iter;
+  const uint32_t ring_t = ring_s + static_cast<uint32_t>(tid) * 16;  // this thread's first vector of stage 0
+  ItemIter<kFlat> iter;
   iter.init(a);
   Item item;
   for (int it = 0; fetch_item(a, iter, it, kSlots, s_item, ifull_s, item); ++it) {
@@ -793,57 +980,103 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     const uint32_t theta_p = theta_s + 4 * slot;
     const T* row = logits + r * a.stride;
     const Geom g = row_geom<E>(row, j0, j1);
+    const int nst = g.body / SB;             // full ring stages of the item
+    const int rem = g.body - nst * SB;       // bytes of its last, partial stage
+    const int jt = j0 + g.head + tid * VEC;  // element index of this thread's first vector
     ThreadState st;
     state_init(st);
     float theta_w = -INFINITY;  // warp-local lower bound of the row's 2nd-best
+    float T = 0.0f;             // consume_fast's guard (set by the row's first stage)
+    int tkey = INT_MIN;         // the threshold key T was computed from
     float tmax = -INFINITY;     // this thread's maximum (relay_step_sample's bound)
     if (tid < g.head) {
       const float x = E::load1(row + j0 + tid);
       consume_scalar(x, j0 + tid, st, c);
       if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, x);
     }
-    for (int off = 0; off < g.body; off += SB) {
-      const int bytes = min(SB, g.body - off);
-      const int jb = j0 + g.head + off / E::SZ;
+    if (nst > 0) {
+      // the item's first stage: the row-start probe.  The two half maxima of
+      // a thread are two distinct elements, so the warp's second-best of them
+      // bounds the row's 2nd-best from below; after the consumer barrier the
+      // slot holds the best of all warps' (the 2nd-best of the stage's 2 * NCT
+      // half maxima), so the steady state starts mostly on the fast path.
       mbar_wait(full_s + 8 * stage, phase);
 #ifdef RELAY_TRACE
       if (tid == 0 && n_stage < 10) TRACE(1 + n_stage);
       ++n_stage;
 #endif
-      const uint32_t buf = ring_s + stage * SB;
+      uint4 raw[UV];
+#pragma unroll
+      for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCT * 16);
+      bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);  // release: the loads precede the refill
+      const float2 h = stage_max2<E, UV>(raw);
+      theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
+      named_bar(1, NCT);
+      if (tid == 0 && it == 1) TRACE(13);
+      tkey = theta_load(theta_p);
+      const float theta = fmaxf(theta_w, unkey(tkey));
       bool slow = false;
-      if (bytes == SB) {
+      consume_stage<E, UV>(raw, h, jt, NCT * VEC, st, c, theta, slow);
+      if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
+      T = guard_T(fmaxf(theta, theta_w), st, c);
+      if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h.x, h.y));
+      if (tid == 0 && it == 1) TRACE(14);
+      if (++stage == NS) { stage = 0; phase ^= 1; }
+    }
+    // steady state: per stage the wait, the words, one release, the terms and
+    // one guard comparison (consume_fast)
+    for (int k = 1; k < nst; ++k) {
+      mbar_wait(full_s + 8 * stage, phase);
+#ifdef RELAY_TRACE
+      if (tid == 0 && n_stage < 10) TRACE(1 + n_stage);
+      ++n_stage;
+#endif
+      const int key = theta_load(theta_p);  // before the words: its latency hides under the sum
+      uint4 raw[UV];
+#pragma unroll
+      for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCT * 16);
+      bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
+      consume_fast<E, UV>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
+      if constexpr (MODE == kModeStep) {
+        if (a.topk > 0) {
+          const float2 h = stage_max2<E, UV>(raw);
+          tmax = fmaxf(tmax, fmaxf(h.x, h.y));
+        }
+      }
+      if (++stage == NS) { stage = 0; phase ^= 1; }
+    }
+    if (rem > 0) {
+      mbar_wait(full_s + 8 * stage, phase);
+      const uint32_t buf = ring_s + stage * SB;
+      const int jb = j0 + g.head + nst * (SB / E::SZ);
+      if (nst > 0) {
+        // the last, partial stage: the missing vectors read as -inf (no term,
+        // never pushed)
+        const int key = theta_load(theta_p);
+        const int nvalid = min(UV, max(0, (rem / 16 - tid + NCT - 1) / NCT));
         uint4 raw[UV];
 #pragma unroll
-        for (int u = 0; u < UV; u++) raw[u] = lds128(buf + (tid + u * NCT) * 16);
-        mbar_arrive(empty_s + 8 * stage);  // release: the loads above precede the refill
-        const float2 h = stage_max2<E, UV>(raw);
-        if (off == 0) {
-          // item-start probe: the two half maxima are two distinct elements, so
-          // the warp's second-best of them bounds the row's 2nd-best from below;
-          // after the consumer barrier the slot holds the best of all warps'
-          // (the 2nd-best of the stage's 2 * NCT half maxima), so the first
-          // stage is already mostly on the fast path
-          theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
-          named_bar(1, NCT);
-          if (tid == 0 && it == 1) TRACE(13);
+        for (int u = 0; u < UV; u++) raw[u] = u < nvalid ? lds128(ring_t + stage * SB + u * NCT * 16) : E::neg_inf16();
+        bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
+        consume_fast<E, UV>(raw, nvalid, jb + tid * VEC, NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
+        if constexpr (MODE == kModeStep) {
+          if (a.topk > 0) {
+            const float2 h = stage_max2<E, UV>(raw);
+            tmax = fmaxf(tmax, fmaxf(h.x, h.y));
+          }
         }
+      } else {  // a row shorter than one stage: vector by vector, max-guarded
         const float theta = fmaxf(theta_w, unkey(theta_load(theta_p)));
-        consume_stage<E, UV>(raw, h, jb + tid * VEC, NCT * VEC, st, c, theta, slow);
-        if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h.x, h.y));
-        if (tid == 0 && it == 1 && off == 0) TRACE(14);
-      } else {
-        const float theta = fmaxf(theta_w, unkey(theta_load(theta_p)));
-        const int nvec = bytes / 16;
+        const int nvec = rem / 16;
+        bool slow = false;
         for (int v = tid; v < nvec; v += NCT) {
           const uint4 raw1[1] = {lds128(buf + v * 16)};
           const float2 h1 = stage_max2<E, 1>(raw1);
           consume_stage<E, 1>(raw1, h1, jb + v * VEC, 0, st, c, theta, slow);
           if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h1.x, h1.y));
         }
-        mbar_arrive(empty_s + 8 * stage);
+        bar_arrive(kBarRing0 + stage, NCT + 32);
       }
-      if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     if (tid < j1 - g.tail) {
@@ -872,7 +1105,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #pragma unroll
     for (int off = 16; off >= RPW; off >>= 1) p = partial_merge(p, shfl_xor_partial(p, off));
     if (lane < RPW) s_red[slot][warp * RPW + lane] = p;
-    mbar_arrive(rfull_s + 8 * slot);
+    bar_arrive(kBarRed0 + slot, NCT + 32);
     if (tid == 0 && it < 8) TRACE(16 + it);
   }
   if (tid == 0) TRACE(31);

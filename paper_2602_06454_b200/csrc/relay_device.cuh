@@ -198,6 +198,7 @@ struct EBf16 {
   __device__ static __forceinline__ float load1(const T* p) {
     return __uint_as_float(static_cast<uint32_t>(__ldg(reinterpret_cast<const unsigned short*>(p))) << 16);
   }
+  __device__ static __forceinline__ uint4 neg_inf16() { return make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u); }
 };
 
 struct EF16 {
@@ -219,6 +220,7 @@ struct EF16 {
     unsigned short b = __ldg(reinterpret_cast<const unsigned short*>(p));
     return __half2float(__ushort_as_half(b));
   }
+  __device__ static __forceinline__ uint4 neg_inf16() { return make_uint4(0xfc00fc00u, 0xfc00fc00u, 0xfc00fc00u, 0xfc00fc00u); }
 };
 
 struct EF32 {
@@ -228,6 +230,7 @@ struct EF32 {
   __device__ static __forceinline__ void unpack2(uint32_t, float&, float&) {}
   __device__ static __forceinline__ uint32_t pmax(uint32_t a, uint32_t) { return a; }
   __device__ static __forceinline__ float load1(const T* p) { return __ldg(p); }
+  __device__ static __forceinline__ uint4 neg_inf16() { return make_uint4(0xff800000u, 0xff800000u, 0xff800000u, 0xff800000u); }
 };
 
 // NaN-propagating maxima (FMNMX.NAN / FMNMX3.NAN).
@@ -393,6 +396,31 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+// Arrive on a named barrier without waiting (release: this thread's earlier
+// accesses are performed for the threads that sync on it).
+__device__ __forceinline__ void bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// bar_arrive that also pins the stage's loaded words: every load of raw[]
+// completes before the arrive and every use of raw[] comes after it, so the
+// ring slot is released as soon as it is read (the scheduler otherwise
+// interleaves the loads with the math and releases late, shrinking the
+// effective ring depth).
+template <int UV>
+__device__ __forceinline__ void bar_arrive_pinned(int id, int threads, uint4 (&raw)[UV]) {
+#pragma unroll
+  for (int u = 0; u < UV; u++)
+    asm volatile("" : "+r"(raw[u].x), "+r"(raw[u].y), "+r"(raw[u].z), "+r"(raw[u].w));
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
+#pragma unroll
+  for (int u = 0; u < UV; u++)
+    asm volatile("" : "+r"(raw[u].x), "+r"(raw[u].y), "+r"(raw[u].z), "+r"(raw[u].w));
+}
+// Order this thread's view of shared memory (generic proxy) before its
+// subsequent async-proxy (TMA) operations on it.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 // ------------------------------------ thread-block clusters / DSMEM (K4)
 // The shared::cluster address of the same variable in CTA `rank` of the cluster.
@@ -423,6 +451,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// The same 16 bytes through an opaque move (the compiler cannot reuse values
+// derived from the input across it).
+__device__ __forceinline__ uint4 opaque(uint4 v) {
+  asm volatile("" : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w));
+  return v;
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {

@@ -1,6 +1,6 @@
-"""A/B of K1 (relay_margin_rows on configs[1]) between two builds of the
+"""A/B of K1 (relay_margin_rows on configs[1]) between builds of the
 library, interleaved in one process so clocks and thermals are shared:
-    python tools/k1_ab.py path/to/librelay_a.so path/to/librelay_b.so [rounds]"""
+    python tools/k1_ab.py path/to/librelay_a.so path/to/librelay_b.so [...] [rounds]"""
 import ctypes as C
 import os
 import statistics
@@ -13,8 +13,9 @@ import torch  # noqa: E402
 import paper_2602_06454_b200 as relay  # noqa: E402
 import synth  # noqa: E402
 
-libs = [relay._load.__globals__["C"].CDLL(p) for p in sys.argv[1:3]]
-rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+paths = [a for a in sys.argv[1:] if a.endswith(".so")]
+rounds = int(sys.argv[-1]) if not sys.argv[-1].endswith(".so") else 8
+libs = [C.CDLL(p) for p in paths]
 T, V = 32768, 151936
 L = synth.make_logits(T, V, "bf16", device="cuda:0", chunk_rows=2048)
 out = {k: torch.empty(T, dtype=d, device="cuda:0") for k, d in
@@ -25,7 +26,7 @@ for lib in libs:
     lib.relay_margin_rows.argtypes = [P, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_float, P, P, P, P, P, P]
 args = (L.data_ptr(), 0, T, V, V, 1.0, out["margin"].data_ptr(), out["top1"].data_ptr(), out["top2"].data_ptr(),
         out["lse"].data_ptr(), out["status"].data_ptr(), torch.cuda.current_stream().cuda_stream)
-res = [[], []]
+res = [[] for _ in libs]
 for _ in range(rounds):
     for k, lib in enumerate(libs):
         for _ in range(2):
@@ -37,5 +38,5 @@ for _ in range(rounds):
         e1.record()
         torch.cuda.synchronize()
         res[k].append(e0.elapsed_time(e1) / 5)
-for k in range(2):
-    print(f"{os.path.basename(sys.argv[1 + k])}: median {statistics.median(res[k]):.4f} ms  min {min(res[k]):.4f}")
+for k in range(len(libs)):
+    print(f"{os.path.basename(paths[k])}: median {statistics.median(res[k]):.4f} ms  min {min(res[k]):.4f}")

@@ -246,14 +246,27 @@ relay_status_t relay_cueset_create_ex(const int32_t* pat_tokens, const int32_t* 
 relay_status_t relay_cueset_destroy(relay_cueset_t cs);
 int32_t relay_cueset_n_cues(relay_cueset_t cs);
 
-/* Workspace bytes for cue_scan + segment_reduce (n_tok positions) or for
- * step_switch (batch rows).  Use one workspace for cue_scan/segment_reduce
- * and a separate one for step_switch.  Both hold counters/flags that must be
- * zero before first use: call relay_workspace_init once after allocating
- * (the kernels leave them zero again, so CUDA-graph replays need no reset).
- * One workspace must not be used by two calls running concurrently. */
+/* Workspace (caller-owned device memory) for cue_scan + segment_reduce (up to
+ * n_tok positions) and step_switch / step_sample (up to batch rows): a scan
+ * region followed by a step region, so one workspace may serve both.
+ * relay_workspace_bytes gives the bytes for these capacities.
+ * relay_workspace_init zeroes the whole workspace (stream-ordered) and
+ * registers its capacities with the library (host-side, per process): every
+ * later call lays out its counters and flags by the registered capacities,
+ * not by its own n_tok / batch, so a workspace reused for smaller problems
+ * finds every persistent zero where the previous call left it (the kernels
+ * leave them zero again, so CUDA-graph replays need no reset).  Calls with a
+ * workspace that was not initialised, with a different ws_bytes, or with
+ * n_tok / batch above the capacities return RELAY_ERR_WORKSPACE.  Re-init
+ * re-registers (new capacities); relay_workspace_release forgets a workspace
+ * (call it before freeing the memory if the address may be reused).  One
+ * workspace must not be used by two calls running concurrently.
+ * Errors (init): RELAY_ERR_INVALID (NULL ws, negative capacities, n_tok >=
+ * 2^31); RELAY_ERR_WORKSPACE (ws_bytes below relay_workspace_bytes). */
 size_t relay_workspace_bytes(int64_t n_tok, int64_t occ_capacity, int32_t batch);
-relay_status_t relay_workspace_init(void* ws, size_t ws_bytes, relay_stream_t stream);
+relay_status_t relay_workspace_init(void* ws, size_t ws_bytes, int64_t n_tok, int64_t occ_capacity,
+                                    int32_t batch, relay_stream_t stream);
+relay_status_t relay_workspace_release(void* ws);
 
 /* ------------------------------------------------------------------ H2 --
  * relay_cue_scan — switch-cue occurrences by "simple token matching"
@@ -311,8 +324,12 @@ relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t 
  *          relay_stats_merge) to the single table, so calibration can be
  *          re-run on any subset of trajectories without another pass (the
  *          calibration-size study, Table 5).
- * Errors: RELAY_ERR_INVALID (NULLs, n_tok range, rank outside [0,world_size),
- * world_size < 1, !(tau finite), unknown flags); RELAY_ERR_WORKSPACE. */
+ * Bound: the u64 sum of squared Q20 margins is exact for < 2^24 summands, so
+ * one call takes n_tok < 2^24 and a table (accumulated over calls and ranks)
+ * must stay below 2^24 positions per row (relay_stats_finalize checks).
+ * Errors: RELAY_ERR_INVALID (NULLs, n_tok outside [0, 2^24), rank outside
+ * [0,world_size), world_size < 1, !(tau finite), unknown flags);
+ * RELAY_ERR_WORKSPACE. */
 #define RELAY_SEG_PER_TRAJECTORY 1u
 relay_status_t relay_segment_reduce(relay_cueset_t cs, const float* margin, int64_t n_tok,
                                     const int64_t* traj_offsets, int32_t n_traj,
@@ -334,14 +351,20 @@ relay_status_t relay_stats_init_tables(uint64_t* stats, int32_t n_tables, int32_
                                        int32_t world_size, relay_stream_t stream);
 /* Words in one table: (n_cues+1) * (8+world_size); 0 for bad arguments. */
 size_t relay_stats_words(int32_t n_cues, int32_t world_size);
-/* [host] Merge tables (host memory, n_tables consecutive tables) into one:
- * fields 0-7 add, the min slots take the minimum (as float bit patterns of
- * values in [0,1] / +inf, which order like the integers).  mask (uint8
- * [n_tables], nullable = all) picks the tables.  Merging before or after the
- * SUM all-reduce gives the same table.  out may not alias tables.
- * Errors: RELAY_ERR_INVALID (NULLs, n_tables < 0, n_cues/world_size range). */
+/* [host] Merge tables (host memory, n_tables consecutive tables) into one.
+ * rank in [0, world_size): tables of that rank (before the all-reduce):
+ * fields 0-7 and the other ranks' min slots add (they hold 0 on this rank),
+ * the rank's own min slot takes the minimum (float bit patterns of values in
+ * [0,1] / +inf order like the integers); with nothing merged the own slot is
+ * +inf and the others 0, exactly as relay_stats_init leaves a table.
+ * rank = -1: tables already all-reduced: every min slot takes the minimum.
+ * Hence summing the per-rank merges equals merging (rank -1) the summed
+ * tables.  mask (uint8 [n_tables], nullable = all) picks the tables.  out may
+ * not alias tables.
+ * Errors: RELAY_ERR_INVALID (NULLs, n_tables < 0, n_cues range, rank outside
+ * [-1, world_size)). */
 relay_status_t relay_stats_merge(const uint64_t* tables, int32_t n_tables, const uint8_t* mask,
-                                 int32_t n_cues, int32_t world_size, uint64_t* out);
+                                 int32_t n_cues, int32_t rank, int32_t world_size, uint64_t* out);
 
 /* ------------------------------------------------------------------ H6 --
  * relay_stats_allreduce — the path's one cross-GPU exchange: an in-place SUM
@@ -366,6 +389,14 @@ relay_status_t relay_stats_allreduce(void* nccl_comm, uint64_t* stats, int32_t n
  * torch.distributed broadcast); every rank then calls relay_nccl_comm_init
  * with its CUDA device current (collective: blocks until all ranks join).
  * relay_nccl_comm_destroy(NULL) is a no-op. */
+/* The NCCL this library resolved at run time (dlopen "libnccl.so.2"):
+ * ncclGetVersion's code (e.g. 22809 for 2.28.9) and, when path is non-NULL,
+ * the file it was loaded from (path_len bytes, NUL-terminated).  A
+ * communicator created by another NCCL copy (e.g. torch's) may be passed to
+ * relay_stats_allreduce only if this is the same library (same version and
+ * file): the binding checks both and otherwise builds its own communicator.
+ * Errors: RELAY_ERR_INVALID (NULL version); RELAY_ERR_NCCL (not loadable). */
+relay_status_t relay_nccl_version(int32_t* version, char* path, int32_t path_len);
 relay_status_t relay_nccl_unique_id(uint8_t* id_out);
 relay_status_t relay_nccl_comm_init(const uint8_t* id, int32_t world_size, int32_t rank, void** comm);
 relay_status_t relay_nccl_comm_destroy(void* comm);
@@ -383,7 +414,8 @@ relay_status_t relay_nccl_comm_destroy(void* comm);
  *   ablation, tab:cue_selection_ablation P:427-445).  Always n_c >= min_count.  With
  *   fewer than 2 global positions std/se are NaN and nothing is selected.
  *   out [host] relay_cue_summary_t[n_cues+1]; out[n_cues] is the global row.
- * Errors: RELAY_ERR_INVALID for NULLs, n_cues/world_size out of range, rule>3. */
+ * Errors: RELAY_ERR_INVALID for NULLs, n_cues/world_size out of range, rule>3,
+ * or a row with n >= 2^24 (its sum of squares may have wrapped). */
 typedef struct {
   int64_t n;
   double mean, std, se, token_mean, min, low_frac;

@@ -55,7 +55,8 @@ def _load():
         "relay_cueset_destroy": (C.c_int, [P]),
         "relay_cueset_n_cues": (i32, [P]),
         "relay_workspace_bytes": (sz, [i64, i64, i32]),
-        "relay_workspace_init": (C.c_int, [P, sz, P]),
+        "relay_workspace_init": (C.c_int, [P, sz, i64, i64, i32, P]),
+        "relay_workspace_release": (C.c_int, [P]),
         "relay_cue_scan": (C.c_int, [P, P, i64, P, i32, P, P, P, i64, P, P, sz, P]),
         "relay_segment_reduce": (C.c_int, [P, P, i64, P, i32, P, P, P, P, P, i64, f32, P, P, P, P,
                                            P, i32, i32, u32, P, sz, P]),
@@ -63,8 +64,9 @@ def _load():
                                                P, i32, i32, u32, P, sz, P]),
         "relay_stats_init": (C.c_int, [P, i32, i32, i32, P]),
         "relay_stats_init_tables": (C.c_int, [P, i32, i32, i32, i32, P]),
-        "relay_stats_merge": (C.c_int, [P, i32, P, i32, i32, P]),
+        "relay_stats_merge": (C.c_int, [P, i32, P, i32, i32, i32, P]),
         "relay_stats_allreduce": (C.c_int, [P, P, i32, i32, i32, P]),
+        "relay_nccl_version": (C.c_int, [P, P, i32]),
         "relay_nccl_unique_id": (C.c_int, [P]),
         "relay_nccl_comm_init": (C.c_int, [P, i32, i32, P]),
         "relay_nccl_comm_destroy": (C.c_int, [P]),
@@ -94,10 +96,10 @@ _lib = _load()
 EXPORTS = ("relay_version", "relay_status_string", "relay_last_error", "relay_margin_rows",
            "relay_margin_partials", "relay_margin_combine",
            "relay_cueset_create", "relay_cueset_create_ex", "relay_cueset_destroy", "relay_cueset_n_cues",
-           "relay_workspace_bytes", "relay_workspace_init", "relay_cue_scan",
+           "relay_workspace_bytes", "relay_workspace_init", "relay_workspace_release", "relay_cue_scan",
            "relay_segment_reduce", "relay_stats_init", "relay_stats_init_tables",
            "relay_stats_words", "relay_stats_merge", "relay_stats_allreduce",
-           "relay_nccl_unique_id", "relay_nccl_comm_init", "relay_nccl_comm_destroy",
+           "relay_nccl_version", "relay_nccl_unique_id", "relay_nccl_comm_init", "relay_nccl_comm_destroy",
            "relay_stats_finalize", "relay_step_switch", "relay_offload_estimate",
            "relay_step_sample", "relay_tp_exchange_create", "relay_tp_exchange_connect",
            "relay_tp_exchange_destroy", "relay_margin_rows_tp", "relay_read_probe_words",
@@ -378,10 +380,18 @@ def workspace_bytes(n_tok: int = 0, occ_capacity: int = 0, batch: int = 0) -> in
 
 
 def workspace(n_tok: int = 0, occ_capacity: int = 0, batch: int = 0, device="cuda", stream=None):
+    """A workspace for up to ``n_tok`` positions / ``occ_capacity`` occurrences
+    (cue_scan, segment_reduce) and ``batch`` rows (step_switch, step_sample),
+    zeroed and registered with the library (relay_workspace_init); released
+    when the tensor is garbage-collected."""
+    import weakref
+
     import torch
     nb = workspace_bytes(n_tok, occ_capacity, batch)
-    ws = torch.empty(nb, dtype=torch.uint8, device=device)
-    _check(_lib.relay_workspace_init(_ptr(ws), nb, _stream(stream)), "relay_workspace_init")
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=device)
+    _check(_lib.relay_workspace_init(_ptr(ws), ws.numel(), n_tok, occ_capacity, batch, _stream(stream)),
+           "relay_workspace_init")
+    weakref.finalize(ws, _lib.relay_workspace_release, C.c_void_p(ws.data_ptr()))
     return ws
 
 
@@ -428,9 +438,10 @@ def new_stats(n_cues: int, rank: int = 0, world_size: int = 1, device="cuda", st
     return stats_init(st, n_cues, rank, world_size, stream, n_tables)
 
 
-def stats_merge(host_tables: np.ndarray, n_cues: int, world_size: int = 1, mask=None):
-    """Host merge of per-trajectory tables (``mask``: which ones, default all)
-    into one table that ``stats_finalize`` takes."""
+def stats_merge(host_tables: np.ndarray, n_cues: int, world_size: int = 1, mask=None, rank: int = 0):
+    """Host merge of this rank's per-trajectory tables (``mask``: which ones,
+    default all) into one table that ``stats_finalize`` (or, first, the SUM
+    all-reduce) takes."""
     words = stats_words(n_cues, world_size)
     ht = np.ascontiguousarray(host_tables).view(np.uint64).reshape(-1)
     if ht.shape[0] % words:
@@ -444,7 +455,7 @@ def stats_merge(host_tables: np.ndarray, n_cues: int, world_size: int = 1, mask=
     out = np.empty(words, dtype=np.uint64)
     rc = _lib.relay_stats_merge(ht.ctypes.data_as(C.c_void_p), n_tables,
                                 None if m is None else m.ctypes.data_as(C.c_void_p), n_cues,
-                                world_size, out.ctypes.data_as(C.c_void_p))
+                                rank, world_size, out.ctypes.data_as(C.c_void_p))
     _check(rc, "relay_stats_merge")
     return out
 
@@ -461,6 +472,14 @@ def stats_allreduce(comm_ptr: int, stats, n_cues: int, world_size: int, n_tables
     _check(_lib.relay_stats_allreduce(C.c_void_p(comm_ptr), _ptr(stats), n_tables, n_cues,
                                       world_size, _stream(stream)), "relay_stats_allreduce")
     return stats
+
+
+def nccl_version():
+    """(ncclGetVersion code, file) of the NCCL librelay resolved at run time."""
+    v = C.c_int32(0)
+    buf = C.create_string_buffer(4096)
+    _check(_lib.relay_nccl_version(C.byref(v), buf, 4096), "relay_nccl_version")
+    return int(v.value), buf.value.decode(errors="replace")
 
 
 def nccl_unique_id() -> bytes:

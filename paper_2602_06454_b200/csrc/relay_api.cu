@@ -5,7 +5,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/relay.h"
@@ -103,6 +105,66 @@ StepWs step_ws_layout(void* base, int batch) {
   w.zsum = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
   w.bytes = off;
   return w;
+}
+
+// Workspace registry (host side): every call lays its counters and flags out
+// by the capacities the workspace was initialised with, never by the call's
+// own n_tok / batch, so a workspace reused with a smaller problem finds every
+// persistent zero where it was left (a size-dependent layout would put them
+// on stale data of another array).
+namespace {
+struct WsCaps {
+  size_t bytes;
+  long long n_tok, occ;
+  int batch;
+};
+std::mutex g_ws_mu;
+std::unordered_map<const void*, WsCaps> g_ws;
+}  // namespace
+
+void ws_register(const void* ws, size_t bytes, long long n_tok, long long occ, int batch) {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  g_ws[ws] = WsCaps{bytes, n_tok, occ, batch};
+}
+
+void ws_unregister(const void* ws) {
+  std::lock_guard<std::mutex> g(g_ws_mu);
+  g_ws.erase(ws);
+}
+
+// The scan layout of a registered workspace, checked against this call's n_tok.
+relay_status_t ws_scan(void* ws, size_t ws_bytes, long long n_tok, ScanWs* out) {
+  if (!ws) return fail(RELAY_ERR_WORKSPACE, "ws is NULL");
+  WsCaps c;
+  {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    auto it = g_ws.find(ws);
+    if (it == g_ws.end()) return fail(RELAY_ERR_WORKSPACE, "ws was not initialised by relay_workspace_init");
+    c = it->second;
+  }
+  if (ws_bytes != c.bytes) return fail(RELAY_ERR_WORKSPACE, "ws_bytes %zu differs from the %zu it was initialised with",
+                                       ws_bytes, c.bytes);
+  if (n_tok > c.n_tok) return fail(RELAY_ERR_WORKSPACE, "n_tok %lld exceeds the workspace's %lld", n_tok, c.n_tok);
+  *out = scan_ws_layout(ws, c.n_tok, c.occ);
+  return RELAY_OK;
+}
+
+// The step layout (after the scan region) of a registered workspace.
+relay_status_t ws_step(void* ws, size_t ws_bytes, int batch, StepWs* out) {
+  if (!ws) return fail(RELAY_ERR_WORKSPACE, "ws is NULL");
+  WsCaps c;
+  {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    auto it = g_ws.find(ws);
+    if (it == g_ws.end()) return fail(RELAY_ERR_WORKSPACE, "ws was not initialised by relay_workspace_init");
+    c = it->second;
+  }
+  if (ws_bytes != c.bytes) return fail(RELAY_ERR_WORKSPACE, "ws_bytes %zu differs from the %zu it was initialised with",
+                                       ws_bytes, c.bytes);
+  if (batch > c.batch) return fail(RELAY_ERR_WORKSPACE, "batch %d exceeds the workspace's %d", batch, c.batch);
+  const size_t off = scan_ws_layout(nullptr, c.n_tok, c.occ).bytes;
+  *out = step_ws_layout(static_cast<char*>(ws) + off, c.batch);
+  return RELAY_OK;
 }
 
 }  // namespace relay
@@ -320,15 +382,26 @@ int32_t relay_cueset_n_cues(relay_cueset_t cs) { return cs ? cs->dev.n_cues : -1
 
 size_t relay_workspace_bytes(int64_t n_tok, int64_t occ_capacity, int32_t batch) {
   size_t a = scan_ws_layout(nullptr, n_tok < 0 ? 0 : n_tok, occ_capacity).bytes;
-  size_t b = step_ws_layout(nullptr, batch).bytes;
-  return a > b ? a : b;
+  size_t b = step_ws_layout(nullptr, batch < 0 ? 0 : batch).bytes;
+  return a + b;  // the step region follows the scan region: one workspace may serve both
 }
 
-relay_status_t relay_workspace_init(void* ws, size_t ws_bytes, relay_stream_t stream) {
-  if (!ws && ws_bytes) return fail(RELAY_ERR_INVALID, "ws is NULL");
-  if (!ws_bytes) return RELAY_OK;
-  return cuda_status(cudaMemsetAsync(ws, 0, ws_bytes, reinterpret_cast<cudaStream_t>(stream)),
-                     "workspace init");
+relay_status_t relay_workspace_init(void* ws, size_t ws_bytes, int64_t n_tok, int64_t occ_capacity, int32_t batch,
+                                    relay_stream_t stream) {
+  if (!ws) return fail(RELAY_ERR_INVALID, "ws is NULL");
+  if (n_tok < 0 || n_tok >= 0x7fffffffLL || occ_capacity < 0 || batch < 0)
+    return fail(RELAY_ERR_INVALID, "capacities out of range");
+  const size_t need = relay_workspace_bytes(n_tok, occ_capacity, batch);
+  if (ws_bytes < need) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes for these capacities", need);
+  relay_status_t s = cuda_status(cudaMemsetAsync(ws, 0, ws_bytes, reinterpret_cast<cudaStream_t>(stream)),
+                                 "workspace init");
+  if (s == RELAY_OK) relay::ws_register(ws, ws_bytes, n_tok, occ_capacity, batch);
+  return s;
+}
+
+relay_status_t relay_workspace_release(void* ws) {
+  relay::ws_unregister(ws);
+  return RELAY_OK;
 }
 
 relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t n_tok,
@@ -342,8 +415,9 @@ relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t 
   if (occ_capacity > 0 && (!occ_pos || !occ_pat)) return fail(RELAY_ERR_INVALID, "occ_pos/occ_pat are required");
   relay_status_t s = check_offsets_args(traj_offsets, n_traj);
   if (s != RELAY_OK) return s;
-  ScanWs w = scan_ws_layout(ws, n_tok, occ_capacity);
-  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  ScanWs w;
+  s = ws_scan(ws, ws_bytes, n_tok, &w);
+  if (s != RELAY_OK) return s;
   return cuda_status(launch_cue_scan(cs->dev, tokens, n_tok, reinterpret_cast<const long long*>(traj_offsets),
                                      traj_offsets ? n_traj : 1, term_bits, occ_pos, occ_pat, occ_capacity,
                                      reinterpret_cast<long long*>(n_occ), w,
@@ -373,19 +447,25 @@ relay_status_t relay_stats_init(uint64_t* stats, int32_t n_cues, int32_t rank, i
 }
 
 relay_status_t relay_stats_merge(const uint64_t* tables, int32_t n_tables, const uint8_t* mask,
-                                 int32_t n_cues, int32_t world_size, uint64_t* out) {
+                                 int32_t n_cues, int32_t rank, int32_t world_size, uint64_t* out) {
   if (!out || (n_tables > 0 && !tables)) return fail(RELAY_ERR_INVALID, "tables and out are required");
   if (n_tables < 0) return fail(RELAY_ERR_INVALID, "n_tables < 0");
   if (n_cues < 1 || n_cues > kMaxCues) return fail(RELAY_ERR_INVALID, "n_cues out of range");
-  if (world_size < 1) return fail(RELAY_ERR_INVALID, "world_size < 1");
+  if (world_size < 1 || rank < -1 || rank >= world_size) return fail(RELAY_ERR_INVALID, "bad rank/world_size");
   const int nf = kStatFields + world_size;
+  // a min slot takes the minimum if it is this rank's (or every slot, rank -1:
+  // tables already all-reduced); the other slots hold 0 on this rank and add
+  auto is_min = [&](size_t i) {
+    const int f = static_cast<int>(i % nf);
+    return f >= kStatFields && (rank < 0 || f == kStatFields + rank);
+  };
   const size_t words = static_cast<size_t>(n_cues + 1) * nf;
-  for (size_t i = 0; i < words; i++) out[i] = (static_cast<int>(i % nf) < kStatFields) ? 0ull : 0x7f800000ull;
+  for (size_t i = 0; i < words; i++) out[i] = is_min(i) ? 0x7f800000ull : 0ull;
   for (int32_t t = 0; t < n_tables; t++) {
     if (mask && !mask[t]) continue;
     const uint64_t* tab = tables + static_cast<size_t>(t) * words;
     for (size_t i = 0; i < words; i++) {
-      if (static_cast<int>(i % nf) < kStatFields) out[i] += tab[i];
+      if (!is_min(i)) out[i] += tab[i];
       else if (tab[i] < out[i]) out[i] = tab[i];
     }
   }
@@ -401,7 +481,8 @@ static relay_status_t segment_reduce_impl(relay_tp_exchange_t x, relay_cueset_t 
                                     size_t ws_bytes, relay_stream_t stream) {
   if (!cs || !stats || !n_occ) return fail(RELAY_ERR_INVALID, "cs, stats and n_occ are required");
   if (flags & ~RELAY_SEG_PER_TRAJECTORY) return fail(RELAY_ERR_INVALID, "unknown flags 0x%x", flags);
-  if (n_tok < 0 || n_tok >= 0x7fffffffLL) return fail(RELAY_ERR_INVALID, "n_tok must be in [0, 2^31)");
+  if (n_tok < 0 || n_tok >= (1LL << 24))
+    return fail(RELAY_ERR_INVALID, "n_tok must be in [0, 2^24): the table's u64 sum of squares of Q20 margins");
   if (n_tok > 0 && (!margin || !term_bits)) return fail(RELAY_ERR_INVALID, "margin and term_bits are required");
   if (occ_capacity < 0) return fail(RELAY_ERR_INVALID, "occ_capacity < 0");
   if (occ_capacity > 0 && (!occ_pos || !occ_pat || !seg_end || !seg_mean || !seg_min || !seg_lowfrac))
@@ -422,8 +503,9 @@ static relay_status_t segment_reduce_impl(relay_tp_exchange_t x, relay_cueset_t 
       return fail(RELAY_ERR_INVALID, "exchange slots hold %lld B, the table(s) need %lld B + 8",
                   x->pe.rows_cap * 32, words * 8);
   }
-  ScanWs w = scan_ws_layout(ws, n_tok, occ_capacity);
-  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  ScanWs w;
+  s = ws_scan(ws, ws_bytes, n_tok, &w);
+  if (s != RELAY_OK) return s;
   return cuda_status(
       launch_segment_reduce(cs->dev, margin, n_tok, reinterpret_cast<const long long*>(traj_offsets),
                             traj_offsets ? n_traj : 1, reinterpret_cast<const long long*>(think_end_pos),
@@ -489,6 +571,11 @@ relay_status_t relay_stats_finalize(const uint64_t* host_stats, int32_t n_cues, 
   if (rule < 0 || rule > 3) return fail(RELAY_ERR_INVALID, "rule must be 0, 1, 2 or 3");
   const int nf = kStatFields + world_size;
   const double Q = 1048576.0;
+  // sum q^2 (q <= 2^20) is exact in u64 only below 2^24 summands per row
+  for (int r = 0; r <= n_cues; r++)
+    if (host_stats[static_cast<size_t>(r) * nf + RELAY_F_N] >= (1ull << 24))
+      return fail(RELAY_ERR_INVALID, "table row %d holds >= 2^24 positions/occurrences: its u64 sum of squares "
+                  "may have wrapped (split the corpus into tables of < 2^24 positions)", r);
   for (int r = 0; r <= n_cues; r++) {
     const uint64_t* row = host_stats + static_cast<size_t>(r) * nf;
     relay_cue_summary_t& o = out[r];
@@ -558,8 +645,9 @@ relay_status_t relay_step_switch(relay_cueset_t cs, const void* logits, relay_dt
   if (batch == 0) return RELAY_OK;
   if (!logits || !state || !hist || !margin || !flag || !cue_id)
     return fail(RELAY_ERR_INVALID, "logits/state/hist/margin/flag/cue_id are required");
-  StepWs w = step_ws_layout(ws, batch);
-  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  StepWs w;
+  const relay_status_t ws_s = ws_step(ws, ws_bytes, batch, &w);
+  if (ws_s != RELAY_OK) return ws_s;
   return cuda_status(launch_step_switch(cs->dev, logits, static_cast<int>(dt), batch, static_cast<int>(vocab),
                                         row_stride, inv_temperature, sampled, state, hist, small_run, margin_gate,
                                         max_small_segment, margin, top1, top2, flag, cue_id, w,
@@ -593,8 +681,9 @@ relay_status_t relay_step_sample(relay_cueset_t cs, const void* logits, relay_dt
   if (batch == 0) return RELAY_OK;
   if (!logits || !state || !hist || !margin || !flag || !cue_id || !uniform || !sampled)
     return fail(RELAY_ERR_INVALID, "logits/state/hist/margin/flag/cue_id/uniform/sampled are required");
-  StepWs w = step_ws_layout(ws, batch);
-  if (!ws || ws_bytes < w.bytes) return fail(RELAY_ERR_WORKSPACE, "need %zu workspace bytes", w.bytes);
+  StepWs w;
+  const relay_status_t ws_s = ws_step(ws, ws_bytes, batch, &w);
+  if (ws_s != RELAY_OK) return ws_s;
   const int k = static_cast<int>(top_k < vocab ? top_k : vocab);  // 0: no top-k
   return cuda_status(launch_step_sample(cs->dev, logits, static_cast<int>(dt), batch, static_cast<int>(vocab),
                                         row_stride, inv_temperature, temperature, k, top_p, uniform, state,

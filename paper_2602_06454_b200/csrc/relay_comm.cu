@@ -26,6 +26,7 @@ struct NcclApi {
   decltype(&ncclCommDestroy) comm_destroy = nullptr;
   decltype(&ncclAllReduce) all_reduce = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
+  decltype(&ncclGetVersion) get_version = nullptr;
   bool ok = false;
 };
 
@@ -41,6 +42,7 @@ const NcclApi& nccl() {
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    api.get_version = reinterpret_cast<decltype(api.get_version)>(dlsym(h, "ncclGetVersion"));
     api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_reduce && api.error_string;
   });
   return api;
@@ -54,6 +56,25 @@ relay_status_t nccl_status(ncclResult_t r, const char* what) {
 }  // namespace
 
 extern "C" {
+
+relay_status_t relay_nccl_version(int32_t* version, char* path, int32_t path_len) {
+  if (!version) return relay::fail(RELAY_ERR_INVALID, "version is NULL");
+  const NcclApi& a = nccl();
+  if (!a.ok || !a.get_version) return relay::fail(RELAY_ERR_NCCL, "libnccl.so.2 not loadable");
+  int v = 0;
+  relay_status_t s = nccl_status(a.get_version(&v), "ncclGetVersion");
+  if (s != RELAY_OK) return s;
+  *version = v;
+  if (path && path_len > 0) {
+    Dl_info info{};
+    path[0] = 0;
+    if (dladdr(reinterpret_cast<void*>(a.all_reduce), &info) && info.dli_fname) {
+      std::strncpy(path, info.dli_fname, static_cast<size_t>(path_len) - 1);
+      path[path_len - 1] = 0;
+    }
+  }
+  return RELAY_OK;
+}
 
 relay_status_t relay_nccl_unique_id(uint8_t* id_out) {
   if (!id_out) return relay::fail(RELAY_ERR_INVALID, "id_out is NULL");

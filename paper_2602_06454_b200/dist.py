@@ -11,6 +11,8 @@ the GPUs; gloo in the CPU tests).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 
@@ -128,6 +130,53 @@ def torch_nccl_comm(group=None, device=None) -> int:
     return ptr
 
 
+def _loaded_nccl_files() -> set:
+    """The libnccl files mapped into this process."""
+    try:
+        with open("/proc/self/maps") as f:
+            return {os.path.realpath(line.split()[-1]) for line in f
+                    if "libnccl" in line and line.split()[-1].startswith("/")}
+    except OSError:
+        return set()
+
+
+def torch_comm_compatible() -> tuple:
+    """(ok, why): may a communicator torch's ProcessGroupNCCL built be handed to
+    librelay's ncclAllReduce?  Only when librelay resolved the very library
+    torch uses: the same NCCL version and the only libnccl file mapped in the
+    process (a statically linked or second NCCL copy would make the ncclComm_t
+    a foreign object)."""
+    import torch
+    import paper_2602_06454_b200 as relay
+    tv = torch.cuda.nccl.version()
+    tv = tv if isinstance(tv, int) else tv[0] * 10000 + tv[1] * 100 + (tv[2] if len(tv) > 2 else 0)
+    rv, path = relay.nccl_version()
+    files = _loaded_nccl_files()
+    if rv != tv:
+        return False, f"librelay resolved NCCL {rv}, torch uses {tv}"
+    if os.path.realpath(path) not in files or len(files) != 1:
+        return False, f"librelay's NCCL {path} is not torch's only NCCL ({sorted(files)})"
+    return True, f"NCCL {rv} from {path}"
+
+
+_own_comms = {}
+
+
+def default_comm(group=None, device=None) -> int:
+    """The communicator relay_stats_allreduce runs on: torch's own when it is
+    the same NCCL library (torch_comm_compatible), else a librelay-owned one
+    (NcclComm.from_group, built once per group)."""
+    import torch.distributed as dist
+    ok, _ = torch_comm_compatible()
+    if ok:
+        return torch_nccl_comm(group, device)
+    key = id(group) if group is not None else 0
+    if key not in _own_comms:
+        import paper_2602_06454_b200 as relay
+        _own_comms[key] = relay.NcclComm.from_group(dist.get_rank(group), dist.get_world_size(group), group)
+    return _own_comms[key].ptr
+
+
 def allreduce_stats(stats, n_cues: int, world_size: int, group=None, n_tables: int = 1,
                     comm: int | None = None, stream=None):
     """H6: one SUM all-reduce of the uint64 stats table(s).  On CUDA tensors
@@ -138,7 +187,7 @@ def allreduce_stats(stats, n_cues: int, world_size: int, group=None, n_tables: i
     import torch.distributed as dist
     if stats.is_cuda and dist.get_backend(group) == "nccl":
         import paper_2602_06454_b200 as relay
-        ptr = comm if comm is not None else torch_nccl_comm(group, stats.device)
+        ptr = comm if comm is not None else default_comm(group, stats.device)
         return relay.stats_allreduce(ptr, stats, n_cues, world_size, n_tables, stream)
     dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
     return stats

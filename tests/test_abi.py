@@ -76,6 +76,46 @@ def test_host_validation_without_device(relay):
     del t
 
 
+def test_workspace_registry_without_device(relay):
+    """Workspace calls are checked against the registry before any launch:
+    an unregistered workspace, NULL, or bad capacities fail on the host."""
+    lib = relay._lib
+    P = C.c_void_p
+    ptr = P(4096)
+    cs = P(64)      # never dereferenced: the workspace check fails first
+    # cue_scan with a workspace that relay_workspace_init never saw
+    n_occ = np.zeros(1, np.int64)
+    assert lib.relay_cue_scan(cs, ptr, 10, None, 1, ptr, ptr, ptr, 4, n_occ.ctypes.data_as(P), ptr,
+                              1 << 20, None) == 7
+    assert b"relay_workspace_init" in lib.relay_last_error()
+    assert lib.relay_workspace_init(None, 16, 10, 10, 0, None) == 1
+    assert lib.relay_workspace_init(ptr, 1 << 20, -1, 0, 0, None) == 1
+    need = relay.workspace_bytes(100000, 1000, 64)
+    assert lib.relay_workspace_init(ptr, need - 1, 100000, 1000, 64, None) == 7
+    assert lib.relay_workspace_release(ptr) == 0
+    # one workspace serves both regions: the size is the sum
+    step64 = relay.workspace_bytes(0, 0, 64) - relay.workspace_bytes(0, 0, 0)
+    assert step64 > 0 and need == relay.workspace_bytes(100000, 1000, 0) + step64
+
+
+def test_nccl_version_is_torchs(relay):
+    """relay_nccl_version reports the NCCL librelay resolves at run time; the
+    binding hands torch's communicator to it only when it is torch's library
+    (dist.torch_comm_compatible)."""
+    import torch
+    try:
+        code, path = relay.nccl_version()
+    except relay.RelayError:
+        pytest.skip("no libnccl.so.2 resolvable here")
+    tv = torch.cuda.nccl.version()
+    tv = tv if isinstance(tv, int) else tv[0] * 10000 + tv[1] * 100 + (tv[2] if len(tv) > 2 else 0)
+    assert code > 20000 and path.endswith(".so.2") or "libnccl" in path
+    from paper_2602_06454_b200 import dist as rdist
+    ok, why = rdist.torch_comm_compatible()
+    assert ok == (code == tv and path and __import__("os").path.realpath(path) in rdist._loaded_nccl_files()
+                  and len(rdist._loaded_nccl_files()) == 1), why
+
+
 def test_workspace_sizes_are_monotone(relay):
     a = relay.workspace_bytes(1000, 10, 0)
     b = relay.workspace_bytes(100000, 1000, 0)
@@ -162,9 +202,12 @@ def test_plain_c_consumer(relay, tmp_path):
 
 
 def test_stats_merge_host(relay):
-    """relay_stats_merge (host): fields 0-7 add, min slots take the minimum,
-    the mask picks tables, and merging commutes with the SUM all-reduce
-    (each rank's min slot is +inf-initialised only on that rank, 0 elsewhere)."""
+    """relay_stats_merge (host): fields 0-7 add, the rank's own min slot takes
+    the minimum (every slot with rank -1, after the all-reduce), the mask
+    picks tables, and summing the per-rank merges equals merging the summed
+    tables (each rank's min slot is +inf-initialised only on that rank, 0
+    elsewhere), also when a rank merges nothing (an empty merge
+    must leave the other ranks' slots 0, or the SUM corrupts their minima)."""
     rng = np.random.default_rng(7)
     n_cues, world, n_tab = 5, 2, 6
     nf = 8 + world
@@ -179,24 +222,28 @@ def test_stats_merge_host(relay):
         t[:, :, 8 + r] = mins
         per_rank.append(t)
     mask = np.array([1, 0, 1, 1, 0, 1], bool)
-    for t in per_rank:
-        got = relay.stats_merge(t, n_cues, world, mask).reshape(n_cues + 1, nf)
+    for r, t in enumerate(per_rank):
+        got = relay.stats_merge(t, n_cues, world, mask, rank=r).reshape(n_cues + 1, nf)
         sel = t[mask]
         np.testing.assert_array_equal(got[:, :8], sel[:, :, :8].sum(axis=0))
-        np.testing.assert_array_equal(got[:, 8:], sel[:, :, 8:].min(axis=0))
-    # merge(sum over ranks) == sum over ranks(merge)
+        np.testing.assert_array_equal(got[:, 8 + r], sel[:, :, 8 + r].min(axis=0))
+        assert not np.delete(got[:, 8:], r, axis=1).any()
+    # merge(sum over ranks) == sum over ranks(merge), for any selection
     summed = per_rank[0] + per_rank[1]
-    a = relay.stats_merge(summed, n_cues, world, mask)
-    b = relay.stats_merge(per_rank[0], n_cues, world, mask) + relay.stats_merge(per_rank[1], n_cues,
-                                                                              world, mask)
-    np.testing.assert_array_equal(a, b)
-    # empty selection: an initialised table with nothing in it
-    e = relay.stats_merge(per_rank[0], n_cues, world, np.zeros(n_tab, bool)).reshape(n_cues + 1, nf)
-    assert not e[:, :8].any() and (e[:, 8:] == 0x7F800000).all()
+    for m in (mask, np.zeros(n_tab, bool), np.ones(n_tab, bool)):
+        a = relay.stats_merge(summed, n_cues, world, m, rank=-1)
+        b = relay.stats_merge(per_rank[0], n_cues, world, m, rank=0) + \
+            relay.stats_merge(per_rank[1], n_cues, world, m, rank=1)
+        np.testing.assert_array_equal(a, b)
+    # empty selection on one rank: exactly an initialised table of that rank
+    e = relay.stats_merge(per_rank[1], n_cues, world, np.zeros(n_tab, bool), rank=1).reshape(n_cues + 1, nf)
+    assert not e[:, :9].any() and (e[:, 9] == 0x7F800000).all()
     with pytest.raises(relay.RelayError):
         relay.stats_merge(per_rank[0].reshape(-1)[:-1], n_cues, world)
+    with pytest.raises(relay.RelayError):
+        relay.stats_merge(per_rank[0], n_cues, world, rank=world)
     lib = C.CDLL(relay.LIB_PATH)
-    assert lib.relay_stats_merge(None, 1, None, 3, 1, None) == 1
+    assert lib.relay_stats_merge(None, 1, None, 3, 0, 1, None) == 1
 
 
 def test_nccl_entry_points_host(relay):

@@ -160,6 +160,29 @@ def test_16bit_decoding_matches_numpy():
                 assert st == 0 and i1 == 0 and lse == x
 
 
+def test_row_stride_skips_nan_padding():
+    """oracle_margin_rows with row_stride > vocab (VERDICT r01 nit): the
+    padding columns hold NaN, so reading one would make the row status 1; every
+    row must equal the sort + math.fsum brute force on its first `vocab`
+    entries, for f32 and for bf16 / f16 bit patterns, at several strides."""
+    rng = np.random.default_rng(17)
+    for vocab, stride in ((5, 8), (7, 7 + 1), (33, 40), (2, 9)):
+        z = rng.integers(-4, 5, (23, vocab)).astype(np.float32)
+        z[rng.random(z.shape) < 0.1] = NINF
+        z[np.all(np.isneginf(z), axis=1), 0] = 1.0
+        pad = np.full((23, stride), np.nan, np.float32)
+        pad[:, :vocab] = z
+        bits = (pad.view(np.uint32) >> 16).astype(np.uint16)       # bf16: exact for these small integers
+        h16 = pad.astype(np.float16).view(np.uint16)
+        for arr, code in ((pad, None), (bits, "bf16"), (h16, "f16")):
+            got = oracle.margin_rows(arr, dtype=code, vocab=vocab)
+            for r in range(23):
+                i1, i2, m = _brute([float(v) for v in z[r]])
+                assert got["status"][r] == 0, (vocab, stride, code, r)
+                assert (got["top1"][r], got["top2"][r]) == (i1, i2)
+                assert abs(got["margin"][r] - m) < 1e-12
+
+
 def test_threads_do_not_change_results():
     rng = np.random.default_rng(7)
     L = rng.normal(0, 2, (37, 513)).astype(np.float32)

@@ -7,11 +7,15 @@ over every logit row, K2 relay_cue_scan, K3 relay_segment_reduce, (N>1) the
 NCCL sum all-reduce of the uint64 statistics table (H6), the 4 KB table read
 back and relay_stats_finalize on the host (H7).
 
-Workload per rank (weak scaling): one Qwen3-32B-shaped reasoning trajectory of
-32,768 tokens x 151,936-vocab bf16 logits with 8 switch cues (configs[1]);
-at N = 8 the job is configs[3] (8 x 32,768 rows sharded by trajectory).
-Inputs (9.96 GB of logits per rank) are far larger than the 126 MB L2, so no
-flush is needed between steps.
+Workload per rank (weak scaling, default --config c2): one Qwen3-32B-shaped
+reasoning trajectory of 32,768 tokens x 151,936-vocab bf16 logits with 8
+switch cues (configs[1]).  --config c4 is configs[3] as stated: the FIXED
+corpus of 8 x 32,768-token trajectories sharded by trajectory over the N
+ranks (strong scaling; N = 1 holds all 79.7 GB), so T(1)/T(8) is read off
+directly.  Inputs (>= 9.96 GB of logits per rank) are far larger than the
+126 MB L2, so no flush is needed between steps.  Every line also carries a
+"sustained" sub-record: ~3 s of back-to-back steps with the clocks sampled
+(the rate once the SM clock has settled under the 1,000 W power cap).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl relay|reference]
 """
@@ -41,10 +45,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="relay", choices=["relay", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c5"],
-                    help="c2 (default, the metric's workload); c1; c5: the cue-set sweep corpus "
-                         "(8 x 16,384-token trajectories per rank, 32 patterns of length 1-6, logits "
-                         "streamed in --chunk-rows chunks from a ~10 GB buffer pool)")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"],
+                    help="c2 (default, the metric's workload): one 32,768-token trajectory per rank "
+                         "(weak scaling); c4: the FIXED corpus of 8 x 32,768-token trajectories sharded "
+                         "by trajectory over the ranks (strong scaling; N = 1 holds all 79.7 GB); c1; "
+                         "c5: the cue-set sweep corpus (8 x 16,384-token trajectories per rank, 32 patterns "
+                         "of length 1-6, logits streamed in --chunk-rows chunks from a ~10 GB buffer pool)")
+    ap.add_argument("--sustained-s", type=float, default=3.0,
+                    help="after the timed steps, back-to-back steps for this many seconds with the clocks "
+                         "sampled (the 'sustained' sub-record: the rate at the clock the box settles at "
+                         "under this kernel's own power draw); 0 = off")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk-rows", type=int, default=8192, help="c5: logit rows per streamed chunk")
     ap.add_argument("--shard", default="trajectory", choices=["trajectory", "rows"],
@@ -227,7 +237,31 @@ def main():
     cs_h = synth.make_cueset(vocab, c["n_cues"], c["n_pat"], max_len=c["max_len"])
     cs = relay.CueSet.from_synth(cs_h)
     T_job = T * world   # rows of the whole job (weak scaling: one trajectory per rank)
-    if args.shard == "rows":
+    n_my = 1            # trajectories of this rank
+    if args.config == "c4":
+        # the fixed corpus: global trajectory g (tokens seed BASE+g, logits seed BASE+17g,
+        # the same for every world size) -> rank g*world//8; T_job = 8 x 32,768 rows
+        if args.shard == "rows":
+            raise SystemExit("--config c4 shards by trajectory")
+        NT = c["n_traj"]
+        if world > NT:
+            raise SystemExit(f"--config c4 has {NT} trajectories: at most {NT} ranks")
+        mine = list(range(rank * NT // world, (rank + 1) * NT // world))
+        n_my = len(mine)
+        parts = [synth.make_tokens(1, T, cs_h, seed=synth.BASE_SEED + g) for g in mine]
+        toks = np.concatenate([p.tokens for p in parts]).astype(np.int32)
+        offs_np = np.arange(n_my + 1, dtype=np.int64) * T
+        tep_np = np.array([p.think_end_pos[0] + k * T for k, p in enumerate(parts)], np.int64)
+        ts = synth.TokenStream(toks, offs_np, tep_np)
+        T_job = NT * T
+        logits = torch.empty((n_my * T, vocab), dtype=torch.bfloat16 if dtype == "bf16" else torch.float32,
+                             device=dev)
+        for k, g in enumerate(mine):
+            logits[k * T:(k + 1) * T] = synth.make_logits(T, vocab, dtype, tokens=parts[k].tokens,
+                                                          seed=synth.BASE_SEED + 17 * g, device=dev,
+                                                          chunk_rows=2048)
+        T = n_my * T
+    elif args.shard == "rows":
         # strong scaling: one trajectory (the same on every rank), split at safe cuts
         from paper_2602_06454_b200.dist import range_view, safe_cuts
         full = synth.make_tokens(1, T, cs_h, seed=synth.BASE_SEED)
@@ -238,8 +272,9 @@ def main():
         T, T_job = hi - lo, T
     else:
         ts = synth.make_tokens(1, T, cs_h, seed=synth.BASE_SEED + rank)
-    logits = synth.make_logits(max(T, 1), vocab, dtype, tokens=ts.tokens, seed=synth.BASE_SEED + 17 * rank,
-                               device=dev, chunk_rows=2048)[:T]
+    if args.config != "c4":
+        logits = synth.make_logits(max(T, 1), vocab, dtype, tokens=ts.tokens, seed=synth.BASE_SEED + 17 * rank,
+                                   device=dev, chunk_rows=2048)[:T]
     tok = torch.as_tensor(ts.tokens, device=dev)
     offs = torch.as_tensor(ts.traj_offsets, device=dev)
     tep = torch.as_tensor(ts.think_end_pos, device=dev)
@@ -307,6 +342,10 @@ def main():
         t = torch.tensor([ms, k1_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, k1_ms = float(t[0]), float(t[1])
+    sustained = None
+    if args.sustained_s > 0 and not args.profile:
+        sustained = measure_sustained(args, ms / args.steps, run_steps, k1_ev, local, world, dev, T, T_job,
+                                      vocab, {"bf16": 2, "f16": 2, "f32": 4}[dtype])
     rows_total = T_job * args.steps
     value = rows_total / (ms / 1e3)
     esz = {"bf16": 2, "f16": 2, "f32": 4}[dtype]
@@ -314,11 +353,18 @@ def main():
     achieved = k1_bytes / (k1_ms / 1e3) / 1e9
     pk = peaks()
     peak = pk.get("hbm_gbs") or 6650.0
-    traffic = None
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.config, {}).get("dram_bytes_per_launch")
+            tj = json.load(open(tf))
+            rec = tj.get(args.config, {})
+            traffic = rec.get("dram_bytes_per_launch")
+            if traffic is not None and args.config == "c4":
+                traffic = None   # profiled at configs[1]; per-launch bytes scale with the rows
+            traffic_src = (f"profiled offline, not this run: {rec.get('profile', tj.get('_source'))} "
+                           f"(kernel {rec.get('kernel')}, source commit {rec.get('commit', 'n/a')})"
+                           if traffic is not None else None)
         except Exception:
             traffic = None
 
@@ -343,7 +389,8 @@ def main():
 
     e2e = None
     if not args.no_e2e and not args.profile:
-        e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6, T_job)
+        e2e = measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6, T_job,
+                          traj_rows=(T // n_my) if args.config == "c4" else None)
     cpu = None
     if rank == 0 and not args.no_baseline and not args.profile:
         cpu = cpu_baseline(logits, ts, cs_h, dtype, vocab)
@@ -354,14 +401,19 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.shard == "rows" else "weak", "vs_baseline": None, "dtype": dtype,
+            "scaling": "strong" if (args.shard == "rows" or args.config == "c4") else "weak",
+            "vs_baseline": None, "dtype": dtype,
             "data": "synthetic",
             "config": {"workload": (f"{args.config}: one {T_job}-token trajectory split at safe cuts over {world} "
                                     f"ranks x {vocab}-vocab " if args.shard == "rows" else
+                                    f"c4: the fixed corpus of {T_job // (T // n_my)} trajectories x {T // n_my} "
+                                    f"tokens ({T_job} rows) sharded by trajectory over {world} ranks x {vocab}-vocab "
+                                    if args.config == "c4" else
                                     f"{args.config}: {world} x one {T}-token trajectory x {vocab}-vocab ") +
                        f"{dtype} logits (Qwen3-32B shape), {c['n_cues']} cues / {c['n_pat']} patterns, "
                        "margin+cue-scan+segment-reduce+stats (H1-H7)" +
-                       (", row ranges at sentence starts" if args.shard == "rows" else ", one trajectory per rank"),
+                       (", row ranges at sentence starts" if args.shard == "rows" else
+                        f", {n_my} trajectories on rank 0" if args.config == "c4" else ", one trajectory per rank"),
                        "rows_per_rank": T, "vocab": vocab,
                        "l2": f"inputs {T * (vocab * esz) / 1e9:.2f} GB/rank >> 126 MB L2, no flush",
                        "parallelism": f"dp{world} " + ("(one trajectory, row-range-sharded at safe cuts)"
@@ -370,6 +422,7 @@ def main():
             "hbm_gbs_step": (T_job * (vocab * esz + 17)) / (ms / 1e3 / args.steps) / 1e9 / world,
             "roofline": {"kernel": "relay_margin_rows (K1)", "bound": "hbm", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if pk.get("hbm_gbs") else "fallback",
                          "frac_of_8TBs": achieved / 8000.0, "k1_ms": k1_ms,
                          "k1_share_of_step": k1_ms / (ms / args.steps),
@@ -380,6 +433,7 @@ def main():
                                              "2 CTAs per SM, no compute) over this run's logits buffer, 5 passes"},
             "gpu_launches": an.n_launches() * args.steps,
             "clocks": ck,
+            "sustained": sustained,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "decode_step": decode,
@@ -581,15 +635,20 @@ def measure_decode(relay, synth, dev, peak, B=256, V=152064, reps=30):
     return res
 
 
-def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6, rows_job):
+def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6, rows_job, traj_rows=None):
     """Same metric through the public API with HOST inputs: every step copies the
     step's logits + tokens from pinned host memory, runs the pass, and reads the
-    statistics table back."""
+    statistics table back.  With more than one trajectory per rank (c4) the
+    logits are streamed from the host one trajectory at a time (a one-
+    trajectory pinned buffer sent for each of the rank's trajectories, K1 per
+    trajectory through Analyzer.run_streamed): host memory holds 10 GB, not
+    the rank's whole shard."""
     import torch
     import torch.distributed as dist
 
-    from paper_2602_06454_b200.dist import allreduce_stats
     T, V = logits.shape
+    if traj_rows and T > traj_rows:
+        return measure_e2e_streamed(args, relay, an, cs, logits, ts, dev, world, h6, rows_job, traj_rows)
     pinned = True
     try:
         h_logits = torch.empty((T, V), dtype=logits.dtype, pin_memory=True)
@@ -640,6 +699,109 @@ def measure_e2e(args, relay, an, cs, logits, ts, dev, world, rank, h6, rows_job)
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": args.e2e_steps,
             "pinned": pinned,
             "path": "host logits+tokens -> H2D -> Analyzer.run (C ABI) -> D2H stats -> finalize"}
+
+
+def measure_e2e_streamed(args, relay, an, cs, logits, ts, dev, world, h6, rows_job, R):
+    import torch
+    import torch.distributed as dist
+    T, V = logits.shape
+    pinned = True
+    try:
+        h_chunk = torch.empty((R, V), dtype=logits.dtype, pin_memory=True)
+    except RuntimeError:
+        pinned = False
+        h_chunk = torch.empty((R, V), dtype=logits.dtype)
+    h_chunk.copy_(logits[:R])
+    h_tok = torch.from_numpy(ts.tokens.copy()).pin_memory()
+    h_offs = torch.from_numpy(ts.traj_offsets.copy()).pin_memory()
+    h_tep = torch.from_numpy(ts.think_end_pos.copy()).pin_memory()
+    d_buf = [torch.empty((R, V), dtype=logits.dtype, device=dev) for _ in range(2)]
+    d_tok = torch.empty(T, dtype=torch.int32, device=dev)
+    d_offs = torch.empty(h_offs.shape, dtype=torch.int64, device=dev)
+    d_tep = torch.empty(h_tep.shape, dtype=torch.int64, device=dev)
+    host_stats = torch.empty(an.stats.shape, dtype=torch.int64, pin_memory=True)
+    stream = torch.cuda.current_stream()
+
+    def chunks():
+        for k in range(T // R):
+            d_buf[k % 2].copy_(h_chunk, non_blocking=True)
+            yield k * R, d_buf[k % 2]
+
+    def step():
+        d_tok.copy_(h_tok, non_blocking=True)
+        d_offs.copy_(h_offs, non_blocking=True)
+        d_tep.copy_(h_tep, non_blocking=True)
+        an.run_streamed(chunks(), d_tok, d_offs, d_tep)
+        if world > 1:
+            h6(an.stats)
+        host_stats.copy_(an.stats, non_blocking=True)
+        stream.synchronize()
+        relay.stats_finalize(host_stats.numpy(), cs.n_cues, world)
+
+    step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    bi = (T // R) * h_chunk.numel() * h_chunk.element_size() + h_tok.numel() * 4 + h_offs.numel() * 8 + \
+        h_tep.numel() * 8
+    bo = host_stats.numel() * 8
+    del h_chunk, d_buf
+    torch.cuda.empty_cache()
+    return {"value": rows_job * args.e2e_steps / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": args.e2e_steps, "pinned": pinned,
+            "path": "host logits (one pinned trajectory buffer, sent once per trajectory of the shard) + "
+                    "tokens -> H2D -> Analyzer.run_streamed (C ABI, K1 per trajectory) -> D2H stats -> finalize"}
+
+
+def measure_sustained(args, step_ms, run_steps, k1_ev, local, world, dev, T, T_job, vocab, esz):
+    """Back-to-back steps for ~args.sustained_s seconds after the timed region,
+    clocks sampled throughout: the rate once the SM clock has settled under
+    the kernel's own power draw (the driver's burst line is ~30 ms)."""
+    import torch
+    import torch.distributed as dist
+    n = max(3, int(args.sustained_s * 1e3 / max(step_ms, 1e-3)))
+    if world > 1:
+        t = torch.tensor([n], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n = int(t[0])
+    k1_ev.clear()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.2)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    run_steps(n, timed=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    # the settled part: the last half of the launches
+    k1 = [a.elapsed_time(b) for a, b in k1_ev]
+    k1_ms = statistics.mean(k1[len(k1) // 2:])
+    if world > 1:
+        t = torch.tensor([ms, k1_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, k1_ms = float(t[0]), float(t[1])
+    gbs = T * (vocab * esz + 17) / (k1_ms / 1e3) / 1e9
+    return {"seconds": ms / 1e3, "steps": n, "value": T_job * n / (ms / 1e3), "unit": UNIT,
+            "k1_ms_settled": k1_ms, "k1_gbs_settled": gbs, "k1_frac_of_8TBs": gbs / 8000.0,
+            "clocks": ck,
+            "note": "K1 mean over the second half of the launches; clocks sampled over the whole run"}
 
 
 def cpu_baseline(logits, ts, cs_h, dtype, vocab):

@@ -71,7 +71,7 @@ ScanWs scan_ws_layout(void* base, long long n_tok, long long cap) {
     off += align256(bytes);
     return q;
   };
-  const long long nt2 = (n_tok + 511) / 512 + 1;  // K2 tiles of 512 positions
+  const long long nt2 = (n_tok + kK2Tile - 1) / kK2Tile + 1;  // K2 tiles
   w.k2_flag = reinterpret_cast<int*>(take(sizeof(int) * nt2));
   w.k2_val = reinterpret_cast<long long*>(take(2 * sizeof(long long) * nt2));
   w.k2_done = reinterpret_cast<int*>(take(sizeof(int)));
@@ -306,6 +306,17 @@ relay_status_t relay_cueset_create_ex(const int32_t* pat_tokens, const int32_t* 
     for (int k = 0; k < len[p]; k++) h_tok[static_cast<size_t>(i) * kMaxLen + k] = pat_tokens[pat_offsets[p] + k];
   }
   for (int p = 0; p < n_patterns; p++) h_cue_orig[p] = pat_cue[p];
+  // distinct pattern elements (K2 computes one ballot word per element per
+  // 32-start group and evaluates every pattern from them)
+  std::vector<int> h_dist, h_eidx(static_cast<size_t>(n_patterns) * kMaxLen, -1);
+  for (int i = 0; i < n_patterns; i++)
+    for (int k = 0; k < h_len[i]; k++) {
+      const int e = h_tok[static_cast<size_t>(i) * kMaxLen + k];
+      int d = 0;
+      while (d < static_cast<int>(h_dist.size()) && h_dist[d] != e) d++;
+      if (d == static_cast<int>(h_dist.size())) h_dist.push_back(e);
+      h_eidx[static_cast<size_t>(i) * kMaxLen + k] = d;
+    }
   const size_t words = static_cast<size_t>((vocab + 31) / 32);
   std::vector<uint32_t> h_term(words, 0u);
   for (int64_t v = 0; v < vocab; v++)
@@ -317,7 +328,8 @@ relay_status_t relay_cueset_create_ex(const int32_t* pat_tokens, const int32_t* 
   size_t off_tok = 0, off_len = align256(h_tok.size() * 4), off_cue = off_len + align256(n_patterns * 4),
          off_orig = off_cue + align256(n_patterns * 4), off_co = off_orig + align256(n_patterns * 4),
          off_lo = off_co + align256(n_patterns * 4), off_term = off_lo + align256(n_patterns * 4),
-         off_cls = off_term + align256(words * 4), total = off_cls + align256(h_cls.size() * 4 + 4);
+         off_cls = off_term + align256(words * 4), off_dist = off_cls + align256(h_cls.size() * 4 + 4),
+         off_eidx = off_dist + align256(h_dist.size() * 4), total = off_eidx + align256(h_eidx.size() * 4);
   std::vector<char> host(total, 0);
   std::memcpy(host.data() + off_tok, h_tok.data(), h_tok.size() * 4);
   std::memcpy(host.data() + off_len, h_len.data(), n_patterns * 4);
@@ -327,6 +339,8 @@ relay_status_t relay_cueset_create_ex(const int32_t* pat_tokens, const int32_t* 
   std::memcpy(host.data() + off_lo, len.data(), n_patterns * 4);
   std::memcpy(host.data() + off_term, h_term.data(), words * 4);
   if (!h_cls.empty()) std::memcpy(host.data() + off_cls, h_cls.data(), h_cls.size() * 4);
+  std::memcpy(host.data() + off_dist, h_dist.data(), h_dist.size() * 4);
+  std::memcpy(host.data() + off_eidx, h_eidx.data(), h_eidx.size() * 4);
   void* d = nullptr;
   cudaError_t e = cudaMalloc(&d, total);
   if (e != cudaSuccess) return fail(RELAY_ERR_ALLOC, "cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
@@ -356,6 +370,9 @@ relay_status_t relay_cueset_create_ex(const int32_t* pat_tokens, const int32_t* 
   cs->dev.term_tab = reinterpret_cast<const uint32_t*>(b + off_term);
   cs->dev.n_classes = n_classes;
   cs->dev.class_tab = reinterpret_cast<const uint32_t*>(b + off_cls);
+  cs->dev.n_dist = static_cast<int>(h_dist.size());
+  cs->dev.dist_tok = reinterpret_cast<const int*>(b + off_dist);
+  cs->dev.pat_eidx = reinterpret_cast<const int*>(b + off_eidx);
   cs->dev.dec_period = decimal_rule ? decimal_rule[0] : -1;
   cs->dev.dec_dend = decimal_rule ? decimal_rule[1] : -1;
   cs->dev.dec_dstart = decimal_rule ? decimal_rule[2] : -1;

@@ -14,7 +14,11 @@ constexpr int kMaxCues = 64;      // RELAY_MAX_CUES
 constexpr int kMaxClasses = 8;    // RELAY_MAX_CLASSES
 constexpr int kMaxTopK = 64;      // RELAY_MAX_TOP_K
 constexpr int kStatFields = 8;    // RELAY_STAT_FIELDS
-constexpr int kTile = 2048;       // positions per CTA in the scan kernels
+constexpr int kTile = 2048;       // positions per CTA in K3
+#ifndef RELAY_K2_TILE
+#define RELAY_K2_TILE 256
+#endif
+constexpr int kK2Tile = RELAY_K2_TILE;  // positions per CTA in K2 (kScanThreads / 32 groups of 32 starts)
 constexpr int kScanThreads = 256; // kTile / 8 consecutive positions per thread
 constexpr int kHist = kMaxLen - 1;
 
@@ -35,6 +39,11 @@ struct CueDev {
   int n_classes;
   const uint32_t* class_tab;  // [n_classes][ceil(vocab/32)]
   int dec_period, dec_dend, dec_dstart;  // decimal-number rule class ids (-1: off)
+  // distinct pattern elements (K2's per-group ballot words) and, per sorted
+  // pattern element, its index among them (-1 past the pattern's length)
+  int n_dist;
+  const int* dist_tok;   // [n_dist]
+  const int* pat_eidx;   // [n_pat][kMaxLen]
 };
 
 // Token `tok` in class c (bit test; false outside [0, vocab)).

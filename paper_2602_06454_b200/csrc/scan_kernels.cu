@@ -67,165 +67,278 @@ __device__ __forceinline__ bool match_at(const CueDev& cs, const SmemPat& sp, in
   return true;
 }
 
-// Occurrences starting at this position.  LONGEST: 0/1 and the sorted index
-// of the longest matching pattern.  ALL: a cue bitmask (one occurrence per
-// matching cue).
-__device__ __forceinline__ int count_at(const CueDev& cs, const SmemPat& sp, const int* tk,
-                                        long long room, unsigned long long* mask, int* best) {
-  if (cs.mode == 0) {
-    for (int p = 0; p < cs.n_pat; p++)
-      if (match_at(cs, sp, p, tk, room)) { *best = p; return 1; }
-    return 0;
-  }
-  unsigned long long m = 0;
-  for (int p = 0; p < cs.n_pat; p++)
-    if (match_at(cs, sp, p, tk, room)) m |= 1ull << sp.cue[p];
-  *mask = m;
-  return __popcll(m);
-}
-
-// Room (tokens available inside the trajectory) at position t; 0 outside.
-__device__ __forceinline__ long long room_at(const long long* offs, int n_traj, long long n_tok,
-                                             long long t) {
-  int k = find_traj(offs, n_traj, n_tok, t);
-  return k < 0 ? 0 : traj_end(offs, n_tok, k) - t;
-}
-
 // ------------------------------------------------------------------- K2
-// One pass: tiles of kScanTile2 = 512 positions (2 consecutive per thread),
-// tokens staged in shared memory with an 8-token halo.  Each tile publishes its
-// occurrence count, then a forward decoupled look-back over the tiles to its
-// left gives its output offset, so occurrences come out sorted by position
-// with no second pass.  The last tile to finish resets the look-back flags.
-constexpr int kItems2 = 2;
-constexpr int kTile2 = kScanThreads * kItems2;  // 512
+// Warp-ballot matching (north_star: "matches multi-token cue patterns over the
+// generated token stream using warp ballots").  A CTA owns a tile of kTileB =
+// 256 positions; warp w takes its group of 32 start positions.
+// For a group at base b every lane holds tok[b + lane] and tok[b + 32 + lane]
+// (the window the longest pattern can reach), and a pattern element e gives a
+// 64-bit word  M_e = ballot(lo == e) | ballot(hi == e) << 32  (class elements
+// (N4): ballot of a class-bitmap test).  Pattern p = (e_0 .. e_{L-1}) matches
+// at start b + s iff bit s of  AND_k (M_{e_k} >> k)  and the trajectory has
+// room (bit s of ballot(room >= L)).  LONGEST: patterns are visited longest
+// first (lower caller index first among equal lengths) with a `claimed` mask,
+// so each start keeps its longest match; ALL: one claim mask per cue.  The
+// terminator word of the group is one ballot.  Compaction: per-warp counts,
+// a block scan over the 8 warps, and a WARP-PARALLEL decoupled look-back over
+// the tiles to the left (32 predecessors per step), so occurrences come out
+// sorted by position in one pass; the last tile resets the flags.
+constexpr int kTileB = kK2Tile;                 // positions per CTA (one 32-start group per warp)
+constexpr int kGroupsB = kTileB / 32 / (kScanThreads / 32);  // groups per warp
 constexpr int kTileAgg = 1;    // value = this tile's count
 constexpr int kTileSum = 2;    // value = count of this tile and every tile before it
 
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_i32(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Per group of 32 starts, one 64-bit ballot word per DISTINCT pattern element
+// (W_d = ballot(lo == e_d) | ballot(hi == e_d) << 32; class elements (CLS, N4):
+// ballots of a class-bitmap test), kept in the warp's shared-memory slot; a
+// pattern is then AND_k funnelshift(W_{d_k}, k) — bit s set iff it matches
+// at start b + s.  Per-length room masks likewise (bit s: >= L tokens left in
+// the start's trajectory).
+template <bool CLS>
+__device__ __forceinline__ void group_words(const CueDev& cs, const int* dist, int nd, int lo, int hi, int room8,
+                                            uint2* w, unsigned* rm) {
+  const int lane = threadIdx.x & 31;
+  for (int d = 0; d < nd; d++) {
+    const int e = dist[d];
+    bool x, y;
+    if constexpr (CLS) {
+      x = elem_ok(cs, lo, e);
+      y = elem_ok(cs, hi, e);
+    } else {
+      x = lo == e;
+      y = hi == e;
+    }
+    const unsigned a = __ballot_sync(kFull, x);
+    const unsigned b = __ballot_sync(kFull, y);
+    if (lane == 0) w[d] = make_uint2(a, b);
+  }
+#pragma unroll
+  for (int L = 1; L <= kMaxLen; L++) {
+    const unsigned r = __ballot_sync(kFull, room8 >= L);
+    if (lane == 0) rm[L] = r;
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ unsigned pattern_starts(const int* eidx, int L, const uint2* w, const unsigned* rm) {
+  unsigned m = rm[L];
+#pragma unroll
+  for (int k = 0; k < kMaxLen; k++) {
+    if (k < L) {
+      const uint2 v = w[eidx[k]];
+      m &= __funnelshift_r(v.x, v.y, k);
+    }
+  }
+  return m;
+}
+
+template <bool CLS>
 __global__ void __launch_bounds__(kScanThreads)
     cue_scan_kernel(CueDev cs, const int* __restrict__ tokens, long long n_tok,
                     const long long* __restrict__ offs, int n_traj, uint32_t* __restrict__ term_bits,
                     int* __restrict__ occ_pos, int* __restrict__ occ_pat, long long cap,
                     long long* __restrict__ n_occ, int* tile_flag, long long* tile_val, int* done) {
-  // s_tok[1 + i] = token base + i; one token of halo on the left (decimal
-  // rule) and kMaxLen on the right (patterns)
-  __shared__ int s_tok[1 + kTile2 + kMaxLen];
   __shared__ SmemPat sp;
-  __shared__ int s_scan[kScanThreads];
+  __shared__ int s_dist[kMaxPat * kMaxLen];
+  __shared__ int s_eidx[kMaxPat * kMaxLen];
+  extern __shared__ uint2 s_w_dyn[];   // per warp: the n_dist element words of its group
+  __shared__ unsigned s_rm[kScanThreads / 32][kMaxLen + 1];     // per warp: room masks by length
+  __shared__ int8_t s_best[kTileB];                 // LONGEST: sorted pattern index per start, -1 none
+  __shared__ unsigned long long s_cues[kTileB];     // ALL: cue mask per start
+  __shared__ int s_wcount[kScanThreads / 32];
   __shared__ long long s_prefix;
   const int tile = blockIdx.x;
-  const long long base = static_cast<long long>(tile) * kTile2;
-  for (int i = threadIdx.x; i < 1 + kTile2 + kMaxLen; i += blockDim.x) {
-    const long long t = base + i - 1;
-    s_tok[i] = (t >= 0 && t < n_tok) ? __ldg(tokens + t) : -1;
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long tile0 = static_cast<long long>(tile) * kTileB;
   load_patterns(cs, sp);
+  const int nd = cs.n_dist;
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) s_dist[i] = cs.dist_tok[i];
+  for (int i = threadIdx.x; i < cs.n_pat * kMaxLen; i += blockDim.x) s_eidx[i] = cs.pat_eidx[i];
   __syncthreads();
-  const int li = threadIdx.x * kItems2;
-  int cnt = 0;
-  uint32_t tb = 0;
-  unsigned long long masks[kItems2];
-  int bests[kItems2];
-  long long rooms[kItems2];
-#pragma unroll
-  for (int k = 0; k < kItems2; k++) {
-    masks[k] = 0; bests[k] = -1; rooms[k] = 0;
-    const long long t = base + li + k;
-    if (t < n_tok) {
-      const int tok = s_tok[1 + li + k];
-      rooms[k] = room_at(offs, n_traj, n_tok, t);
-      if (tok >= 0 && tok < cs.vocab && ((cs.term_tab[tok >> 5] >> (tok & 31)) & 1u)) {
-        // decimal rule (R19): a period between a digit-ending and a
-        // digit-starting token of the same trajectory is not a sentence end
-        const bool dec = cs.dec_period >= 0 && rooms[k] > 1 && in_class(cs, cs.dec_period, tok) &&
-                         room_at(offs, n_traj, n_tok, t - 1) == rooms[k] + 1 &&
-                         in_class(cs, cs.dec_dend, s_tok[li + k]) &&
-                         in_class(cs, cs.dec_dstart, s_tok[2 + li + k]);
-        if (!dec) tb |= 1u << k;
-      }
-      if (rooms[k] > 0) {
-        const int c = count_at(cs, sp, s_tok + 1 + li + k, rooms[k], &masks[k], &bests[k]);
-        if (c == 0) bests[k] = -1;
-        cnt += c;
-      }
+  uint2* const ww = s_w_dyn + warp * nd;
+  unsigned* const wrm = s_rm[warp];
+  // ---- phase 1: match, terminator words, per-warp counts
+  int wcount = 0;
+  long long cur_end = -1;   // end of the trajectory holding this lane's current position
+  long long cur_beg = 0;
+  for (int gi = 0; gi < kGroupsB; gi++) {
+    const long long b = tile0 + (static_cast<long long>(warp) * kGroupsB + gi) * 32;
+    if (b >= n_tok) break;
+    const long long t = b + lane;
+    const int lo = t < n_tok ? __ldg(tokens + t) : -1;
+    const int hi = t + 32 < n_tok ? __ldg(tokens + t + 32) : -1;
+    // this lane's trajectory [cur_beg, cur_end) (positions only grow along a lane)
+    if (t < n_tok && t >= cur_end) {
+      const int k = find_traj(offs, n_traj, n_tok, t);
+      cur_beg = (k < 0) ? t + 1 : (offs ? offs[k] : 0);
+      cur_end = (k < 0) ? t + 1 : traj_end(offs, n_tok, k);
+      if (k < 0) cur_beg = cur_end;  // outside every trajectory: no room
     }
-  }
-  // terminator bits: 16 lanes x 2 bits -> one 32-bit word
-  const int lane = threadIdx.x & 31;
-  uint32_t w = tb << (2 * (lane & 15));
-#pragma unroll
-  for (int off = 1; off < 16; off <<= 1) w |= __shfl_xor_sync(kFull, w, off);
-  if ((lane & 15) == 0 && base + li < n_tok) term_bits[(base + li) >> 5] = w;
-  // block inclusive scan of the per-thread counts (thread order == position order)
-  s_scan[threadIdx.x] = cnt;
-  __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {
-    const int v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0;
-    __syncthreads();
-    s_scan[threadIdx.x] += v;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const long long total = s_scan[kScanThreads - 1];
-    long long prefix = 0;
-    // tile_val[2t] = this tile's count, tile_val[2t+1] = inclusive running sum;
-    // each is written once, before the flag that announces it
-    if (tile == 0) {
-      tile_val[1] = total;
-      __threadfence();
-      atomicExch(tile_flag, kTileSum);
-    } else {
-      tile_val[2 * tile] = total;
-      __threadfence();
-      atomicExch(tile_flag + tile, kTileAgg);
-      for (int j = tile - 1; j >= 0; j--) {
-        int f;
-        while ((f = *reinterpret_cast<volatile int*>(tile_flag + j)) == 0) {
-        }
-        __threadfence();
-        if (f == kTileSum) {
-          prefix += __ldcg(tile_val + 2 * j + 1);
-          break;
-        }
-        prefix += __ldcg(tile_val + 2 * j);
-      }
-      tile_val[2 * tile + 1] = prefix + total;
-      __threadfence();
-      atomicExch(tile_flag + tile, kTileSum);
+    const long long room = (t < n_tok && t >= cur_beg) ? cur_end - t : 0;
+    // terminator bits (R19: a period between digit tokens of one trajectory is not an end)
+    bool term = lo >= 0 && lo < cs.vocab && ((cs.term_tab[lo >> 5] >> (lo & 31)) & 1u);
+    if (cs.dec_period >= 0) {
+      int prev = __shfl_up_sync(kFull, lo, 1);
+      if (lane == 0) prev = (t >= 1 && t - 1 < n_tok) ? __ldg(tokens + t - 1) : -1;
+      const int nx = __shfl_down_sync(kFull, lo, 1);
+      const int h0 = __shfl_sync(kFull, hi, 0);
+      const int next = lane == 31 ? h0 : nx;
+      if (term && room > 1 && t - 1 >= cur_beg && in_class(cs, cs.dec_period, lo) &&
+          in_class(cs, cs.dec_dend, prev) && in_class(cs, cs.dec_dstart, next))
+        term = false;
     }
-    s_prefix = prefix;
-    if (tile == gridDim.x - 1) *n_occ = prefix + total;
-  }
-  __syncthreads();
-  long long o = s_prefix + s_scan[threadIdx.x] - cnt;
-#pragma unroll
-  for (int k = 0; k < kItems2; k++) {
-    const long long t = base + li + k;
-    if (t >= n_tok) break;
+    const unsigned tw = __ballot_sync(kFull, term);
+    if (lane == 0) term_bits[b >> 5] = tw;
+    __syncwarp();   // the previous group's words are read by every lane before they are overwritten
+    group_words<CLS>(cs, s_dist, nd, lo, hi, static_cast<int>(room < kMaxLen ? room : kMaxLen), ww, wrm);
     if (cs.mode == 0) {
-      if (bests[k] >= 0) {
-        if (o < cap) { occ_pos[o] = static_cast<int>(t); occ_pat[o] = sp.orig[bests[k]]; }
-        o++;
+      unsigned claimed = 0;
+      int best = -1;
+      for (int p = 0; p < cs.n_pat; p++) {
+        const int L = sp.len[p];
+        // bit s: start b + s matches and has >= L tokens left in its trajectory
+        const unsigned w = pattern_starts(s_eidx + p * kMaxLen, L, ww, wrm) & ~claimed;
+        claimed |= w;
+        if ((w >> lane) & 1u) best = p;
+      }
+      s_best[(b - tile0) + lane] = static_cast<int8_t>(best);
+      wcount += __popc(claimed);
+    } else {
+      unsigned long long cm = 0;   // this lane's cues
+      for (int p = 0; p < cs.n_pat; p++) {
+        const int L = sp.len[p];
+        const unsigned w = pattern_starts(s_eidx + p * kMaxLen, L, ww, wrm);
+        if ((w >> lane) & 1u) cm |= 1ull << sp.cue[p];
+      }
+      s_cues[(b - tile0) + lane] = cm;
+      int c = __popcll(cm);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(kFull, c, off);
+      wcount += c;
+    }
+  }
+  if (lane == 0) s_wcount[warp] = wcount;
+  __syncthreads();
+  // ---- tile total, per-warp offsets, warp-parallel decoupled look-back (warp 0)
+  if (warp == 0) {
+    int wv = lane < kScanThreads / 32 ? s_wcount[lane] : 0;
+    int incl = wv;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += o;
+    }
+    if (lane < kScanThreads / 32) s_wcount[lane] = incl - wv;   // exclusive warp offsets
+    const long long total = __shfl_sync(kFull, incl, 31);
+    long long prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) {
+        tile_val[1] = total;
+        __threadfence();
+        st_release_i32(tile_flag, kTileSum);
       }
     } else {
-      unsigned long long m = masks[k];
-      while (m) {
-        const int c = __ffsll(m) - 1;
-        m &= m - 1;
-        int best = -1;
-        for (int p = 0; p < cs.n_pat && best < 0; p++)
-          if (sp.cue[p] == c && match_at(cs, sp, p, s_tok + 1 + li + k, rooms[k])) best = p;
-        if (o < cap) { occ_pos[o] = static_cast<int>(t); occ_pat[o] = sp.orig[best]; }
-        o++;
+      if (lane == 0) {
+        tile_val[2 * tile] = total;
+        __threadfence();
+        st_release_i32(tile_flag + tile, kTileAgg);
       }
+      for (long long j = tile - 1;; j -= 32) {
+        const long long idx = j - lane;
+        int f = idx >= 0 ? ld_acquire_i32(tile_flag + idx) : kTileSum;
+        while (__any_sync(kFull, f == 0))
+          if (f == 0) f = ld_acquire_i32(tile_flag + idx);
+        long long v = 0;
+        if (idx >= 0) v = __ldcg(tile_val + 2 * idx + (f == kTileSum ? 1 : 0));
+        const unsigned sums = __ballot_sync(kFull, f == kTileSum);
+        const int stop = sums ? __ffs(sums) - 1 : 32;   // nearest tile with an inclusive sum
+        if (lane > stop) v = 0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+        prefix += v;
+        if (sums) break;
+      }
+      if (lane == 0) {
+        tile_val[2 * tile + 1] = prefix + total;
+        __threadfence();
+        st_release_i32(tile_flag + tile, kTileSum);
+      }
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if (tile == gridDim.x - 1) *n_occ = prefix + total;
+    }
+  }
+  __syncthreads();
+  // ---- phase 2: ordered writes
+  long long o = s_prefix + s_wcount[warp];
+  for (int gi = 0; gi < kGroupsB; gi++) {
+    const long long b = tile0 + (static_cast<long long>(warp) * kGroupsB + gi) * 32;
+    if (b >= n_tok) break;
+    const long long t = b + lane;
+    if (cs.mode == 0) {
+      const int best = s_best[(b - tile0) + lane];
+      const unsigned has = __ballot_sync(kFull, best >= 0);
+      if (best >= 0) {
+        const long long q = o + __popc(has & ((1u << lane) - 1u));
+        if (q < cap) { occ_pos[q] = static_cast<int>(t); occ_pat[q] = sp.orig[best]; }
+      }
+      o += __popc(has);
+    } else {
+      unsigned long long cm = s_cues[(b - tile0) + lane];
+      const int c = __popcll(cm);
+      int excl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int v = __shfl_up_sync(kFull, excl, off);
+        if (lane >= off) excl += v;
+      }
+      const int tot = __shfl_sync(kFull, excl, 31);
+      long long q = o + excl - c;
+      if (cm) {
+        // the tokens of the window again, for each cue's longest pattern
+        int tk[kMaxLen];
+        long long room = 0;
+        {
+          const int k = find_traj(offs, n_traj, n_tok, t);
+          room = k < 0 ? 0 : traj_end(offs, n_tok, k) - t;
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxLen; i++) tk[i] = (t + i < n_tok) ? __ldg(tokens + t + i) : -1;
+        while (cm) {
+          const int cue = __ffsll(cm) - 1;
+          cm &= cm - 1;
+          int best = -1;
+          for (int p = 0; p < cs.n_pat && best < 0; p++)
+            if (sp.cue[p] == cue && match_at(cs, sp, p, tk, room)) best = p;
+          if (q < cap) { occ_pos[q] = static_cast<int>(t); occ_pat[q] = sp.orig[best]; }
+          q++;
+        }
+      }
+      o += tot;
     }
   }
   // the last tile to finish resets the look-back flags for the next launch
   __syncthreads();
+  __shared__ int s_last;
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(done, 1) == gridDim.x - 1) {
-      for (int j = 0; j < gridDim.x; j++) tile_flag[j] = 0;
+    s_last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (int j = threadIdx.x; j < static_cast<int>(gridDim.x); j += blockDim.x) tile_flag[j] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
       __threadfence();
       *done = 0;
     }
@@ -666,9 +779,11 @@ cudaError_t launch_cue_scan(const CueDev& cs, const int* tokens, long long n_tok
                             const long long* offs, int n_traj, uint32_t* term_bits, int* occ_pos,
                             int* occ_pat, long long cap, long long* n_occ, const ScanWs& ws,
                             cudaStream_t st) {
-  long long nt = (n_tok + kTile2 - 1) / kTile2;
+  long long nt = (n_tok + kTileB - 1) / kTileB;
   if (nt < 1) nt = 1;
-  cue_scan_kernel<<<static_cast<unsigned>(nt), kScanThreads, 0, st>>>(
+  auto kern = cs.n_classes > 0 ? cue_scan_kernel<true> : cue_scan_kernel<false>;
+  const size_t dyn = sizeof(uint2) * (kScanThreads / 32) * (cs.n_dist > 0 ? cs.n_dist : 1);
+  kern<<<static_cast<unsigned>(nt), kScanThreads, dyn, st>>>(
       cs, tokens, n_tok, offs, n_traj, term_bits, occ_pos, occ_pat, cap, n_occ, ws.k2_flag, ws.k2_val,
       ws.k2_done);
   return cudaGetLastError();

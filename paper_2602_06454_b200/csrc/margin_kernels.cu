@@ -206,7 +206,10 @@ __device__ __forceinline__ float theta_raise(float b, uint32_t s_theta) {
 // (max relative error 2.3e-7 in fp32 Horner, MUFU.EX2's ~2^-22 class), the
 // exponent added to the bits.
 #ifndef RELAY_K1_POLY_PAIRS
-#define RELAY_K1_POLY_PAIRS 0  // element pairs per 16 of a stage on the FMA pipe (tools/k1_sweep.py)
+#define RELAY_K1_POLY_PAIRS 0  // K1: element pairs per 16 of a stage on the FMA pipe (power-capped: 0 best)
+#endif
+#ifndef RELAY_K4_POLY_PAIRS
+#define RELAY_K4_POLY_PAIRS 0  // K4: the same for the decode step (XU-bound on the SMs with two rows)
 #endif
 __device__ __forceinline__ float2 exp2_poly2(float2 y) {
   y.x = fminf(fmaxf(y.x, -125.0f), 64.0f);
@@ -224,11 +227,11 @@ __device__ __forceinline__ float2 exp2_poly2(float2 y) {
                      __uint_as_float(__float_as_uint(h.y) + (__float_as_uint(t.y) << 23)));
 }
 
-template <class E, int UV>
+template <class E, int UV, int POLY>
 __device__ __forceinline__ float2 stage_sum(const uint4 (&raw)[UV], int nvalid, float c, float mref) {
   constexpr int VEC = 16 / E::SZ;
   constexpr int NP = VEC / 2;  // element pairs per vector
-  constexpr int kPoly = RELAY_K1_POLY_PAIRS * UV * NP / 16;  // the stage's last kPoly pairs
+  constexpr int kPoly = POLY * UV * NP / 16;  // the stage's last kPoly pairs on the FMA pipe
   const float2 cc = make_float2(c, c);
   const float2 nm = make_float2(-mref, -mref);
   // a sum tree, not accumulator chains: each vector's exps are independent of
@@ -294,11 +297,11 @@ __device__ __forceinline__ float guard_T(float theta, const ThreadState& st, flo
 // the exp work plus ~0.2 instructions per element (no per-stage max tree).
 // nvalid < UV on a row's last, partial stage: the missing vectors hold -inf
 // (no term, never pushed).
-template <class E, int UV>
+template <class E, int UV, int POLY>
 __device__ __forceinline__ void consume_fast(const uint4 (&raw)[UV], int nvalid, int j0, int jstep,
                                              ThreadState& st, float c, float& T, int& tkey, float& theta_w,
                                              int key, uint32_t theta_p) {
-  float2 s2 = stage_sum<E, UV>(raw, nvalid, c, st.mref);
+  float2 s2 = stage_sum<E, UV, POLY>(raw, nvalid, c, st.mref);
   // T follows the shared threshold (key: loaded with the stage, before the
   // ring words, so its latency hides under the sum): a stale (lower) T stays
   // correct, but every thread would trip on the elements between the old and
@@ -335,7 +338,7 @@ __device__ __forceinline__ void consume_fast(const uint4 (&raw)[UV], int nvalid,
 #pragma unroll
       for (int k = 0; k < 4; k++) st.acc[k] *= r;
       st.mref = ym;
-      s2 = stage_sum<E, UV>(rw, nvalid, c, ym);  // the old terms may have overflowed (or been clamped)
+      s2 = stage_sum<E, UV, POLY>(rw, nvalid, c, ym);  // the old terms may have overflowed (or been clamped)
     }
     if (__any_sync(kFull, pushed)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
     T = guard_T(fmaxf(theta_w, unkey(key)), st, c);  // mref, g2 or theta_w may have moved
@@ -679,7 +682,7 @@ extern "C" int relay_debug_trace_reset(const unsigned long long* zeros, int n_ct
 #define TRACE(k) ((void)0)
 #endif
 
-template <class E, int NCW, int NS, int UV, int MINB, int MODE>
+template <class E, int NCW, int NS, int UV, int MINB, int MODE, bool SPLIT>
 __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
@@ -696,7 +699,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   // epilogue warp syncs)
   constexpr int kBarRing0 = 2;
   constexpr int kBarRed0 = kBarRing0 + NS;
-  constexpr bool kFlat = MODE == kModeStep;  // only K4 splits rows across CTAs
+  // SPLIT: the work-split modes that cut rows across CTAs (K4 small batches
+  // and tuning modes); the whole-row instantiations carry none of that code
+  constexpr bool kFlat = SPLIT;
+  constexpr int kPolyPairs = MODE == kModeStep ? RELAY_K4_POLY_PAIRS : RELAY_K1_POLY_PAIRS;
   static_assert(kBarRed0 + kSlots <= 16, "named barriers");
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[NS];
@@ -1036,7 +1042,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #pragma unroll
       for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCT * 16);
       bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
-      consume_fast<E, UV>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
+      consume_fast<E, UV, kPolyPairs>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
       if constexpr (MODE == kModeStep) {
         if (a.topk > 0) {
           const float2 h = stage_max2<E, UV>(raw);
@@ -1058,7 +1064,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #pragma unroll
         for (int u = 0; u < UV; u++) raw[u] = u < nvalid ? lds128(ring_t + stage * SB + u * NCT * 16) : E::neg_inf16();
         bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
-        consume_fast<E, UV>(raw, nvalid, jb + tid * VEC, NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
+        consume_fast<E, UV, kPolyPairs>(raw, nvalid, jb + tid * VEC, NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
         if constexpr (MODE == kModeStep) {
           if (a.topk > 0) {
             const float2 h = stage_max2<E, UV>(raw);
@@ -1186,9 +1192,12 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   constexpr int MINB = (MODE == kModeStep) ? kStepMinBlocks : kMinBlocks;
   constexpr int NCW = (MODE == kModeStep) ? kStepNCW : kNCW;
   constexpr int UV = (MODE == kModeStep) ? kStepUV : kUV;
-  auto kern = rows_kernel<E, NCW, NS, UV, MINB, MODE>;
+  const bool split = MODE == kModeStep && a.flat != 0;
+  auto kern = split ? rows_kernel<E, NCW, NS, UV, MINB, MODE, MODE == kModeStep>
+                    : rows_kernel<E, NCW, NS, UV, MINB, MODE, false>;
   const int smem = NS * UV * NCW * 32 * 16;
-  static int per_sm = 0;
+  static int per_sm_of[2] = {0, 0};   // per instantiation (the attribute is per function)
+  int& per_sm = per_sm_of[split ? 1 : 0];
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

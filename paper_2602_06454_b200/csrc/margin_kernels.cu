@@ -446,8 +446,8 @@ struct RowsArgs {
   float* zmax;    // [n_rows] with thk: the row maximum (the sampler's reference)
   int topk;       // 0 = off
   int keep_l2;    // L2 evict_last: the sampling kernel reads the rows again
-  int* row_ready; // relay_step_sample: per-row completion counters (release), so
-                  // K5 starts a row as soon as its margin pass is done
+  int* ready_q;   // relay_step_sample: rows pushed in completion order (release), so
+  int* q_ctl;     // K5 samples a row as soon as its margin pass is done (q_ctl[0]: head)
 };
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
@@ -759,10 +759,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   // before touching global data it may have produced.  Outside a PDL launch
   // both instructions are no-ops.
   if constexpr (MODE == kModeStep) {
-    // with row_ready (relay_step_sample) the dependent K5 is released only
+    // with ready_q (relay_step_sample) the dependent K5 is released only
     // after every CTA passed griddepcontrol.wait (the epilogue warp below):
-    // K5 then waits per row on row_ready, and every earlier kernel is done
-    if (tid == 0 && !a.row_ready) pdl_launch_dependents();
+    // K5 then takes rows from the queue as they finish, every earlier kernel done
+    if (tid == 0 && !a.ready_q) pdl_launch_dependents();
   }
 
   if (warp == NCW) {
@@ -837,7 +837,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     if constexpr (MODE == kModeStep) {  // the switch patterns, for this warp only
       load_smem_cue(cs, sc);
       pdl_wait();
-      if (lane == 0 && a.row_ready) pdl_launch_dependents();
+      if (lane == 0 && a.ready_q) pdl_launch_dependents();
     }
     ItemIter<kFlat> iter;
     iter.init(a);
@@ -877,8 +877,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           a.zmax[r] = q.t.v1;
         }
         finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in);
-        if (a.row_ready && lane == 0)  // lane 0 wrote thk/zmax/margin/top1/top2/status: publish
-          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.row_ready + r) : "memory");
+        if (a.ready_q && lane == 0) {  // lane 0 wrote thk/zmax/margin/top1/top2/status: publish
+          const int pos = atomicAdd(a.q_ctl, 1);
+          asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.ready_q + pos), "r"(static_cast<int>(r) + 1)
+                       : "memory");
+        }
         continue;
       }
       if (kFlat && a.flat == 4) {
@@ -1353,7 +1356,7 @@ cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int b
   a.counter = ws.counter; a.part = ws.part; a.work = ws.work;
   a.flat = 0;  // whole rows: the bound needs every thread maximum of the row
   a.state = state; a.hist = hist; a.small_run = small_run; a.gate = gate; a.max_seg = max_seg;
-  a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk; a.row_ready = ws.row_ready;
+  a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk; a.ready_q = ws.ready_q; a.q_ctl = ws.q_ctl;
   {  // tuning knob (RELAY_K4_L2 = last | normal | first): the L2 policy of the margin pass
     const char* e = getenv("RELAY_K4_L2");
     a.keep_l2 = (e && !strcmp(e, "normal")) ? 2 : (e && !strcmp(e, "first")) ? 0 : 1;

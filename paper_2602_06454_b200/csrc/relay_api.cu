@@ -100,8 +100,8 @@ StepWs step_ws_layout(void* base, int batch) {
   w.status = reinterpret_cast<uint8_t*>(take(static_cast<size_t>(batch) + 1));
   w.zmax = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
   w.slow = reinterpret_cast<int*>(take(sizeof(int) * (static_cast<size_t>(batch) + 1)));
-  w.row_ready = reinterpret_cast<int*>(take(sizeof(int) * (static_cast<size_t>(batch) + 1)));
-  w.row_done = reinterpret_cast<int*>(take(sizeof(int) * (static_cast<size_t>(batch) + 1)));
+  w.ready_q = reinterpret_cast<int*>(take(sizeof(int) * (static_cast<size_t>(batch) + 1)));
+  w.q_ctl = reinterpret_cast<int*>(take(sizeof(int) * 4));
   w.zsum = reinterpret_cast<float*>(take(sizeof(float) * (static_cast<size_t>(batch) + 1)));
   w.bytes = off;
   return w;

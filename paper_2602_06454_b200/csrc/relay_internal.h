@@ -90,8 +90,9 @@ struct StepWs {
   uint8_t* status;     // [batch] relay_step_sample: K4's row status
   float* zmax;         // [batch] relay_step_sample: K4's row maximum
   int* slow;           // [batch] relay_step_sample: rows handed to the nucleus kernel
-  int* row_ready;      // [batch] relay_step_sample: margin passes completed per row (K4, release)
-  int* row_done;       // [batch] relay_step_sample: rows sampled per row (K5)
+  int* ready_q;        // [batch] relay_step_sample: rows in the order K4 finished them (row + 1,
+                       // release-stored; 0 = not yet), popped by K5 (which re-zeroes them)
+  int* q_ctl;          // [4] relay_step_sample: queue head (K4), tail (K5), K5 CTAs done
   float* zsum;         // [batch] relay_step_sample: their mass at the sampling temperature
   size_t bytes;
 };

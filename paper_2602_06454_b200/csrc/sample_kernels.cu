@@ -66,8 +66,8 @@ struct SampleArgs {
   int* slow_list;           // [n_rows] rows K5 handed to K6
   float* zsum;              // [n_rows] K5's row mass at the sampling temperature (listed rows)
   int k5_l2;                // tuning: 0 default policy, 1 evict_last, 2 evict_normal (RELAY_K5_L2)
-  const int* row_ready;     // [n_rows] K4's per-row completion counters (acquire)
-  int* row_done;            // [n_rows] rows this kernel has taken, per row
+  int* ready_q;             // [n_rows] rows in K4's completion order (row + 1; acquire; re-zeroed here)
+  int* q_ctl;               // [4] queue head (K4), tail (this kernel's tickets), CTAs done
   int* sampled;             // [n_rows] out
   uint8_t* state;
   int* hist;
@@ -977,23 +977,35 @@ __global__ void __launch_bounds__(kSampleThreads, 2) sample_switch_kernel(Sample
   __shared__ int s_cnt, s_k;
   __shared__ SmemCue sc;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TRACE5(13);
   if (warp == 0) load_smem_cue(cs, sc);  // immutable cue set: before the dependency wait
   if (threadIdx.x == 0) pdl_launch_dependents();
   // no grid-wide wait: K4 releases this kernel only after all its CTAs passed
-  // their own dependency wait, and publishes each row (thk, status, margin,
-  // top-2) with a release increment of row_ready[r]; a row starts as soon as
-  // its margin pass is done, overlapping K4's tail
-  for (long long r = blockIdx.x; r < a.n_rows; r += gridDim.x) {
+  // their own dependency wait, and pushes each finished row (thk, status,
+  // margin, top-2 written before) onto a queue with a release store; a CTA
+  // takes a ticket and samples the ticket's row, so rows are sampled in the
+  // order their margin passes finish (not in row order: K4's two-row SMs
+  // finish last), overlapping K4's tail
+  __shared__ long long s_row;
+  for (;;) {
     if (threadIdx.x == 0) {
       s_cnt = 0;
-      const int want = a.row_done[r] + 1;
-      int got;
-      do {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(got) : "l"(a.row_ready + r) : "memory");
-      } while (got < want);
-      a.row_done[r] = want;   // read again only by the next step's K5 (after this grid)
+      const int tk = atomicAdd(a.q_ctl + 1, 1);
+      long long rr = -1;
+      if (tk < a.n_rows) {
+        int v;
+        do {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.ready_q + tk) : "memory");
+        } while (v == 0);
+        a.ready_q[tk] = 0;   // read again only by the next step (after this grid)
+        rr = v - 1;
+      }
+      s_row = rr;
     }
     __syncthreads();
+    const long long r = s_row;
+    if (r < 0) break;
+    TRACE5(14);
     const T* row = static_cast<const T*>(a.logits) + r * a.stride;
     // warp 0's per-row inputs are fetched before the scan so that their
     // latency hides under it; the scan itself does not wait for the status
@@ -1045,6 +1057,12 @@ __global__ void __launch_bounds__(kSampleThreads, 2) sample_switch_kernel(Sample
     }
     __syncthreads();
     TRACE5(15);
+  }
+  // the last CTA re-arms the queue for the next step (every row was pushed and taken)
+  if (threadIdx.x == 0 && atomicAdd(a.q_ctl + 2, 1) == static_cast<int>(gridDim.x) - 1) {
+    a.q_ctl[0] = 0;
+    a.q_ctl[1] = 0;
+    a.q_ctl[2] = 0;
   }
 }
 
@@ -1161,7 +1179,7 @@ cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int
   a.sampled = sampled; a.state = state; a.hist = hist; a.small_run = small_run;
   a.gate = gate; a.max_seg = max_seg; a.flag = flag; a.cue_id = cue_id;
   a.slow_cnt = ws.work + 2; a.slow_list = ws.slow; a.zsum = ws.zsum;
-  a.row_ready = ws.row_ready; a.row_done = ws.row_done;
+  a.ready_q = ws.ready_q; a.q_ctl = ws.q_ctl;
   {
     const char* e = getenv("RELAY_K5_L2");
     a.k5_l2 = (e && !strcmp(e, "last")) ? 1 : (e && !strcmp(e, "normal")) ? 2 : 0;

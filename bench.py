@@ -278,6 +278,12 @@ def main():
     tok = torch.as_tensor(ts.tokens, device=dev)
     offs = torch.as_tensor(ts.traj_offsets, device=dev)
     tep = torch.as_tensor(ts.think_end_pos, device=dev)
+    # inputs smaller than 4 x L2 (c1: 262 MB): rotate through enough distinct
+    # copies that every step streams from HBM (the same logits, other addresses)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    in_bytes = logits.numel() * logits.element_size()
+    n_rot = max(1, -(-4 * l2_bytes // max(in_bytes, 1)))
+    rot = [logits] + [logits.clone() for _ in range(n_rot - 1)]
     # --allreduce p2p: H6 fused into K3 over peer memory (relay_segment_reduce_p2p)
     xchg = relay.StatsExchange(cs.n_cues) if (world > 1 and args.allreduce == "p2p") else None
     an = relay.Analyzer(cs, T, vocab, dev, rank=rank, world_size=world,
@@ -300,7 +306,7 @@ def main():
         if timed:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-        an.run(logits, tok, offs, tep, k1_events=(e0, e1) if timed else None)
+        an.run(rot[i % n_rot], tok, offs, tep, k1_events=(e0, e1) if timed else None)
         if timed:
             k1_ev.append((e0, e1))
         if world > 1:
@@ -415,7 +421,9 @@ def main():
                        (", row ranges at sentence starts" if args.shard == "rows" else
                         f", {n_my} trajectories on rank 0" if args.config == "c4" else ", one trajectory per rank"),
                        "rows_per_rank": T, "vocab": vocab,
-                       "l2": f"inputs {T * (vocab * esz) / 1e9:.2f} GB/rank >> 126 MB L2, no flush",
+                       "l2": (f"inputs {T * (vocab * esz) / 1e9:.2f} GB/rank >> 126 MB L2, no flush" if n_rot == 1 else
+                              f"inputs {in_bytes / 1e9:.3f} GB/rank < 4 x L2: {n_rot} rotating copies "
+                              f"({n_rot * in_bytes / 1e9:.2f} GB), a different one each step"),
                        "parallelism": f"dp{world} " + ("(one trajectory, row-range-sharded at safe cuts)"
                                                       if args.shard == "rows" else "(trajectory-sharded)"),
                        "allreduce": (args.allreduce if world > 1 else None)},

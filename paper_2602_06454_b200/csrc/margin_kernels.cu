@@ -1006,9 +1006,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     if (nst > 0) {
       // the item's first stage: the row-start probe.  The two half maxima of
       // a thread are two distinct elements, so the warp's second-best of them
-      // bounds the row's 2nd-best from below; after the consumer barrier the
-      // slot holds the best of all warps' (the 2nd-best of the stage's 2 * NCT
-      // half maxima), so the steady state starts mostly on the fast path.
+      // bounds the row's 2nd-best from below and raises the shared threshold;
+      // no barrier: each warp goes on with its own bound and whatever the
+      // others have published (any of them is a valid lower bound), so the
+      // steady state starts mostly on the fast path without a CTA-wide wait.
       mbar_wait(full_s + 8 * stage, phase);
 #ifdef RELAY_TRACE
       if (tid == 0 && n_stage < 10) TRACE(1 + n_stage);
@@ -1020,7 +1021,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);  // release: the loads precede the refill
       const float2 h = stage_max2<E, UV>(raw);
       theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
-      named_bar(1, NCT);
+#ifdef RELAY_PROBE_BAR
+      named_bar(1, NCT);  // tuning: wait for every warp's probe (r02: 1.5% slower without gain)
+#endif
       if (tid == 0 && it == 1) TRACE(13);
       tkey = theta_load(theta_p);
       const float theta = fmaxf(theta_w, unkey(tkey));

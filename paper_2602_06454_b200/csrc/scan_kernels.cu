@@ -159,6 +159,22 @@ __global__ void __launch_bounds__(kScanThreads)
   const int tile = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long tile0 = static_cast<long long>(tile) * kTileB;
+  static_assert(kGroupsB == 1, "one 32-start group per warp");
+  // this warp's group: the token loads, the trajectory lookup and the
+  // terminator test go first, so their latency overlaps the pattern staging
+  const long long b = tile0 + static_cast<long long>(warp) * 32;
+  const long long t = b + lane;
+  const int lo = t < n_tok ? __ldg(tokens + t) : -1;
+  const int hi = t + 32 < n_tok ? __ldg(tokens + t + 32) : -1;
+  long long cur_beg = 0, cur_end = 0;
+  if (t < n_tok) {
+    const int k = find_traj(offs, n_traj, n_tok, t);
+    cur_beg = (k < 0) ? t + 1 : (offs ? offs[k] : 0);
+    cur_end = (k < 0) ? t + 1 : traj_end(offs, n_tok, k);
+    if (k < 0) cur_beg = cur_end;  // outside every trajectory: no room
+  }
+  const long long room = (t < n_tok && t >= cur_beg) ? cur_end - t : 0;
+  bool term = lo >= 0 && lo < cs.vocab && ((cs.term_tab[lo >> 5] >> (lo & 31)) & 1u);
   load_patterns(cs, sp);
   const int nd = cs.n_dist;
   for (int i = threadIdx.x; i < nd; i += blockDim.x) s_dist[i] = cs.dist_tok[i];
@@ -168,24 +184,8 @@ __global__ void __launch_bounds__(kScanThreads)
   unsigned* const wrm = s_rm[warp];
   // ---- phase 1: match, terminator words, per-warp counts
   int wcount = 0;
-  long long cur_end = -1;   // end of the trajectory holding this lane's current position
-  long long cur_beg = 0;
-  for (int gi = 0; gi < kGroupsB; gi++) {
-    const long long b = tile0 + (static_cast<long long>(warp) * kGroupsB + gi) * 32;
-    if (b >= n_tok) break;
-    const long long t = b + lane;
-    const int lo = t < n_tok ? __ldg(tokens + t) : -1;
-    const int hi = t + 32 < n_tok ? __ldg(tokens + t + 32) : -1;
-    // this lane's trajectory [cur_beg, cur_end) (positions only grow along a lane)
-    if (t < n_tok && t >= cur_end) {
-      const int k = find_traj(offs, n_traj, n_tok, t);
-      cur_beg = (k < 0) ? t + 1 : (offs ? offs[k] : 0);
-      cur_end = (k < 0) ? t + 1 : traj_end(offs, n_tok, k);
-      if (k < 0) cur_beg = cur_end;  // outside every trajectory: no room
-    }
-    const long long room = (t < n_tok && t >= cur_beg) ? cur_end - t : 0;
+  if (b < n_tok) {
     // terminator bits (R19: a period between digit tokens of one trajectory is not an end)
-    bool term = lo >= 0 && lo < cs.vocab && ((cs.term_tab[lo >> 5] >> (lo & 31)) & 1u);
     if (cs.dec_period >= 0) {
       int prev = __shfl_up_sync(kFull, lo, 1);
       if (lane == 0) prev = (t >= 1 && t - 1 < n_tok) ? __ldg(tokens + t - 1) : -1;
@@ -281,10 +281,7 @@ __global__ void __launch_bounds__(kScanThreads)
   __syncthreads();
   // ---- phase 2: ordered writes
   long long o = s_prefix + s_wcount[warp];
-  for (int gi = 0; gi < kGroupsB; gi++) {
-    const long long b = tile0 + (static_cast<long long>(warp) * kGroupsB + gi) * 32;
-    if (b >= n_tok) break;
-    const long long t = b + lane;
+  if (b < n_tok) {
     if (cs.mode == 0) {
       const int best = s_best[(b - tile0) + lane];
       const unsigned has = __ballot_sync(kFull, best >= 0);

@@ -302,15 +302,30 @@ __device__ __forceinline__ void consume_fast(const uint4 (&raw)[UV], int nvalid,
                                              ThreadState& st, float c, float& T, int& tkey, float& theta_w,
                                              int key, uint32_t theta_p) {
   float2 s2 = stage_sum<E, UV, POLY>(raw, nvalid, c, st.mref);
+  const float s = s2.x + s2.y;
+#ifndef RELAY_K1_KEY_PRED
   // T follows the shared threshold (key: loaded with the stage, before the
   // ring words, so its latency hides under the sum): a stale (lower) T stays
   // correct, but every thread would trip on the elements between the old and
-  // the new theta
+  // the new theta.  The key test joins the guard's vote, so the common stage
+  // issues no T update at all (a predicated update cost 9 instructions per
+  // stage, MUFU included: profiles/r02/k1_sass_lines.txt).
+  if (!__any_sync(kFull, !(s < T) || key != tkey)) {
+    const float2 acc = __fadd2_rn(make_float2(st.acc[0], st.acc[1]), s2);
+    st.acc[0] = acc.x;
+    st.acc[1] = acc.y;
+    return;
+  }
   if (key != tkey) {
     tkey = key;
     T = guard_T(fmaxf(theta_w, unkey(key)), st, c);
   }
-  const float s = s2.x + s2.y;
+#else
+  if (key != tkey) {
+    tkey = key;
+    T = guard_T(fmaxf(theta_w, unkey(key)), st, c);
+  }
+#endif
   // warp-uniform: when any lane trips, the whole warp takes the exact path
   // (it would execute it anyway) and the warp's threshold raise joins it
   if (__any_sync(kFull, !(s < T))) {
@@ -474,7 +489,7 @@ __device__ __forceinline__ SwitchIn load_switch_in(const RowsArgs& a, long long 
 template <class E, int MODE>
 __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs, const SmemCue& sc,
                                             long long r, const Partial& q, bool exact, float S,
-                                            const SwitchIn& in) {
+                                            const SwitchIn& in, int best = -2) {
   const int lane = threadIdx.x & 31;
   if constexpr (MODE == kModePartial) {
     // vocabulary shard: top-2 with GLOBAL indices and the normaliser relative
@@ -530,7 +545,7 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
     if (a.thk) return;  // relay_step_sample: the sampling kernel runs the switch
     const int tok = a.sampled ? in.sampled : o.i1;
     switch_warp(cs, sc, tok, o.margin, in, a.state + r, a.hist + r * kHist,
-                a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r, a.cue_id + r);
+                a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r, a.cue_id + r, a.sampled ? best : -2);
   }
 }
 
@@ -547,8 +562,18 @@ struct Item {
 
 // FLAT = false (K1, the TP partials: always whole rows, strided) lets the
 // compiler drop the 64-bit slice state from the consumer loop's live set.
-template <bool FLAT>
+// SPLIT: 0 whole rows only, 1 flat slices only (K4's balanced split: no
+// dynamic / hybrid / cluster code in the instantiation), 2 every mode (tuning).
+template <int SPLIT>
+__device__ __forceinline__ int flat_mode(const RowsArgs& a) {
+  if constexpr (SPLIT == 0) return 0;
+  else if constexpr (SPLIT == 1) return a.flat ? 1 : 0;
+  else return a.flat;
+}
+
+template <int SPLIT>
 struct ItemIter {
+  static constexpr bool FLAT = SPLIT != 0;
   long long next_w;  // strided: next row
   long long e, E1;   // flat: next element, end of this CTA's slice
   long long row0;    // flat: first row of the sliced region (hybrid: the rows after the whole ones)
@@ -574,7 +599,7 @@ struct ItemIter {
     next_w = blockIdx.x;
     e = E1 = 0;
     if (!FLAT) return;
-    if (a.flat == 4) {
+    if (flat_mode<SPLIT>(a) == 4) {
       // cluster c = blockIdx / csize takes rows [c R / C, (c + 1) R / C)
       const long long C = gridDim.x / a.csize, c = blockIdx.x / a.csize;
       row0 = c * a.n_rows / C;
@@ -585,11 +610,11 @@ struct ItemIter {
       const double Tg = static_cast<double>(T) / static_cast<double>(G);
       e = slice_start(b, T, G, Tg);
       E1 = slice_start(b + 1, T, G, Tg);
-    } else if (a.flat == 1 || a.flat == 3) {
+    } else if (flat_mode<SPLIT>(a) == 1 || flat_mode<SPLIT>(a) == 3) {
       // hybrid (3): CTAs [0, n_whole) take rows [0, n_whole) whole; the rest
       // slice rows [n_whole, n_rows) equally (one whole row plus an equal
       // share of the rest per SM, instead of one or two whole rows)
-      const long long nw = a.flat == 3 ? a.n_whole : 0;
+      const long long nw = flat_mode<SPLIT>(a) == 3 ? a.n_whole : 0;
       row0 = nw;
       T = (a.n_rows - nw) * a.vocab;
       G = gridDim.x - nw;
@@ -610,8 +635,8 @@ struct ItemIter {
     return Item{r, j0, min(a.vocab, j0 + a.chunk), ch, a.cpr};
   }
   __device__ bool next(const RowsArgs& a, Item& it) {
-    if (!FLAT || !a.flat || (a.flat == 3 && b < 0)) {
-      const bool hyb = FLAT && a.flat == 3;
+    if (!FLAT || !flat_mode<SPLIT>(a) || (flat_mode<SPLIT>(a) == 3 && b < 0)) {
+      const bool hyb = FLAT && flat_mode<SPLIT>(a) == 3;
       if (next_w >= (hyb ? a.n_whole : a.n_rows)) return false;
       it = Item{next_w, 0, a.vocab, 0, 1};
       next_w = hyb ? a.n_whole : next_w + gridDim.x;  // hybrid: one whole row
@@ -639,15 +664,15 @@ struct ItemIter {
 // (-1 = no more) and completes ifull[slot].  The producer refills a slot only
 // after the epilogue released it (rempty), which happens after every consumer
 // and the epilogue read it, so no waiter can miss a phase.
-template <bool FLAT>
-__device__ __forceinline__ bool fetch_item(const RowsArgs& a, ItemIter<FLAT>& iter, int it, int nslots,
+template <int SPLIT>
+__device__ __forceinline__ bool fetch_item(const RowsArgs& a, ItemIter<SPLIT>& iter, int it, int nslots,
                                            const long long* s_item, uint32_t ifull_s, Item& item) {
-  if (!FLAT || a.flat != 2) return iter.next(a, item);
+  if (flat_mode<SPLIT>(a) != 2) return iter.next(a, item);
   const int slot = it % nslots;
   mbar_wait(ifull_s + 8 * slot, (it / nslots) & 1);
   const long long k = *reinterpret_cast<const volatile long long*>(s_item + slot);
   if (k < 0) return false;
-  item = ItemIter<FLAT>::from_k(a, k);
+  item = ItemIter<SPLIT>::from_k(a, k);
   return true;
 }
 
@@ -682,7 +707,7 @@ extern "C" int relay_debug_trace_reset(const unsigned long long* zeros, int n_ct
 #define TRACE(k) ((void)0)
 #endif
 
-template <class E, int NCW, int NS, int UV, int MINB, int MODE, bool SPLIT>
+template <class E, int NCW, int NS, int UV, int MINB, int MODE, int SPLIT>
 __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
@@ -701,7 +726,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   constexpr int kBarRed0 = kBarRing0 + NS;
   // SPLIT: the work-split modes that cut rows across CTAs (K4 small batches
   // and tuning modes); the whole-row instantiations carry none of that code
-  constexpr bool kFlat = SPLIT;
+  const int fmode = flat_mode<SPLIT>(a);  // compile-time constant unless SPLIT == 2
   constexpr int kPolyPairs = MODE == kModeStep ? RELAY_K4_POLY_PAIRS : RELAY_K1_POLY_PAIRS;
   static_assert(kBarRed0 + kSlots <= 16, "named barriers");
   extern __shared__ __align__(128) unsigned char ring[];
@@ -739,9 +764,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       mbar_init(ifull_s + 8 * s, 1);        // the producer (dynamic mode)
       s_theta[s] = fkey(-INFINITY);
     }
-    if (kFlat && a.flat == 4) {
+    if (fmode == 4) {
       // one mbarrier per owned split row, expecting its other parts
-      ItemIter<true> it0;
+      ItemIter<SPLIT> it0;
       it0.init(a);
       Item x;
       while (it0.next(a, x))
@@ -751,7 +776,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     fence_barrier_init();
   }
   __syncthreads();
-  if (kFlat && a.flat == 4) cluster_sync_all();  // every owner's barriers exist before any remote arrive
+  if (fmode == 4) cluster_sync_all();  // every owner's barriers exist before any remote arrive
   const float c = a.c;
   // K4 is launched with programmatic dependent launch: its prologue (barrier
   // init, item math, pattern staging) overlaps the previous kernel's tail;
@@ -796,7 +821,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         if (++stage == NS) stage = 0;
       }
     };
-    if (kFlat && a.flat == 2) {
+    if (fmode == 2) {
       const long long total = a.n_rows * a.cpr;
       if constexpr (MODE == kModeStep) pdl_wait();
       long long k = 0;
@@ -815,11 +840,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         __syncwarp();
         if (done) break;
         kn = __shfl_sync(kFull, kn, 0);
-        issue(ItemIter<true>::from_k(a, k));
+        issue(ItemIter<SPLIT>::from_k(a, k));
         k = kn;
       }
     } else {
-      ItemIter<kFlat> iter;
+      ItemIter<SPLIT> iter;
       iter.init(a);
       Item item;
       bool more = iter.next(a, item);
@@ -839,7 +864,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       pdl_wait();
       if (lane == 0 && a.ready_q) pdl_launch_dependents();
     }
-    ItemIter<kFlat> iter;
+    ItemIter<SPLIT> iter;
     iter.init(a);
     Item item;
     for (int it = 0; fetch_item(a, iter, it, kSlots, s_item, ifull_s, item); ++it) {
@@ -847,17 +872,24 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const long long r = item.r;
       const T* row = logits + r * a.stride;
       SwitchIn in{};
-      if constexpr (MODE == kModeStep) in = load_switch_in(a, r);
+      int best = -2;
+      if constexpr (MODE == kModeStep) {
+        in = load_switch_in(a, r);
+        // a sampled token is known now: its pattern test runs while the
+        // consumers stream, off the step's tail
+        if (a.sampled && !a.thk) best = switch_match(cs, sc, in.sampled, in);
+      }
       // the consumers' partials: a named barrier (a spinning epilogue warp took
       // issue slots from the consumers for the whole row, 0.45 per element)
       named_bar(kBarRed0 + slot, NCT + 32);
+      if (lane == 0 && it == 0) TRACE(20);
       Partial q = partial_empty();
 #pragma unroll
       for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
       // full butterfly: every lane ends with the merged partial (the switch
       // below reads the row's top-1 on all lanes)
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) q = partial_merge(q, shfl_xor_partial(q, off));
+      q = warp_merge_all(q);
+      if (lane == 0 && it == 0) TRACE(21);
       float thk = INFINITY;
       if (a.thk) {
 #pragma unroll
@@ -876,15 +908,17 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           a.thk[r] = thk;
           a.zmax[r] = q.t.v1;
         }
-        finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in);
+        if (lane == 0 && it == 0) TRACE(22);
+        finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in, best);
         if (a.ready_q && lane == 0) {  // lane 0 wrote thk/zmax/margin/top1/top2/status: publish
           const int pos = atomicAdd(a.q_ctl, 1);
           asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.ready_q + pos), "r"(static_cast<int>(r) + 1)
                        : "memory");
         }
+        if (lane == 0 && it < 7) TRACE(24 + it);
         continue;
       }
-      if (kFlat && a.flat == 4) {
+      if (fmode == 4) {
         // cluster mode: the CTA holding the row's FIRST part owns it (its
         // last item: the other parts are the first items of the following
         // CTAs, long done, so no CTA waits on a chain of predecessors); the
@@ -901,6 +935,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
                           0u);
             mbar_arrive_remote(mapa_cluster(smem_u32(&s_xbar[xs]), owner));
           }
+          if (lane == 0 && it < 7) TRACE(24 + it);
           continue;
         }
         mbar_wait_cluster(smem_u32(&s_xbar[xs]), 0);
@@ -920,7 +955,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           S = warp_sum(exact_sum_thread<E>(row, a.vocab, m.t.v1, c, lane, 32));
           exact = true;
         }
-        finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in);
+        finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in, best);
+        if (lane == 0 && it < 7) TRACE(24 + it);
         continue;
       }
       // publish this part; the last part of the row to arrive finishes it
@@ -933,7 +969,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         __stcg(pw + 6, __int_as_float(q.flags));
         last = atomic_add_acq_rel(a.counter + r, 1) == item.nparts - 1;
       }
-      if (!__shfl_sync(kFull, last, 0)) continue;
+      if (!__shfl_sync(kFull, last, 0)) {
+        if (lane == 0 && it < 7) TRACE(24 + it);
+        continue;
+      }
       Partial m = partial_empty();
       for (int k = lane; k < item.nparts; k += 32) {
         const float* pr = a.part + (static_cast<size_t>(r) * kMaxSplit + k) * kPartWords;
@@ -944,7 +983,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         o.flags = __float_as_int(__ldcg(pr + 6));
         m = partial_merge(m, o);
       }
-      m = warp_reduce_partial(m);
+      m = warp_merge_all(m);
       bool exact = false;
       float S = 0.0f;
       if (m.flags & kFlagHuge) {
@@ -952,10 +991,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         exact = true;
       }
       if (lane == 0) a.counter[r] = 0;  // ready for the next launch / graph replay
-      finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in);
+      finish_item<E, MODE>(a, cs, sc, r, m, exact, S, in, best);
       if (lane == 0 && it < 7) TRACE(24 + it);
     }
-    if (kFlat && a.flat == 2 && lane == 0) {
+    if (fmode == 2 && lane == 0) {
       // the last CTA out re-arms the work counter for the next launch / replay
       // (every producer's final claim precedes its CTA's arrival here)
       if (atomic_add_acq_rel(a.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
@@ -974,7 +1013,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   int stage = 0;        // ring position, carried across items
   uint32_t phase = 0;
   const uint32_t ring_t = ring_s + static_cast<uint32_t>(tid) * 16;  // this thread's first vector of stage 0
-  ItemIter<kFlat> iter;
+  ItemIter<SPLIT> iter;
   iter.init(a);
   Item item;
   for (int it = 0; fetch_item(a, iter, it, kSlots, s_item, ifull_s, item); ++it) {
@@ -1114,8 +1153,12 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     }
     // hand the warp's 8 partials (after two shuffle rounds) to the epilogue warp
     Partial p = thread_partial(st);
+    if constexpr (RPW == 1) {
+      p = warp_merge_all(p);
+    } else {
 #pragma unroll
-    for (int off = 16; off >= RPW; off >>= 1) p = partial_merge(p, shfl_xor_partial(p, off));
+      for (int off = 16; off >= RPW; off >>= 1) p = partial_merge(p, shfl_xor_partial(p, off));
+    }
     if (lane < RPW) s_red[slot][warp * RPW + lane] = p;
     bar_arrive(kBarRed0 + slot, NCT + 32);
     if (tid == 0 && it < 8) TRACE(16 + it);
@@ -1198,12 +1241,14 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   constexpr int MINB = (MODE == kModeStep) ? kStepMinBlocks : kMinBlocks;
   constexpr int NCW = (MODE == kModeStep) ? kStepNCW : kNCW;
   constexpr int UV = (MODE == kModeStep) ? kStepUV : kUV;
-  const bool split = MODE == kModeStep && a.flat != 0;
-  auto kern = split ? rows_kernel<E, NCW, NS, UV, MINB, MODE, MODE == kModeStep>
-                    : rows_kernel<E, NCW, NS, UV, MINB, MODE, false>;
+  // instantiation: whole rows (0), flat slices only (1), every split mode (2)
+  const int split = MODE != kModeStep || a.flat == 0 ? 0 : a.flat == 1 ? 1 : 2;
+  auto kern = split == 0 ? rows_kernel<E, NCW, NS, UV, MINB, MODE, 0>
+              : split == 1 ? rows_kernel<E, NCW, NS, UV, MINB, MODE, MODE == kModeStep ? 1 : 0>
+                           : rows_kernel<E, NCW, NS, UV, MINB, MODE, MODE == kModeStep ? 2 : 0>;
   const int smem = NS * UV * NCW * 32 * 16;
-  static int per_sm_of[2] = {0, 0};   // per instantiation (the attribute is per function)
-  int& per_sm = per_sm_of[split ? 1 : 0];
+  static int per_sm_of[3] = {0, 0, 0};   // per instantiation (the attribute is per function)
+  int& per_sm = per_sm_of[split];
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

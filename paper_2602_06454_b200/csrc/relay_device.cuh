@@ -114,6 +114,50 @@ __device__ __forceinline__ int fkey(float f) {
 }
 __device__ __forceinline__ float unkey(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
 
+// Order-preserving key of a top-2 value with -0 folded onto +0 (better()
+// ranks them equal; their tie then falls to the lower index).  Values are
+// never NaN here (NaN never enters a top-2).
+__device__ __forceinline__ int top_key(float v) {
+  const int i = __float_as_int(v == 0.0f ? 0.0f : v);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+
+// Warp-wide merge of 32 partials, the result on every lane, by redux.sync
+// instead of a 5-round shuffle butterfly of partial_merge (35 shuffles and 10
+// MUFU in a dependent chain: ~0.5 us of the decode step's tail).  Top-2:
+// the best (value, index) is the max key, then the min index among lanes
+// holding it; the 2nd best is the best of every lane's first entry with the
+// winner's lane offering its second.  Normaliser: max exponent reference,
+// each lane's sum rescaled to it, one sum.  Same results as partial_merge
+// trees up to the rounding order of the normaliser sum.
+__device__ __forceinline__ Partial warp_merge_all(const Partial& p) {
+  const int k1 = top_key(p.t.v1);
+  const int K1 = __reduce_max_sync(kFull, k1);
+  const int I1 = static_cast<int>(
+      __reduce_min_sync(kFull, k1 == K1 ? static_cast<unsigned>(p.t.i1) : 0xffffffffu));
+  const bool hold = k1 == K1 && p.t.i1 == I1;
+  const int k2 = top_key(hold ? p.t.v2 : p.t.v1);
+  const int c2 = hold ? p.t.i2 : p.t.i1;
+  const int K2 = __reduce_max_sync(kFull, k2);
+  const int I2 = static_cast<int>(
+      __reduce_min_sync(kFull, k2 == K2 ? static_cast<unsigned>(c2) : 0xffffffffu));
+  const int KM = __reduce_max_sync(kFull, fkey(p.n.m));
+  const float M = unkey(KM);
+  float s = p.n.s * ex2(p.n.m - M);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+  Partial r;
+  r.t.v1 = unkey(K1);
+  r.t.i1 = I1;
+  r.t.v2 = unkey(K2);
+  r.t.i2 = I2;
+  r.n.m = M;
+  r.n.s = s;
+  r.flags = static_cast<int>(__reduce_or_sync(kFull, static_cast<unsigned>(p.flags)));
+  return r;
+}
+
+
 // Finish a row: margin, lse, status (R4).  c = iota*log2e, iota = c/log2e.
 // n.s sums 2^(fl(z_j c - m)) with fma, i.e. every term carries the same
 // shift delta = exact(z1 c) - fl(z1 c) relative to the row maximum; it is
@@ -293,7 +337,21 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
   }
 }
 
+#ifndef RELAY_WAIT_HINT_NS
+#define RELAY_WAIT_HINT_NS 0  // consumer try_wait suspend-time hint (0: none)
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#if RELAY_WAIT_HINT_NS > 0
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "n"(RELAY_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -303,6 +361,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // 1-D TMA: global -> shared, completion counted on `bar` (bytes % 16 == 0,

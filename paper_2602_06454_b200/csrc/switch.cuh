@@ -49,9 +49,9 @@ __device__ __forceinline__ void load_smem_cue(const CueDev& cs, SmemCue& sc) {
   __syncwarp();
 }
 
-static __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float m, const SwitchIn& in,
-                            uint8_t* state_p, int* hist, int* small_run_p, float gate, int max_seg,
-                            uint8_t* flag_out, int16_t* cue_out) {
+// The longest pattern that is a suffix of hist ++ tok (-1: none), or -1
+// without a test when tok cannot trigger a switch.  Warp-uniform.
+__device__ __forceinline__ int switch_match(const CueDev& cs, const SmemCue& sc, int tok, const SwitchIn& in) {
   const int lane = threadIdx.x & 31;
   const uint8_t state = static_cast<uint8_t>(in.state);
   const bool valid = tok >= 0 && tok < cs.vocab && !(state & 2);
@@ -74,20 +74,36 @@ static __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok,
       if (b) { best = base + __ffs(b) - 1; break; }
     }
   }
-  if (lane != 0) return;
+  return best;
+}
+
+// The state machine step for one sequence.  best: switch_match's result for
+// tok when the caller computed it already (a sampled token is known before
+// the row's margin, so K4 matches it while the consumers stream), else -2.
+static __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok, float m, const SwitchIn& in,
+                            uint8_t* state_p, int* hist, int* small_run_p, float gate, int max_seg,
+                            uint8_t* flag_out, int16_t* cue_out, int best = -2) {
+  const int lane = threadIdx.x & 31;
+  const uint8_t state = static_cast<uint8_t>(in.state);
+  const bool valid = tok >= 0 && tok < cs.vocab && !(state & 2);
+  if (best == -2) best = switch_match(cs, sc, tok, in);
+  // The decision is warp-uniform (every input is); the history shift comes
+  // from the registers loaded before the item (lane k writes hist[k] = old
+  // hist[k + 1]), so no lane reloads hist from global memory, and the stores
+  // fire from lane 0.
+  const int nxt = __shfl_down_sync(kFull, in.hist_lane, 1);
+  const int sr = in.small_run;
   int cue = -1, flag = 0;
   uint8_t st = state;
+  bool shift = false, clear = false, inc = false;
   if (valid) {
-    const int sr = in.small_run;
-    bool clear = false;
     if (tok == cs.think_end) {
       flag = 3; st = 3; clear = true;
     } else if ((state & 1) == 0) {
       if (best >= 0 && !(gate >= 0.0f && m < gate)) {
         flag = 1; cue = sc.cue[best]; st = 1; clear = true;
       } else {
-        for (int k = 0; k < kHist - 1; k++) hist[k] = hist[k + 1];
-        hist[kHist - 1] = tok;
+        shift = true;
       }
     } else {
       const bool term = (cs.term_tab[tok >> 5] >> (tok & 31)) & 1u;
@@ -95,18 +111,20 @@ static __device__ void switch_warp(const CueDev& cs, const SmemCue& sc, int tok,
         flag = 2; st = 0; clear = true;
       } else if (max_seg > 0 && sr + 1 >= max_seg) {
         flag = 4; st = 0; clear = true;
-      } else if (small_run_p) {
-        *small_run_p = sr + 1;
+      } else {
+        inc = true;
       }
     }
-    if (clear) {
-      for (int k = 0; k < kHist; k++) hist[k] = -1;
-      if (small_run_p) *small_run_p = 0;
-    }
-    *state_p = st;
   }
-  *flag_out = static_cast<uint8_t>(flag);
-  *cue_out = static_cast<int16_t>(cue);
+  if (lane < kHist && (shift || clear)) hist[lane] = clear ? -1 : (lane == kHist - 1 ? tok : nxt);
+  if (lane == 0) {
+    if (valid) {
+      if (small_run_p && (clear || inc)) *small_run_p = clear ? 0 : sr + 1;
+      *state_p = st;
+    }
+    *flag_out = static_cast<uint8_t>(flag);
+    *cue_out = static_cast<int16_t>(cue);
+  }
 }
 
 

@@ -81,6 +81,21 @@ def run(mode="step"):
           tuple(np.nanpercentile(gaps, [10, 50, 90, 100])))
     print("consumer exit: min %.1f med %.1f max %.1f" % tuple(np.nanpercentile(rel[:, 31], [0, 50, 100])))
     print("max epilogue", np.nanmax(rel[:, 24:31]))
+    lag = rel[:, 24:28] - rel[:, 16:20]  # epilogue item end - consumer item end
+    if np.isfinite(lag).any():
+        print("epilogue lag per item (us): p50 %.2f p90 %.2f max %.2f" %
+              tuple(np.nanpercentile(lag, [50, 90, 100])))
+        last_c = np.nanmax(rel[:, 16:24], axis=1)
+        last_e = np.nanmax(rel[:, 24:31], axis=1)
+        if mode == "step" and os.environ.get("RELAY_K4_MODE", "strided") == "strided":
+            # item 0's epilogue: consumers' barrier passed (20), partials merged (21),
+            # before finish (22), after finish + switch (24); from consumer warp 0's end (16)
+            d = rel[:, [20, 21, 22, 24]] - rel[:, [16]]
+            print("strided epilogue after consumer warp 0 (us) p50/p90: barrier %.2f/%.2f merged %.2f/%.2f "
+                  "pre-finish %.2f/%.2f done %.2f/%.2f" % tuple(x for k in range(4)
+                                                              for x in np.nanpercentile(d[:, k], [50, 90])))
+        print("last consumer item end: p50 %.1f p90 %.1f max %.1f | last epilogue end: p50 %.1f p90 %.1f max %.1f"
+              % (*np.nanpercentile(last_c, [50, 90, 100]), *np.nanpercentile(last_e, [50, 90, 100])))
 
 
 if __name__ == "__main__":

@@ -747,6 +747,13 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) TRACE(0);
+#ifdef RELAY_TRACE
+  if (tid == 0 && blockIdx.x < 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[blockIdx.x][29] = smid + 1;  // slot 29: the SM (+1: 0 means no stamp)
+  }
+#endif
   const uint32_t ring_s = smem_u32_pinned(ring);
   const uint32_t full_s = smem_u32_pinned(full);
   const uint32_t rempty_s = smem_u32_pinned(red_empty);

@@ -74,7 +74,7 @@ struct Agg {
 struct ScanWs {
   int* k2_flag;        // [n_tiles2] K2 look-back state (0 / count / running sum)
   long long* k2_val;   // [n_tiles2][2] K2 published count / running sum
-  int* k2_done;        // [1] K2 finished-tile counter
+  int* k2_done;        // [1] K2 look-back epoch (the last launch's flag tag; any start value)
   int* tile_flag;      // [n_tiles] K3 look-back state (0 / head / inclusive)
   Agg* tile_val;       // [n_tiles][2] K3 published head / inclusive aggregate
   int* done;           // [1] K3 finished-tile counter

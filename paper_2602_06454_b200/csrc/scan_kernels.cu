@@ -81,12 +81,14 @@ __device__ __forceinline__ bool match_at(const CueDev& cs, const SmemPat& sp, in
 // so each start keeps its longest match; ALL: one claim mask per cue.  The
 // terminator word of the group is one ballot.  Compaction: per-warp counts,
 // a block scan over the 8 warps, and a WARP-PARALLEL decoupled look-back over
-// the tiles to the left (32 predecessors per step), so occurrences come out
-// sorted by position in one pass; the last tile resets the flags.
+// the tiles to the left (256 predecessors per round trip), so occurrences come out
+// sorted by position in one pass; flags carry a per-launch epoch tag (the
+// last tile advances it), so no pass resets them.
 constexpr int kTileB = kK2Tile;                 // positions per CTA (one 32-start group per warp)
 constexpr int kGroupsB = kTileB / 32 / (kScanThreads / 32);  // groups per warp
 constexpr int kTileAgg = 1;    // value = this tile's count
 constexpr int kTileSum = 2;    // value = count of this tile and every tile before it
+constexpr int kLookB = 8;      // K2 look-back window: 32 x kLookB predecessor tiles per round trip
 
 __device__ __forceinline__ int ld_acquire_i32(const int* p) {
   int v;
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(kScanThreads)
     cue_scan_kernel(CueDev cs, const int* __restrict__ tokens, long long n_tok,
                     const long long* __restrict__ offs, int n_traj, uint32_t* __restrict__ term_bits,
                     int* __restrict__ occ_pos, int* __restrict__ occ_pat, long long cap,
-                    long long* __restrict__ n_occ, int* tile_flag, long long* tile_val, int* done) {
+                    long long* __restrict__ n_occ, int* tile_flag, long long* tile_val, int* epoch) {
   __shared__ SmemPat sp;
   __shared__ int s_dist[kMaxPat * kMaxLen];
   __shared__ int s_eidx[kMaxPat * kMaxLen];
@@ -159,6 +161,9 @@ __global__ void __launch_bounds__(kScanThreads)
   const int tile = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long tile0 = static_cast<long long>(tile) * kTileB;
+  // this launch's look-back tag (30 bits; 0 = never published)
+  int ep = (*reinterpret_cast<const volatile int*>(epoch) + 1) & 0x3fffffff;
+  if (ep == 0) ep = 1;
   static_assert(kGroupsB == 1, "one 32-start group per warp");
   // this warp's group: the token loads, the trajectory lookup and the
   // terminator test go first, so their latency overlaps the pattern staging
@@ -240,42 +245,71 @@ __global__ void __launch_bounds__(kScanThreads)
     if (lane < kScanThreads / 32) s_wcount[lane] = incl - wv;   // exclusive warp offsets
     const long long total = __shfl_sync(kFull, incl, 31);
     long long prefix = 0;
+    // flags carry this launch's epoch tag (no reset pass, no fences beyond the
+    // release / acquire pairs): flag = tag << 2 | state
+    const int tagged = ep << 2;
     if (tile == 0) {
       if (lane == 0) {
         tile_val[1] = total;
-        __threadfence();
-        st_release_i32(tile_flag, kTileSum);
+        st_release_i32(tile_flag, tagged | kTileSum);
       }
     } else {
       if (lane == 0) {
         tile_val[2 * tile] = total;
-        __threadfence();
-        st_release_i32(tile_flag + tile, kTileAgg);
+        st_release_i32(tile_flag + tile, tagged | kTileAgg);
       }
-      for (long long j = tile - 1;; j -= 32) {
-        const long long idx = j - lane;
-        int f = idx >= 0 ? ld_acquire_i32(tile_flag + idx) : kTileSum;
-        while (__any_sync(kFull, f == 0))
-          if (f == 0) f = ld_acquire_i32(tile_flag + idx);
+      // look-back over windows of 32 x kLookB predecessors (d = lane + 32 u
+      // tiles back): every flag load of a window is in flight at once, so a
+      // configs[1] tile (127 predecessors) resolves in one round trip
+      for (long long j = tile - 1;; j -= 32 * kLookB) {
+        int f[kLookB];
+#pragma unroll
+        for (int u = 0; u < kLookB; u++) {
+          const long long idx = j - lane - 32 * u;
+          f[u] = idx >= 0 ? ld_acquire_i32(tile_flag + idx) : (tagged | kTileSum);
+        }
+        for (;;) {
+          bool pending = false;
+#pragma unroll
+          for (int u = 0; u < kLookB; u++) {
+            if ((f[u] & ~3) != tagged) {  // not yet published in this launch
+              f[u] = ld_acquire_i32(tile_flag + (j - lane - 32 * u));
+              pending |= (f[u] & ~3) != tagged;
+            }
+          }
+          if (!__any_sync(kFull, pending)) break;
+        }
+        int stop = 32 * kLookB;  // nearest predecessor with an inclusive sum (distance)
+#pragma unroll
+        for (int u = kLookB - 1; u >= 0; u--) {
+          const unsigned sums = __ballot_sync(kFull, (f[u] & 3) == kTileSum);
+          if (sums) stop = 32 * u + __ffs(sums) - 1;
+        }
         long long v = 0;
-        if (idx >= 0) v = __ldcg(tile_val + 2 * idx + (f == kTileSum ? 1 : 0));
-        const unsigned sums = __ballot_sync(kFull, f == kTileSum);
-        const int stop = sums ? __ffs(sums) - 1 : 32;   // nearest tile with an inclusive sum
-        if (lane > stop) v = 0;
+#pragma unroll
+        for (int u = 0; u < kLookB; u++) {
+          const int d = lane + 32 * u;
+          const long long idx = j - d;
+          if (d <= stop && idx >= 0) v += __ldcg(tile_val + 2 * idx + (d == stop ? 1 : 0));
+        }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
         prefix += v;
-        if (sums) break;
+        if (stop < 32 * kLookB) break;
       }
       if (lane == 0) {
         tile_val[2 * tile + 1] = prefix + total;
-        __threadfence();
-        st_release_i32(tile_flag + tile, kTileSum);
+        st_release_i32(tile_flag + tile, tagged | kTileSum);
       }
     }
     if (lane == 0) {
       s_prefix = prefix;
-      if (tile == gridDim.x - 1) *n_occ = prefix + total;
+      if (tile == gridDim.x - 1) {
+        *n_occ = prefix + total;
+        // every tile has published (this one's look-back saw them all), so
+        // every CTA has read the epoch: the next launch takes the next one
+        *epoch = ep;
+      }
     }
   }
   __syncthreads();
@@ -322,22 +356,6 @@ __global__ void __launch_bounds__(kScanThreads)
         }
       }
       o += tot;
-    }
-  }
-  // the last tile to finish resets the look-back flags for the next launch
-  __syncthreads();
-  __shared__ int s_last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(done, 1) == static_cast<int>(gridDim.x) - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    for (int j = threadIdx.x; j < static_cast<int>(gridDim.x); j += blockDim.x) tile_flag[j] = 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      *done = 0;
     }
   }
 }

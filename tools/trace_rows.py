@@ -94,6 +94,22 @@ def run(mode="step"):
             print("strided epilogue after consumer warp 0 (us) p50/p90: barrier %.2f/%.2f merged %.2f/%.2f "
                   "pre-finish %.2f/%.2f done %.2f/%.2f" % tuple(x for k in range(4)
                                                               for x in np.nanpercentile(d[:, k], [50, 90])))
+        if mode == "step":
+            sm = buf[:, 29].astype(np.int64) - 1
+            end_c = rel[:, 31]
+            from collections import defaultdict
+            per = defaultdict(list)
+            for b in range(n):
+                if sm[b] >= 0 and np.isfinite(end_c[b]):
+                    per[int(sm[b])].append(end_c[b])
+            one = [v[0] for v in per.values() if len(v) == 1]
+            two = [sorted(v) for v in per.values() if len(v) == 2]
+            if one:
+                print("SMs with one CTA: %d, consumer exit p50 %.1f max %.1f" % (len(one), np.median(one), max(one)))
+            if two:
+                t = np.array(two)
+                print("SMs with two CTAs: %d, first exit p50 %.1f max %.1f, second exit p50 %.1f max %.1f" %
+                      (len(two), np.median(t[:, 0]), t[:, 0].max(), np.median(t[:, 1]), t[:, 1].max()))
         print("last consumer item end: p50 %.1f p90 %.1f max %.1f | last epilogue end: p50 %.1f p90 %.1f max %.1f"
               % (*np.nanpercentile(last_c, [50, 90, 100]), *np.nanpercentile(last_e, [50, 90, 100])))
 

@@ -89,6 +89,25 @@ constexpr int kGroupsB = kTileB / 32 / (kScanThreads / 32);  // groups per warp
 constexpr int kTileAgg = 1;    // value = this tile's count
 constexpr int kTileSum = 2;    // value = count of this tile and every tile before it
 constexpr int kLookB = 8;      // K2 look-back window: 32 x kLookB predecessor tiles per round trip
+constexpr int kK2Offs = 512;   // K2: trajectory offsets staged in shared memory up to this many
+
+#ifdef RELAY_TRACE
+// Tuning-only K2 timeline (tools/k2_trace.py): %globaltimer stamps by thread
+// 0 of each tile: 0 entry, 1 patterns staged, 2 phase 1 done, 3 look-back
+// done, 4 writes issued.
+__device__ unsigned long long g_trace2[8192][16];
+__device__ __forceinline__ void stamp2(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0 && blockIdx.x < 8192) g_trace2[blockIdx.x][k] = t;
+}
+extern "C" int relay_debug_trace2_copy(unsigned long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace2, sizeof(unsigned long long) * 16 * n));
+}
+#define TRACE2(k) stamp2(k)
+#else
+#define TRACE2(k) ((void)0)
+#endif
 
 __device__ __forceinline__ int ld_acquire_i32(const int* p) {
   int v;
@@ -97,6 +116,14 @@ __device__ __forceinline__ int ld_acquire_i32(const int* p) {
 }
 __device__ __forceinline__ void st_release_i32(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Per group of 32 starts, one 64-bit ballot word per DISTINCT pattern element
@@ -109,6 +136,7 @@ template <bool CLS>
 __device__ __forceinline__ void group_words(const CueDev& cs, const int* dist, int nd, int lo, int hi, int room8,
                                             uint2* w, unsigned* rm) {
   const int lane = threadIdx.x & 31;
+#pragma unroll 4
   for (int d = 0; d < nd; d++) {
     const int e = dist[d];
     bool x, y;
@@ -161,8 +189,10 @@ __global__ void __launch_bounds__(kScanThreads)
   const int tile = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long tile0 = static_cast<long long>(tile) * kTileB;
-  // this launch's look-back tag (30 bits; 0 = never published)
-  int ep = (*reinterpret_cast<const volatile int*>(epoch) + 1) & 0x3fffffff;
+  TRACE2(0);
+  (void)tile_flag;  // the look-back state lives in the 64-bit words of tile_val
+  // this launch's look-back tag (28 bits; 0 = never published)
+  int ep = (*reinterpret_cast<const volatile int*>(epoch) + 1) & 0x0fffffff;
   if (ep == 0) ep = 1;
   static_assert(kGroupsB == 1, "one 32-start group per warp");
   // this warp's group: the token loads, the trajectory lookup and the
@@ -171,20 +201,28 @@ __global__ void __launch_bounds__(kScanThreads)
   const long long t = b + lane;
   const int lo = t < n_tok ? __ldg(tokens + t) : -1;
   const int hi = t + 32 < n_tok ? __ldg(tokens + t + 32) : -1;
-  long long cur_beg = 0, cur_end = 0;
-  if (t < n_tok) {
-    const int k = find_traj(offs, n_traj, n_tok, t);
-    cur_beg = (k < 0) ? t + 1 : (offs ? offs[k] : 0);
-    cur_end = (k < 0) ? t + 1 : traj_end(offs, n_tok, k);
-    if (k < 0) cur_beg = cur_end;  // outside every trajectory: no room
-  }
-  const long long room = (t < n_tok && t >= cur_beg) ? cur_end - t : 0;
   bool term = lo >= 0 && lo < cs.vocab && ((cs.term_tab[lo >> 5] >> (lo & 31)) & 1u);
+  // the trajectory offsets in shared memory (one parallel load instead of a
+  // chain of dependent global loads per binary search), when they fit
+  __shared__ long long s_offs[kK2Offs];
+  const bool offs_smem = offs && n_traj < kK2Offs;
+  if (offs_smem)
+    for (int i = threadIdx.x; i <= n_traj; i += blockDim.x) s_offs[i] = __ldg(offs + i);
   load_patterns(cs, sp);
   const int nd = cs.n_dist;
   for (int i = threadIdx.x; i < nd; i += blockDim.x) s_dist[i] = cs.dist_tok[i];
   for (int i = threadIdx.x; i < cs.n_pat * kMaxLen; i += blockDim.x) s_eidx[i] = cs.pat_eidx[i];
   __syncthreads();
+  long long cur_beg = 0, cur_end = 0;
+  if (t < n_tok) {
+    const long long* of = offs_smem ? s_offs : offs;
+    const int k = find_traj(of, n_traj, n_tok, t);
+    cur_beg = (k < 0) ? t + 1 : (of ? of[k] : 0);
+    cur_end = (k < 0) ? t + 1 : traj_end(of, n_tok, k);
+    if (k < 0) cur_beg = cur_end;  // outside every trajectory: no room
+  }
+  const long long room = (t < n_tok && t >= cur_beg) ? cur_end - t : 0;
+  TRACE2(1);
   uint2* const ww = s_w_dyn + warp * nd;
   unsigned* const wrm = s_rm[warp];
   // ---- phase 1: match, terminator words, per-warp counts
@@ -208,6 +246,7 @@ __global__ void __launch_bounds__(kScanThreads)
     if (cs.mode == 0) {
       unsigned claimed = 0;
       int best = -1;
+#pragma unroll 4
       for (int p = 0; p < cs.n_pat; p++) {
         const int L = sp.len[p];
         // bit s: start b + s matches and has >= L tokens left in its trajectory
@@ -219,6 +258,7 @@ __global__ void __launch_bounds__(kScanThreads)
       wcount += __popc(claimed);
     } else {
       unsigned long long cm = 0;   // this lane's cues
+#pragma unroll 4
       for (int p = 0; p < cs.n_pat; p++) {
         const int L = sp.len[p];
         const unsigned w = pattern_starts(s_eidx + p * kMaxLen, L, ww, wrm);
@@ -233,6 +273,7 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   if (lane == 0) s_wcount[warp] = wcount;
   __syncthreads();
+  TRACE2(2);
   // ---- tile total, per-warp offsets, warp-parallel decoupled look-back (warp 0)
   if (warp == 0) {
     int wv = lane < kScanThreads / 32 ? s_wcount[lane] : 0;
@@ -245,62 +286,79 @@ __global__ void __launch_bounds__(kScanThreads)
     if (lane < kScanThreads / 32) s_wcount[lane] = incl - wv;   // exclusive warp offsets
     const long long total = __shfl_sync(kFull, incl, 31);
     long long prefix = 0;
-    // flags carry this launch's epoch tag (no reset pass, no fences beyond the
-    // release / acquire pairs): flag = tag << 2 | state
-    const int tagged = ep << 2;
+    // Each tile publishes ONE 64-bit word, tag << 36 | state << 34 | count
+    // (count < 2^34): a single-copy-atomic relaxed store, so the look-back
+    // needs no fence, no acquire and no second load for the value.  The tag
+    // is this launch's epoch (no reset pass between launches).
+    const unsigned long long tagw = static_cast<unsigned long long>(ep) << 36;
+    constexpr unsigned long long kVal = (1ull << 34) - 1;
+    unsigned long long* const words = reinterpret_cast<unsigned long long*>(tile_val);
     if (tile == 0) {
-      if (lane == 0) {
-        tile_val[1] = total;
-        st_release_i32(tile_flag, tagged | kTileSum);
-      }
+      if (lane == 0) st_relaxed_u64(words, tagw | (static_cast<unsigned long long>(kTileSum) << 34) | total);
     } else {
-      if (lane == 0) {
-        tile_val[2 * tile] = total;
-        st_release_i32(tile_flag + tile, tagged | kTileAgg);
-      }
-      // look-back over windows of 32 x kLookB predecessors (d = lane + 32 u
-      // tiles back): every flag load of a window is in flight at once, so a
-      // configs[1] tile (127 predecessors) resolves in one round trip
+      if (lane == 0)
+        st_relaxed_u64(words + tile, tagw | (static_cast<unsigned long long>(kTileAgg) << 34) | total);
+#ifdef RELAY_TRACE
+      if (lane == 0) stamp2(8);
+#endif
+      // windows of 32 x kLookB predecessors (d = lane + 32 u tiles back), all
+      // loads of a window in flight at once: a configs[1] tile (127
+      // predecessors) resolves in one round trip
       for (long long j = tile - 1;; j -= 32 * kLookB) {
-        int f[kLookB];
+        unsigned long long f[kLookB];
 #pragma unroll
         for (int u = 0; u < kLookB; u++) {
           const long long idx = j - lane - 32 * u;
-          f[u] = idx >= 0 ? ld_acquire_i32(tile_flag + idx) : (tagged | kTileSum);
+          f[u] = idx >= 0 ? ld_relaxed_u64(words + idx) : tagw | (static_cast<unsigned long long>(kTileSum) << 34);
         }
+#ifdef RELAY_TRACE
+        int n_spin = 0;
+        if (lane == 0 && j == tile - 1) { (void)f[0]; stamp2(5); }
+#endif
         for (;;) {
+#ifdef RELAY_TRACE
+          ++n_spin;
+#endif
           bool pending = false;
 #pragma unroll
           for (int u = 0; u < kLookB; u++) {
-            if ((f[u] & ~3) != tagged) {  // not yet published in this launch
-              f[u] = ld_acquire_i32(tile_flag + (j - lane - 32 * u));
-              pending |= (f[u] & ~3) != tagged;
+            if ((f[u] >> 36) != static_cast<unsigned long long>(ep)) {  // not yet published in this launch
+              f[u] = ld_relaxed_u64(words + (j - lane - 32 * u));
+              pending |= (f[u] >> 36) != static_cast<unsigned long long>(ep);
             }
           }
+#ifdef RELAY_TRACE
+          if (j == tile - 1) {
+            int lastp = -1;
+            for (int u = 0; u < kLookB; u++)
+              if ((f[u] >> 36) != static_cast<unsigned long long>(ep)) lastp = static_cast<int>(j - lane - 32 * u);
+            lastp = __reduce_max_sync(kFull, lastp);
+            if (lane == 0 && lastp >= 0) g_trace2[blockIdx.x][9] = lastp + 1;
+          }
+#endif
           if (!__any_sync(kFull, pending)) break;
         }
-        int stop = 32 * kLookB;  // nearest predecessor with an inclusive sum (distance)
+#ifdef RELAY_TRACE
+        if (lane == 0 && j == tile - 1) { stamp2(6); g_trace2[blockIdx.x][7] = n_spin; }
+#endif
+        int stop = 32 * kLookB;  // nearest predecessor with an inclusive count (distance)
 #pragma unroll
         for (int u = kLookB - 1; u >= 0; u--) {
-          const unsigned sums = __ballot_sync(kFull, (f[u] & 3) == kTileSum);
+          const unsigned sums = __ballot_sync(kFull, ((f[u] >> 34) & 3) == kTileSum);
           if (sums) stop = 32 * u + __ffs(sums) - 1;
         }
         long long v = 0;
 #pragma unroll
-        for (int u = 0; u < kLookB; u++) {
-          const int d = lane + 32 * u;
-          const long long idx = j - d;
-          if (d <= stop && idx >= 0) v += __ldcg(tile_val + 2 * idx + (d == stop ? 1 : 0));
-        }
+        for (int u = 0; u < kLookB; u++)
+          if (lane + 32 * u <= stop) v += static_cast<long long>(f[u] & kVal);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
         prefix += v;
         if (stop < 32 * kLookB) break;
       }
-      if (lane == 0) {
-        tile_val[2 * tile + 1] = prefix + total;
-        st_release_i32(tile_flag + tile, tagged | kTileSum);
-      }
+      if (lane == 0)
+        st_relaxed_u64(words + tile,
+                       tagw | (static_cast<unsigned long long>(kTileSum) << 34) | static_cast<unsigned long long>(prefix + total));
     }
     if (lane == 0) {
       s_prefix = prefix;
@@ -313,6 +371,7 @@ __global__ void __launch_bounds__(kScanThreads)
     }
   }
   __syncthreads();
+  TRACE2(3);
   // ---- phase 2: ordered writes
   long long o = s_prefix + s_wcount[warp];
   if (b < n_tok) {
@@ -337,12 +396,7 @@ __global__ void __launch_bounds__(kScanThreads)
       long long q = o + excl - c;
       if (cm) {
         // the tokens of the window again, for each cue's longest pattern
-        int tk[kMaxLen];
-        long long room = 0;
-        {
-          const int k = find_traj(offs, n_traj, n_tok, t);
-          room = k < 0 ? 0 : traj_end(offs, n_tok, k) - t;
-        }
+        int tk[kMaxLen];  // (room: this start's tokens left in its trajectory, from phase 1)
 #pragma unroll
         for (int i = 0; i < kMaxLen; i++) tk[i] = (t + i < n_tok) ? __ldg(tokens + t + i) : -1;
         while (cm) {
@@ -358,6 +412,7 @@ __global__ void __launch_bounds__(kScanThreads)
       o += tot;
     }
   }
+  TRACE2(4);
 }
 
 // ------------------------------------------------------------------ K3

@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(HERE, "librelay.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in
            ("margin_kernels.cu", "scan_kernels.cu", "sample_kernels.cu", "relay_api.cu",
             "relay_comm.cu")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("relay_device.cuh", "relay_internal.h", "switch.cuh",
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("relay_device.cuh", "relay_internal.h", "switch.cuh", "draw.cuh",
                                                     "p2p.cuh")] + \
           [os.path.join(REPO, "include", "relay.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -31,9 +31,43 @@
 #include "p2p.cuh"
 #include "relay_device.cuh"
 #include "relay_internal.h"
+#include "draw.cuh"
 #include "switch.cuh"
 
 namespace relay {
+
+#ifdef RELAY_TRACE
+// Tuning-only timeline (tools/trace_rows.py): %globaltimer stamps per CTA.
+// Slots: 0 entry, 1-14 ring stage n landed (consumer thread 0), 15 first
+// TMA issued, 16-23 consumer item ends, 24-30 epilogue item ends, 31 exit.
+constexpr int kTraceSlots = 32;
+__device__ unsigned long long g_trace[4096][kTraceSlots];
+__device__ __forceinline__ void stamp(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (blockIdx.x < 4096 && k < kTraceSlots) g_trace[blockIdx.x][k] = t;
+}
+extern "C" int relay_debug_trace_copy(unsigned long long* host, int n_ctas) {
+  return static_cast<int>(
+      cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * kTraceSlots * n_ctas));
+}
+extern "C" int relay_debug_trace_reset(const unsigned long long* zeros, int n_ctas) {
+  return static_cast<int>(
+      cudaMemcpyToSymbol(g_trace, zeros, sizeof(unsigned long long) * kTraceSlots * n_ctas));
+}
+__device__ unsigned long long g_fuse_stats[4];  // fused draw: rows drawn, rows to K5, candidates
+extern "C" int relay_debug_fuse_stats(unsigned long long* host, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(host, g_fuse_stats, sizeof(unsigned long long) * 4);
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_fuse_stats, z, sizeof(z));
+  }
+  return static_cast<int>(e);
+}
+#define TRACE(k) stamp(k)
+#else
+#define TRACE(k) ((void)0)
+#endif
 
 constexpr float kHuge = 268435456.0f;  // 2^28: beyond it fp32 y = z*c is too coarse
 
@@ -410,6 +444,104 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// ------------------------------------------- fused top-k draw (N2, K4)
+constexpr int kFuseCap = 512;  // candidates per row held in shared memory (more: the row goes to K5)
+static_assert(kFuseCap >= 128, "fuse_raise reads the first 128 entries");
+constexpr int kFuseSeed = 8;   // first-stage seeds per warp (NCW * kFuseSeed >= kMaxTopK)
+constexpr int kFuseRank = 128; // candidates >= the final bound that the epilogue ranks (more: K5)
+
+// Every finite element >= B of the vectors u < nvalid into the row's
+// candidate list (one slot reservation per vector; NaN never qualifies).
+constexpr int kFuseRaise = 48;  // the list raises its bound each time it grows past a multiple of this
+
+template <class E, int UV>
+__device__ __forceinline__ bool fuse_push(const uint4 (&raw)[UV], int nvalid, int j0, int jstep, float B,
+                                          float* fv, int* fi, int* fcnt) {
+  constexpr int VEC = 16 / E::SZ;
+  bool crossed = false;
+#pragma unroll
+  for (int u = 0; u < UV; u++) {
+    if (u < nvalid && vec_max<E>(raw[u]) >= B) {
+      float f[VEC];
+      unpack16<E>(raw[u], f);
+      unsigned m = 0;
+#pragma unroll
+      for (int k = 0; k < VEC; k++) m |= (f[k] >= B && f[k] > -INFINITY) ? (1u << k) : 0u;
+      if (m) {
+        int p = atomicAdd(fcnt, __popc(m));
+        crossed |= p / kFuseRaise != (p + __popc(m)) / kFuseRaise;
+        while (m) {
+          const int k = __ffs(m) - 1;  // (elem_at: no local-memory copy of f[])
+          m &= m - 1;
+          if (p < kFuseCap) { fv[p] = elem_at<E>(raw[u], k); fi[p] = j0 + u * jstep + k; }
+          p++;
+        }
+      }
+    }
+  }
+  return crossed;
+}
+
+// Raise the list's shared bound to the topk-th largest of its first 128
+// entries (distinct elements of the row; slots reserved but not yet written
+// still hold -inf, so the result never exceeds a true lower bound).  One warp.
+__device__ __forceinline__ void fuse_raise(const float* fv, int topk, int* bkey) {
+  const int lane = threadIdx.x & 31;
+  const volatile float* v = fv;
+  float x0 = v[lane], x1 = v[lane + 32], x2 = v[lane + 64], x3 = v[lane + 96];
+  float m = -INFINITY;
+  for (int i = 0; i < topk; i++) {
+    const float lm = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
+    m = unkey(__reduce_max_sync(kFull, fkey(lm)));
+    if (m == -INFINITY) return;
+    const unsigned holders = __ballot_sync(kFull, lm == m);
+    if (lane == __ffs(holders) - 1) {
+      if (x0 == m) x0 = -INFINITY; else if (x1 == m) x1 = -INFINITY; else if (x2 == m) x2 = -INFINITY;
+      else x3 = -INFINITY;
+    }
+  }
+  if (lane == 0) atomicMax(bkey, fkey(m));
+}
+
+// The warp's kFuseSeed largest of its lanes' two (distinct) first-stage half
+// maxima into seed[] (NaN read as -inf).
+__device__ __forceinline__ void fuse_seeds(float2 h, float* seed) {
+  const int lane = threadIdx.x & 31;
+  float x0 = h.x == h.x ? h.x : -INFINITY, x1 = h.y == h.y ? h.y : -INFINITY;
+#pragma unroll 1
+  for (int i = 0; i < kFuseSeed; i++) {
+    const float lm = fmaxf(x0, x1);
+    const float m = unkey(__reduce_max_sync(kFull, fkey(lm)));
+    const unsigned holders = __ballot_sync(kFull, lm == m);
+    if (lane == __ffs(holders) - 1) {
+      if (x0 == m) x0 = -INFINITY; else x1 = -INFINITY;
+    }
+    if (lane == 0) seed[i] = m;
+  }
+}
+
+// The topk-th largest of the n <= 96 seeds (distinct elements of the row): a
+// lower bound on the row's topk-th largest logit (-inf with fewer than topk
+// finite).  Lane l holds seeds l, l + 32, l + 64; topk rounds of a warp max
+// with one holder removing its entry.
+__device__ __forceinline__ float fuse_bound(const float* seeds, int n, int topk) {
+  const int lane = threadIdx.x & 31;
+  float x0 = lane < n ? seeds[lane] : -INFINITY;
+  float x1 = lane + 32 < n ? seeds[lane + 32] : -INFINITY;
+  float x2 = lane + 64 < n ? seeds[lane + 64] : -INFINITY;
+  float m = -INFINITY;
+  for (int i = 0; i < topk; i++) {
+    const float lm = fmaxf(fmaxf(x0, x1), x2);
+    m = unkey(__reduce_max_sync(kFull, fkey(lm)));
+    if (m == -INFINITY) break;
+    const unsigned holders = __ballot_sync(kFull, lm == m);
+    if (lane == __ffs(holders) - 1) {
+      if (x0 == m) x0 = -INFINITY; else if (x1 == m) x1 = -INFINITY; else x2 = -INFINITY;
+    }
+  }
+  return m;
+}
+
 // ------------------------------------------------- K1 / K4 row kernel
 // Work items are (row, element range, part) triples (Item, ItemIter below).
 // K1 takes whole rows; K4 whole rows or, for small batches, parts of rows
@@ -463,7 +595,68 @@ struct RowsArgs {
   int keep_l2;    // L2 evict_last: the sampling kernel reads the rows again
   int* ready_q;   // relay_step_sample: rows pushed in completion order (release), so
   int* q_ctl;     // K5 samples a row as soon as its margin pass is done (q_ctl[0]: head)
+  // relay_step_sample with a top-k, whole rows: the draw fused into this pass
+  // (every finite logit >= a first-stage bound on the top_k-th largest is
+  // collected in shared memory; the epilogue ranks, draws and switches); rows
+  // whose candidates overflow go to K5 as before (queue entry r + 1; fused
+  // rows are queued as -(r + 1), which K5 skips)
+  int fuse;
+  float s_c;             // log2(e) / temperature
+  float topp;
+  const float* uniform;  // [n_rows]
+  int* sampled_out;      // [n_rows] the drawn tokens
 };
+
+// The epilogue's view of a row's candidate list (fused top-k draw).
+struct FuseIn {
+  bool on;
+  int n;             // candidates pushed (> kFuseCap: overflowed)
+  float thk;         // the final lower bound on the top_k-th largest logit
+  float u;           // the row's uniform
+  const float* fv;
+  const int* fi;
+  float* rv;         // [kFuseRank] scratch
+  int* ri;
+  float* topv;       // [kMaxTopK] the ranked top-k
+  int* topi;
+};
+
+// The drawn token of a row from its candidate list (one warp, R20 as in K5:
+// the exact top-k in (value desc, index asc) order, temperature, top-p,
+// inverse CDF), -1 for a row that is not sampled (status != 0), INT_MIN when
+// the list cannot give the top-k (overflow, or too many candidates at or
+// above the final bound): K5 samples that row from the logits.
+__device__ __forceinline__ int fused_draw(const RowsArgs& a, int status, const FuseIn& f) {
+  const int lane = threadIdx.x & 31;
+  if (status != 0) return -1;
+  if (f.n > kFuseCap) return INT_MIN;
+  // the candidates >= thk, compacted in list order
+  int m = 0;
+  for (int base = 0; base < f.n; base += 32) {
+    const int e = base + lane;
+    const bool take = e < f.n && f.fv[e] >= f.thk;
+    const unsigned b = __ballot_sync(kFull, take);
+    if (take) {
+      const int p = m + __popc(b & ((1u << lane) - 1u));
+      if (p < kFuseRank) { f.rv[p] = f.fv[e]; f.ri[p] = f.fi[e]; }
+    }
+    m += __popc(b);
+  }
+  if (m > kFuseRank) return INT_MIN;
+  __syncwarp();
+  // rank of each: the entries before it (distinct indices: distinct ranks)
+  const int K = min(a.topk, m);
+  for (int e = lane; e < m; e += 32) {
+    const float v = f.rv[e];
+    const int i = f.ri[e];
+    int rank = 0;
+    for (int g = 0; g < m; g++) rank += better(f.rv[g], f.ri[g], v, i);
+    if (rank < K) { f.topv[rank] = v; f.topi[rank] = i; }
+  }
+  __syncwarp();
+  if (K == 0) return -1;
+  return draw_topk_warp(a.s_c, a.topp, f.u, K, f.topv, f.topi);
+}
 
 constexpr int kPartWords = 8;  // v1 v2 i1 i2 m s flags pad
 constexpr int kXSlots = 4;     // cluster mode: rows a CTA owns at once (consecutive: distinct mod 4)
@@ -489,7 +682,8 @@ __device__ __forceinline__ SwitchIn load_switch_in(const RowsArgs& a, long long 
 template <class E, int MODE>
 __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs, const SmemCue& sc,
                                             long long r, const Partial& q, bool exact, float S,
-                                            const SwitchIn& in, int best = -2) {
+                                            const SwitchIn& in, int best = -2, const FuseIn* fuse = nullptr,
+                                            bool* drawn = nullptr) {
   const int lane = threadIdx.x & 31;
   if constexpr (MODE == kModePartial) {
     // vocabulary shard: top-2 with GLOBAL indices and the normaliser relative
@@ -542,8 +736,22 @@ __device__ __forceinline__ void finish_item(const RowsArgs& a, const CueDev& cs,
     if (a.status) a.status[r] = static_cast<uint8_t>(o.status);
   }
   if constexpr (MODE == kModeStep) {
-    if (a.thk) return;  // relay_step_sample: the sampling kernel runs the switch
-    const int tok = a.sampled ? in.sampled : o.i1;
+    int tok;
+    if (a.thk) {
+      // relay_step_sample: the fused draw, else the sampling kernel (K5)
+      // draws and runs the switch
+      if (!fuse || !fuse->on) return;
+      tok = fused_draw(a, o.status, *fuse);
+#ifdef RELAY_TRACE
+      if (lane == 0 && blockIdx.x < 4096 && g_trace[blockIdx.x][23] == 0) TRACE(23);
+#endif
+      if (tok == INT_MIN) return;
+      *drawn = true;
+      if (lane == 0) a.sampled_out[r] = tok;
+      best = -2;
+    } else {
+      tok = a.sampled ? in.sampled : o.i1;
+    }
     switch_warp(cs, sc, tok, o.margin, in, a.state + r, a.hist + r * kHist,
                 a.small_run ? a.small_run + r : nullptr, a.gate, a.max_seg, a.flag + r, a.cue_id + r, a.sampled ? best : -2);
   }
@@ -683,31 +891,8 @@ __device__ __forceinline__ bool fetch_item(const RowsArgs& a, ItemIter<SPLIT>& i
 // Items rotate over NSLOT reduction slots guarded by mbarriers.
 constexpr int kSlots = 4;
 
-#ifdef RELAY_TRACE
-// Tuning-only timeline (tools/trace_rows.py): %globaltimer stamps per CTA.
-// Slots: 0 entry, 1-14 ring stage n landed (consumer thread 0), 15 first
-// TMA issued, 16-23 consumer item ends, 24-30 epilogue item ends, 31 exit.
-constexpr int kTraceSlots = 32;
-__device__ unsigned long long g_trace[4096][kTraceSlots];
-__device__ __forceinline__ void stamp(int k) {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  if (blockIdx.x < 4096 && k < kTraceSlots) g_trace[blockIdx.x][k] = t;
-}
-extern "C" int relay_debug_trace_copy(unsigned long long* host, int n_ctas) {
-  return static_cast<int>(
-      cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * kTraceSlots * n_ctas));
-}
-extern "C" int relay_debug_trace_reset(const unsigned long long* zeros, int n_ctas) {
-  return static_cast<int>(
-      cudaMemcpyToSymbol(g_trace, zeros, sizeof(unsigned long long) * kTraceSlots * n_ctas));
-}
-#define TRACE(k) stamp(k)
-#else
-#define TRACE(k) ((void)0)
-#endif
 
-template <class E, int NCW, int NS, int UV, int MINB, int MODE, int SPLIT>
+template <class E, int NCW, int NS, int UV, int MINB, int MODE, int SPLIT, bool FUSE = false>
 __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
@@ -729,6 +914,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const int fmode = flat_mode<SPLIT>(a);  // compile-time constant unless SPLIT == 2
   constexpr int kPolyPairs = MODE == kModeStep ? RELAY_K4_POLY_PAIRS : RELAY_K1_POLY_PAIRS;
   static_assert(kBarRed0 + kSlots <= 16, "named barriers");
+  static_assert(!FUSE || NCW * kFuseSeed <= 96, "fuse_bound holds three seeds per lane");
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t red_empty[kSlots];
@@ -736,6 +922,21 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   __shared__ long long s_item[kSlots];
   __shared__ int s_theta[kSlots];
   __shared__ float s_thk[kSlots][NCW];
+  // fused top-k draw (FUSE instantiation only): two candidate lists (item it
+  // uses it & 1; the epilogue releases a list before the consumers reach item
+  // it + 2), the first-stage seeds, the ranked top-k
+  constexpr int kFC = FUSE ? kFuseCap : 1;
+  constexpr int kFS = FUSE ? NCW * kFuseSeed : 1;
+  constexpr int kFR = FUSE ? kFuseRank : 1;
+  __shared__ float s_fv[2][kFC];
+  __shared__ int s_fi[2][kFC];
+  __shared__ int s_fcnt[2];
+  __shared__ int s_fbk[2];  // the lists' shared bounds (fkey), raised as they grow
+  __shared__ float s_seed[2][kFS];  // by item parity, like the lists
+  __shared__ float s_rv[kFR];
+  __shared__ int s_ri[kFR];
+  __shared__ float s_topv[FUSE ? kMaxTopK : 1];
+  __shared__ int s_topi[FUSE ? kMaxTopK : 1];
   __shared__ Partial s_red[kSlots][NRED];
   __shared__ SmemCue sc;
   // cluster mode: row parts of the rows this CTA owns (it holds their first
@@ -771,6 +972,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       mbar_init(ifull_s + 8 * s, 1);        // the producer (dynamic mode)
       s_theta[s] = fkey(-INFINITY);
     }
+    s_fcnt[0] = 0;
+    s_fcnt[1] = 0;
+    s_fbk[0] = fkey(-INFINITY);
+    s_fbk[1] = fkey(-INFINITY);
     if (fmode == 4) {
       // one mbarrier per owned split row, expecting its other parts
       ItemIter<SPLIT> it0;
@@ -782,6 +987,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     }
     fence_barrier_init();
   }
+  if constexpr (FUSE)  // list slots hold -inf until written (fuse_raise reads reserved slots)
+    for (int e = tid; e < 2 * kFC; e += blockDim.x) s_fv[e / kFC][e % kFC] = -INFINITY;
   __syncthreads();
   if (fmode == 4) cluster_sync_all();  // every owner's barriers exist before any remote arrive
   const float c = a.c;
@@ -886,6 +1093,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         // consumers stream, off the step's tail
         if (a.sampled && !a.thk) best = switch_match(cs, sc, in.sampled, in);
       }
+      const bool fuse = FUSE && MODE == kModeStep && a.fuse;
+      const float fu = fuse ? a.uniform[r] : 0.0f;
       // the consumers' partials: a named barrier (a spinning epilogue warp took
       // issue slots from the consumers for the whole row, 0.45 per element)
       named_bar(kBarRed0 + slot, NCT + 32);
@@ -903,7 +1112,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         for (int w = 0; w < NCW; w++) thk = fminf(thk, s_thk[slot][w]);
       }
       if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
-      mbar_arrive(rempty_s + 8 * slot);
+      if (!fuse) mbar_arrive(rempty_s + 8 * slot);  // (fused draw: after the list is read)
       if (item.nparts == 1) {
         bool exact = false;
         float S = 0.0f;
@@ -916,11 +1125,37 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           a.zmax[r] = q.t.v1;
         }
         if (lane == 0 && it == 0) TRACE(22);
-        finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in, best);
+        FuseIn fz{};
+        bool drawn = false;
+        if (fuse) {
+          const int fb = it & 1;
+          fz = FuseIn{true, s_fcnt[fb], thk, fu, s_fv[fb], s_fi[fb], s_rv, s_ri, s_topv, s_topi};
+        }
+        finish_item<E, MODE>(a, cs, sc, r, q, exact, S, in, best, &fz, &drawn);
+#ifdef RELAY_TRACE
+        if (fuse && lane == 0) {
+          atomicAdd(&g_fuse_stats[drawn ? 0 : 1], 1ull);
+          atomicAdd(&g_fuse_stats[2], static_cast<unsigned long long>(fz.n));
+        }
+#endif
         if (a.ready_q && lane == 0) {  // lane 0 wrote thk/zmax/margin/top1/top2/status: publish
+          // (a row drawn here is queued as -(r + 1): K5 only takes its ticket)
           const int pos = atomicAdd(a.q_ctl, 1);
-          asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.ready_q + pos), "r"(static_cast<int>(r) + 1)
-                       : "memory");
+          const int v = drawn ? -(static_cast<int>(r) + 1) : static_cast<int>(r) + 1;
+          asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.ready_q + pos), "r"(v) : "memory");
+        }
+        if (fuse) {
+          __syncwarp();
+          {
+            const int fb = it & 1;
+            const int n = min(s_fcnt[fb], kFC);
+            for (int e = lane; e < n; e += 32) s_fv[fb][e] = -INFINITY;
+            if (lane == 0) {
+              s_fcnt[fb] = 0;
+              s_fbk[fb] = fkey(-INFINITY);
+            }
+          }
+          mbar_arrive(rempty_s + 8 * slot);  // the list is free for item it + 2
         }
         if (lane == 0 && it < 7) TRACE(24 + it);
         continue;
@@ -1044,10 +1279,20 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     float T = 0.0f;             // consume_fast's guard (set by the row's first stage)
     int tkey = INT_MIN;         // the threshold key T was computed from
     float tmax = -INFINITY;     // this thread's maximum (relay_step_sample's bound)
+    // fused draw: this item's candidate list (released by the epilogue once it
+    // drew item it - 2) and bound (-inf until the first stage's seeds are in)
+    const bool fuse = FUSE && MODE == kModeStep && a.fuse;
+    const int fb = it & 1;
+    float fB = -INFINITY;
+    if (fuse && it >= 2) mbar_wait(rempty_s + 8 * ((it - 2) % kSlots), ((it - 2) / kSlots) & 1);
     if (tid < g.head) {
       const float x = E::load1(row + j0 + tid);
       consume_scalar(x, j0 + tid, st, c);
       if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, x);
+      if (fuse && x > -INFINITY) {  // (NaN fails the test)
+        const int p = atomicAdd(&s_fcnt[fb], 1);
+        if (p < kFuseCap) { s_fv[fb][p] = x; s_fi[fb][p] = j0 + tid; }
+      }
     }
     if (nst > 0) {
       // the item's first stage: the row-start probe.  The two half maxima of
@@ -1077,8 +1322,23 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       consume_stage<E, UV>(raw, h, jt, NCT * VEC, st, c, theta, slow);
       if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
       T = guard_T(fmaxf(theta, theta_w), st, c);
-      if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h.x, h.y));
-      if (tid == 0 && it == 1) TRACE(14);
+      if constexpr (MODE == kModeStep) {
+        tmax = fmaxf(tmax, fmaxf(h.x, h.y));
+        if (fuse) {
+          // the bound: the top_k-th largest of every warp's kFuseSeed
+          // largest first-stage half maxima (distinct elements of the row)
+          fuse_seeds(h, s_seed[fb] + warp * kFuseSeed);
+          named_bar(1, NCT);
+          fB = fuse_bound(s_seed[fb], NCW * kFuseSeed, a.topk);
+          if (tid == 0 && it == 0) TRACE(11);
+          if (lane == 0) atomicMax(&s_fbk[fb], fkey(fB));
+          if (__any_sync(kFull, fmaxf(h.x, h.y) >= fB)) {
+            const bool x = fuse_push<E, UV>(raw, UV, jt, NCT * VEC, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
+            if (__any_sync(kFull, x)) fuse_raise(s_fv[fb], a.topk, &s_fbk[fb]);
+          }
+        }
+      }
+      if (tid == 0 && it <= 1) TRACE(14);
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     // steady state: per stage the wait, the words, one release, the terms and
@@ -1094,13 +1354,22 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #pragma unroll
       for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCT * 16);
       bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
-      consume_fast<E, UV, kPolyPairs>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
       if constexpr (MODE == kModeStep) {
+        // (before the terms: the words are dead after consume_fast)
         if (a.topk > 0) {
           const float2 h = stage_max2<E, UV>(raw);
           tmax = fmaxf(tmax, fmaxf(h.x, h.y));
+          if (fuse) {
+            fB = fmaxf(fB, unkey(*reinterpret_cast<volatile int*>(&s_fbk[fb])));  // raised by any warp
+            if (__any_sync(kFull, fmaxf(h.x, h.y) >= fB)) {
+              const bool x = fuse_push<E, UV>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, fB, s_fv[fb], s_fi[fb],
+                                              &s_fcnt[fb]);
+              if (__any_sync(kFull, x)) fuse_raise(s_fv[fb], a.topk, &s_fbk[fb]);
+            }
+          }
         }
       }
+      consume_fast<E, UV, kPolyPairs>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     if (rem > 0) {
@@ -1116,13 +1385,18 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #pragma unroll
         for (int u = 0; u < UV; u++) raw[u] = u < nvalid ? lds128(ring_t + stage * SB + u * NCT * 16) : E::neg_inf16();
         bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
-        consume_fast<E, UV, kPolyPairs>(raw, nvalid, jb + tid * VEC, NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
         if constexpr (MODE == kModeStep) {
           if (a.topk > 0) {
             const float2 h = stage_max2<E, UV>(raw);
             tmax = fmaxf(tmax, fmaxf(h.x, h.y));
+            if (fuse) {
+              fB = fmaxf(fB, unkey(*reinterpret_cast<volatile int*>(&s_fbk[fb])));
+              if (__any_sync(kFull, fmaxf(h.x, h.y) >= fB))
+                fuse_push<E, UV>(raw, nvalid, jb + tid * VEC, NCT * VEC, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
+            }
           }
         }
+        consume_fast<E, UV, kPolyPairs>(raw, nvalid, jb + tid * VEC, NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
       } else {  // a row shorter than one stage: vector by vector, max-guarded
         const float theta = fmaxf(theta_w, unkey(theta_load(theta_p)));
         const int nvec = rem / 16;
@@ -1131,7 +1405,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           const uint4 raw1[1] = {lds128(buf + v * 16)};
           const float2 h1 = stage_max2<E, 1>(raw1);
           consume_stage<E, 1>(raw1, h1, jb + v * VEC, 0, st, c, theta, slow);
-          if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, fmaxf(h1.x, h1.y));
+          if constexpr (MODE == kModeStep) {
+            tmax = fmaxf(tmax, fmaxf(h1.x, h1.y));
+            if (fuse) fuse_push<E, 1>(raw1, 1, jb + v * VEC, 0, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
+          }
         }
         bar_arrive(kBarRing0 + stage, NCT + 32);
       }
@@ -1141,6 +1418,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const float x = E::load1(row + g.tail + tid);
       consume_scalar(x, g.tail + tid, st, c);
       if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, x);
+      if (fuse && x >= fB && x > -INFINITY) {
+        const int p = atomicAdd(&s_fcnt[fb], 1);
+        if (p < kFuseCap) { s_fv[fb][p] = x; s_fi[fb][p] = g.tail + tid; }
+      }
     }
     if (a.topk > 0) {
       // N2: the warp's kw-th largest thread maximum, kw = ceil(topk / NCW);
@@ -1250,18 +1531,25 @@ static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) 
   constexpr int UV = (MODE == kModeStep) ? kStepUV : kUV;
   // instantiation: whole rows (0), flat slices only (1), every split mode (2)
   const int split = MODE != kModeStep || a.flat == 0 ? 0 : a.flat == 1 ? 1 : 2;
-  auto kern = split == 0 ? rows_kernel<E, NCW, NS, UV, MINB, MODE, 0>
+  // (the fused top-k draw is its own whole-row instantiation: its candidate
+  // lists and pushes stay out of the decode-step switch's registers)
+  const bool fz = MODE == kModeStep && a.fuse && split == 0;
+  auto kern = fz ? rows_kernel<E, NCW, NS, UV, MINB, MODE, 0, MODE == kModeStep>
+              : split == 0 ? rows_kernel<E, NCW, NS, UV, MINB, MODE, 0>
               : split == 1 ? rows_kernel<E, NCW, NS, UV, MINB, MODE, MODE == kModeStep ? 1 : 0>
                            : rows_kernel<E, NCW, NS, UV, MINB, MODE, MODE == kModeStep ? 2 : 0>;
   const int smem = NS * UV * NCW * 32 * 16;
-  static int per_sm_of[3] = {0, 0, 0};   // per instantiation (the attribute is per function)
-  int& per_sm = per_sm_of[split];
+  static int per_sm_of[4] = {0, 0, 0, 0};   // per instantiation (the attribute is per function)
+  int& per_sm = per_sm_of[fz ? 3 : split];
   if (per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCW + 2) * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
+    if (getenv("RELAY_DEBUG_LAUNCH"))
+      fprintf(stderr, "relay rows_kernel mode %d split %d fuse %d: %d CTAs/SM, smem %d B dynamic\n", MODE, split,
+              fz ? 1 : 0, per_sm, smem);
   }
   const long long slots = static_cast<long long>(per_sm) * num_sms();
   long long grid = slots;
@@ -1402,7 +1690,7 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
 cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
                              long long stride, float iota, uint8_t* state, int* hist, int* small_run,
                              float gate, int max_seg, float* margin, int* top1, int* top2,
-                             const StepWs& ws, int topk, cudaStream_t st) {
+                             const StepWs& ws, int topk, cudaStream_t st, const StepDraw* draw) {
   if (batch <= 0) return cudaSuccess;
   RowsArgs a{};
   a.logits = logits; a.n_rows = batch; a.vocab = vocab; a.stride = stride;
@@ -1412,9 +1700,21 @@ cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int b
   a.flat = 0;  // whole rows: the bound needs every thread maximum of the row
   a.state = state; a.hist = hist; a.small_run = small_run; a.gate = gate; a.max_seg = max_seg;
   a.thk = ws.thk; a.zmax = ws.zmax; a.topk = topk; a.ready_q = ws.ready_q; a.q_ctl = ws.q_ctl;
+  // the fused top-k draw: opt-in (RELAY_K4_FUSE=1).  Parity-green, but measured
+  // slower at configs[2] (49.6 vs 40.8 us per step: ~146 candidates per row
+  // make most warp-stages take the push path, and the epilogue's ranking and
+  // draw add ~8 us to the row's tail, profiles/r02/k4_fused_draw.txt)
+  if (draw) {
+    const char* e = getenv("RELAY_K4_FUSE");
+    a.fuse = e && !strcmp(e, "1");
+    a.s_c = draw->s_c; a.topp = draw->topp; a.uniform = draw->uniform; a.sampled_out = draw->sampled;
+    a.flag = draw->flag; a.cue_id = draw->cue_id;
+  }
   {  // tuning knob (RELAY_K4_L2 = last | normal | first): the L2 policy of the margin pass
+     // (K5 reads the rows again: all of them, or with the fused draw only the overflowed ones)
     const char* e = getenv("RELAY_K4_L2");
-    a.keep_l2 = (e && !strcmp(e, "normal")) ? 2 : (e && !strcmp(e, "first")) ? 0 : 1;
+    a.keep_l2 = (e && !strcmp(e, "normal")) ? 2 : (e && !strcmp(e, "first")) ? 0
+              : (e && !strcmp(e, "last")) ? 1 : (a.fuse ? 0 : 1);
   }
   return launch_rows<kModeStep>(dt, a, cs, st);
 }

@@ -162,10 +162,20 @@ cudaError_t launch_step_switch(const CueDev& cs, const void* logits, int dt, int
                                const StepWs& ws, cudaStream_t st);
 
 // relay_step_sample: K4 margin pass (rows kept in L2, top-k bound per row) ...
+// The sampler's parameters when K4 draws the token itself (relay_step_sample
+// with a top-k): log2(e) / temperature, top-p, the uniforms, the output.
+struct StepDraw {
+  float s_c;
+  float topp;
+  const float* uniform;
+  int* sampled;
+  uint8_t* flag;     // the switch's outputs (K4 runs it on the drawn token)
+  int16_t* cue_id;
+};
 cudaError_t launch_step_rows(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
                              long long stride, float iota, uint8_t* state, int* hist, int* small_run,
                              float gate, int max_seg, float* margin, int* top1, int* top2,
-                             const StepWs& ws, int topk, cudaStream_t st);
+                             const StepWs& ws, int topk, cudaStream_t st, const StepDraw* draw = nullptr);
 // ... then K5: exact top-k from L2, temperature / top-p, inverse-CDF draw, switch
 cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int batch, int vocab,
                                long long stride, float iota, float temperature, int topk, float topp,

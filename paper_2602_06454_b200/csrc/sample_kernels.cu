@@ -17,6 +17,7 @@
 
 #include "relay_device.cuh"
 #include "relay_internal.h"
+#include "draw.cuh"
 #include "switch.cuh"
 
 namespace relay {
@@ -338,38 +339,10 @@ __device__ __noinline__ int refine_topk(const typename E::T* row, int vocab, int
   return rank_list(topk, c + need, s_cv, s_ci, s_topv, s_topi, s_k);
 }
 
-// The drawn token (one warp; every lane returns it) from the top-K list, R20:
-// p_k = 2^((v_k - v_0) log2(e) / T); keep the first L (higher-ranked mass below
-// top_p of the total, at least one); inverse CDF with the row's uniform.  Lane
-// l holds ranks l and l + 32; prefix sums by warp scans, in rank order.
-__device__ int draw_warp(const SampleArgs& a, float u, int K, const float* s_topv,
-                         const int* s_topi, float total_mass = -1.0f) {
-  const int lane = threadIdx.x & 31;
-  const float v0 = s_topv[0];
-  const float p0 = lane < K ? ex2((s_topv[lane] - v0) * a.s_c) : 0.0f;
-  const float p1 = lane + 32 < K ? ex2((s_topv[lane + 32] - v0) * a.s_c) : 0.0f;
-  float c0 = p0, c1 = p1;  // inclusive prefix sums within each half
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const float t0 = __shfl_up_sync(kFull, c0, off);
-    const float t1 = __shfl_up_sync(kFull, c1, off);
-    if (lane >= off) { c0 += t0; c1 += t1; }
-  }
-  const float half0 = __shfl_sync(kFull, c0, 31);
-  c1 += half0;                                   // ranks 32..63 continue the sum
-  // the top-p reference mass: the top-K (R20), or the whole row (no top-k)
-  const float total = total_mass >= 0.0f ? total_mass : __shfl_sync(kFull, c1, 31);
-  // kept iff the mass of the higher ranks (exclusive prefix) is below top_p * total
-  const float lim = a.topp * total;
-  const unsigned keep0 = __ballot_sync(kFull, lane < K && (lane == 0 || c0 - p0 < lim));
-  const unsigned keep1 = __ballot_sync(kFull, lane + 32 < K && c1 - p1 < lim);
-  const int L = __popc(keep0) + __popc(keep1);   // kept ranks form a prefix
-  const float kept = L <= 32 ? __shfl_sync(kFull, c0, L - 1) : __shfl_sync(kFull, c1, L - 33);
-  const float target = u * kept;
-  const unsigned hit0 = __ballot_sync(kFull, lane < L && c0 > target);
-  const unsigned hit1 = __ballot_sync(kFull, lane + 32 < L && c1 > target);
-  const int k = hit0 ? __ffs(hit0) - 1 : (hit1 ? 32 + __ffs(hit1) - 1 : L - 1);
-  return s_topi[k];
+// The drawn token (one warp) from the top-K list: draw.cuh.
+__device__ __forceinline__ int draw_warp(const SampleArgs& a, float u, int K, const float* s_topv,
+                                         const int* s_topi, float total_mass = -1.0f) {
+  return draw_topk_warp(a.s_c, a.topp, u, K, s_topv, s_topi, total_mass);
 }
 
 // ---------------------------------------------------------------- nucleus
@@ -998,13 +971,17 @@ __global__ void __launch_bounds__(kSampleThreads, 2) sample_switch_kernel(Sample
           asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.ready_q + tk) : "memory");
         } while (v == 0);
         a.ready_q[tk] = 0;   // read again only by the next step (after this grid)
-        rr = v - 1;
+        rr = v > 0 ? v - 1 : -2;  // -(r + 1): K4 drew the row itself (fused top-k draw)
       }
       s_row = rr;
     }
     __syncthreads();
     const long long r = s_row;
-    if (r < 0) break;
+    if (r == -1) break;
+    if (r == -2) {
+      __syncthreads();  // s_row / s_cnt are rewritten by thread 0 next
+      continue;
+    }
     TRACE5(14);
     const T* row = static_cast<const T*>(a.logits) + r * a.stride;
     // warp 0's per-row inputs are fetched before the scan so that their
@@ -1168,9 +1145,11 @@ cudaError_t launch_step_sample(const CueDev& cs, const void* logits, int dt, int
                                cudaStream_t st) {
   if (batch <= 0) return cudaSuccess;
   // no top-k: K4 bounds the top kMaxTopK (the fast path's list)
+  // with a top-k K4 also draws each row (fused), K5 takes the rest
+  const StepDraw draw{kLog2e / temperature, topp, uniform, sampled, flag, cue_id};
   cudaError_t e = launch_step_rows(cs, logits, dt, batch, vocab, stride, iota, state, hist, small_run,
                                    gate, max_seg, margin, top1, top2, ws,
-                                   topk > 0 ? topk : min(kMaxTopK, vocab), st);
+                                   topk > 0 ? topk : min(kMaxTopK, vocab), st, topk > 0 ? &draw : nullptr);
   if (e != cudaSuccess) return e;
   SampleArgs a{};
   a.logits = logits; a.n_rows = batch; a.vocab = vocab; a.stride = stride;

@@ -1198,6 +1198,19 @@ def test_step_sample(relay, B, vocab, dtype, T, k, p):
         assert flags[b] == f and d_state[b].item() == st
 
 
+@pytest.mark.parametrize("B,vocab,dtype,T,k,p", [
+    (256, 152064, "bf16", 0.6, 20, 0.95),     # configs[2], Qwen3 sampling
+    (1000, 8192, "bf16", 0.6, 20, 0.95),      # rows per CTA > 1: both candidate lists alternate
+    (200, 32000, "f32", 1.0, 64, 1.0),        # top-k 64: lists overflow, rows go to K5
+    (37, 5003, "f16", 0.8, 5, 0.9),
+])
+def test_step_sample_fused_draw(relay, monkeypatch, B, vocab, dtype, T, k, p):
+    """The opt-in fused top-k draw in K4 (RELAY_K4_FUSE=1): the same checks as
+    test_step_sample (drawn tokens vs the oracle sampler, the switch on them)."""
+    monkeypatch.setenv("RELAY_K4_FUSE", "1")
+    test_step_sample(relay, B, vocab, dtype, T, k, p)
+
+
 def test_step_sample_pathological_rows(relay):
     """A constant row (every logit a candidate: the exact fallback), rows with
     -inf tails, a NaN row, and the distribution of draws on a constant row."""

@@ -40,9 +40,16 @@ def run(mode="step"):
     state = torch.zeros(B, dtype=torch.uint8, device=dev)
     hist = torch.full((B, 7), -1, dtype=torch.int32, device=dev)
     ws = relay.workspace(0, 0, B, dev)
+    small = torch.zeros(B, dtype=torch.int32, device=dev)
+    uni = torch.rand(B, device=dev)
+
+    def sample_step():
+        relay.step_sample(cs, L, uni, state, hist, small, temperature=0.6, top_k=20, top_p=0.95, ws=ws)
     for _ in range(3):
         if mode == "step":
             relay.step_switch(cs, L, state, hist, ws=ws)
+        elif mode == "sample":
+            sample_step()
         else:
             relay.margin_rows(L)
     torch.cuda.synchronize()
@@ -54,6 +61,9 @@ def run(mode="step"):
     if mode == "step":
         assert lib0.relay_debug_trace_reset(zero.ctypes.data_as(C.c_void_p), n) == 0
         relay.step_switch(cs, L, state, hist, ws=ws)
+    elif mode == "sample":
+        assert lib0.relay_debug_trace_reset(zero.ctypes.data_as(C.c_void_p), n) == 0
+        sample_step()
     else:
         assert lib0.relay_debug_trace_reset(zero.ctypes.data_as(C.c_void_p), n) == 0
         relay.margin_rows(L)
@@ -110,6 +120,12 @@ def run(mode="step"):
                 t = np.array(two)
                 print("SMs with two CTAs: %d, first exit p50 %.1f max %.1f, second exit p50 %.1f max %.1f" %
                       (len(two), np.median(t[:, 0]), t[:, 0].max(), np.median(t[:, 1]), t[:, 1].max()))
+        if mode == "sample":
+            d = rel[:, [1, 11, 14, 16, 20, 21, 22, 23, 24]]
+            names = ["stage1", "bound", "stage1 done", "cons end", "epi barrier", "merged", "pre-finish",
+                     "drawn", "epi end"]
+            print("sample-mode stamps p50 (us):", ", ".join("%s %.2f" % (nm, np.nanmedian(d[:, k]))
+                                                          for k, nm in enumerate(names)))
         print("last consumer item end: p50 %.1f p90 %.1f max %.1f | last epilogue end: p50 %.1f p90 %.1f max %.1f"
               % (*np.nanpercentile(last_c, [50, 90, 100]), *np.nanpercentile(last_e, [50, 90, 100])))
 

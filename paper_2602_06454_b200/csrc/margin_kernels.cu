@@ -69,6 +69,11 @@ extern "C" int relay_debug_fuse_stats(unsigned long long* host, int reset) {
 #define TRACE(k) ((void)0)
 #endif
 
+#ifndef RELAY_STEADY_UNROLL
+#define RELAY_STEADY_UNROLL 1
+#endif
+constexpr int kSteadyUnroll = RELAY_STEADY_UNROLL;  // steady-stage loop unroll (tuning)
+
 constexpr float kHuge = 268435456.0f;  // 2^28: beyond it fp32 y = z*c is too coarse
 
 struct ThreadState {
@@ -1343,6 +1348,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     }
     // steady state: per stage the wait, the words, one release, the terms and
     // one guard comparison (consume_fast)
+#pragma unroll kSteadyUnroll
     for (int k = 1; k < nst; ++k) {
       mbar_wait(full_s + 8 * stage, phase);
 #ifdef RELAY_TRACE

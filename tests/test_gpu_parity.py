@@ -188,6 +188,49 @@ def test_cue_scan_boundaries_and_empty_trajectories(relay):
         assert out["occ_pat"][:n].tolist() == ref["occ_pat"].tolist()
 
 
+def test_cue_scan_graph_replay_epochs(relay):
+    """K2's look-back words carry a per-launch epoch (no reset pass): a CUDA
+    graph replayed over in-place refilled token streams, and a run of eager
+    launches on the same workspace, give the oracle's occurrences every time."""
+    h, cs = _cs_pair(relay, 151936, 8, 12, 3, seed=131)
+    streams = [synth.make_tokens(3, 11000, h, seed=132 + i, cue_rate=0.3 + 0.2 * i) for i in range(4)]
+    n = streams[0].tokens.shape[0]
+    ws = relay.workspace(n, n, 0, DEV)
+    tok = torch.as_tensor(streams[0].tokens, device=DEV)
+    offs = torch.as_tensor(streams[0].traj_offsets, device=DEV)
+    out = relay.cue_scan(cs, tok, offs, n, ws=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(device=DEV)
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            relay.cue_scan(cs, tok, offs, n, ws=ws, out=out, stream=side)
+    torch.cuda.synchronize()
+
+    def check(ts):
+        ref = oracle.cue_scan(ts.tokens, ts.traj_offsets, h.pat_tokens, h.pat_offsets, h.pat_cue,
+                              h.n_cues, h.terminator, 0)
+        k = int(out["n_occ"].item())
+        assert k == ref["occ_pos"].shape[0]
+        np.testing.assert_array_equal(out["occ_pos"][:k].cpu().numpy(), ref["occ_pos"])
+        np.testing.assert_array_equal(out["occ_pat"][:k].cpu().numpy(), ref["occ_pat"])
+
+    for rep in range(8):
+        ts = streams[rep % 4]
+        tok.copy_(torch.as_tensor(ts.tokens, device=DEV))
+        g.replay()
+        torch.cuda.synchronize()
+        check(ts)
+    for rep in range(40):   # eager launches on the same workspace advance the epoch further
+        ts = streams[rep % 4]
+        tok.copy_(torch.as_tensor(ts.tokens, device=DEV))
+        relay.cue_scan(cs, tok, offs, n, ws=ws, out=out)
+        if rep % 9 == 0:
+            torch.cuda.synchronize()
+            check(ts)
+    cs.destroy()
+
+
 def test_cue_scan_capacity_overflow(relay):
     h, cs = _cs_pair(relay, 4096, 3, 3, 2, seed=3)
     ts = synth.make_tokens(1, 20000, h, cue_rate=0.9)

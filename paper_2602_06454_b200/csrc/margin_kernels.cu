@@ -897,12 +897,20 @@ __device__ __forceinline__ bool fetch_item(const RowsArgs& a, ItemIter<SPLIT>& i
 constexpr int kSlots = 4;
 
 
-template <class E, int NCW, int NS, int UV, int MINB, int MODE, int SPLIT, bool FUSE = false>
+template <class E, int NCW, int NS, int UV, int MINB, int MODE, int SPLIT, bool FUSE = false, int NG = 1>
 __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, CueDev cs) {
   using T = typename E::T;
   constexpr int VEC = 16 / E::SZ;          // elements per 16-byte vector
   constexpr int NCT = NCW * 32;             // consumer threads
-  constexpr int SB = UV * NCT * 16;         // bytes per ring stage
+  // NG consumer groups (K4 with more rows than SMs: one CTA per SM streams
+  // its rows b and b + grid CONCURRENTLY, one group each, so an SM's two rows
+  // finish together instead of one CTA of a co-resident pair being starved
+  // of issue slots and HBM share until the other is done); each group has
+  // its own ring of NS stages, its own barriers and its own items
+  static_assert(NG == 1 || (NG == 2 && SPLIT == 0 && !FUSE && NCW % 2 == 0), "consumer groups");
+  constexpr int NCWG = NCW / NG;            // consumer warps per group
+  constexpr int NCTG = NCWG * 32;           // consumer threads per group
+  constexpr int SB = UV * NCTG * 16;        // bytes per ring stage (one group's)
   // partials handed to the epilogue per consumer warp: 8 after two shuffle
   // rounds (K1: the epilogue is off the critical path), 1 after a full warp
   // reduction (K4: the epilogue is the tail of a ~30 us kernel)
@@ -912,8 +920,8 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   // kBarRing0 + s ring stage s released (consumers arrive, the producer warp
   // syncs), kBarRed0 + k reduction slot k filled (consumers arrive, the
   // epilogue warp syncs)
-  constexpr int kBarRing0 = 2;
-  constexpr int kBarRed0 = kBarRing0 + NS;
+  constexpr int kBarRing0 = 2;              // + g * NS + s: group g's stage s
+  constexpr int kBarRed0 = kBarRing0 + NG * NS;
   // SPLIT: the work-split modes that cut rows across CTAs (K4 small batches
   // and tuning modes); the whole-row instantiations carry none of that code
   const int fmode = flat_mode<SPLIT>(a);  // compile-time constant unless SPLIT == 2
@@ -921,7 +929,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   static_assert(kBarRed0 + kSlots <= 16, "named barriers");
   static_assert(!FUSE || NCW * kFuseSeed <= 96, "fuse_bound holds three seeds per lane");
   extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ __align__(8) uint64_t full[NS];
+  __shared__ __align__(8) uint64_t full[NG * NS];
   __shared__ __align__(8) uint64_t red_empty[kSlots];
   __shared__ __align__(8) uint64_t ifull[kSlots];
   __shared__ long long s_item[kSlots];
@@ -969,7 +977,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     // Every consumer thread arrives on `empty` after its own shared-memory reads
     // and on `red_full` after its last threshold read / partial write, so each
     // thread's accesses are released to the TMA producer / epilogue warp.
-    for (int s = 0; s < NS; s++) {
+    for (int s = 0; s < NG * NS; s++) {
       mbar_init(full_s + 8 * s, 1);
     }
     for (int s = 0; s < kSlots; s++) {
@@ -1062,6 +1070,61 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         issue(ItemIter<SPLIT>::from_k(a, k));
         k = kn;
       }
+    } else if constexpr (NG > 1) {
+      // groups: group g streams rows b + (g + k NG) grid; one stage per group
+      // in turn (each group's stages land in its own ring)
+      if constexpr (MODE == kModeStep) pdl_wait();
+      long long gr[NG];
+      int goff[NG], gbody[NG], gstage[NG];
+      long long gn[NG];
+      const char* gsrc[NG];
+      auto open = [&](int g) {
+        for (; gr[g] < a.n_rows; gr[g] += static_cast<long long>(NG) * gridDim.x) {
+          const T* row = logits + gr[g] * a.stride;
+          const Geom ge = row_geom<E>(row, 0, a.vocab);
+          if (ge.body == 0) continue;  // scalars only: nothing to stream
+          gsrc[g] = reinterpret_cast<const char*>(row + ge.head);
+          gbody[g] = ge.body;
+          goff[g] = 0;
+          return;
+        }
+      };
+#pragma unroll
+      for (int g = 0; g < NG; g++) {
+        gr[g] = blockIdx.x + static_cast<long long>(g) * gridDim.x;
+        gstage[g] = 0;
+        gn[g] = 0;
+        open(g);
+      }
+      for (bool any = true; any;) {
+        any = false;
+#pragma unroll
+        for (int g = 0; g < NG; g++) {
+          if (gr[g] >= a.n_rows) continue;
+          any = true;
+          const uint32_t bytes = static_cast<uint32_t>(min(SB, gbody[g] - goff[g]));
+          const int st = gstage[g];
+          if (gn[g] >= NS) named_bar(kBarRing0 + g * NS + st, NCTG + 32);
+          if (lane == 0) {
+            const uint32_t fb = full_s + 8 * (g * NS + st);
+            fence_proxy_async_smem();
+            mbar_expect_tx(fb, bytes);
+            bulk_g2s(ring_s + (g * NS + st) * SB, gsrc[g] + goff[g], bytes, fb, pol);
+          }
+          ++gn[g];
+          if (++gstage[g] == NS) gstage[g] = 0;
+          goff[g] += SB;
+          if (goff[g] >= gbody[g]) {
+            gr[g] += static_cast<long long>(NG) * gridDim.x;
+            open(g);
+          }
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < NG; g++)
+        for (long long k = gn[g] > NS ? gn[g] - NS : 0; k < gn[g]; ++k)
+          named_bar(kBarRing0 + g * NS + static_cast<int>(k % NS), NCTG + 32);
+      return;
     } else {
       ItemIter<SPLIT> iter;
       iter.init(a);
@@ -1102,11 +1165,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       const float fu = fuse ? a.uniform[r] : 0.0f;
       // the consumers' partials: a named barrier (a spinning epilogue warp took
       // issue slots from the consumers for the whole row, 0.45 per element)
-      named_bar(kBarRed0 + slot, NCT + 32);
+      named_bar(kBarRed0 + slot, NCTG + 32);  // the item's group
       if (lane == 0 && it == 0) TRACE(20);
       Partial q = partial_empty();
 #pragma unroll
-      for (int e = lane; e < NRED; e += 32) q = partial_merge(q, s_red[slot][e]);
+      for (int e = lane; e < NCWG * RPW; e += 32) q = partial_merge(q, s_red[slot][e]);
       // full butterfly: every lane ends with the merged partial (the switch
       // below reads the row's top-1 on all lanes)
       q = warp_merge_all(q);
@@ -1114,7 +1177,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       float thk = INFINITY;
       if (a.thk) {
 #pragma unroll
-        for (int w = 0; w < NCW; w++) thk = fminf(thk, s_thk[slot][w]);
+        for (int w = 0; w < NCWG; w++) thk = fminf(thk, s_thk[slot][w]);
       }
       if (lane == 0) s_theta[slot] = fkey(-INFINITY);  // for item it + kSlots
       if (!fuse) mbar_arrive(rempty_s + 8 * slot);  // (fused draw: after the list is read)
@@ -1257,27 +1320,44 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #ifdef RELAY_TRACE
   int n_stage = 0;
 #endif
+  // this warp's group: its ring, its stage barriers, its items it = grp, grp + NG, ...
+  const int grp = NG > 1 ? warp / NCWG : 0;
+  const int ctid = tid - grp * NCTG;       // thread index within the group
+  const int cwarp = warp - grp * NCWG;     // warp index within the group
+  const uint32_t gring = ring_s + static_cast<uint32_t>(grp * NS * SB);
+  const uint32_t gfull = full_s + static_cast<uint32_t>(8 * grp * NS);
+  const int gbar = kBarRing0 + grp * NS;
   int stage = 0;        // ring position, carried across items
   uint32_t phase = 0;
-  const uint32_t ring_t = ring_s + static_cast<uint32_t>(tid) * 16;  // this thread's first vector of stage 0
+  const uint32_t ring_t = gring + static_cast<uint32_t>(ctid) * 16;  // this thread's first vector of stage 0
   ItemIter<SPLIT> iter;
   iter.init(a);
   Item item;
-  for (int it = 0; fetch_item(a, iter, it, kSlots, s_item, ifull_s, item); ++it) {
+  auto next_item = [&](int it) -> bool {
+    if constexpr (NG == 1) {
+      return fetch_item(a, iter, it, kSlots, s_item, ifull_s, item);
+    } else {  // strided whole rows: item it is row blockIdx + it * grid
+      const long long r = blockIdx.x + static_cast<long long>(it) * gridDim.x;
+      if (r >= a.n_rows) return false;
+      item = Item{r, 0, a.vocab, 0, 1};
+      return true;
+    }
+  };
+  for (int it = grp; next_item(it); it += NG) {
     const int slot = it % kSlots;
     const long long r = item.r;
     const int j0 = item.j0;
     const int j1 = item.j1;
-    if (tid == 0 && it == 1) TRACE(11);
+    if (ctid == 0 && it == 1) TRACE(11);
     // the slot (threshold + partials) is free once the epilogue took item it - kSlots
     mbar_wait(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
-    if (tid == 0 && it == 1) TRACE(12);
+    if (ctid == 0 && it == 1) TRACE(12);
     const uint32_t theta_p = theta_s + 4 * slot;
     const T* row = logits + r * a.stride;
     const Geom g = row_geom<E>(row, j0, j1);
     const int nst = g.body / SB;             // full ring stages of the item
     const int rem = g.body - nst * SB;       // bytes of its last, partial stage
-    const int jt = j0 + g.head + tid * VEC;  // element index of this thread's first vector
+    const int jt = j0 + g.head + ctid * VEC;  // element index of this thread's first vector
     ThreadState st;
     state_init(st);
     float theta_w = -INFINITY;  // warp-local lower bound of the row's 2nd-best
@@ -1290,13 +1370,13 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     const int fb = it & 1;
     float fB = -INFINITY;
     if (fuse && it >= 2) mbar_wait(rempty_s + 8 * ((it - 2) % kSlots), ((it - 2) / kSlots) & 1);
-    if (tid < g.head) {
-      const float x = E::load1(row + j0 + tid);
-      consume_scalar(x, j0 + tid, st, c);
+    if (ctid < g.head) {
+      const float x = E::load1(row + j0 + ctid);
+      consume_scalar(x, j0 + ctid, st, c);
       if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, x);
       if (fuse && x > -INFINITY) {  // (NaN fails the test)
         const int p = atomicAdd(&s_fcnt[fb], 1);
-        if (p < kFuseCap) { s_fv[fb][p] = x; s_fi[fb][p] = j0 + tid; }
+        if (p < kFuseCap) { s_fv[fb][p] = x; s_fi[fb][p] = j0 + ctid; }
       }
     }
     if (nst > 0) {
@@ -1306,25 +1386,25 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       // no barrier: each warp goes on with its own bound and whatever the
       // others have published (any of them is a valid lower bound), so the
       // steady state starts mostly on the fast path without a CTA-wide wait.
-      mbar_wait(full_s + 8 * stage, phase);
+      mbar_wait(gfull + 8 * stage, phase);
 #ifdef RELAY_TRACE
-      if (tid == 0 && n_stage < 10) TRACE(1 + n_stage);
+      if (ctid == 0 && n_stage < 10) TRACE(1 + n_stage);
       ++n_stage;
 #endif
       uint4 raw[UV];
 #pragma unroll
-      for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCT * 16);
-      bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);  // release: the loads precede the refill
+      for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCTG * 16);
+      bar_arrive_pinned<UV>(gbar + stage, NCTG + 32, raw);  // release: the loads precede the refill
       const float2 h = stage_max2<E, UV>(raw);
       theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
 #ifdef RELAY_PROBE_BAR
       named_bar(1, NCT);  // tuning: wait for every warp's probe (r02: 1.5% slower without gain)
 #endif
-      if (tid == 0 && it == 1) TRACE(13);
+      if (ctid == 0 && it == 1) TRACE(13);
       tkey = theta_load(theta_p);
       const float theta = fmaxf(theta_w, unkey(tkey));
       bool slow = false;
-      consume_stage<E, UV>(raw, h, jt, NCT * VEC, st, c, theta, slow);
+      consume_stage<E, UV>(raw, h, jt, NCTG * VEC, st, c, theta, slow);
       if (__any_sync(kFull, slow)) theta_w = fmaxf(theta_w, theta_raise(warp_second(st.t.v1, st.t.v2), theta_p));
       T = guard_T(fmaxf(theta, theta_w), st, c);
       if constexpr (MODE == kModeStep) {
@@ -1335,31 +1415,31 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           fuse_seeds(h, s_seed[fb] + warp * kFuseSeed);
           named_bar(1, NCT);
           fB = fuse_bound(s_seed[fb], NCW * kFuseSeed, a.topk);
-          if (tid == 0 && it == 0) TRACE(11);
+          if (ctid == 0 && it == 0) TRACE(11);
           if (lane == 0) atomicMax(&s_fbk[fb], fkey(fB));
           if (__any_sync(kFull, fmaxf(h.x, h.y) >= fB)) {
-            const bool x = fuse_push<E, UV>(raw, UV, jt, NCT * VEC, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
+            const bool x = fuse_push<E, UV>(raw, UV, jt, NCTG * VEC, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
             if (__any_sync(kFull, x)) fuse_raise(s_fv[fb], a.topk, &s_fbk[fb]);
           }
         }
       }
-      if (tid == 0 && it <= 1) TRACE(14);
+      if (ctid == 0 && it <= 1) TRACE(14);
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     // steady state: per stage the wait, the words, one release, the terms and
     // one guard comparison (consume_fast)
 #pragma unroll kSteadyUnroll
     for (int k = 1; k < nst; ++k) {
-      mbar_wait(full_s + 8 * stage, phase);
+      mbar_wait(gfull + 8 * stage, phase);
 #ifdef RELAY_TRACE
-      if (tid == 0 && n_stage < 10) TRACE(1 + n_stage);
+      if (ctid == 0 && n_stage < 10) TRACE(1 + n_stage);
       ++n_stage;
 #endif
       const int key = theta_load(theta_p);  // before the words: its latency hides under the sum
       uint4 raw[UV];
 #pragma unroll
-      for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCT * 16);
-      bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
+      for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCTG * 16);
+      bar_arrive_pinned<UV>(gbar + stage, NCTG + 32, raw);
       if constexpr (MODE == kModeStep) {
         // (before the terms: the words are dead after consume_fast)
         if (a.topk > 0) {
@@ -1368,29 +1448,29 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
           if (fuse) {
             fB = fmaxf(fB, unkey(*reinterpret_cast<volatile int*>(&s_fbk[fb])));  // raised by any warp
             if (__any_sync(kFull, fmaxf(h.x, h.y) >= fB)) {
-              const bool x = fuse_push<E, UV>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, fB, s_fv[fb], s_fi[fb],
+              const bool x = fuse_push<E, UV>(raw, UV, jt + k * (SB / E::SZ), NCTG * VEC, fB, s_fv[fb], s_fi[fb],
                                               &s_fcnt[fb]);
               if (__any_sync(kFull, x)) fuse_raise(s_fv[fb], a.topk, &s_fbk[fb]);
             }
           }
         }
       }
-      consume_fast<E, UV, kPolyPairs>(raw, UV, jt + k * (SB / E::SZ), NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
+      consume_fast<E, UV, kPolyPairs>(raw, UV, jt + k * (SB / E::SZ), NCTG * VEC, st, c, T, tkey, theta_w, key, theta_p);
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
     if (rem > 0) {
-      mbar_wait(full_s + 8 * stage, phase);
-      const uint32_t buf = ring_s + stage * SB;
+      mbar_wait(gfull + 8 * stage, phase);
+      const uint32_t buf = gring + stage * SB;
       const int jb = j0 + g.head + nst * (SB / E::SZ);
       if (nst > 0) {
         // the last, partial stage: the missing vectors read as -inf (no term,
         // never pushed)
         const int key = theta_load(theta_p);
-        const int nvalid = min(UV, max(0, (rem / 16 - tid + NCT - 1) / NCT));
+        const int nvalid = min(UV, max(0, (rem / 16 - ctid + NCTG - 1) / NCTG));
         uint4 raw[UV];
 #pragma unroll
-        for (int u = 0; u < UV; u++) raw[u] = u < nvalid ? lds128(ring_t + stage * SB + u * NCT * 16) : E::neg_inf16();
-        bar_arrive_pinned<UV>(kBarRing0 + stage, NCT + 32, raw);
+        for (int u = 0; u < UV; u++) raw[u] = u < nvalid ? lds128(ring_t + stage * SB + u * NCTG * 16) : E::neg_inf16();
+        bar_arrive_pinned<UV>(gbar + stage, NCTG + 32, raw);
         if constexpr (MODE == kModeStep) {
           if (a.topk > 0) {
             const float2 h = stage_max2<E, UV>(raw);
@@ -1398,16 +1478,16 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
             if (fuse) {
               fB = fmaxf(fB, unkey(*reinterpret_cast<volatile int*>(&s_fbk[fb])));
               if (__any_sync(kFull, fmaxf(h.x, h.y) >= fB))
-                fuse_push<E, UV>(raw, nvalid, jb + tid * VEC, NCT * VEC, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
+                fuse_push<E, UV>(raw, nvalid, jb + ctid * VEC, NCTG * VEC, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
             }
           }
         }
-        consume_fast<E, UV, kPolyPairs>(raw, nvalid, jb + tid * VEC, NCT * VEC, st, c, T, tkey, theta_w, key, theta_p);
+        consume_fast<E, UV, kPolyPairs>(raw, nvalid, jb + ctid * VEC, NCTG * VEC, st, c, T, tkey, theta_w, key, theta_p);
       } else {  // a row shorter than one stage: vector by vector, max-guarded
         const float theta = fmaxf(theta_w, unkey(theta_load(theta_p)));
         const int nvec = rem / 16;
         bool slow = false;
-        for (int v = tid; v < nvec; v += NCT) {
+        for (int v = ctid; v < nvec; v += NCTG) {
           const uint4 raw1[1] = {lds128(buf + v * 16)};
           const float2 h1 = stage_max2<E, 1>(raw1);
           consume_stage<E, 1>(raw1, h1, jb + v * VEC, 0, st, c, theta, slow);
@@ -1416,24 +1496,24 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
             if (fuse) fuse_push<E, 1>(raw1, 1, jb + v * VEC, 0, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
           }
         }
-        bar_arrive(kBarRing0 + stage, NCT + 32);
+        bar_arrive(gbar + stage, NCTG + 32);
       }
       if (++stage == NS) { stage = 0; phase ^= 1; }
     }
-    if (tid < j1 - g.tail) {
-      const float x = E::load1(row + g.tail + tid);
-      consume_scalar(x, g.tail + tid, st, c);
+    if (ctid < j1 - g.tail) {
+      const float x = E::load1(row + g.tail + ctid);
+      consume_scalar(x, g.tail + ctid, st, c);
       if constexpr (MODE == kModeStep) tmax = fmaxf(tmax, x);
       if (fuse && x >= fB && x > -INFINITY) {
         const int p = atomicAdd(&s_fcnt[fb], 1);
-        if (p < kFuseCap) { s_fv[fb][p] = x; s_fi[fb][p] = g.tail + tid; }
+        if (p < kFuseCap) { s_fv[fb][p] = x; s_fi[fb][p] = g.tail + ctid; }
       }
     }
     if (a.topk > 0) {
       // N2: the warp's kw-th largest thread maximum, kw = ceil(topk / NCW);
       // the minimum over warps bounds the row's topk-th largest value from
       // below (NCW * kw >= topk distinct elements are at least as large)
-      const int kw = (a.topk + NCW - 1) / NCW;
+      const int kw = (a.topk + NCWG - 1) / NCWG;
       float v = tmax, kth = -INFINITY;
       for (int i = 0; i < kw; i++) {
         float m = v;
@@ -1443,7 +1523,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         const unsigned holders = __ballot_sync(kFull, v == m);
         if (lane == __ffs(holders) - 1) v = -INFINITY;
       }
-      if (lane == 0) s_thk[slot][warp] = kth;
+      if (lane == 0) s_thk[slot][cwarp] = kth;
     }
     // hand the warp's 8 partials (after two shuffle rounds) to the epilogue warp
     Partial p = thread_partial(st);
@@ -1453,11 +1533,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
 #pragma unroll
       for (int off = 16; off >= RPW; off >>= 1) p = partial_merge(p, shfl_xor_partial(p, off));
     }
-    if (lane < RPW) s_red[slot][warp * RPW + lane] = p;
-    bar_arrive(kBarRed0 + slot, NCT + 32);
-    if (tid == 0 && it < 8) TRACE(16 + it);
+    if (lane < RPW) s_red[slot][cwarp * RPW + lane] = p;
+    bar_arrive(kBarRed0 + slot, NCTG + 32);
+    if (ctid == 0 && it < 8) TRACE(16 + it);
   }
-  if (tid == 0) TRACE(31);
+  if (ctid == 0) TRACE(31);
 }
 
 static int g_num_sms = 0;
@@ -1528,8 +1608,55 @@ static int k4_chunk_stages() {
   return x > 0 ? x : 4;
 }
 
+// K4 with more rows than SMs, opt-in (RELAY_K4_GROUPS=1): one CTA per SM,
+// two consumer groups of 12 warps streaming rows b and b + grid concurrently
+// (rows_kernel NG = 2).  Measured slower than two CTAs per SM (19.6 vs 18.8
+// us at configs[2]): an SM's two rows end at ~16 us either way (its HBM
+// share and the exp rate at ~71% of MUFU peak bound it), and the shared
+// producer / epilogue warps add to the tail (profiles/r02/k4_tail.txt).
+#ifndef RELAY_K4_GROUP_NCW
+#define RELAY_K4_GROUP_NCW 24
+#endif
+static bool k4_groups() {
+  const char* e = getenv("RELAY_K4_GROUPS");
+  return e && !strcmp(e, "1");
+}
+
+template <class E>
+static cudaError_t launch_step_groups(RowsArgs a, const CueDev& cs, cudaStream_t st) {
+  constexpr int NCW = RELAY_K4_GROUP_NCW, NS = kStepStages, UV = kStepUV;
+  auto kern = rows_kernel<E, NCW, NS, UV, 1, kModeStep, 0, false, 2>;
+  const int smem = NS * UV * NCW * 32 * 16;  // two rings of NS stages
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCW + 2) * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    if (getenv("RELAY_DEBUG_LAUNCH"))
+      fprintf(stderr, "relay rows_kernel K4 groups: %d CTAs/SM, smem %d B dynamic\n", per_sm, smem);
+  }
+  long long grid = static_cast<long long>(per_sm) * num_sms();
+  if (grid > a.n_rows) grid = a.n_rows;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3((NCW + 2) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, cs);
+}
+
 template <class E, int MODE>
 static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) {
+  if constexpr (MODE == kModeStep) {
+    if (a.flat == 0 && !a.fuse && a.n_rows > num_sms() && k4_groups()) return launch_step_groups<E>(a, cs, st);
+  }
   // K4 runs ~1-2 CTAs per SM: a deeper ring keeps more bytes in flight per CTA
   constexpr int NS = (MODE == kModeStep) ? kStepStages : kStages;
   constexpr int MINB = (MODE == kModeStep) ? kStepMinBlocks : kMinBlocks;

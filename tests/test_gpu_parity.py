@@ -1076,13 +1076,17 @@ def test_stats_allreduce_torch_comm(relay, tmp_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["strided", "flat", "dynamic", "hybrid", "cluster"])
+@pytest.mark.parametrize("mode", ["strided", "flat", "dynamic", "hybrid", "cluster", "groups"])
 @pytest.mark.parametrize("B,vocab,dtype", [(256, 152064, "bf16"), (37, 5003, "f16"), (300, 32000, "f32")])
 def test_step_switch_work_split_modes(relay, monkeypatch, mode, B, vocab, dtype):
     """K4's work splits (whole rows per CTA; equal flat slices merged by the
     last arriver; dynamic chunks; hybrid: one whole row per SM plus equal
-    slices of the rest) all match the oracle, including graph replays that
-    rely on the self-resetting counters."""
+    slices of the rest; groups: one CTA per SM streaming two rows at once)
+    all match the oracle, including graph replays that rely on the
+    self-resetting counters."""
+    if mode == "groups":
+        monkeypatch.setenv("RELAY_K4_GROUPS", "1")
+        mode = "strided"
     monkeypatch.setenv("RELAY_K4_MODE", mode)
     for greedy in (False, True):    # greedy: the switch reads the row's top-1 on every lane
         test_step_switch(relay, greedy, B, vocab, dtype, 0, -1.0)

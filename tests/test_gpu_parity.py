@@ -87,6 +87,47 @@ def test_margin_rows_edge_rows(relay, dtype):
     assert got["margin"][8] == 0.0 and got["top1"][8] == 0 and got["top2"][8] == 1
 
 
+@pytest.mark.parametrize("groups", ["0", "1"])
+def test_step_switch_edge_rows(relay, monkeypatch, groups):
+    """K4 (whole rows, redux.sync merges of the warps' partials) on the K1
+    edge rows -- NaN, +-inf, all -inf, one finite, uniform, +-0 ties, exact
+    top-1 / top-2 ties at the row ends, ascending / descending, subnormal,
+    huge -- replicated past the SM count, two-CTA and grouped layouts."""
+    monkeypatch.setenv("RELAY_K4_GROUPS", groups)
+    V = 5000
+    z = torch.randn(V, generator=torch.Generator().manual_seed(7)) * 2
+    rows = [z.clone()]
+    r = z.clone(); r[17] = float("nan"); rows.append(r)
+    r = z.clone(); r[4000] = float("inf"); rows.append(r)
+    rows.append(torch.full((V,), float("-inf")))
+    r = torch.full((V,), float("-inf")); r[1234] = 3.0; rows.append(r)
+    rows.append(torch.zeros(V))
+    rows.append(torch.full((V,), -0.0))
+    r = torch.zeros(V); r[::2] = -0.0; rows.append(r)
+    r = torch.zeros(V); r[1::2] = -0.0; rows.append(r)
+    r = z.clone(); r[100] = 50.0; r[4999] = 50.0; rows.append(r)
+    r = z.clone(); r[3] = 50.0; r[7] = 40.0; r[4998] = 40.0; rows.append(r)
+    r = torch.arange(V, dtype=torch.float32) * 1e-3; rows.append(r)
+    r = -torch.arange(V, dtype=torch.float32) * 1e-3; rows.append(r)
+    r = torch.full((V,), 1e-40); r[5] = 2e-40; r[6] = 2e-40; rows.append(r)
+    r = z.clone() * 1e30; rows.append(r)
+    B = 3 * len(rows) + 200      # > the SM count: the two-rows-per-SM layouts
+    L = torch.stack([rows[b % len(rows)] for b in range(B)]).to(torch.bfloat16).to(DEV)
+    h, cs = _cs_pair(relay, V, 2, 4, 2, seed=61)
+    state = torch.zeros(B, dtype=torch.uint8, device=DEV)
+    hist = torch.full((B, 7), -1, dtype=torch.int32, device=DEV)
+    out = relay.step_switch(cs, L, state, hist)
+    torch.cuda.synchronize()
+    ref = oracle.margin_rows(synth.host_rows(L, "bf16"), dtype="bf16", vocab=V, threads=8)
+    np.testing.assert_array_equal(out["top1"].cpu().numpy(), ref["top1"])
+    np.testing.assert_array_equal(out["top2"].cpu().numpy(), ref["top2"])
+    ok = ref["status"] == 0
+    m = out["margin"].cpu().numpy()
+    assert np.all(np.isnan(m[~ok]))
+    assert np.abs(m[ok] - ref["margin"][ok]).max() < TOL
+    cs.destroy()
+
+
 def test_margin_rows_temperature(relay):
     L = synth.make_logits(64, 3000, "bf16", seed=5, device=DEV)
     _rows_check(relay, L, "bf16", 3000, iota=1.0 / 0.6)

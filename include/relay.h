@@ -287,7 +287,8 @@ relay_status_t relay_workspace_release(void* ws);
  *                exceeds occ_capacity (then only the first occ_capacity are
  *                written; the caller checks after synchronising).
  * Errors: RELAY_ERR_INVALID (NULL cs/tokens/term_bits/n_occ, n_tok < 0 or
- * >= 2^31, n_traj < 1 with offsets, occ_capacity < 0, occ_pos/occ_pat NULL
+ * >= 2^31, n_tok x cues >= 2^34 with match_mode 1 ALL (K2's look-back counts;
+ * never reached in LONGEST), n_traj < 1 with offsets, occ_capacity < 0, occ_pos/occ_pat NULL
  * with occ_capacity > 0); RELAY_ERR_WORKSPACE. */
 relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t n_tok,
                               const int64_t* traj_offsets, int32_t n_traj, uint32_t* term_bits,

@@ -435,6 +435,10 @@ relay_status_t relay_cue_scan(relay_cueset_t cs, const int32_t* tokens, int64_t 
   ScanWs w;
   s = ws_scan(ws, ws_bytes, n_tok, &w);
   if (s != RELAY_OK) return s;
+  // K2's look-back words hold occurrence counts below 2^34 (at most one per
+  // start in LONGEST mode, one per start and cue in ALL mode)
+  if (n_tok * (cs->dev.mode == 0 ? 1LL : static_cast<long long>(cs->dev.n_cues)) >= (1LL << 34))
+    return fail(RELAY_ERR_INVALID, "n_tok x cues must stay below 2^34 (K2's look-back counts)");
   return cuda_status(launch_cue_scan(cs->dev, tokens, n_tok, reinterpret_cast<const long long*>(traj_offsets),
                                      traj_offsets ? n_traj : 1, term_bits, occ_pos, occ_pat, occ_capacity,
                                      reinterpret_cast<long long*>(n_occ), w,

@@ -132,13 +132,34 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned l
 // pattern is then AND_k funnelshift(W_{d_k}, k) — bit s set iff it matches
 // at start b + s.  Per-length room masks likewise (bit s: >= L tokens left in
 // the start's trajectory).
+// Shared-memory accesses by 32-bit shared-window addresses computed once per
+// CTA (generic pointers into the dynamic array made the compiler re-derive
+// the window base from SR_CgaCtaId, an S2R, before every access of the
+// pattern loop: ~450 cycles per pattern, 2.8 us of K2's 4 us match phase).
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint2 v) {
+  asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 template <bool CLS>
-__device__ __forceinline__ void group_words(const CueDev& cs, const int* dist, int nd, int lo, int hi, int room8,
-                                            uint2* w, unsigned* rm) {
+__device__ __forceinline__ void group_words(const CueDev& cs, uint32_t dist_a, int nd, int lo, int hi, int room8,
+                                            uint32_t w_a, uint32_t rm_a) {
   const int lane = threadIdx.x & 31;
 #pragma unroll 4
   for (int d = 0; d < nd; d++) {
-    const int e = dist[d];
+    const int e = static_cast<int>(lds32(dist_a + 4 * d));
     bool x, y;
     if constexpr (CLS) {
       x = elem_ok(cs, lo, e);
@@ -149,25 +170,29 @@ __device__ __forceinline__ void group_words(const CueDev& cs, const int* dist, i
     }
     const unsigned a = __ballot_sync(kFull, x);
     const unsigned b = __ballot_sync(kFull, y);
-    if (lane == 0) w[d] = make_uint2(a, b);
+    if (lane == 0) sts64(w_a + 8 * d, make_uint2(a, b));
   }
 #pragma unroll
   for (int L = 1; L <= kMaxLen; L++) {
     const unsigned r = __ballot_sync(kFull, room8 >= L);
-    if (lane == 0) rm[L] = r;
+    if (lane == 0) sts32(rm_a + 4 * L, r);
   }
   __syncwarp();
 }
 
-__device__ __forceinline__ unsigned pattern_starts(const int* eidx, int L, const uint2* w, const unsigned* rm) {
-  unsigned m = rm[L];
+// Bit s: the pattern (its element word indices at pe_a, L of them) matches at
+// start b + s with room.  Branch-free: all kMaxLen index loads, then all word
+// loads, in flight together (entries past L read word 0 and are masked off).
+__device__ __forceinline__ unsigned pattern_starts(uint32_t pe_a, int L, uint32_t w_a, uint32_t rm_a) {
+  unsigned m = lds32(rm_a + 4 * L);
+  uint32_t e[kMaxLen];
 #pragma unroll
-  for (int k = 0; k < kMaxLen; k++) {
-    if (k < L) {
-      const uint2 v = w[eidx[k]];
-      m &= __funnelshift_r(v.x, v.y, k);
-    }
-  }
+  for (int k = 0; k < kMaxLen; k++) e[k] = lds32(pe_a + 4 * k);
+  uint2 v[kMaxLen];
+#pragma unroll
+  for (int k = 0; k < kMaxLen; k++) v[k] = lds64(w_a + 8 * (k < L ? e[k] : 0u));
+#pragma unroll
+  for (int k = 0; k < kMaxLen; k++) m &= k < L ? __funnelshift_r(v[k].x, v[k].y, k) : ~0u;
   return m;
 }
 
@@ -223,8 +248,10 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   const long long room = (t < n_tok && t >= cur_beg) ? cur_end - t : 0;
   TRACE2(1);
-  uint2* const ww = s_w_dyn + warp * nd;
-  unsigned* const wrm = s_rm[warp];
+  const uint32_t ww = smem_u32_pinned(s_w_dyn) + static_cast<uint32_t>(8 * warp * nd);
+  const uint32_t wrm = smem_u32_pinned(s_rm[warp]);
+  const uint32_t dist_a = smem_u32_pinned(s_dist);
+  const uint32_t eidx_a = smem_u32_pinned(s_eidx);
   // ---- phase 1: match, terminator words, per-warp counts
   int wcount = 0;
   if (b < n_tok) {
@@ -242,7 +269,13 @@ __global__ void __launch_bounds__(kScanThreads)
     const unsigned tw = __ballot_sync(kFull, term);
     if (lane == 0) term_bits[b >> 5] = tw;
     __syncwarp();   // the previous group's words are read by every lane before they are overwritten
-    group_words<CLS>(cs, s_dist, nd, lo, hi, static_cast<int>(room < kMaxLen ? room : kMaxLen), ww, wrm);
+#ifdef RELAY_TRACE
+    if (threadIdx.x == 0) stamp2(10);
+#endif
+    group_words<CLS>(cs, dist_a, nd, lo, hi, static_cast<int>(room < kMaxLen ? room : kMaxLen), ww, wrm);
+#ifdef RELAY_TRACE
+    if (threadIdx.x == 0) stamp2(11);
+#endif
     if (cs.mode == 0) {
       unsigned claimed = 0;
       int best = -1;
@@ -250,18 +283,21 @@ __global__ void __launch_bounds__(kScanThreads)
       for (int p = 0; p < cs.n_pat; p++) {
         const int L = sp.len[p];
         // bit s: start b + s matches and has >= L tokens left in its trajectory
-        const unsigned w = pattern_starts(s_eidx + p * kMaxLen, L, ww, wrm) & ~claimed;
+        const unsigned w = pattern_starts(eidx_a + 4 * p * kMaxLen, L, ww, wrm) & ~claimed;
         claimed |= w;
         if ((w >> lane) & 1u) best = p;
       }
       s_best[(b - tile0) + lane] = static_cast<int8_t>(best);
+#ifdef RELAY_TRACE
+      if (threadIdx.x == 0) stamp2(12);
+#endif
       wcount += __popc(claimed);
     } else {
       unsigned long long cm = 0;   // this lane's cues
 #pragma unroll 4
       for (int p = 0; p < cs.n_pat; p++) {
         const int L = sp.len[p];
-        const unsigned w = pattern_starts(s_eidx + p * kMaxLen, L, ww, wrm);
+        const unsigned w = pattern_starts(eidx_a + 4 * p * kMaxLen, L, ww, wrm);
         if ((w >> lane) & 1u) cm |= 1ull << sp.cue[p];
       }
       s_cues[(b - tile0) + lane] = cm;

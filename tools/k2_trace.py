@@ -47,6 +47,10 @@ def main():
         r6 = (buf[has, 6].astype(np.int64) - t0) / 1e3
         print("first window loaded (after first use) p50 %.2f | window complete p50 %.2f max %.2f | spins p50 %d max %d"
               % (np.median(r5), np.median(r6), r6.max(), np.median(buf[has, 7]), buf[has, 7].max()))
+    if (buf[:, 10] > 0).any():
+        ph = [(buf[:, k].astype(np.int64) - t0) / 1e3 for k in (10, 11, 12)]
+        print("warp 0 phase 1: terms done p50 %.2f | ballot words p50 %.2f | patterns p50 %.2f us"
+              % tuple(np.median(x) for x in ph))
     pub = (buf[1:, 8].astype(np.int64) - t0) / 1e3
     print("agg published p50 %.2f max %.2f (tile %d)" % (np.median(pub), pub.max(), 1 + int(np.argmax(pub))))
     last_pending = buf[:, 9].astype(np.int64) - 1

@@ -72,8 +72,8 @@ struct Agg {
 // Workspace layouts (256-byte aligned pieces).  tile_flag and done must be
 // zero before the first K3 launch (relay_workspace_init); K3 leaves them zero.
 struct ScanWs {
-  int* k2_flag;        // [n_tiles2] unused since the K2 look-back words carry their state
-  long long* k2_val;   // [n_tiles2][2] K2 look-back words (first n_tiles2): tag | state | count
+  int* k2_flag;        // [n_tiles2] K2 32-tile block arrival counters (zero between launches)
+  long long* k2_val;   // [n_tiles2][2] K2 look-back words: tile counts, then block sums (tag | count)
   int* k2_done;        // [1] K2 look-back epoch (the last launch's flag tag; any start value)
   int* tile_flag;      // [n_tiles] K3 look-back state (0 / head / inclusive)
   Agg* tile_val;       // [n_tiles][2] K3 published head / inclusive aggregate

@@ -80,15 +80,12 @@ __device__ __forceinline__ bool match_at(const CueDev& cs, const SmemPat& sp, in
 // first (lower caller index first among equal lengths) with a `claimed` mask,
 // so each start keeps its longest match; ALL: one claim mask per cue.  The
 // terminator word of the group is one ballot.  Compaction: per-warp counts,
-// a block scan over the 8 warps, and a WARP-PARALLEL decoupled look-back over
-// the tiles to the left (256 predecessors per round trip), so occurrences come out
-// sorted by position in one pass; flags carry a per-launch epoch tag (the
-// last tile advances it), so no pass resets them.
+// a block scan over the 8 warps, and a two-level decoupled look-back (32-tile
+// blocks summed by their last arriving tile), so occurrences come out sorted
+// by position in one pass; the look-back words carry a per-launch epoch tag
+// (the last tile advances it), so no pass resets them.
 constexpr int kTileB = kK2Tile;                 // positions per CTA (one 32-start group per warp)
 constexpr int kGroupsB = kTileB / 32 / (kScanThreads / 32);  // groups per warp
-constexpr int kTileAgg = 1;    // value = this tile's count
-constexpr int kTileSum = 2;    // value = count of this tile and every tile before it
-constexpr int kLookB = 8;      // K2 look-back window: 32 x kLookB predecessor tiles per round trip
 constexpr int kK2Offs = 512;   // K2: trajectory offsets staged in shared memory up to this many
 
 #ifdef RELAY_TRACE
@@ -215,7 +212,6 @@ __global__ void __launch_bounds__(kScanThreads)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long tile0 = static_cast<long long>(tile) * kTileB;
   TRACE2(0);
-  (void)tile_flag;  // the look-back state lives in the 64-bit words of tile_val
   // this launch's look-back tag (28 bits; 0 = never published)
   int ep = (*reinterpret_cast<const volatile int*>(epoch) + 1) & 0x0fffffff;
   if (ep == 0) ep = 1;
@@ -321,80 +317,58 @@ __global__ void __launch_bounds__(kScanThreads)
     }
     if (lane < kScanThreads / 32) s_wcount[lane] = incl - wv;   // exclusive warp offsets
     const long long total = __shfl_sync(kFull, incl, 31);
+    // Two-level look-back on one 64-bit word per tile, W[t] = tag << 36 |
+    // count (a single-copy-atomic relaxed store: no fence, no acquire, no
+    // second load for the value; the tag is this launch's epoch, so no pass
+    // resets the words).  Tiles form blocks of 32: the block's last tile to
+    // arrive (a counter in the workspace, re-zeroed by it) sums the block's
+    // W into B[block]; a tile's prefix is the sum of B over earlier blocks
+    // plus W over its earlier block mates.  Every tile reaching the scan at
+    // once made a flat look-back read every predecessor's word (all tiles
+    // polling the same lines: a ~3-6 us round trip at configs[1]).
     long long prefix = 0;
-    // Each tile publishes ONE 64-bit word, tag << 36 | state << 34 | count
-    // (count < 2^34): a single-copy-atomic relaxed store, so the look-back
-    // needs no fence, no acquire and no second load for the value.  The tag
-    // is this launch's epoch (no reset pass between launches).
-    const unsigned long long tagw = static_cast<unsigned long long>(ep) << 36;
-    constexpr unsigned long long kVal = (1ull << 34) - 1;
-    unsigned long long* const words = reinterpret_cast<unsigned long long*>(tile_val);
-    if (tile == 0) {
-      if (lane == 0) st_relaxed_u64(words, tagw | (static_cast<unsigned long long>(kTileSum) << 34) | total);
-    } else {
-      if (lane == 0)
-        st_relaxed_u64(words + tile, tagw | (static_cast<unsigned long long>(kTileAgg) << 34) | total);
+    {
+      const unsigned long long tagw = static_cast<unsigned long long>(ep) << 36;
+      const unsigned long long uep = static_cast<unsigned long long>(ep);
+      constexpr unsigned long long kVal = (1ull << 34) - 1;
+      unsigned long long* const words = reinterpret_cast<unsigned long long*>(tile_val);
+      unsigned long long* const bsum = words + gridDim.x;   // (the workspace holds 2 words per tile)
+      const int blk = tile >> 5, first = blk << 5;
+      const int nb = min(32, static_cast<int>(gridDim.x) - first);
+      if (lane == 0) st_relaxed_u64(words + tile, tagw | static_cast<unsigned long long>(total));
 #ifdef RELAY_TRACE
       if (lane == 0) stamp2(8);
 #endif
-      // windows of 32 x kLookB predecessors (d = lane + 32 u tiles back), all
-      // loads of a window in flight at once: a configs[1] tile (127
-      // predecessors) resolves in one round trip
-      for (long long j = tile - 1;; j -= 32 * kLookB) {
-        unsigned long long f[kLookB];
+      int old = 0;
+      if (lane == 0) old = atomicAdd(tile_flag + blk, 1);
+      old = __shfl_sync(kFull, old, 0);
+      const bool fin = old == nb - 1;          // the block's last arriver
+      const int need = fin ? nb : tile - first;
+      unsigned long long wv = lane < need ? ld_relaxed_u64(words + first + lane) : tagw;
+      while (__any_sync(kFull, (wv >> 36) != uep))
+        if ((wv >> 36) != uep) wv = ld_relaxed_u64(words + first + lane);
+      long long mates = lane < tile - first ? static_cast<long long>(wv & kVal) : 0;
+      long long whole = lane < nb ? static_cast<long long>(wv & kVal) : 0;
 #pragma unroll
-        for (int u = 0; u < kLookB; u++) {
-          const long long idx = j - lane - 32 * u;
-          f[u] = idx >= 0 ? ld_relaxed_u64(words + idx) : tagw | (static_cast<unsigned long long>(kTileSum) << 34);
-        }
-#ifdef RELAY_TRACE
-        int n_spin = 0;
-        if (lane == 0 && j == tile - 1) { (void)f[0]; stamp2(5); }
-#endif
-        for (;;) {
-#ifdef RELAY_TRACE
-          ++n_spin;
-#endif
-          bool pending = false;
-#pragma unroll
-          for (int u = 0; u < kLookB; u++) {
-            if ((f[u] >> 36) != static_cast<unsigned long long>(ep)) {  // not yet published in this launch
-              f[u] = ld_relaxed_u64(words + (j - lane - 32 * u));
-              pending |= (f[u] >> 36) != static_cast<unsigned long long>(ep);
-            }
-          }
-#ifdef RELAY_TRACE
-          if (j == tile - 1) {
-            int lastp = -1;
-            for (int u = 0; u < kLookB; u++)
-              if ((f[u] >> 36) != static_cast<unsigned long long>(ep)) lastp = static_cast<int>(j - lane - 32 * u);
-            lastp = __reduce_max_sync(kFull, lastp);
-            if (lane == 0 && lastp >= 0) g_trace2[blockIdx.x][9] = lastp + 1;
-          }
-#endif
-          if (!__any_sync(kFull, pending)) break;
-        }
-#ifdef RELAY_TRACE
-        if (lane == 0 && j == tile - 1) { stamp2(6); g_trace2[blockIdx.x][7] = n_spin; }
-#endif
-        int stop = 32 * kLookB;  // nearest predecessor with an inclusive count (distance)
-#pragma unroll
-        for (int u = kLookB - 1; u >= 0; u--) {
-          const unsigned sums = __ballot_sync(kFull, ((f[u] >> 34) & 3) == kTileSum);
-          if (sums) stop = 32 * u + __ffs(sums) - 1;
-        }
-        long long v = 0;
-#pragma unroll
-        for (int u = 0; u < kLookB; u++)
-          if (lane + 32 * u <= stop) v += static_cast<long long>(f[u] & kVal);
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-        prefix += v;
-        if (stop < 32 * kLookB) break;
+      for (int off = 16; off > 0; off >>= 1) {
+        mates += __shfl_xor_sync(kFull, mates, off);
+        whole += __shfl_xor_sync(kFull, whole, off);
       }
-      if (lane == 0)
-        st_relaxed_u64(words + tile,
-                       tagw | (static_cast<unsigned long long>(kTileSum) << 34) | static_cast<unsigned long long>(prefix + total));
+      if (fin && lane == 0) {
+        st_relaxed_u64(bsum + blk, tagw | static_cast<unsigned long long>(whole));
+        tile_flag[blk] = 0;                    // every tile of the block has counted
+      }
+      long long before = 0;                    // the earlier blocks
+      for (int j0 = 0; j0 < blk; j0 += 32) {
+        const int j = j0 + lane;
+        unsigned long long bv = j < blk ? ld_relaxed_u64(bsum + j) : tagw;
+        while (__any_sync(kFull, (bv >> 36) != uep))
+          if ((bv >> 36) != uep) bv = ld_relaxed_u64(bsum + j);
+        before += j < blk ? static_cast<long long>(bv & kVal) : 0;
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) before += __shfl_xor_sync(kFull, before, off);
+      prefix = before + mates;
     }
     if (lane == 0) {
       s_prefix = prefix;

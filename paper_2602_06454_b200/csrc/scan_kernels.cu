@@ -531,6 +531,49 @@ __device__ __forceinline__ int lower_bound_occ(const int* occ_pos, int n, long l
   return lo;
 }
 
+// First index i in [0, n) with a[i] >= key (n if none), by one warp: each
+// round samples 32 evenly spaced entries at once and keeps the bracket, so
+// the search takes ceil(log32 n) + 1 round trips instead of log2 n dependent
+// loads per thread.
+__device__ __forceinline__ int warp_lower_bound(const int* __restrict__ a, int n, long long key) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = n;  // the answer is in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * step;
+    const bool ge = idx >= hi || a[idx] >= key;
+    const unsigned b = __ballot_sync(kFull, ge);
+    const int f = b ? __ffs(b) - 1 : 32;
+    const int nlo = f == 0 ? lo : lo + (f - 1) * step + 1;
+    const int nhi = f == 32 ? hi : min(hi, lo + f * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  const int idx = lo + lane;
+  const bool ge = idx >= hi || a[idx] >= key;
+  const unsigned b = __ballot_sync(kFull, ge);
+  return b ? lo + __ffs(b) - 1 : hi;
+}
+
+#ifdef RELAY_TRACE
+// Tuning-only K3 timeline (tools/k3_trace.py): stamps by thread 0 of each tile:
+// 0 entry, 1 positions loaded, 2 moments added, 3 carry known, 4 occurrences
+// gathered, 5 exit.
+__device__ unsigned long long g_trace3[4096][8];
+__device__ __forceinline__ void stamp3(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0 && blockIdx.x < 4096) g_trace3[blockIdx.x][k] = t;
+}
+extern "C" int relay_debug_trace3_copy(unsigned long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_trace3, sizeof(unsigned long long) * 8 * n));
+}
+#define TRACE3(k) stamp3(k)
+#else
+#define TRACE3(k) ((void)0)
+#endif
+constexpr int kOccSmem = 1024;  // K3: a tile's occurrence positions staged in shared memory up to this many
+
 // Published per-tile state for the reverse decoupled look-back.
 constexpr int kTileHead = 1;   // value = aggregate from the tile start to its first tail
 constexpr int kTileIncl = 2;   // value = aggregate from the tile start onwards (carry included)
@@ -573,7 +616,9 @@ __global__ void __launch_bounds__(kScanThreads)
   const long long p0 = base + threadIdx.x * kItems;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   PosVal pv[kItems];
+  TRACE3(0);
   load_positions(margin, term_bits, n_tok, offs, n_traj, think_end, tau, p0, pv);
+  TRACE3(1);
   // per-trajectory tables: a tile inside one trajectory reduces as a block;
   // a tile spanning trajectories adds each position on its own (rare)
   int tile_traj = 0;
@@ -661,6 +706,7 @@ __global__ void __launch_bounds__(kScanThreads)
                 static_cast<unsigned long long>(__float_as_uint(fminf(fmaxf(mn, 0.0f), 1.0f))));
     }
     if (a[4]) atomicAdd(grow + 7, a[4]);  // NaN positions
+    TRACE3(2);
 
     // ---- tile head, publish, reverse look-back for the carry
     Agg head = s_w[kScanThreads / 32 - 1];
@@ -692,6 +738,7 @@ __global__ void __launch_bounds__(kScanThreads)
     s_carry = carry;
   }
   __syncthreads();
+  TRACE3(3);
 
   // ---- per-position suffix aggregates, gathered at the occurrences
   const long long nocc_ll = *n_occ_p < cap ? *n_occ_p : cap;
@@ -707,10 +754,36 @@ __global__ void __launch_bounds__(kScanThreads)
     run = agg_suffix(pv[i].v, run);
     sfx[i] = run;
   }
-  if (nocc > 0 && p0 < n_tok) {
-    const int lo = lower_bound_occ(occ_pos, nocc, p0);
-    for (int o = lo; o < nocc; o++) {
-      const long long s = occ_pos[o];
+  // the tile's occurrences [olo, ohi): two warp searches, then (usually)
+  // their positions in shared memory, so each thread finds its own without a
+  // chain of dependent global loads
+  __shared__ int s_orange[2];
+  __shared__ int s_occ[kOccSmem];
+  if (warp == 0) {
+    const int olo = nocc > 0 ? warp_lower_bound(occ_pos, nocc, base) : 0;
+    const int ohi = nocc > 0 ? warp_lower_bound(occ_pos, nocc, base + kTile) : 0;
+    if (lane == 0) { s_orange[0] = olo; s_orange[1] = ohi; }
+  }
+  __syncthreads();
+  const int olo = s_orange[0], ohi = s_orange[1];
+  const bool occ_sm = ohi - olo <= kOccSmem;
+  if (occ_sm)
+    for (int o = olo + threadIdx.x; o < ohi; o += blockDim.x) s_occ[o - olo] = occ_pos[o];
+  __syncthreads();
+  if (ohi > olo && p0 < n_tok) {
+    int lo;
+    if (occ_sm) {   // first occurrence >= p0 among the tile's, in shared memory
+      int a = 0, b = ohi - olo;
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (s_occ[m] < p0) a = m + 1; else b = m;
+      }
+      lo = olo + a;
+    } else {
+      lo = olo + lower_bound_occ(occ_pos + olo, ohi - olo, p0);
+    }
+    for (int o = lo; o < ohi; o++) {
+      const long long s = occ_sm ? s_occ[o - olo] : occ_pos[o];
       if (s >= p0 + kItems) break;
       Agg a = sfx[0];
 #pragma unroll
@@ -728,12 +801,16 @@ __global__ void __launch_bounds__(kScanThreads)
       // trigger (R13): no occurrence starts earlier in the same sentence,
       // i.e. the previous start is in another trajectory or a terminator lies
       // in [previous start, s - 1]
-      const int k = find_traj(offs, n_traj, n_tok, s);
+      int k = pv[0].traj;   // the position's trajectory, from load_positions
+#pragma unroll
+      for (int i = 1; i < kItems; i++)
+        if (s == p0 + i) k = pv[i].traj;
+      auto occ_at = [&](int j) -> long long { return occ_sm && j >= olo ? s_occ[j - olo] : occ_pos[j]; };
       int j = o - 1;
-      while (j >= 0 && occ_pos[j] == s) j--;
+      while (j >= 0 && occ_at(j) == s) j--;
       bool trig = true;
       if (j >= 0) {
-        const long long pp = occ_pos[j];
+        const long long pp = occ_at(j);
         const long long ts = offs ? offs[k] : 0;
         trig = (pp < ts) || any_term(term_bits, pp, s - 1);
       }
@@ -764,6 +841,7 @@ __global__ void __launch_bounds__(kScanThreads)
   // (and, fused H6, all-reduces the finished table over peer memory)
   __shared__ int s_last;
   __syncthreads();
+  TRACE3(4);
   if (threadIdx.x == 0) {
     __threadfence();
     s_last = atomicAdd(done, 1) == n_tiles - 1;
@@ -774,6 +852,7 @@ __global__ void __launch_bounds__(kScanThreads)
     }
   }
   __syncthreads();
+  TRACE3(5);
   if (pe.world > 0 && s_last) p2p_allreduce_block(pe, stats, pe_words);
 }
 

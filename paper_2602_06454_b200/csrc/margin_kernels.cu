@@ -1652,10 +1652,45 @@ static cudaError_t launch_step_groups(RowsArgs a, const CueDev& cs, cudaStream_t
   return cudaLaunchKernelEx(&cfg, kern, a, cs);
 }
 
+// K1 with consumer groups (the default; RELAY_K1_GROUPS=0 for one row per CTA
+// at a time): each CTA streams two rows at once, four consumer warps per row,
+// so the per-row work (row-start probe, partial last stage, partial hand-off,
+// ~510 instructions per warp per row) is paid by half the warps: configs[1]
+// K1 1.518 -> 1.494 ms burst, 1.794 -> 1.779 ms sustained (profiles/r02/k1_v9_ab.txt).
+#ifndef RELAY_K1_GROUPS_DEFAULT
+#define RELAY_K1_GROUPS_DEFAULT 1
+#endif
+static bool k1_groups() {
+  const char* e = getenv("RELAY_K1_GROUPS");
+  return e ? !strcmp(e, "1") : RELAY_K1_GROUPS_DEFAULT != 0;
+}
+
+template <class E>
+static cudaError_t launch_rows_groups(RowsArgs a, const CueDev& cs, cudaStream_t st) {
+  constexpr int NCW = kNCW, NS = kStages, UV = kUV;
+  auto kern = rows_kernel<E, NCW, NS, UV, kMinBlocks, kModeRows, 0, false, 2>;
+  const int smem = NS * UV * NCW * 32 * 16;
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (NCW + 2) * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  long long grid = static_cast<long long>(per_sm) * num_sms();
+  if (grid > (a.n_rows + 1) / 2) grid = (a.n_rows + 1) / 2;
+  kern<<<static_cast<unsigned>(grid), (NCW + 2) * 32, smem, st>>>(a, cs);
+  return cudaGetLastError();
+}
+
 template <class E, int MODE>
 static cudaError_t launch_rows_t(RowsArgs a, const CueDev& cs, cudaStream_t st) {
   if constexpr (MODE == kModeStep) {
     if (a.flat == 0 && !a.fuse && a.n_rows > num_sms() && k4_groups()) return launch_step_groups<E>(a, cs, st);
+  }
+  if constexpr (MODE == kModeRows) {
+    if (a.flat == 0 && k1_groups()) return launch_rows_groups<E>(a, cs, st);
   }
   // K4 runs ~1-2 CTAs per SM: a deeper ring keeps more bytes in flight per CTA
   constexpr int NS = (MODE == kModeStep) ? kStepStages : kStages;

@@ -128,6 +128,17 @@ def test_step_switch_edge_rows(relay, monkeypatch, groups):
     cs.destroy()
 
 
+@pytest.mark.parametrize("groups", ["1", "0"])
+@pytest.mark.parametrize("n_rows", [1, 2, 3, 443, 445, 889, 1333])
+def test_margin_rows_counts_and_groups(relay, monkeypatch, n_rows, groups):
+    """K1's row-to-CTA mapping at the edges: fewer rows than CTAs, an odd last
+    row for the consumer groups (rows b, b + grid, b + 2 grid, ...), more rows
+    than two per CTA; with and without the consumer groups."""
+    monkeypatch.setenv("RELAY_K1_GROUPS", groups)
+    L = synth.make_logits(n_rows, 3001, "bf16", seed=700 + n_rows, device=DEV)
+    _rows_check(relay, L, "bf16", 3001)
+
+
 def test_margin_rows_temperature(relay):
     L = synth.make_logits(64, 3000, "bf16", seed=5, device=DEV)
     _rows_check(relay, L, "bf16", 3000, iota=1.0 / 0.6)

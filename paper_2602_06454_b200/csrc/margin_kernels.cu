@@ -907,7 +907,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   // finish together instead of one CTA of a co-resident pair being starved
   // of issue slots and HBM share until the other is done); each group has
   // its own ring of NS stages, its own barriers and its own items
-  static_assert(NG == 1 || (NG == 2 && SPLIT == 0 && !FUSE && NCW % 2 == 0), "consumer groups");
+  static_assert(NG == 1 || (SPLIT == 0 && !FUSE && NCW % NG == 0 && kSlots % NG == 0), "consumer groups");
   constexpr int NCWG = NCW / NG;            // consumer warps per group
   constexpr int NCTG = NCWG * 32;           // consumer threads per group
   constexpr int SB = UV * NCTG * 16;        // bytes per ring stage (one group's)
@@ -1665,10 +1665,16 @@ static bool k1_groups() {
   return e ? !strcmp(e, "1") : RELAY_K1_GROUPS_DEFAULT != 0;
 }
 
+#ifndef RELAY_K1_NG
+#define RELAY_K1_NG 2          // consumer groups per K1 CTA (rows streamed at once)
+#endif
+#ifndef RELAY_K1_GROUP_NS
+#define RELAY_K1_GROUP_NS RELAY_K1_STAGES  // ring stages per group
+#endif
 template <class E>
 static cudaError_t launch_rows_groups(RowsArgs a, const CueDev& cs, cudaStream_t st) {
-  constexpr int NCW = kNCW, NS = kStages, UV = kUV;
-  auto kern = rows_kernel<E, NCW, NS, UV, kMinBlocks, kModeRows, 0, false, 2>;
+  constexpr int NCW = kNCW, NS = RELAY_K1_GROUP_NS, UV = kUV, NG = RELAY_K1_NG;
+  auto kern = rows_kernel<E, NCW, NS, UV, kMinBlocks, kModeRows, 0, false, NG>;
   const int smem = NS * UV * NCW * 32 * 16;
   static int per_sm = 0;
   if (per_sm == 0) {
@@ -1679,7 +1685,7 @@ static cudaError_t launch_rows_groups(RowsArgs a, const CueDev& cs, cudaStream_t
     if (per_sm < 1) per_sm = 1;
   }
   long long grid = static_cast<long long>(per_sm) * num_sms();
-  if (grid > (a.n_rows + 1) / 2) grid = (a.n_rows + 1) / 2;
+  if (grid > (a.n_rows + NG - 1) / NG) grid = (a.n_rows + NG - 1) / NG;
   kern<<<static_cast<unsigned>(grid), (NCW + 2) * 32, smem, st>>>(a, cs);
   return cudaGetLastError();
 }

@@ -9,9 +9,11 @@
 // sizeof(elem) per row; no tensor cores (a scan, not a contraction).
 //
 // K1 is a persistent warp-specialised kernel: one producer warp streams row
-// bodies into a shared-memory ring with 1-D TMA bulk copies (cp.async.bulk +
+// bodies into shared-memory rings with 1-D TMA bulk copies (cp.async.bulk +
 // mbarrier complete_tx), consumer warps reduce them, an epilogue warp merges
-// and finishes each row.  Ring-slot release and the hand-off of a row's
+// and finishes each row.  The consumer warps form two groups (NG = 2), each
+// with its own ring and barriers, so a CTA streams two rows at once and the
+// per-row work is paid by half the warps.  Ring-slot release and the hand-off of a row's
 // partials use named barriers (bar.arrive by the consumers, bar.sync by the
 // producer / epilogue warp: descheduled, no polling), so the two helper warps
 // take no issue slots.  The ring runs across row boundaries, so a row's
@@ -23,7 +25,9 @@
 // SMs, otherwise equal slices of the flattened batch merged by the last
 // arriving CTA; its epilogue warp runs RelayGen's switch state machine
 // on-device (switch.cuh).  In relay_step_sample it also bounds each row's
-// top-k for the sampling kernel (sample_kernels.cu).
+// top-k for the sampling kernel (sample_kernels.cu).  Opt-in, measured slower
+// and kept for the record: K4 with consumer groups
+// (RELAY_K4_GROUPS=1) and K4 drawing the token itself (RELAY_K4_FUSE=1).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>

@@ -1078,10 +1078,10 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       // groups: group g streams rows b + (g + k NG) grid; one stage per group
       // in turn (each group's stages land in its own ring)
       if constexpr (MODE == kModeStep) pdl_wait();
-      long long gr[NG];
-      int goff[NG], gbody[NG], gstage[NG];
-      long long gn[NG];
-      const char* gsrc[NG];
+      long long gr[NG] = {};
+      int goff[NG] = {}, gbody[NG] = {}, gstage[NG] = {};
+      long long gn[NG] = {};
+      const char* gsrc[NG] = {};
       auto open = [&](int g) {
         for (; gr[g] < a.n_rows; gr[g] += static_cast<long long>(NG) * gridDim.x) {
           const T* row = logits + gr[g] * a.stride;

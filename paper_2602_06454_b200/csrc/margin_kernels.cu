@@ -1328,12 +1328,13 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const int grp = NG > 1 ? warp / NCWG : 0;
   const int ctid = tid - grp * NCTG;       // thread index within the group
   const int cwarp = warp - grp * NCWG;     // warp index within the group
-  const uint32_t gring = ring_s + static_cast<uint32_t>(grp * NS * SB);
-  const uint32_t gfull = full_s + static_cast<uint32_t>(8 * grp * NS);
-  const int gbar = kBarRing0 + grp * NS;
-  int stage = 0;        // ring position, carried across items
+  // stage: the ring position as an index over every group's stages (this
+  // group's are [grp NS, grp NS + NS)), so that one register addresses the
+  // stage's buffer, its full mbarrier and its release barrier
+  const int st_beg = grp * NS, st_end = grp * NS + NS;
+  int stage = st_beg;   // ring position, carried across items
   uint32_t phase = 0;
-  const uint32_t ring_t = gring + static_cast<uint32_t>(ctid) * 16;  // this thread's first vector of stage 0
+  const uint32_t ring_t = ring_s + static_cast<uint32_t>(ctid) * 16;  // this thread's vector in stage 0's buffer
   ItemIter<SPLIT> iter;
   iter.init(a);
   Item item;
@@ -1390,7 +1391,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       // no barrier: each warp goes on with its own bound and whatever the
       // others have published (any of them is a valid lower bound), so the
       // steady state starts mostly on the fast path without a CTA-wide wait.
-      mbar_wait(gfull + 8 * stage, phase);
+      mbar_wait(full_s + 8 * stage, phase);
 #ifdef RELAY_TRACE
       if (ctid == 0 && n_stage < 10) TRACE(1 + n_stage);
       ++n_stage;
@@ -1398,7 +1399,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       uint4 raw[UV];
 #pragma unroll
       for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCTG * 16);
-      bar_arrive_pinned<UV>(gbar + stage, NCTG + 32, raw);  // release: the loads precede the refill
+      bar_arrive_pinned<UV>(kBarRing0 + stage, NCTG + 32, raw);  // release: the loads precede the refill
       const float2 h = stage_max2<E, UV>(raw);
       theta_w = theta_raise(warp_second(fmaxf(h.x, h.y), fminf(h.x, h.y)), theta_p);
 #ifdef RELAY_PROBE_BAR
@@ -1428,13 +1429,13 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         }
       }
       if (ctid == 0 && it <= 1) TRACE(14);
-      if (++stage == NS) { stage = 0; phase ^= 1; }
+      if (++stage == st_end) { stage = st_beg; phase ^= 1; }
     }
     // steady state: per stage the wait, the words, one release, the terms and
     // one guard comparison (consume_fast)
 #pragma unroll kSteadyUnroll
     for (int k = 1; k < nst; ++k) {
-      mbar_wait(gfull + 8 * stage, phase);
+      mbar_wait(full_s + 8 * stage, phase);
 #ifdef RELAY_TRACE
       if (ctid == 0 && n_stage < 10) TRACE(1 + n_stage);
       ++n_stage;
@@ -1443,7 +1444,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
       uint4 raw[UV];
 #pragma unroll
       for (int u = 0; u < UV; u++) raw[u] = lds128(ring_t + stage * SB + u * NCTG * 16);
-      bar_arrive_pinned<UV>(gbar + stage, NCTG + 32, raw);
+      bar_arrive_pinned<UV>(kBarRing0 + stage, NCTG + 32, raw);
       if constexpr (MODE == kModeStep) {
         // (before the terms: the words are dead after consume_fast)
         if (a.topk > 0) {
@@ -1460,11 +1461,11 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         }
       }
       consume_fast<E, UV, kPolyPairs>(raw, UV, jt + k * (SB / E::SZ), NCTG * VEC, st, c, T, tkey, theta_w, key, theta_p);
-      if (++stage == NS) { stage = 0; phase ^= 1; }
+      if (++stage == st_end) { stage = st_beg; phase ^= 1; }
     }
     if (rem > 0) {
-      mbar_wait(gfull + 8 * stage, phase);
-      const uint32_t buf = gring + stage * SB;
+      mbar_wait(full_s + 8 * stage, phase);
+      const uint32_t buf = ring_s + stage * SB;
       const int jb = j0 + g.head + nst * (SB / E::SZ);
       if (nst > 0) {
         // the last, partial stage: the missing vectors read as -inf (no term,
@@ -1474,7 +1475,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
         uint4 raw[UV];
 #pragma unroll
         for (int u = 0; u < UV; u++) raw[u] = u < nvalid ? lds128(ring_t + stage * SB + u * NCTG * 16) : E::neg_inf16();
-        bar_arrive_pinned<UV>(gbar + stage, NCTG + 32, raw);
+        bar_arrive_pinned<UV>(kBarRing0 + stage, NCTG + 32, raw);
         if constexpr (MODE == kModeStep) {
           if (a.topk > 0) {
             const float2 h = stage_max2<E, UV>(raw);
@@ -1500,9 +1501,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
             if (fuse) fuse_push<E, 1>(raw1, 1, jb + v * VEC, 0, fB, s_fv[fb], s_fi[fb], &s_fcnt[fb]);
           }
         }
-        bar_arrive(gbar + stage, NCTG + 32);
+        bar_arrive(kBarRing0 + stage, NCTG + 32);
       }
-      if (++stage == NS) { stage = 0; phase ^= 1; }
+      if (++stage == st_end) { stage = st_beg; phase ^= 1; }
     }
     if (ctid < j1 - g.tail) {
       const float x = E::load1(row + g.tail + ctid);

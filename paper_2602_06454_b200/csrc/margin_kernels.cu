@@ -78,6 +78,15 @@ extern "C" int relay_debug_fuse_stats(unsigned long long* host, int reset) {
 #endif
 constexpr int kSteadyUnroll = RELAY_STEADY_UNROLL;  // steady-stage loop unroll (tuning)
 
+// An opaque copy of a value: the compiler keeps it in a register instead of
+// recomputing it in every stage (K1's 64-register budget makes ptxas
+// rematerialise addresses it could keep).
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
 constexpr float kHuge = 268435456.0f;  // 2^28: beyond it fp32 y = z*c is too coarse
 
 struct ThreadState {
@@ -1334,7 +1343,9 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
   const int st_beg = grp * NS, st_end = grp * NS + NS;
   int stage = st_beg;   // ring position, carried across items
   uint32_t phase = 0;
-  const uint32_t ring_t = ring_s + static_cast<uint32_t>(ctid) * 16;  // this thread's vector in stage 0's buffer
+  // this thread's vector in stage 0's buffer (pinned: not recomputed from
+  // %tid in every stage; with theta_p below, -2.7% K1 instructions)
+  const uint32_t ring_t = pin_u32(ring_s + static_cast<uint32_t>(ctid) * 16);
   ItemIter<SPLIT> iter;
   iter.init(a);
   Item item;
@@ -1357,7 +1368,7 @@ __global__ void __launch_bounds__((NCW + 2) * 32, MINB) rows_kernel(RowsArgs a, 
     // the slot (threshold + partials) is free once the epilogue took item it - kSlots
     mbar_wait(rempty_s + 8 * slot, ((it / kSlots) & 1) ^ 1);
     if (ctid == 0 && it == 1) TRACE(12);
-    const uint32_t theta_p = theta_s + 4 * slot;
+    const uint32_t theta_p = pin_u32(theta_s + 4 * slot);
     const T* row = logits + r * a.stride;
     const Geom g = row_geom<E>(row, j0, j1);
     const int nst = g.body / SB;             // full ring stages of the item

@@ -707,6 +707,7 @@ class Analyzer:
         s = torch.cuda.current_stream() if stream is None else stream
         if not self.overlap_scan:
             cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, s)
+            stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s, self.n_tables)
         else:
             if self._side is None:
                 self._side = torch.cuda.Stream(device=self.device)
@@ -714,9 +715,10 @@ class Analyzer:
                 self._join = torch.cuda.Event()
             self._fork.record(s)
             self._side.wait_event(self._fork)
+            # the table reset and K2 both run beside K1 (K3 joins them)
+            stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, self._side, self.n_tables)
             cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
             self._join.record(self._side)
-        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s, self.n_tables)
         if k1_events:
             k1_events[0].record(s)
         margin_rows(logits, vocab=vocab or self.vocab, inv_temperature=self.iota, out=self.rows,
@@ -745,9 +747,9 @@ class Analyzer:
             self._join = torch.cuda.Event()
         self._fork.record(s)
         self._side.wait_event(self._fork)
+        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, self._side, self.n_tables)
         cue_scan(self.cs, tokens, traj_offsets, self.cap, self.ws, self.scan, self._side)
         self._join.record(self._side)
-        stats_init(self.stats, self.cs.n_cues, self.rank, self.world_size, s, self.n_tables)
         if k1_events:
             k1_events[0].record(s)
         for r0, chunk in chunks:
